@@ -1,0 +1,445 @@
+"""Python mirror of the reference codec API (slicer/codec.py), backed by sm_100a kernels.
+
+Reference boundary (slicer/__init__.py:15-25) and what replaces it here:
+
+    encode(x, cfg, seed) -> CompressedIF      codec.py:186   encode(x, cfg, seed) -> Payload
+    serialize(c) -> bytes                     codec.py:283   serialize(p) -> bytes (D2H copy)
+    deserialize(data) -> CompressedIF         codec.py:320   deserialize(data) -> Payload (checked)
+    decode(c) -> DenseTensor                  codec.py:254   decode(p) -> torch fp32 (N, K) on CUDA
+    payload_bits_exact(c) -> int              codec.py:269   payload_bits_exact(p)
+    atkf_filter(x, s, lam, seed)              atkf.py:44     atkf_filter(...) -> AtkfResult
+
+A `Payload` is the exact `.sif` byte stream held in device memory; the GPU encoder writes
+the serialized form directly, so `serialize(encode(x))` equals the reference's bytes.
+Errors are raised with the reference exception classes (see errors.py).  There is no
+CPU fallback: every call goes through libsif.so on a CUDA device.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import struct
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ConfigError, NonFiniteError, ShapeError, raise_for
+
+Q_MAX = 16
+MODE_ABQ = "abq"
+MODE_FIXED = "fixed_q"
+_MODE_CODES = {MODE_ABQ: 0, MODE_FIXED: 1}
+HEADER_BYTES = 32
+BLOCK_FIXED_BYTES = 13
+CRC_BYTES = 4
+DTYPE_F32 = 0
+DTYPE_BF16 = 1
+KIND_RESNET = 0
+KIND_LLM = 1
+
+
+def _L():
+    return _lib.load()
+
+
+def col_bits(k: int) -> int:
+    """codec.py:57-58."""
+    return max(1, (k - 1).bit_length())
+
+
+def keep_count(s: float, t: int) -> int:
+    """atkf.py:31-34 (computed by the native library with identical float64 rounding)."""
+    return int(_L().sif_keep_count(float(s), int(t)))
+
+
+@dataclass(frozen=True)
+class CodecConfig:
+    """codec.py:61-92, same fields, defaults and ConfigError validation."""
+
+    s: float
+    lam: float = 0.0
+    m_plus: int = 1
+    m_minus: int = 1
+    q_bit: int = 8
+    delta: float = 0.01
+    mode: str = MODE_ABQ
+    fixed_q: tuple = ()
+
+    def __post_init__(self):
+        if not 0.0 <= self.s <= 1.0:
+            raise ConfigError(f"s must be in [0, 1], got {self.s}")
+        if not 0.0 <= self.lam < 1.0:
+            raise ConfigError(f"lambda must be in [0, 1), got {self.lam}")
+        if self.m_plus < 1 or self.m_minus < 1:
+            raise ConfigError("block counts must be >= 1")
+        if not 1 <= self.q_bit <= Q_MAX:
+            raise ConfigError(f"q_bit must be in [1, {Q_MAX}], got {self.q_bit}")
+        if self.delta < 0:
+            raise ConfigError(f"delta must be >= 0, got {self.delta}")
+        if self.mode not in _MODE_CODES:
+            raise ConfigError(f"unknown mode {self.mode!r}")
+        if self.mode == MODE_FIXED:
+            if len(self.fixed_q) != self.m_plus + self.m_minus:
+                raise ConfigError(f"fixed_q needs {self.m_plus + self.m_minus} entries, got {len(self.fixed_q)}")
+            if any(not 1 <= int(q) <= Q_MAX for q in self.fixed_q):
+                raise ConfigError("fixed_q entries must be in [1, 16]")
+
+    def _c(self):
+        """Returns (sif_codec_cfg, keep-alive buffer)."""
+        q = (ctypes.c_uint8 * max(1, len(self.fixed_q)))(*[int(v) for v in self.fixed_q])
+        c = _lib.CodecCfgC(float(self.s), float(self.lam), float(self.delta), int(self.m_plus),
+                           int(self.m_minus), int(self.q_bit), _MODE_CODES[self.mode],
+                           ctypes.cast(q, ctypes.c_void_p) if self.fixed_q else None)
+        return c, q
+
+
+def broadcast_q(q_per_plane, m_plus: int, m_minus: int) -> tuple:
+    """codec.py:95-105."""
+    q = tuple(int(v) for v in q_per_plane)
+    if len(q) == m_plus + m_minus:
+        return q
+    if len(q) == m_plus == m_minus:
+        return q + q
+    raise ConfigError(f"Q vector of length {len(q)} fits neither {m_plus}+{m_minus} nor a per-plane broadcast")
+
+
+def max_payload_bytes(rows: int, cols: int, cfg: CodecConfig) -> int:
+    c, _keep = cfg._c()
+    return int(_L().sif_max_payload_bytes(rows, cols, ctypes.byref(c)))
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _check_seed(seed: int) -> int:
+    seed = int(seed)
+    if seed < 0 or seed >= 1 << 64:  # np.uint64(seed) raises OverflowError (rng.py:65)
+        raise OverflowError(f"seed {seed} out of range for uint64")
+    return seed
+
+
+def _as_if(x) -> tuple[torch.Tensor, int]:
+    if not isinstance(x, torch.Tensor):
+        x = torch.as_tensor(np.asarray(x, dtype=np.float32))
+    if x.dim() != 2:
+        raise ShapeError(f"IF must be 2-D (rows x cols), got shape {tuple(x.shape)}")
+    if x.shape[0] < 1 or x.shape[1] < 1:
+        raise ShapeError(f"tensor shape must be positive, got {x.shape[0]}x{x.shape[1]}")
+    if x.dtype not in (torch.float32, torch.bfloat16):
+        x = x.to(torch.float32)
+    if not x.is_cuda:
+        x = x.cuda()
+    x = x.contiguous()
+    if x.data_ptr() % 16:
+        x = x.clone()
+    return x, (DTYPE_F32 if x.dtype == torch.float32 else DTYPE_BF16)
+
+
+class Payload:
+    """One `.sif` stream in device memory (bytes [0, nbytes) of `buf`)."""
+
+    def __init__(self, buf: torch.Tensor, nbytes: int, rows: int, cols: int):
+        self.buf = buf
+        self.nbytes = int(nbytes)
+        self.rows = int(rows)
+        self.cols = int(cols)
+
+    @property
+    def shape(self):
+        return (self.rows, self.cols)
+
+    @property
+    def payload_bits(self) -> int:
+        return 8 * self.nbytes
+
+    def tensor(self) -> torch.Tensor:
+        return self.buf[: self.nbytes]
+
+    def to_bytes(self) -> bytes:
+        return bytes(self.buf[: self.nbytes].cpu().numpy().tobytes())
+
+    __bytes__ = to_bytes
+
+    def header(self) -> dict:
+        h = self.buf[:HEADER_BYTES].cpu().numpy().tobytes()
+        ver, n, k, s, lam, qb, dl, mode, mp, mm = struct.unpack_from("<HIIffBfBHH", h, 4)
+        return dict(version=ver, rows=n, cols=k, s=s, lam=lam, q_bit=qb, delta=dl,
+                    mode=MODE_FIXED if mode == 1 else MODE_ABQ, m_plus=mp, m_minus=mm)
+
+    def blocks(self) -> list:
+        """Per-block metadata (q, o, v_min, nnz) read from the device block table."""
+        return _parse_table(self)
+
+    def __eq__(self, other):
+        if not isinstance(other, Payload):
+            return NotImplemented
+        return self.nbytes == other.nbytes and bool(torch.equal(self.tensor(), other.tensor()))
+
+
+# ---------------------------------------------------------------------------- encode
+def _enc_descs(xs, outs, caps, seeds, dtypes):
+    n = len(xs)
+    arr = (_lib.EncDesc * max(1, n))()
+    for i in range(n):
+        x = xs[i]
+        arr[i].x = x.data_ptr()
+        arr[i].out = outs[i]
+        arr[i].out_cap = caps[i]
+        arr[i].seed = seeds[i]
+        arr[i].rows = x.shape[0]
+        arr[i].cols = x.shape[1]
+        arr[i].dtype = dtypes[i]
+    return arr
+
+
+class BatchEncoder:
+    """Plan + uploaded descriptors for a fixed batch of IF buffers (reusable across steps).
+
+    `xs` is a (B, rows, cols) CUDA tensor (fp32 or bf16); payloads are written into
+    `self.out` (B, cap) uint8 with exact lengths in `self.out_len` and per-IF status in
+    `self.status`.  `run()` only launches kernels (no host sync)."""
+
+    def __init__(self, xs: torch.Tensor, cfg: CodecConfig, seeds, stream=None):
+        if xs.dim() != 3:
+            raise ShapeError("batch must be (B, rows, cols)")
+        self.xs = xs.contiguous()
+        self.cfg = cfg
+        self.B, self.rows, self.cols = self.xs.shape
+        self.dtype = DTYPE_F32 if self.xs.dtype == torch.float32 else DTYPE_BF16
+        self.cap = max_payload_bytes(self.rows, self.cols, cfg)
+        dev = self.xs.device
+        self.out = torch.zeros((self.B, self.cap), dtype=torch.uint8, device=dev)
+        self.out_len = torch.zeros(self.B, dtype=torch.int64, device=dev)
+        self.status = torch.full((self.B,), -1, dtype=torch.int32, device=dev)
+        self.seeds = [_check_seed(s) for s in seeds]
+        xs_list = [self.xs[i] for i in range(self.B)]
+        outs = [self.out.data_ptr() + i * self.cap for i in range(self.B)]
+        self._descs = _enc_descs(xs_list, outs, [self.cap] * self.B, self.seeds, [self.dtype] * self.B)
+        self._cfg_c, self._keep = cfg._c()
+        self.plan = _lib.Plan()
+        raise_for(_L().sif_enc_plan(self._descs, self.B, ctypes.byref(self._cfg_c), ctypes.byref(self.plan)),
+                  "sif_enc_plan")
+        self.ws = torch.empty(max(1, self.plan.ws_bytes), dtype=torch.uint8, device=dev)
+        raise_for(_L().sif_enc_upload(ctypes.byref(self.plan), self._descs, ctypes.byref(self._cfg_c),
+                                      ctypes.c_void_p(self.ws.data_ptr()), _stream()), "sif_enc_upload")
+
+    def run(self):
+        raise_for(_L().sif_enc_run(ctypes.byref(self.plan), ctypes.byref(self._cfg_c),
+                                   ctypes.c_void_p(self.ws.data_ptr()), ctypes.c_void_p(self.out_len.data_ptr()),
+                                   ctypes.c_void_p(self.status.data_ptr()), _stream()), "sif_enc_run")
+        return self
+
+    def check(self):
+        st = self.status.cpu().numpy()
+        bad = np.flatnonzero(st != 0)
+        if bad.size:
+            raise_for(int(st[bad[0]]), f"IF {int(bad[0])} of the batch")
+        return self
+
+    def payloads(self) -> list:
+        lens = self.out_len.cpu().numpy()
+        return [Payload(self.out[i], int(lens[i]), self.rows, self.cols) for i in range(self.B)]
+
+
+def encode(x, cfg: CodecConfig, seed: int = 0) -> Payload:
+    """serialize(encode(x, cfg, seed)) of the reference, computed on the GPU."""
+    if not isinstance(cfg, CodecConfig):
+        raise ConfigError("cfg must be a CodecConfig")
+    seed = _check_seed(seed)
+    xt, dt = _as_if(x)
+    enc = BatchEncoder(xt.unsqueeze(0), cfg, [seed])
+    enc.run().check()
+    return enc.payloads()[0]
+
+
+def encode_batch(xs: torch.Tensor, cfg: CodecConfig, seeds) -> list:
+    enc = BatchEncoder(xs, cfg, list(seeds))
+    enc.run().check()
+    return enc.payloads()
+
+
+def serialize(p: Payload) -> bytes:
+    return p.to_bytes()
+
+
+def payload_bits_exact(p: Payload) -> int:
+    return 8 * p.nbytes
+
+
+# ---------------------------------------------------------------------------- decode
+class BatchDecoder:
+    """Plan + descriptors for decoding B streams into a (B, rows, cols) fp32 tensor."""
+
+    def __init__(self, bufs, lens, rows: int, cols: int, out: torch.Tensor | None = None,
+                 parse_only: bool = False):
+        self.B = len(lens)
+        self.rows, self.cols = int(rows), int(cols)
+        dev = torch.device("cuda")
+        self.out = out if out is not None else torch.empty((self.B, self.rows, self.cols), dtype=torch.float32,
+                                                            device=dev)
+        self.status = torch.full((self.B,), -1, dtype=torch.int32, device=dev)
+        self.parse_only = 1 if parse_only else 0
+        arr = (_lib.DecDesc * max(1, self.B))()
+        for i in range(self.B):
+            arr[i].inp = bufs[i]
+            arr[i].in_len = int(lens[i])
+            arr[i].out = self.out.data_ptr() + i * self.rows * self.cols * 4
+            arr[i].rows = self.rows
+            arr[i].cols = self.cols
+        self._descs = arr
+        self.plan = _lib.Plan()
+        raise_for(_L().sif_dec_plan(arr, self.B, ctypes.byref(self.plan)), "sif_dec_plan")
+        self.ws = torch.empty(max(1, self.plan.ws_bytes), dtype=torch.uint8, device=dev)
+        raise_for(_L().sif_dec_upload(ctypes.byref(self.plan), arr, ctypes.c_void_p(self.ws.data_ptr()), _stream()),
+                  "sif_dec_upload")
+
+    def run(self):
+        raise_for(_L().sif_dec_run(ctypes.byref(self.plan), self.parse_only, ctypes.c_void_p(self.ws.data_ptr()),
+                                   ctypes.c_void_p(self.status.data_ptr()), _stream()), "sif_dec_run")
+        return self
+
+    def check(self):
+        st = self.status.cpu().numpy()
+        bad = np.flatnonzero(st != 0)
+        if bad.size:
+            raise_for(int(st[bad[0]]), f"stream {int(bad[0])} of the batch")
+        return self
+
+    def table(self, i: int) -> np.ndarray:
+        stride = int(_L().sif_dec_table_stride(ctypes.byref(self.plan)))
+        base = self.plan.ws_aux_off + i * stride
+        return self.ws[base: base + stride].cpu().numpy().view(np.uint32).reshape(-1, 16)
+
+
+def _device_bytes(data) -> tuple[torch.Tensor, int]:
+    if isinstance(data, Payload):
+        return data.buf, data.nbytes
+    if isinstance(data, torch.Tensor):
+        t = data.reshape(-1).to(torch.uint8)
+        n = t.numel()
+    else:
+        b = bytes(data)
+        n = len(b)
+        t = torch.from_numpy(np.frombuffer(b, dtype=np.uint8).copy()) if n else torch.zeros(0, dtype=torch.uint8)
+    buf = torch.zeros(max(16, (n + 15) // 16 * 16 + 16), dtype=torch.uint8, device="cuda")
+    if n:
+        buf[:n].copy_(t.cuda() if not t.is_cuda else t)
+    return buf, n
+
+
+def _header_shape(buf: torch.Tensor, n: int) -> tuple[int, int]:
+    if n < HEADER_BYTES + CRC_BYTES:
+        return 0, 0
+    h = buf[:HEADER_BYTES].cpu().numpy().tobytes()
+    if h[:4] != b"SIF1":
+        return 0, 0
+    return struct.unpack_from("<II", h, 6)
+
+
+def deserialize(data) -> Payload:
+    """codec.py:320-399 checks (length, magic, CRC, version, mode, framing, q range) on
+    the device; raises StreamFormatError / CorruptStreamError like the reference."""
+    buf, n = _device_bytes(data)
+    rows, cols = _header_shape(buf, n)
+    dec = BatchDecoder([buf.data_ptr()], [n], rows, cols, out=torch.empty((1, 0, 0), device="cuda"),
+                       parse_only=True)
+    dec.run().check()
+    return Payload(buf, n, rows, cols)
+
+
+def decode(p) -> torch.Tensor:
+    """decode(deserialize(bytes)) of the reference: fp32 (rows, cols) CUDA tensor."""
+    if not isinstance(p, Payload):
+        buf, n = _device_bytes(p)
+        rows, cols = _header_shape(buf, n)
+        p = Payload(buf, n, rows, cols)
+    dec = BatchDecoder([p.buf.data_ptr()], [p.nbytes], p.rows, p.cols)
+    dec.run().check()
+    return dec.out[0]
+
+
+def decode_batch(payloads: list, out: torch.Tensor | None = None) -> torch.Tensor:
+    if not payloads:
+        return torch.empty((0, 0, 0), device="cuda")
+    rows, cols = payloads[0].rows, payloads[0].cols
+    dec = BatchDecoder([p.buf.data_ptr() for p in payloads], [p.nbytes for p in payloads], rows, cols, out=out)
+    dec.run().check()
+    return dec.out
+
+
+def _parse_table(p: Payload) -> list:
+    dec = BatchDecoder([p.buf.data_ptr()], [p.nbytes], p.rows, p.cols, out=torch.empty((1, 0, 0), device="cuda"),
+                       parse_only=True)
+    dec.run().check()
+    tab = dec.table(0)
+    nb = int(tab[0, 7])
+    out = []
+    for b in range(nb):
+        r = tab[2 + b]
+        out.append(dict(q=int(r[0]), nnz=int(r[1]), o=float(np.uint32(r[2]).view(np.float32)),
+                        v_min=float(np.uint32(r[3]).view(np.float32)), plane="plus" if b < int(tab[0, 3]) else "minus"))
+    return out
+
+
+# ---------------------------------------------------------------------------- ATKF
+@dataclass(frozen=True)
+class AtkfResult:
+    """atkf.py:20-28."""
+
+    kept_indices: torch.Tensor = field(repr=False)  # sorted flat indices (int64, CUDA)
+    tau: float
+    tau_plus: float
+    tau_minus: float
+    k_keep: int
+    tau_is_fallback: bool = False
+    x: torch.Tensor = field(default=None, repr=False)
+
+    @property
+    def filtered(self) -> torch.Tensor:
+        out = torch.zeros(self.x.numel(), dtype=torch.float32, device=self.x.device)
+        xv = self.x.reshape(-1).to(torch.float32)
+        out[self.kept_indices] = xv[self.kept_indices]
+        return out.reshape(self.x.shape)
+
+
+def atkf_filter(x, s: float, lam: float, seed: int) -> AtkfResult:
+    """atkf.py:44-96 on the GPU: exact-cardinality asymmetric top-K with splitmix ties."""
+    if not 0.0 <= s <= 1.0:
+        raise ConfigError(f"sparsity s must be in [0, 1], got {s}")
+    if not 0.0 <= lam < 1.0:
+        raise ConfigError(f"asymmetry lambda must be in [0, 1), got {lam}")
+    seed = _check_seed(seed)
+    xt, dt = _as_if(x)
+    cfg = CodecConfig(s=s, lam=lam)
+    k = keep_count(s, xt.numel())
+    descs = _enc_descs([xt], [0], [0], [seed], [dt])
+    c, _keep = cfg._c()
+    plan = _lib.Plan()
+    # the ATKF plan sizes the workspace like the encoder (same kernel, ATKF-only mode)
+    dummy = torch.empty(16, dtype=torch.uint8, device=xt.device)
+    descs[0].out = dummy.data_ptr()
+    raise_for(_L().sif_enc_plan(descs, 1, ctypes.byref(c), ctypes.byref(plan)), "plan")
+    ws = torch.empty(plan.ws_bytes + 4096, dtype=torch.uint8, device=xt.device)
+    kept = torch.empty(max(1, k), dtype=torch.int64, device=xt.device)
+    tau3 = torch.zeros(3, dtype=torch.float64, device=xt.device)
+    status = torch.full((1,), -1, dtype=torch.int32, device=xt.device)
+    raise_for(_L().sif_atkf_batched(descs, 1, ctypes.byref(c), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                    ctypes.c_void_p(kept.data_ptr()), ctypes.c_void_p(tau3.data_ptr()),
+                                    ctypes.c_void_p(status.data_ptr()), _stream()), "sif_atkf_batched")
+    raise_for(int(status.item()), "atkf")
+    t = tau3.cpu().numpy()
+    return AtkfResult(kept[:k], float(t[0]), float(t[1]), float(t[2]), k, k == 0, xt)
+
+
+# ---------------------------------------------------------------------------- synthetic
+def synthetic(kind: int, rows: int, cols: int, sid: int, dtype=torch.float32, out: torch.Tensor | None = None):
+    """Integer-exact synthetic IF generated on the device."""
+    if out is None:
+        out = torch.empty((rows, cols), dtype=dtype, device="cuda")
+    dt = DTYPE_F32 if out.dtype == torch.float32 else DTYPE_BF16
+    raise_for(_L().sif_gen_synthetic(ctypes.c_void_p(out.data_ptr()), rows, cols, dt, kind, int(sid), _stream()),
+              "sif_gen_synthetic")
+    return out

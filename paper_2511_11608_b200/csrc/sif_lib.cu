@@ -1,0 +1,363 @@
+// sif_lib.cu -- C ABI (include/sif.h) of the B200 SLICER IF codec: planning, workspace
+// layout, uploads and kernel launches.  One translation unit: the kernels are included.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "sif.h"
+#include "sif_decode.cu"
+#include "sif_encode.cu"
+#include "sif_synth.cu"
+
+namespace {
+
+constexpr int kSmemBudget = 227 * 1024 - 4 * 1024;  // dynamic; leaves room for static smem
+constexpr int kDecTileElems = 4096;
+constexpr int kDecRpcCap = 2048;
+
+inline uint64_t up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+int check_cuda(cudaError_t e) { return e == cudaSuccess ? SIF_OK : SIF_ERR_CUDA; }
+
+int choose_cluster(uint64_t tmax) {
+  const char* env = getenv("SIF_CLUSTER");
+  if (env && *env) {
+    int g = atoi(env);
+    if (g == 1 || g == 2 || g == 4 || g == 8 || g == 16) return g;
+  }
+  (void)tmax;
+  return 1;
+}
+
+uint64_t enc_block_bytes(int maxb) {
+  // b_sum, b_pre, b_N, b_off x4, b_o64, b_or (u64) + 8 u32 arrays + wcnt/woff
+  return (uint64_t)maxb * (8 * 3 + 8 * 4 + 8 * 2 + 4 * 8) + 2ull * sif::NW * 4 * maxb + 64;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sif_version(void) { return 1; }
+
+uint64_t sif_keep_count(double s, uint64_t t) { return sif::keep_count(s, t); }
+
+uint32_t sif_col_bits(uint32_t k) { return sif::col_bits(k); }
+
+const char* sif_status_string(int st) {
+  switch (st) {
+    case SIF_OK: return "ok";
+    case SIF_ERR_CONFIG: return "ConfigError";
+    case SIF_ERR_NONFINITE: return "NonFiniteError";
+    case SIF_ERR_SHAPE: return "ShapeError";
+    case SIF_ERR_STREAM_FORMAT: return "StreamFormatError";
+    case SIF_ERR_CORRUPT_STREAM: return "CorruptStreamError";
+    case SIF_ERR_CAPACITY: return "CapacityError";
+    case SIF_ERR_CUDA: return "CudaError";
+    case SIF_ERR_INVALID_ARG: return "InvalidArgument";
+    default: return "unknown";
+  }
+}
+
+// codec.py:72-92
+int sif_validate_cfg(const sif_codec_cfg* c) {
+  if (!c) return SIF_ERR_INVALID_ARG;
+  if (!(c->s >= 0.0 && c->s <= 1.0)) return SIF_ERR_CONFIG;
+  if (!(c->lam >= 0.0 && c->lam < 1.0)) return SIF_ERR_CONFIG;
+  if (c->m_plus < 1 || c->m_minus < 1) return SIF_ERR_CONFIG;
+  if (c->q_bit < 1 || c->q_bit > 16) return SIF_ERR_CONFIG;
+  if (!(c->delta >= 0.0)) return SIF_ERR_CONFIG;
+  if (c->mode != SIF_MODE_ABQ && c->mode != SIF_MODE_FIXED) return SIF_ERR_CONFIG;
+  if (c->mode == SIF_MODE_FIXED) {
+    if (!c->fixed_q) return SIF_ERR_CONFIG;
+    for (int i = 0; i < c->m_plus + c->m_minus; ++i)
+      if (c->fixed_q[i] < 1 || c->fixed_q[i] > 16) return SIF_ERR_CONFIG;
+  }
+  if (c->m_plus > 65535 || c->m_minus > 65535) return SIF_ERR_CONFIG;
+  return SIF_OK;
+}
+
+// Sound capacity bound (planner.py:33-64 charges q_bit only, which under-counts fixed-Q
+// blocks with q > q_bit; here every block is charged max(q_bit, max fixed q)).
+uint64_t sif_max_payload_bytes(uint32_t rows, uint32_t cols, const sif_codec_cfg* c) {
+  if (sif_validate_cfg(c) != SIF_OK) return 0;
+  const uint64_t T = (uint64_t)rows * cols;
+  const uint64_t k = sif::keep_count(c->s, T);
+  uint32_t qmax = (uint32_t)c->q_bit;
+  if (c->mode == SIF_MODE_FIXED)
+    for (int i = 0; i < c->m_plus + c->m_minus; ++i) qmax = std::max<uint32_t>(qmax, c->fixed_q[i]);
+  const uint64_t kk = std::max<uint64_t>(1, k);
+  const uint64_t B = std::min<uint64_t>(c->m_plus, kk) + std::min<uint64_t>(c->m_minus, kk);
+  uint64_t bytes = 36 + (c->mode == SIF_MODE_FIXED ? B : 0);
+  bytes += B * (13 + 4ull * ((uint64_t)rows + 1) + 2);
+  bytes += (k * (sif::col_bits(cols) + qmax) + 7) / 8;
+  return up(bytes, 16);
+}
+
+// ------------------------------------------------------------------ encode
+static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, int atkf, sif_plan* p) {
+  if (!d || !p || n < 0) return SIF_ERR_INVALID_ARG;
+  int st = sif_validate_cfg(c);
+  if (st) return st;
+  memset(p, 0, sizeof(*p));
+  uint64_t tmax = 1, kmax = 0;
+  for (int i = 0; i < n; ++i) {
+    if (d[i].rows < 1 || d[i].cols < 1) return SIF_ERR_SHAPE;  // tensor.py:27-28
+    const uint64_t T = (uint64_t)d[i].rows * d[i].cols;
+    if (T >= (1ull << 31)) return SIF_ERR_INVALID_ARG;
+    if (d[i].dtype != SIF_DTYPE_F32 && d[i].dtype != SIF_DTYPE_BF16) return SIF_ERR_INVALID_ARG;
+    if (!d[i].x || (reinterpret_cast<uintptr_t>(d[i].x) & 15)) return SIF_ERR_INVALID_ARG;
+    if (!atkf && (!d[i].out || (reinterpret_cast<uintptr_t>(d[i].out) & 15))) return SIF_ERR_INVALID_ARG;
+    tmax = std::max(tmax, T);
+    kmax = std::max(kmax, sif::keep_count(c->s, T));
+  }
+  const int G = choose_cluster(tmax);
+  const uint64_t kk = std::max<uint64_t>(1, kmax);
+  const int maxb = (int)(std::min<uint64_t>(c->m_plus, kk) + std::min<uint64_t>(c->m_minus, kk));
+  const uint64_t fixed = 1024 + (uint64_t)(G > 1 ? 2 : 1) * sif::MAXT * sif::HB * 4 + enc_block_bytes(maxb) + 16;
+  if (fixed + 12ull * 256 > (uint64_t)kSmemBudget) return SIF_ERR_CONFIG;  // too many blocks
+  const uint64_t slice = (tmax + G - 1) / G;
+  uint64_t cap = ((uint64_t)kSmemBudget - fixed) / 12;
+  cap = std::min<uint64_t>(cap, up(slice, 32));
+  p->n = n;
+  p->cluster = G;
+  p->threads = sif::NT;
+  p->cap_smem = (int32_t)cap;
+  p->smem_bytes = (int32_t)(fixed + 12 * cap);
+  p->max_blocks = maxb;
+  p->flags = atkf;
+  const uint64_t spill_cta = up(12ull * (slice > cap ? slice - cap : 0), 256);
+  uint64_t off = 0;
+  p->ws_desc_off = off;
+  off += up(sizeof(sif_enc_desc) * (uint64_t)std::max(n, 1), 256);
+  p->ws_aux_off = off;  // fixed_q bytes, then kept offsets (atkf)
+  off += up((uint64_t)c->m_plus + c->m_minus, 256) + up(8ull * std::max(n, 1), 256);
+  p->ws_spill_off = off;
+  off += spill_cta * (uint64_t)std::max(n, 1) * G;
+  p->ws_bytes = up(off, 256);
+  p->tiles = (int32_t)(spill_cta / 256);  // spill stride in 256-byte units
+  return SIF_OK;
+}
+
+int sif_enc_plan(const sif_enc_desc* d, int n, const sif_codec_cfg* c, sif_plan* p) {
+  return enc_plan_impl(d, n, c, 0, p);
+}
+
+int sif_enc_upload(const sif_plan* p, const sif_enc_desc* d, const sif_codec_cfg* c, void* ws, void* stream) {
+  if (!p || !ws) return SIF_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t* w = (uint8_t*)ws;
+  if (p->n > 0 && check_cuda(cudaMemcpyAsync(w + p->ws_desc_off, d, sizeof(sif_enc_desc) * p->n, cudaMemcpyHostToDevice, s)))
+    return SIF_ERR_CUDA;
+  if (c->mode == SIF_MODE_FIXED &&
+      check_cuda(cudaMemcpyAsync(w + p->ws_aux_off, c->fixed_q, (size_t)(c->m_plus + c->m_minus), cudaMemcpyHostToDevice, s)))
+    return SIF_ERR_CUDA;
+  return SIF_OK;
+}
+
+static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint64_t* out_len, int32_t* status,
+                      int atkf, int64_t* kept, double* tau3, cudaStream_t s) {
+  if (p->n == 0) return SIF_OK;
+  uint8_t* w = (uint8_t*)ws;
+  sif::EncArgs a;
+  memset(&a, 0, sizeof(a));
+  a.descs = reinterpret_cast<const sif_enc_desc*>(w + p->ws_desc_off);
+  a.n = p->n;
+  a.atkf_only = atkf;
+  a.s = c->s; a.lam = c->lam; a.delta = c->delta;
+  a.m_plus = c->m_plus; a.m_minus = c->m_minus; a.q_bit = c->q_bit; a.mode = c->mode;
+  a.fixed_q = w + p->ws_aux_off;
+  a.spill = w + p->ws_spill_off;
+  a.spill_stride = (uint64_t)p->tiles * 256;
+  a.cap = p->cap_smem;
+  a.maxb = p->max_blocks;
+  a.out_len = out_len;
+  a.status = status;
+  a.kept_out = kept;
+  a.kept_off = reinterpret_cast<const uint64_t*>(w + p->ws_aux_off + up((uint64_t)c->m_plus + c->m_minus, 256));
+  a.tau3 = tau3;
+  if (check_cuda(cudaFuncSetAttribute(sif::sif_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem_bytes)))
+    return SIF_ERR_CUDA;
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)(p->n * p->cluster));
+  cfg.blockDim = dim3(sif::NT);
+  cfg.dynamicSmemBytes = (size_t)p->smem_bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  if (p->cluster > 1) {
+    if (p->cluster > 8)
+      cudaFuncSetAttribute(sif::sif_encode_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)p->cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  if (check_cuda(cudaLaunchKernelEx(&cfg, sif::sif_encode_kernel, a))) return SIF_ERR_CUDA;
+  return check_cuda(cudaGetLastError());
+}
+
+int sif_enc_run(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint64_t* out_len, int32_t* status, void* stream) {
+  if (!p || !c || !ws || !out_len || !status) return SIF_ERR_INVALID_ARG;
+  return enc_launch(p, c, ws, out_len, status, 0, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+int sif_encode_batched(const sif_enc_desc* d, int n, const sif_codec_cfg* c, void* ws, size_t ws_bytes,
+                       uint64_t* out_len, int32_t* status, void* stream) {
+  sif_plan p;
+  int st = sif_enc_plan(d, n, c, &p);
+  if (st) return st;
+  if (ws_bytes < p.ws_bytes) return SIF_ERR_CAPACITY;
+  st = sif_enc_upload(&p, d, c, ws, stream);
+  if (st) return st;
+  return sif_enc_run(&p, c, ws, out_len, status, stream);
+}
+
+int sif_atkf_batched(const sif_enc_desc* d, int n, const sif_codec_cfg* c, void* ws, size_t ws_bytes, int64_t* kept,
+                     double* tau3, int32_t* status, void* stream) {
+  sif_plan p;
+  int st = enc_plan_impl(d, n, c, 1, &p);
+  if (st) return st;
+  if (ws_bytes < p.ws_bytes) return SIF_ERR_CAPACITY;
+  cudaStream_t s = (cudaStream_t)stream;
+  st = sif_enc_upload(&p, d, c, ws, stream);
+  if (st) return st;
+  std::vector<uint64_t> off((size_t)std::max(n, 1), 0);
+  uint64_t acc = 0;
+  for (int i = 0; i < n; ++i) {
+    off[i] = acc;
+    acc += sif::keep_count(c->s, (uint64_t)d[i].rows * d[i].cols);
+  }
+  uint8_t* w = (uint8_t*)ws;
+  if (n > 0 &&
+      check_cuda(cudaMemcpyAsync(w + p.ws_aux_off + up((uint64_t)c->m_plus + c->m_minus, 256), off.data(), 8ull * n,
+                                 cudaMemcpyHostToDevice, s)))
+    return SIF_ERR_CUDA;
+  return enc_launch(&p, c, ws, nullptr, status, 1, kept, tau3, s);
+}
+
+// ------------------------------------------------------------------ decode
+int sif_dec_plan(const sif_dec_desc* d, int n, sif_plan* p) {
+  if (!p || (n > 0 && !d) || n < 0) return SIF_ERR_INVALID_ARG;
+  memset(p, 0, sizeof(*p));
+  uint64_t ntiles = 0, maxrows = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!d[i].in || (reinterpret_cast<uintptr_t>(d[i].in) & 3)) return SIF_ERR_INVALID_ARG;
+    const uint64_t rows = d[i].rows, cols = d[i].cols;
+    uint64_t tiles = 1;
+    if (rows > 0 && cols > 0) {
+      const uint64_t kc = std::min<uint64_t>(cols, kDecTileElems);
+      const uint64_t r = std::max<uint64_t>(1, kDecTileElems / kc);
+      tiles = ((rows + r - 1) / r) * ((cols + kc - 1) / kc);
+    }
+    ntiles += tiles;
+    const uint64_t blk = d[i].in_len > 32 ? (d[i].in_len - 32) / 17 + 1 : 1;
+    maxrows = std::max(maxrows, blk);
+  }
+  if (ntiles >= (1ull << 31)) return SIF_ERR_INVALID_ARG;
+  p->n = n;
+  p->threads = sif::DNT;
+  p->tiles = (int32_t)ntiles;
+  p->max_blocks = (int32_t)std::min<uint64_t>(maxrows, 1u << 30);
+  p->smem_bytes = kDecTileElems * 8 + 2 * ((kDecTileElems + 31) / 32) * 4 + kDecRpcCap * 4;
+  uint64_t off = 0;
+  p->ws_desc_off = off;
+  off += up(sizeof(sif_dec_desc) * (uint64_t)std::max(n, 1), 256);
+  p->ws_aux_off = off;  // tables
+  off += up((2 + maxrows) * 64ull * std::max(n, 1), 256);
+  p->ws_spill_off = off;  // tiles, then accumulators
+  off += up(sizeof(sif::DecTile) * std::max<uint64_t>(ntiles, 1), 256);
+  off += up(16ull * std::max(n, 1), 256);
+  p->ws_bytes = off;
+  return SIF_OK;
+}
+
+uint64_t sif_dec_table_stride(const sif_plan* p) { return p ? (2ull + (uint64_t)p->max_blocks) * 64ull : 0; }
+
+int sif_dec_upload(const sif_plan* p, const sif_dec_desc* d, void* ws, void* stream) {
+  if (!p || !ws) return SIF_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t* w = (uint8_t*)ws;
+  if (p->n == 0) return SIF_OK;
+  if (check_cuda(cudaMemcpyAsync(w + p->ws_desc_off, d, sizeof(sif_dec_desc) * p->n, cudaMemcpyHostToDevice, s)))
+    return SIF_ERR_CUDA;
+  std::vector<sif::DecTile> tiles;
+  tiles.reserve((size_t)p->tiles);
+  for (int i = 0; i < p->n; ++i) {
+    const uint32_t rows = d[i].rows, cols = d[i].cols;
+    if (rows == 0 || cols == 0) {
+      tiles.push_back({(uint32_t)i, 0, 1, 0, 0, 0, 0, 0});
+      continue;
+    }
+    const uint32_t kc = std::min<uint32_t>(cols, kDecTileElems);
+    const uint32_t r = std::max<uint32_t>(1, kDecTileElems / kc);
+    const uint32_t nr = (rows + r - 1) / r, nc = (cols + kc - 1) / kc;
+    const uint32_t nt = nr * nc;
+    uint32_t ti = 0;
+    for (uint32_t a = 0; a < nr; ++a)
+      for (uint32_t b = 0; b < nc; ++b, ++ti)
+        tiles.push_back({(uint32_t)i, ti, nt, a * r, std::min(rows, (a + 1) * r), b * kc, std::min(cols, (b + 1) * kc), 0});
+  }
+  const uint64_t tab_bytes = up((2 + (uint64_t)p->max_blocks) * 64ull * p->n, 256);
+  uint8_t* tile_ptr = w + p->ws_spill_off;
+  uint8_t* acc_ptr = tile_ptr + up(sizeof(sif::DecTile) * std::max<uint64_t>(tiles.size(), 1), 256);
+  (void)tab_bytes;
+  if (check_cuda(cudaMemcpyAsync(tile_ptr, tiles.data(), sizeof(sif::DecTile) * tiles.size(), cudaMemcpyHostToDevice, s)))
+    return SIF_ERR_CUDA;
+  if (check_cuda(cudaMemsetAsync(acc_ptr, 0, 16ull * p->n, s))) return SIF_ERR_CUDA;
+  return SIF_OK;
+}
+
+int sif_dec_run(const sif_plan* p, int parse_only, void* ws, int32_t* status, void* stream) {
+  if (!p || !ws || !status) return SIF_ERR_INVALID_ARG;
+  if (p->n == 0) return SIF_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t* w = (uint8_t*)ws;
+  sif::DecArgs a;
+  memset(&a, 0, sizeof(a));
+  a.descs = reinterpret_cast<const sif_dec_desc*>(w + p->ws_desc_off);
+  a.n = p->n;
+  a.table = reinterpret_cast<uint32_t*>(w + p->ws_aux_off);
+  a.table_stride = (2ull + (uint64_t)p->max_blocks) * sif::TROW_U32;
+  a.tiles = reinterpret_cast<const sif::DecTile*>(w + p->ws_spill_off);
+  a.acc = reinterpret_cast<uint32_t*>(w + p->ws_spill_off + up(sizeof(sif::DecTile) * std::max<int>(p->tiles, 1), 256));
+  a.ntiles = p->tiles;
+  a.parse_only = parse_only;
+  a.tile_elems = kDecTileElems;
+  a.rpc_cap = kDecRpcCap;
+  a.status = status;
+  sif::sif_parse_kernel<<<(p->n + 127) / 128, 128, 0, s>>>(a);
+  if (check_cuda(cudaGetLastError())) return SIF_ERR_CUDA;
+  if (check_cuda(cudaFuncSetAttribute(sif::sif_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem_bytes)))
+    return SIF_ERR_CUDA;
+  sif::sif_scatter_kernel<<<p->tiles, sif::DNT, p->smem_bytes, s>>>(a);
+  return check_cuda(cudaGetLastError());
+}
+
+int sif_decode_batched(const sif_dec_desc* d, int n, int parse_only, void* ws, size_t ws_bytes, int32_t* status,
+                       void* stream) {
+  sif_plan p;
+  int st = sif_dec_plan(d, n, &p);
+  if (st) return st;
+  if (ws_bytes < p.ws_bytes) return SIF_ERR_CAPACITY;
+  st = sif_dec_upload(&p, d, ws, stream);
+  if (st) return st;
+  return sif_dec_run(&p, parse_only, ws, status, stream);
+}
+
+// ------------------------------------------------------------------ synthetic inputs
+int sif_gen_synthetic(void* x, uint32_t rows, uint32_t cols, uint32_t dtype, uint32_t kind, uint64_t sid, void* stream) {
+  if (!x || rows == 0 || cols == 0) return SIF_ERR_INVALID_ARG;
+  const uint64_t T = (uint64_t)rows * cols;
+  const unsigned grid = (unsigned)std::min<uint64_t>((T + 255) / 256, 148ull * 16);
+  sif::sif_synth_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(x, rows, cols, dtype, kind, sid);
+  return check_cuda(cudaGetLastError());
+}
+
+}  // extern "C"
