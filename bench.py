@@ -1,0 +1,342 @@
+"""Benchmark: SLICER IF codec encode+decode throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c3|c4]
+
+One step = encode of the whole per-GPU batch of synthetic IFs (ATKF -> MS -> ABQ -> CSR
+bit-pack -> .sif with CRC) followed by decode of those payloads back to dense fp32, inputs
+resident in HBM.  N>1: one process per GPU (torchrun), independent IF streams per rank
+(sid = rank * B + i), no data-path collectives ("scaling": "weak"); the timing is the max
+over ranks.  `--impl reference` times the CPU reference restatement (oracle/) on the
+host cores on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "IF encode+decode GB/s per GPU (and 8-GPU aggregate) vs HBM roofline; bits/element"
+
+CONFIGS = {
+    # BASELINE.json configs[1]: ResNet-50 IF batch 256 (headline, N=1 workload)
+    "c2": dict(kind=0, rows=1024, cols=196, batch=256, dtype="fp32",
+               workload="C2: ResNet-50 split-point IF 1x1024x14x14 fp32 (rows=1024 channels, cols=196), "
+                        "batch 256 clients per GPU, synthetic ReLU-sparse"),
+    # configs[2]: Llama decode-step hidden states, 1 token x 4096, 1024 clients
+    "c3": dict(kind=1, rows=1, cols=4096, batch=1024, dtype="bf16",
+               workload="C3: Llama-class decode-step hidden state 1x4096 bf16, 1024 concurrent clients"),
+    # configs[3]: Llama prefill IF 2048 x 4096 bf16, batch 32
+    "c4": dict(kind=1, rows=2048, cols=4096, batch=32, dtype="bf16",
+               workload="C4: Llama-class prefill IF 2048x4096 bf16, batch 32"),
+}
+CODEC = dict(s=0.9, lam=0.0, m_plus=3, m_minus=3, q_bit=8, delta=0.01)
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6552.0)), "measured"
+    return 6650.0, "fallback"
+
+
+def _ncu_traffic(config: str):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(config)
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = f"/tmp/sif_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except OSError:
+            return None
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 3 + i and "Active" in r[3 + i]
+                          and "Not" not in r[3 + i]})
+        return dict(sm_mhz=statistics.median(sm) if sm else None, sm_max_mhz=max(mx) if mx else None,
+                    reasons=reasons, samples=len(rows))
+
+
+# ------------------------------------------------------------------------- CPU arm
+def _cpu_worker(args):
+    kind, rows, cols, sid, cfgd = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import sif_oracle as O
+    from oracle.synth import synth
+
+    x = synth(kind, rows, cols, sid)
+    t0 = time.perf_counter()
+    blob = O.encode_bytes(x, O.Cfg(**cfgd), sid)
+    y = O.decode_bytes(blob)
+    dt = time.perf_counter() - t0
+    return dt, len(blob), int(y.size)
+
+
+def cpu_measure(conf, n_if: int, steps: int, warmup: int, cores: int):
+    """Times the oracle (CPU restatement of the reference) on host cores: each step
+    encodes+decodes a bounded sample of `n_if` IFs of the workload shape in a process pool."""
+    import multiprocessing as mp
+
+    b_in = 4 if conf["dtype"] == "fp32" else 2
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        jobs = [(conf["kind"], conf["rows"], conf["cols"], 100000 + i, CODEC) for i in range(n_if)]
+        for _ in range(warmup):
+            pool.map(_cpu_worker, jobs[: max(1, cores)])
+        t0 = time.perf_counter()
+        plen = 0
+        for _ in range(steps):
+            res = pool.map(_cpu_worker, jobs)
+            plen = sum(r[1] for r in res)
+        wall = time.perf_counter() - t0
+    raw = steps * n_if * conf["rows"] * conf["cols"] * b_in
+    return dict(value=raw / wall / 1e9, seconds=wall, payload_bytes=plen, raw_bytes=raw)
+
+
+def run_reference(args, conf, rank):
+    if rank != 0:
+        return
+    cores = len(os.sched_getaffinity(0))
+    per_if = {"c2": 0.15, "c3": 0.004, "c4": 8.0}[args.config]
+    n_if = max(cores, int(min(conf["batch"], max(cores, 2.0 * cores / per_if))))
+    n_if = min(n_if, conf["batch"])
+    r = cpu_measure(conf, n_if, args.steps, args.warmup, cores)
+    sample = f"{n_if} IFs of the workload shape per step (of {conf['batch']}), {cores} processes, oracle/ NumPy port"
+    line = dict(metric=METRIC, value=round(r["value"], 6), unit="GB/s", n_gpus=args.gpus, steps=args.steps,
+                warmup=args.warmup, ms_per_step=r["seconds"] * 1e3 / max(1, args.steps), higher_is_better=True,
+                scaling="weak", vs_baseline=None, dtype=conf["dtype"], data="synthetic",
+                config=dict(workload=conf["workload"], codec=CODEC, sample=sample),
+                impl="reference",
+                cpu_baseline=dict(value=round(r["value"], 6), unit="GB/s", cores=cores, kind="port", sample=sample),
+                e2e=dict(value=round(r["value"], 6), unit="GB/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0),
+                bits_per_element=8.0 * r["payload_bytes"] / (n_if * conf["rows"] * conf["cols"]))
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------- GPU arm
+def run_ours(args, conf, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import paper_2511_11608_b200 as sif
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    B, N, K = conf["batch"], conf["rows"], conf["cols"]
+    tdt = torch.float32 if conf["dtype"] == "fp32" else torch.bfloat16
+    b_in = 4 if conf["dtype"] == "fp32" else 2
+    xs = torch.empty((B, N, K), dtype=tdt, device=dev)
+    for i in range(B):
+        sif.synthetic(conf["kind"], N, K, rank * B + i, out=xs[i])
+    cfg = sif.CodecConfig(**CODEC)
+    enc = sif.BatchEncoder(xs, cfg, [rank * B + i for i in range(B)])
+    enc.run().check()
+    lens = enc.out_len.cpu().numpy()
+    cap = enc.cap
+    ys = torch.empty((B, N, K), dtype=torch.float32, device=dev)
+    dec = sif.BatchDecoder([enc.out.data_ptr() + i * cap for i in range(B)], lens, N, K, out=ys)
+    dec.run().check()
+    torch.cuda.synchronize()
+    payload_total = int(lens.sum())
+    raw_bytes = B * N * K * b_in
+    alg_enc = raw_bytes + payload_total
+    alg_dec = payload_total + B * N * K * 4
+    stream = torch.cuda.current_stream()
+
+    def step():
+        enc.run()
+        dec.run()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            enc.run()
+            ev[i][1].record(stream)
+            dec.run()
+            ev[i][2].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    enc_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps
+    dec_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps
+    st_ms = total_ms / args.steps
+    # status after timing (must all be OK)
+    enc.check()
+    dec.check()
+    if pg:
+        t = torch.tensor([st_ms, enc_ms, dec_ms], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        st_ms, enc_ms, dec_ms = [float(v) for v in t.cpu().numpy()]
+
+    # ---- e2e through the public API with host buffers (pinned), copies inside the timing
+    x_host = xs.cpu().pin_memory()
+    pay_host = torch.empty((B, cap), dtype=torch.uint8).pin_memory()
+    y_host = torch.empty((B, N, K), dtype=torch.float32).pin_memory()
+    rx = torch.empty((B, cap), dtype=torch.uint8, device=dev)
+    dec_rx = sif.BatchDecoder([rx.data_ptr() + i * cap for i in range(B)], lens, N, K, out=ys)
+
+    def e2e_step():
+        xs.copy_(x_host, non_blocking=True)
+        enc.run()
+        pay_host.copy_(enc.out, non_blocking=True)
+        rx.copy_(pay_host, non_blocking=True)
+        dec_rx.run()
+        y_host.copy_(ys, non_blocking=True)
+
+    e2e_steps = max(2, min(args.steps, 10))
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    dec_rx.check()
+    assert torch.equal(y_host, ys.cpu()), "e2e decode differs"
+    if pg:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    cpu = None
+    if rank == 0 and args.cpu_baseline:
+        cores = len(os.sched_getaffinity(0))
+        per_if = {"c2": 0.15, "c3": 0.004, "c4": 8.0}[args.config]
+        n_if = min(conf["batch"], max(cores, int(2.0 * cores / per_if)))
+        r = cpu_measure(conf, n_if, 2, 1, cores)
+        cpu = dict(value=round(r["value"], 6), unit="GB/s", cores=cores, kind="port",
+                   sample=f"{n_if} IFs of the workload shape x 2 steps, {cores} processes, oracle/ NumPy port "
+                          f"({r['seconds']:.1f} s)")
+
+    if rank == 0:
+        hbm, peak_kind = _peaks()
+        value = world * raw_bytes / (st_ms * 1e-3) / 1e9
+        enc_gbs = alg_enc / (enc_ms * 1e-3) / 1e9
+        dec_gbs = alg_dec / (dec_ms * 1e-3) / 1e9
+        step_gbs = (alg_enc + alg_dec) / (st_ms * 1e-3) / 1e9
+        dominant = "sif_encode_kernel" if enc_ms >= dec_ms else "sif_scatter_kernel"
+        dom_ach = enc_gbs if enc_ms >= dec_ms else dec_gbs
+        traffic = _ncu_traffic(args.config)
+        line = dict(
+            metric=METRIC, value=round(value, 3), unit="GB/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
+            ms_per_step=round(st_ms, 5), higher_is_better=True, scaling="weak", vs_baseline=None,
+            dtype=conf["dtype"], data="synthetic (integer-exact device generator, SURVEY.md §8(d))",
+            config=dict(workload=conf["workload"], codec=CODEC, if_shape=[N, K], batch_per_gpu=B,
+                        parallelism=f"dp{world} (independent IF streams per GPU, no collectives)",
+                        l2="per-step inputs %.0f MB/GPU exceed the 126 MB L2; no flush" % (raw_bytes / 1e6)),
+            roofline=dict(bound="hbm", kernel=dominant, achieved=round(dom_ach, 2), peak=hbm, unit="GB/s",
+                          frac=round(dom_ach / hbm, 4), traffic=(traffic or {}).get(dominant),
+                          peak_source=peak_kind,
+                          algorithmic_bytes_per_launch=alg_enc if dominant == "sif_encode_kernel" else alg_dec),
+            roofline_step=dict(achieved=round(step_gbs, 2), frac=round(step_gbs / hbm, 4),
+                               algorithmic_bytes_per_step=alg_enc + alg_dec,
+                               encode_ms=round(enc_ms, 5), decode_ms=round(dec_ms, 5),
+                               encode_gbs=round(enc_gbs, 2), decode_gbs=round(dec_gbs, 2)),
+            bits_per_element=round(8.0 * payload_total / (B * N * K), 6),
+            raw_gbs_per_gpu=round(raw_bytes / (st_ms * 1e-3) / 1e9, 3),
+            e2e=dict(value=round(world * raw_bytes / (e2e_ms * 1e-3) / 1e9, 3), unit="GB/s",
+                     h2d_bytes_per_step=int(x_host.numel() * x_host.element_size() + pay_host.numel()),
+                     d2h_bytes_per_step=int(pay_host.numel() + y_host.numel() * 4),
+                     ms_per_step=round(e2e_ms, 4)),
+            gpu_launches=3 * args.steps,
+            clocks=clk.summary(),
+            cpu_baseline=cpu,
+        )
+        print(json.dumps(line), flush=True)
+    if pg:
+        pg.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    conf = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, conf, rank)
+        return
+    run_ours(args, conf, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -63,14 +63,11 @@ __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 
 // combine as raw(A||B) = raw(A)*x^(8|B|) ^ raw(B) and
 // zlib.crc32(m) = raw(m) ^ (0xFFFFFFFF * x^(8|m|)) ^ 0xFFFFFFFF.
 __device__ __forceinline__ uint32_t crc_mult(uint32_t a, uint32_t b) {
-  uint32_t m = 1u << 31, p = 0;
-  for (;;) {
-    if (a & m) {
-      p ^= b;
-      if ((a & (m - 1u)) == 0) break;
-    }
-    m >>= 1;
-    b = (b & 1u) ? (b >> 1) ^ kCrcPoly : b >> 1;
+  uint32_t p = 0;
+#pragma unroll 4
+  for (int i = 31; i >= 0; --i) {
+    if ((a >> i) & 1u) p ^= b;
+    b = (b >> 1) ^ ((b & 1u) ? kCrcPoly : 0u);
   }
   return p;
 }
@@ -90,31 +87,155 @@ __device__ __forceinline__ uint32_t crc_shift(uint32_t c, uint64_t nbytes) {
 __device__ __forceinline__ uint32_t crc_finish(uint32_t raw_total, uint64_t len) {
   return raw_total ^ crc_mult(crc_x8n(len), 0xFFFFFFFFu) ^ 0xFFFFFFFFu;
 }
-// Raw CRC of bytes [b0, b1) of a 4-byte aligned buffer, read through L2 (ld.global.cg).
+// Raw CRC of bytes [b0, b1) of a 4-byte aligned buffer (read through L2), slice-by-4.
+// t4 = 4 x 256 table in shared memory (kCrcTab4).
 __device__ __forceinline__ uint32_t crc_raw_range(const uint8_t* base, uint64_t b0, uint64_t b1,
-                                                  const uint32_t* tab) {
+                                                  const uint32_t* t4) {
   uint32_t c = 0;
   if (b0 >= b1) return 0;
   const uint32_t* w = reinterpret_cast<const uint32_t*>(base);
   uint64_t i = b0;
-  uint32_t word = __ldcg(w + (i >> 2));
-  while (i < b1) {
-    if ((i & 3u) == 0u && i + 4 <= b1) {
-      word = __ldcg(w + (i >> 2));
-      c = tab[(c ^ word) & 0xFFu] ^ (c >> 8);
-      c = tab[(c ^ (word >> 8)) & 0xFFu] ^ (c >> 8);
-      c = tab[(c ^ (word >> 16)) & 0xFFu] ^ (c >> 8);
-      c = tab[(c ^ (word >> 24)) & 0xFFu] ^ (c >> 8);
-      i += 4;
-      continue;
-    }
-    if ((i & 3u) == 0u || i == b0) word = __ldcg(w + (i >> 2));
-    uint32_t byte = (word >> (8u * (uint32_t)(i & 3u))) & 0xFFu;
-    c = tab[(c ^ byte) & 0xFFu] ^ (c >> 8);
+  while (i < b1 && (i & 3u)) {
+    const uint32_t byte = (__ldcg(w + (i >> 2)) >> (8u * (uint32_t)(i & 3u))) & 0xFFu;
+    c = t4[(c ^ byte) & 0xFFu] ^ (c >> 8);
     ++i;
+  }
+  while (i + 4 <= b1) {
+    const uint32_t x = __ldcg(w + (i >> 2)) ^ c;
+    c = t4[768 + (x & 0xFFu)] ^ t4[512 + ((x >> 8) & 0xFFu)] ^ t4[256 + ((x >> 16) & 0xFFu)] ^ t4[x >> 24];
+    i += 4;
+  }
+  if (i < b1) {
+    const uint32_t word = __ldcg(w + (i >> 2));
+    while (i < b1) {
+      const uint32_t byte = (word >> (8u * (uint32_t)(i & 3u))) & 0xFFu;
+      c = t4[(c ^ byte) & 0xFFu] ^ (c >> 8);
+      ++i;
+    }
   }
   return c;
 }
+// Raw CRC of [b0, b1) computed by all NT threads of a CTA.  256-byte chunks are aligned to
+// b1 so each combine level uses a constant multiplier x^(8*256*2^k) = kX2n[11+k] (leading
+// zero bytes do not change a raw CRC, so the partial first chunk needs no special case).
+// Result returned in every thread.  red: >= NT/32 + 1 u32 of shared memory.
+template <int NT>
+__device__ uint32_t crc_cta_raw(const uint8_t* base, uint64_t b0, uint64_t b1, const uint32_t* t4, uint32_t* red) {
+  constexpr int NW = NT / 32;
+  constexpr int LOGNW = NW >= 16 ? 4 : NW >= 8 ? 3 : NW >= 4 ? 2 : NW >= 2 ? 1 : 0;
+  constexpr uint64_t L = 256;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t n = b1 > b0 ? b1 - b0 : 0;
+  const uint64_t span = L * NT;
+  const int64_t rounds = (int64_t)((n + span - 1) / span);
+  uint32_t total = 0;
+  for (int64_t q = rounds - 1; q >= 0; --q) {
+    const int64_t rs = (int64_t)b1 - (int64_t)span * (q + 1);
+    int64_t c0 = rs + (int64_t)L * tid, c1 = c0 + (int64_t)L;
+    if (c0 < (int64_t)b0) c0 = (int64_t)b0;
+    uint32_t c = c1 > c0 ? crc_raw_range(base, (uint64_t)c0, (uint64_t)c1, t4) : 0u;
+#pragma unroll 1
+    for (int k = 0; k < 5; ++k) {
+      const uint32_t v2 = __shfl_down_sync(0xFFFFFFFFu, c, 1 << k);
+      if ((lane & ((2 << k) - 1)) == 0) c = crc_mult(c, kX2n[11 + k]) ^ v2;
+    }
+    if (lane == 0) red[wid] = c;
+    __syncthreads();
+    if (wid == 0) {
+      c = lane < NW ? red[lane] : 0u;
+#pragma unroll 1
+      for (int k = 0; k < LOGNW; ++k) {
+        const uint32_t v2 = __shfl_down_sync(0xFFFFFFFFu, c, 1 << k);
+        if ((lane & ((2 << k) - 1)) == 0) c = crc_mult(c, kX2n[16 + k]) ^ v2;
+      }
+      if (lane == 0) total = crc_mult(total, kX2n[11 + 5 + LOGNW]) ^ c;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) red[NW] = total;
+  __syncthreads();
+  const uint32_t r = red[NW];
+  __syncthreads();
+  return r;
+}
+
+// Same as crc_cta_raw but each round of 64*NT bytes is first staged into shared memory
+// with coalesced loads (one memory round trip per round); chunks are 64 bytes, so the
+// combine multipliers are x^(8*64*2^k) = kX2n[9+k].  stage: >= 16*NT u32.
+template <int NT>
+__device__ uint32_t crc_cta_staged(const uint8_t* base, uint64_t b0, uint64_t b1, const uint32_t* t4, uint32_t* red,
+                                   uint32_t* stage) {
+  constexpr int NW = NT / 32;
+  constexpr int LOGNW = NW >= 16 ? 4 : NW >= 8 ? 3 : NW >= 4 ? 2 : NW >= 2 ? 1 : 0;
+  constexpr int64_t L = 64, SPAN = L * NT, WORDS = SPAN / 4;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t n = b1 > b0 ? b1 - b0 : 0;
+  const int64_t rounds = (int64_t)((n + SPAN - 1) / SPAN);
+  const uint32_t* gw = reinterpret_cast<const uint32_t*>(base);
+  uint32_t total = 0;
+  for (int64_t q = rounds - 1; q >= 0; --q) {
+    const int64_t rs = (int64_t)b1 - SPAN * (q + 1);  // byte address of stage[0]
+    const int64_t fl = rs >= 0 ? rs / 4 : -((-rs + 3) / 4);
+    const uint32_t sh8 = (uint32_t)(rs - 4 * fl) * 8u;
+    for (int64_t j = tid; j < WORDS; j += NT) {
+      // bytes [rs + 4j, rs + 4j + 4): funnel of two aligned words; bytes before b0 are zero
+      const int64_t a = rs + 4 * j;
+      uint32_t v = 0;
+      if (a + 4 > (int64_t)b0) {
+        const int64_t w0 = fl + j;
+        const uint32_t lo = (w0 >= 0 && 4 * w0 + 4 > (int64_t)b0) ? __ldcg(gw + w0) : 0u;
+        const uint32_t hi = (sh8 && 4 * (w0 + 1) < (int64_t)b1) ? __ldcg(gw + w0 + 1) : 0u;
+        v = sh8 ? __funnelshift_r(lo, hi, sh8) : lo;
+        if (a < (int64_t)b0) v &= 0xFFFFFFFFu << (8u * (uint32_t)((int64_t)b0 - a));
+      }
+      stage[j] = v;
+    }
+    __syncthreads();
+    uint32_t c = 0;
+    const uint32_t* w = stage + tid * (L / 4);
+#pragma unroll 4
+    for (int k = 0; k < L / 4; ++k) {
+      const uint32_t x = w[k] ^ c;
+      c = t4[768 + (x & 0xFFu)] ^ t4[512 + ((x >> 8) & 0xFFu)] ^ t4[256 + ((x >> 16) & 0xFFu)] ^ t4[x >> 24];
+    }
+#pragma unroll 1
+    for (int k = 0; k < 5; ++k) {
+      const uint32_t v2 = __shfl_down_sync(0xFFFFFFFFu, c, 1 << k);
+      if ((lane & ((2 << k) - 1)) == 0) c = crc_mult(c, kX2n[9 + k]) ^ v2;
+    }
+    if (lane == 0) red[wid] = c;
+    __syncthreads();
+    if (wid == 0) {
+      c = lane < NW ? red[lane] : 0u;
+#pragma unroll 1
+      for (int k = 0; k < LOGNW; ++k) {
+        const uint32_t v2 = __shfl_down_sync(0xFFFFFFFFu, c, 1 << k);
+        if ((lane & ((2 << k) - 1)) == 0) c = crc_mult(c, kX2n[14 + k]) ^ v2;
+      }
+      if (lane == 0) total = crc_mult(total, kX2n[9 + 5 + LOGNW]) ^ c;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) red[NW] = total;
+  __syncthreads();
+  const uint32_t r = red[NW];
+  __syncthreads();
+  return r;
+}
+
+// Fast exact u32 division / modulo by an invariant divisor (Lemire fastmod, 64-bit M).
+struct FastDiv {
+  uint64_t M;
+  uint32_t d;
+  __host__ __device__ void init(uint32_t dd) {
+    d = dd;
+    M = dd ? (~0ull / dd + 1ull) : 0ull;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t x) const { return d == 1 ? x : (uint32_t)__umul64hi(M, (uint64_t)x); }
+  __device__ __forceinline__ uint32_t mod(uint32_t x) const {
+    return d == 1 ? 0u : (uint32_t)__umul64hi(M * (uint64_t)x, (uint64_t)d);
+  }
+};
 
 // ---------------------------------------------------------------- byte stream helpers
 // Unaligned little-endian u32 read from a 4-byte aligned buffer.

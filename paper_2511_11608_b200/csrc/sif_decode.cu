@@ -37,6 +37,7 @@ struct DecArgs {
   int tile_elems;
   int rpc_cap;
   int32_t* status;
+  const uint32_t* tiles_per_if;
 };
 
 // ------------------------------------------------------------------------------- parse
@@ -106,44 +107,44 @@ __global__ void sif_parse_kernel(DecArgs a) {
 __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ uint32_t hdr[2 * TROW_U32];
-  __shared__ uint32_t crctab[256];
-  __shared__ uint32_t red[DNT / 32];
+  __shared__ uint32_t red[DNT / 32 + 2];
   __shared__ uint32_t sflags;
   __shared__ int s_last;
-  const DecTile t = a.tiles[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31;
+  // CTAs past the tile list compute one stream's CRC-32 each (codec.py:325-327)
+  const bool crc_cta = (int)blockIdx.x >= a.ntiles;
+  DecTile t;
+  if (crc_cta) {
+    t.ifi = blockIdx.x - a.ntiles;
+    t.ti = 0; t.nt = 0; t.r0 = t.r1 = t.c0 = t.c1 = 0;
+  } else {
+    t = a.tiles[blockIdx.x];
+  }
   const sif_dec_desc d = a.descs[t.ifi];
   const uint32_t* tab = a.table + (uint64_t)t.ifi * a.table_stride;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid < 2 * TROW_U32) hdr[tid] = tab[tid];
-  for (int k = tid; k < 256; k += DNT) crctab[k] = kCrcTab[k];
   if (tid == 0) sflags = 0;
   __syncthreads();
   const uint32_t walk = hdr[0], N = hdr[1], K = hdr[2], mp = hdr[3], nb = hdr[7];
   const uint32_t pre = hdr[TROW_U32 + 0];
   const uint64_t len = d.in_len;
   const uint8_t* in = d.in;
+  // number of CTAs that report to this stream's accumulator: its tiles + the CRC CTA
+  uint32_t ntiles_if = t.nt;
 
-  // ---- CRC-32 of this tile's chunk of bytes [4, len-4)
-  if (!pre) {
-    const uint64_t Lc = len - 8;
-    const uint64_t c0 = 4 + Lc * t.ti / t.nt, c1 = 4 + Lc * (t.ti + 1) / t.nt;
-    const uint64_t n = c1 - c0;
-    const uint64_t b0 = c0 + n * tid / DNT, b1 = c0 + n * (tid + 1) / DNT;
-    uint32_t raw = crc_raw_range(in, b0, b1, crctab);
-    raw = crc_shift(raw, (len - 4) - b1);
-    raw = warp_xor(raw);
-    if (lane == 0) red[wid] = raw;
+  if (crc_cta) {
+    uint32_t* t4 = reinterpret_cast<uint32_t*>(dsm);
+    for (int k = tid; k < 1024; k += DNT) t4[k] = (&kCrcTab4[0][0])[k];
     __syncthreads();
-    if (tid == 0) {
-      uint32_t v = 0;
-      for (int w = 0; w < DNT / 32; ++w) v ^= red[w];
-      if (v) atomicXor(a.acc + 4ull * t.ifi + 0, v);
+    if (!pre) {
+      const uint32_t raw = crc_cta_staged<DNT>(in, 4, len - 4, t4, red, t4 + 1024);
+      if (tid == 0) a.acc[4ull * t.ifi + 0] = raw;
     }
+    ntiles_if = a.tiles_per_if[t.ifi];
   }
-
   // ---- validate + dequantize + scatter this row slab
   const bool shape_ok = a.parse_only || (N == d.rows && K == d.cols);
-  if (!a.parse_only && !pre && !walk && shape_ok) {
+  if (!crc_cta && !a.parse_only && !pre && !walk && shape_ok) {
     const uint32_t R = t.r1 - t.r0, Kc = t.c1 - t.c0;
     const uint32_t E = R * Kc;
     double* tile = reinterpret_cast<double*>(dsm);
@@ -221,12 +222,12 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
   // ---- last CTA of this stream folds everything into the reference error precedence
   __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = atomicAdd(a.acc + 4ull * t.ifi + 2, 1u) == t.nt - 1;
+  if (tid == 0) s_last = atomicAdd(a.acc + 4ull * t.ifi + 2, 1u) == ntiles_if;  // tiles + CRC CTA
   __syncthreads();
   if (s_last && tid == 0) {
     __threadfence();
     uint32_t* acc = a.acc + 4ull * t.ifi;
-    const uint32_t crc_raw = atomicAdd(acc + 0, 0u);
+    const uint32_t crc_raw = *((volatile uint32_t*)(acc + 0));
     const uint32_t flags = atomicAdd(acc + 1, 0u);
     int st = SIF_OK;
     if (pre) st = (int)pre;

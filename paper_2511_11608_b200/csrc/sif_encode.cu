@@ -1,22 +1,22 @@
 // sif_encode.cu -- fused B200 (sm_100a) encoder for the SLICER IF codec.
 //
-// One thread-block cluster ("group", G CTAs, G = 1..8) encodes one IF end to end:
+// One thread-block cluster ("group", G CTAs, G = 1..8) encodes one IF end to end; every
+// CTA owns a contiguous flat slice of the IF.  Phases (reference semantics cited):
 //
-//   stream x once from HBM (128-bit loads)            atkf.py:49-55 (finite check, |x|)
-//     -> bracketed candidate compaction in SMEM        (sample -> [lo,hi) bracket on |x|)
-//   radix select of tau (3 x 11-bit SMEM histograms)  atkf.py:71  np.partition
-//   lambda>0: strict class + second select             atkf.py:72-84
-//   tie break: 64-bit radix select on splitmix keys    atkf.py:37-41, rng.py:60-68
-//   kept set (stable, flat order)                      atkf.py:86-88
-//   MS cut elements by rank (value desc, idx asc)      msplit.py:54-80 (no sort)
-//   per-block members in CSR order (flat order)        msplit.py:83-101
-//   ABQ descent with warp-reduced DS sums (float64)    quant.py:44-64, :88-115
-//   .sif layout, header/meta, row_ptr, MSB-first       codec.py:283-317
-//     bit packing with warp shuffles, CRC-32 combine   zlib.crc32 (codec.py:316)
+//   S  sample 4096 elements -> bracket [lo, hi) around the k-th |x|     (speculation only)
+//   A  stream the slice once from HBM (128-bit loads, software-pipelined):
+//      NaN/Inf check (atkf.py:49-51), counts, stable compaction of candidates |x| >= lo
+//   B  exact select of tau and of the tie cut: histogram -> gather the target bin ->
+//      rank by (|x| desc, splitmix64 asc) (atkf.py:37-41, :71-84, rng.py:60-68)
+//   C  kept set, stable in flat order (atkf.py:83-88)
+//   D  MS cut elements at ranks j*base by (value desc, flat idx asc) (msplit.py:54-80)
+//   E  block members in CSR order (warp-segmented stable walk)           (msplit.py:83-101)
+//   F  v_min / v_max per block, G  ABQ descent (quant.py:44-64, :88-115)
+//   H  .sif layout, header/meta, row_ptr, MSB-first word packing, CRC-32 (codec.py:283-317)
 //
-// The result is byte-identical to serialize(encode(x, cfg, seed)) of the reference.
-// Lists (candidates / kept elements / block members) live in shared memory up to
-// `cap` entries per CTA and spill to a per-CTA global region beyond that.
+// The output is byte-identical to serialize(encode(x, cfg, seed)) of the reference.
+// Lists live in shared memory up to `cap` entries per CTA and spill to a per-CTA global
+// region beyond that.
 
 #include <math.h>
 #include <stdint.h>
@@ -25,10 +25,8 @@
 
 namespace sif {
 
-constexpr int NT = 512;
-constexpr int NW = NT / 32;
-constexpr int MAXT = 4;        // select targets handled per batch
-constexpr int HB = 2048;       // histogram bins (11-bit digits)
+constexpr int HB = 2048;           // histogram bins (11-bit digits)
+constexpr int GCAP = 1024;         // gather capacity (group total) for exact ranking
 constexpr uint32_t kInfKey = 0xFFFFFFFFu;
 
 struct EncArgs {
@@ -42,12 +40,22 @@ struct EncArgs {
   uint64_t spill_stride;   // bytes per CTA
   int cap;                 // list entries per CTA held in SMEM
   int maxb;                // max blocks (m_plus + m_minus)
+  int scratch_words;       // selection scratch (histograms + gather buffers), u32 words
   uint64_t* out_len;
   int32_t* status;
   int64_t* kept_out;       // atkf mode
   const uint64_t* kept_off;
   double* tau3;
+  uint64_t* prof;          // optional per-IF phase timestamps (globaltimer ns), 32 per IF
 };
+
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SIF_PHASE(k) \
+  do { if (a.prof && g.rank == 0 && threadIdx.x == 0) a.prof[(uint64_t)ifi * 32 + (k)] = gtimer(); } while (0)
 
 // ---------------------------------------------------------------------------------------
 // Two-tier list of (float bits, flat index) pairs.
@@ -63,8 +71,10 @@ struct List {
     if (i < cap) { sb[i] = b; si[i] = x; }
     else { __stcg(gb + (i - cap), b); __stcg(gi + (i - cap), x); }
   }
+  __device__ __forceinline__ void set_bits(uint32_t i, uint32_t b) const {
+    if (i < cap) sb[i] = b; else __stcg(gb + (i - cap), b);
+  }
 };
-// Member permutation (indices into the kept list), two-tier.
 struct Perm {
   uint32_t* s;
   uint32_t* g;
@@ -75,8 +85,28 @@ struct Perm {
   }
 };
 
+// Visit every list element (order-free).  Shared-memory-resident lists are read with
+// 128-bit loads (4 elements per thread per step) and no per-element spill branch.
+template <int NT, class F>
+__device__ __forceinline__ void list_foreach(const List& L, uint32_t n, F f) {
+  if (n <= L.cap) {
+    const uint32_t n4 = n & ~3u;
+    for (uint32_t i = threadIdx.x * 4; i < n4; i += NT * 4) {
+      const uint4 b4 = *reinterpret_cast<const uint4*>(L.sb + i);
+      const uint4 x4 = *reinterpret_cast<const uint4*>(L.si + i);
+      f(b4.x, x4.x);
+      f(b4.y, x4.y);
+      f(b4.z, x4.z);
+      f(b4.w, x4.w);
+    }
+    for (uint32_t i = n4 + threadIdx.x; i < n; i += NT) f(L.sb[i], L.si[i]);
+  } else {
+    for (uint32_t i = threadIdx.x; i < n; i += NT) f(L.bits(i), L.idx(i));
+  }
+}
+
 // ---------------------------------------------------------------------------------------
-// Group (cluster) helper: all-reduce of small u64 vectors and histogram sums via DSMEM.
+// Group (cluster) helper: small-vector all-reduce and DSMEM access.
 struct Grp {
   uint32_t rank, size;
   uint64_t* slots;   // [2][64] u64 in smem
@@ -87,8 +117,8 @@ struct Grp {
     else __syncthreads();
   }
   __device__ __forceinline__ uint64_t* slot() { return slots + parity * 64; }
-  // Sum `V` (<= 64) values the caller wrote to slot()[0..V) over the group into out[0..V)
-  // (smem); optionally the exclusive prefix over lower ranks into pre[0..V).
+  // Sum V (<= 64) values the caller wrote to slot()[0..V) over the group into out[0..V);
+  // optionally the exclusive prefix over lower ranks into pre[0..V).
   __device__ void allsum(int V, uint64_t* out, uint64_t* pre) {
     uint64_t* my = slot();
     sync();
@@ -102,7 +132,7 @@ struct Grp {
       for (int v = threadIdx.x; v < V; v += blockDim.x) {
         uint64_t s = 0, p = 0;
         for (uint32_t r = 0; r < size; ++r) {
-          uint64_t x = *cl.map_shared_rank(my + v, r);
+          const uint64_t x = *cl.map_shared_rank(my + v, r);
           if (r < rank) p += x;
           s += x;
         }
@@ -115,143 +145,325 @@ struct Grp {
   }
 };
 
-// ---------------------------------------------------------------------------------------
-struct Sel {
-  uint64_t prefix, mask;
-  uint64_t r;      // remaining rank (1-based, from the top)
-  uint64_t n_gt;   // elements strictly above the final key
-  uint64_t n_eq;   // elements equal to the final key
-  uint32_t ok;
+struct GatE {
+  uint32_t key;
+  uint32_t idx;
+  uint64_t sec;
 };
 
 struct Shared {
   uint64_t scan[40];
   uint64_t vec[64];
   uint64_t pre[64];
-  uint32_t fd_digit[MAXT];
-  uint64_t fd_above[MAXT], fd_eq[MAXT];
-  uint32_t fd_found[MAXT];
-  // per-IF decisions
-  uint32_t lo, hi, lo_neg, tau_key;
-  uint32_t key_star, cls_star, tie_all, tie_skip;
-  uint64_t hkey;
-  uint64_t n_cand, n_kept;
-  uint64_t m_eff[2], base[2], nnz[2];
-  uint32_t cidx_found[MAXT];
-  uint64_t run[MAXT];
+  uint32_t red[40];
+  uint32_t fd_digit;
+  uint64_t fd_above, fd_eq;
+  uint32_t fd_found;
+  uint32_t gcount;
+  uint32_t sel_key;
+  uint64_t sel_sec;
+  uint32_t sel_found;
+  uint64_t n_cand;
   uint64_t total_len;
-  uint32_t done;
+  uint32_t cidx_found;
 };
 
-// Find the digit d of a (group-summed) histogram such that above(d) < r <= above(d)+h[d],
-// scanning from the top.  Histograms of the whole group are summed through DSMEM.
-__device__ void find_digit(Grp& g, Shared& sh, const uint32_t* H, int nb, int t, uint64_t r) {
-  const int per = (nb + NT - 1) / NT;  // 4 / 2 / 1
-  uint64_t hv[4];
-  uint64_t s = 0;
+// Find digit d of a (group-summed) histogram with above(d) < r <= above(d) + h[d], from
+// the top.  Histograms of the whole group are summed through DSMEM.
+template <int NT>
+__device__ void find_digit(Grp& g, Shared& sh, const uint32_t* H, int nb, uint64_t r) {
+  const int per = (nb + NT - 1) / NT;
   cg::cluster_group cl = cg::this_cluster();
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    hv[k] = 0;
-    if (k < per) {
-      int b = nb - 1 - (threadIdx.x * per + k);
-      if (b >= 0) {
-        if (g.size == 1) hv[k] = H[b];
-        else
-          for (uint32_t rr = 0; rr < g.size; ++rr) hv[k] += *cl.map_shared_rank(H + b, rr);
-      }
-      s += hv[k];
-    }
+  auto bin = [&](int b) -> uint64_t {
+    if (g.size == 1) return H[b];
+    uint64_t v = 0;
+    for (uint32_t rr = 0; rr < g.size; ++rr) v += *cl.map_shared_rank(H + b, rr);
+    return v;
+  };
+  uint64_t s = 0;
+  for (int k = 0; k < per; ++k) {
+    const int b = nb - 1 - (threadIdx.x * per + k);
+    if (b >= 0) s += bin(b);
   }
   uint64_t tot;
-  uint64_t ex = block_excl_scan_u64(s, sh.scan, &tot);
-  if (threadIdx.x == 0) sh.fd_found[t] = 0;
+  const uint64_t ex = block_excl_scan_u64(s, sh.scan, &tot);
+  if (threadIdx.x == 0) sh.fd_found = 0;
   __syncthreads();
-  uint64_t cum = ex;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    if (k < per) {
-      int b = nb - 1 - (threadIdx.x * per + k);
-      if (b >= 0 && cum < r && r <= cum + hv[k]) {
-        sh.fd_digit[t] = (uint32_t)b;
-        sh.fd_above[t] = cum;
-        sh.fd_eq[t] = hv[k];
-        sh.fd_found[t] = 1;
+  if (ex < r && r <= ex + s) {
+    uint64_t cum = ex;
+    for (int k = 0; k < per; ++k) {
+      const int b = nb - 1 - (threadIdx.x * per + k);
+      if (b < 0) break;
+      const uint64_t h = bin(b);
+      if (cum < r && r <= cum + h) {
+        sh.fd_digit = (uint32_t)b;
+        sh.fd_above = cum;
+        sh.fd_eq = h;
+        sh.fd_found = 1;
+        break;
       }
-      cum += hv[k];
+      cum += h;
     }
   }
   __syncthreads();
 }
 
-// Generic batched radix select ("r-th largest key") over a list of n elements.
-// KeyFn(t, bits, idx, &key) -> bool : element participates in target t with key.
-template <typename KeyT, class KeyFn>
-__device__ void select_batch(Grp& g, Shared& sh, uint32_t* hist, const List& L, uint32_t n, int nt,
-                             Sel* st, KeyFn fn) {
-  constexpr int NL = sizeof(KeyT) == 8 ? 6 : 3;
-  const int shifts32[3] = {21, 10, 0};
-  const int widths32[3] = {11, 11, 10};
-  const int shifts64[6] = {53, 42, 31, 20, 9, 0};
-  const int widths64[6] = {11, 11, 11, 11, 11, 9};
-  for (int lev = 0; lev < NL; ++lev) {
-    const int shf = sizeof(KeyT) == 8 ? shifts64[lev] : shifts32[lev];
-    const int wid = sizeof(KeyT) == 8 ? widths64[lev] : widths32[lev];
-    const int nb = 1 << wid;
-    uint32_t* H = hist + (g.size > 1 ? g.hpar * MAXT * HB : 0);
+// Multi-level radix select on 64-bit keys ("r-th largest") over list elements accepted by
+// fn(bits, idx, &key).  Fallback for huge single-value tie sets.
+template <int NT, class KeyFn>
+__device__ uint64_t radix_select64(Grp& g, Shared& sh, uint32_t* hist, const List& L, uint32_t n, uint64_t r,
+                                   KeyFn fn) {
+  const int shifts[6] = {53, 42, 31, 20, 9, 0};
+  const int widths[6] = {11, 11, 11, 11, 11, 9};
+  uint64_t prefix = 0, mask = 0;
+  for (int lev = 0; lev < 6; ++lev) {
+    const int shf = shifts[lev], nb = 1 << widths[lev];
+    uint32_t* H = hist + (g.size > 1 ? g.hpar * HB : 0);
     g.hpar ^= 1;
-    for (int i = threadIdx.x; i < nt * HB; i += NT) H[i] = 0;
+    for (int i = threadIdx.x; i < nb; i += NT) H[i] = 0;
     __syncthreads();
-    uint64_t pf[MAXT], mk[MAXT];
-#pragma unroll
-    for (int t = 0; t < MAXT; ++t) {
-      pf[t] = t < nt ? st[t].prefix : 0;
-      mk[t] = t < nt ? st[t].mask : 0;
-    }
     for (uint32_t i = threadIdx.x; i < n; i += NT) {
-      uint32_t b = L.bits(i), x = L.idx(i);
-#pragma unroll
-      for (int t = 0; t < MAXT; ++t) {
-        if (t < nt) {
-          KeyT k;
-          if (fn(t, b, x, k) && (((uint64_t)k & mk[t]) == pf[t]))
-            atomicAdd(&H[t * HB + (int)(((uint64_t)k >> shf) & (uint64_t)(nb - 1))], 1u);
-        }
-      }
+      uint64_t k;
+      if (fn(L.bits(i), L.idx(i), k) && (k & mask) == prefix) atomicAdd(&H[(int)((k >> shf) & (uint64_t)(nb - 1))], 1u);
     }
     g.sync();
-    for (int t = 0; t < nt; ++t) {
-      find_digit(g, sh, H + t * HB, nb, t, st[t].r);
-      if (sh.fd_found[t]) {
-        st[t].prefix |= (uint64_t)sh.fd_digit[t] << shf;
-        st[t].r -= sh.fd_above[t];
-        st[t].n_gt += sh.fd_above[t];
-        st[t].n_eq = sh.fd_eq[t];
-      } else {
-        st[t].ok = 0;
-      }
-      st[t].mask |= (uint64_t)(nb - 1) << shf;
-    }
+    find_digit<NT>(g, sh, H, nb, r);
+    prefix |= (uint64_t)sh.fd_digit << shf;
+    mask |= (uint64_t)(nb - 1) << shf;
+    r -= sh.fd_above;
     if (g.size == 1) __syncthreads();
   }
+  return prefix;
 }
 
-__device__ __forceinline__ Sel sel_init(uint64_t r) {
-  Sel s;
-  s.prefix = 0; s.mask = 0; s.r = r; s.n_gt = 0; s.n_eq = 0; s.ok = 1;
-  return s;
+// Result of an exact select: the element at 1-based rank r by (key desc, sec asc).
+struct SelRes {
+  uint32_t key;    // key of the cut element
+  uint64_t sec;    // its secondary key (valid unless all_ties)
+  uint64_t n_gt;   // elements with key > key
+  uint64_t n_eq;   // elements with key == key
+  uint64_t r_eq;   // how many of the key == key elements rank at or above the cut
+  int all_ties;    // r_eq == n_eq (no secondary test needed)
+};
+
+// Exact select.  Levels of 2048-bin histograms narrow [klo, khi) to the bin holding rank
+// r; the bin's elements are gathered and ranked exactly by (key desc, sec asc).  If the bin
+// is one key value with more than GCAP members, the secondary order is resolved by a radix
+// select on the hash, or by the flat-order ordinal for indices.
+template <int NT, class Pred, class KeyF, class SecF>
+__device__ SelRes select_exact(Grp& g, Shared& sh, uint32_t* scratch, const List& L, uint32_t n, Pred pred,
+                               KeyF keyf, SecF secf, uint64_t klo, uint64_t khi, uint64_t r, bool sec_is_idx) {
+  constexpr int NW = NT / 32;
+  uint32_t* hist = scratch;
+  GatE* gl = reinterpret_cast<GatE*>(scratch + 2 * HB);
+  GatE* gc = g.size > 1 ? gl + GCAP : gl;
+  const int tid = threadIdx.x;
+  uint64_t n_gt = 0, cnt = 0;
+  for (;;) {
+    const uint64_t span = khi - klo;
+    const int bl = span > 1 ? 64 - __clzll(span - 1) : 0;
+    const int shf = bl > 11 ? bl - 11 : 0;
+    const int nb = (int)(((span - 1) >> shf) + 1);
+    uint32_t* H = hist + (g.size > 1 ? g.hpar * HB : 0);
+    g.hpar ^= 1;
+    for (int i = tid; i < nb; i += NT) H[i] = 0;
+    __syncthreads();
+    list_foreach<NT>(L, n, [&](uint32_t b, uint32_t x) {
+      if (pred(b, x)) {
+        const uint64_t k = keyf(b);
+        if (k >= klo && k < khi) atomicAdd(&H[(int)((k - klo) >> shf)], 1u);
+      }
+    });
+    g.sync();
+    find_digit<NT>(g, sh, H, nb, r);
+    const uint64_t dg = sh.fd_digit;
+    n_gt += sh.fd_above;
+    r -= sh.fd_above;
+    cnt = sh.fd_eq;
+    klo = klo + (dg << shf);
+    const uint64_t nhi = klo + (1ull << shf);
+    khi = nhi < khi ? nhi : khi;
+    if (g.size == 1) __syncthreads();
+    if (cnt <= GCAP || shf == 0) break;
+  }
+  SelRes res;
+  if (cnt > GCAP) {
+    // one key value with a huge tie set (e.g. bf16 or constant tensors)
+    res.key = (uint32_t)klo;
+    res.n_gt = n_gt;
+    res.n_eq = cnt;
+    res.r_eq = r;
+    res.all_ties = r == cnt;
+    res.sec = 0;
+    if (!res.all_ties) {
+      const uint32_t kk = (uint32_t)klo;
+      if (!sec_is_idx) {
+        const uint64_t top = radix_select64<NT>(g, sh, hist, L, n, r, [&](uint32_t b, uint32_t x, uint64_t& k) {
+          if (!pred(b, x) || keyf(b) != kk) return false;
+          k = ~secf(b, x);
+          return true;
+        });
+        res.sec = ~top;
+      } else {
+        // r-th match in flat order: per-warp counts over contiguous segments, then locate
+        const uint32_t seg = (n + NW - 1) / NW;
+        const int wid = tid >> 5, lane = tid & 31;
+        const uint32_t w0 = wid * seg, w1 = w0 + seg < n ? w0 + seg : n;
+        uint32_t c = 0;
+        for (uint32_t i = w0 + lane; i < w1; i += 32) c += (pred(L.bits(i), L.idx(i)) && keyf(L.bits(i)) == kk);
+        c = __reduce_add_sync(0xFFFFFFFFu, c);
+        if (lane == 0) sh.red[wid] = c;
+        __syncthreads();
+        uint64_t* slot = g.slot();
+        if (tid == 0) {
+          uint64_t t = 0;
+          for (int w = 0; w < NW; ++w) t += sh.red[w];
+          slot[0] = t;
+          sh.cidx_found = 0;
+        }
+        g.allsum(1, sh.vec, sh.pre);
+        const uint64_t want = r - 1;  // 0-based ordinal among ties, group-wide
+        uint64_t base = sh.pre[0];
+        for (int w = 0; w < NW; ++w) {
+          if (want >= base && want < base + sh.red[w] && wid == w) {
+            uint64_t run = base;
+            for (uint32_t i0 = w0; i0 < w1; i0 += 32) {
+              const uint32_t i = i0 + lane;
+              const bool m = i < w1 && pred(L.bits(i), L.idx(i)) && keyf(L.bits(i)) == kk;
+              const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m);
+              if (m && run + __popc(bal & ((1u << lane) - 1u)) == want) {
+                sh.sel_sec = L.idx(i);
+                sh.cidx_found = 1;
+              }
+              run += __popc(bal);
+            }
+          }
+          base += sh.red[w];
+        }
+        __syncthreads();
+        uint64_t* slot2 = g.slot();
+        if (tid == 0) slot2[0] = sh.cidx_found ? sh.sel_sec + 1 : 0;
+        g.allsum(1, sh.vec, nullptr);
+        res.sec = sh.vec[0] - 1;
+      }
+    }
+    return res;
+  }
+  // gather the bin's elements (unordered) and rank them exactly
+  if (tid == 0) sh.gcount = 0;
+  __syncthreads();
+  list_foreach<NT>(L, n, [&](uint32_t b, uint32_t x) {
+    if (pred(b, x)) {
+      const uint64_t k = keyf(b);
+      if (k >= klo && k < khi) {
+        const uint32_t p = atomicAdd(&sh.gcount, 1u);
+        gl[p].key = (uint32_t)k;
+        gl[p].idx = x;
+        gl[p].sec = secf(b, x);
+      }
+    }
+  });
+  const uint32_t m = (uint32_t)cnt;
+  if (g.size > 1) {
+    g.sync();
+    cg::cluster_group cl = cg::this_cluster();
+    // concatenate every CTA's gather buffer (rank order) into gc
+    uint32_t off = 0;
+    for (uint32_t rr = 0; rr < g.size; ++rr) {
+      const uint32_t c = *cl.map_shared_rank(&sh.gcount, rr);
+      const GatE* src = cl.map_shared_rank(gl, rr);
+      for (uint32_t i = tid; i < c; i += NT) gc[off + i] = src[i];
+      off += c;
+    }
+    g.sync();  // peers may now reuse their gather buffers
+  } else {
+    __syncthreads();
+  }
+  // rank: element at 0-based position r-1 by (key desc, sec asc)
+  if (tid == 0) sh.sel_found = 0;
+  __syncthreads();
+  if (m <= 256) {
+    for (uint32_t i = tid; i < m; i += NT) {
+      const uint32_t ki = gc[i].key;
+      const uint64_t si = gc[i].sec;
+      uint32_t rank = 0;
+      for (uint32_t j = 0; j < m; ++j) {
+        const uint32_t kj = gc[j].key;
+        rank += (kj > ki) || (kj == ki && gc[j].sec < si);
+      }
+      if (rank == r - 1) {
+        sh.sel_key = ki;
+        sh.sel_sec = si;
+        sh.sel_found = 1;
+      }
+    }
+  } else {
+    // bitonic sort (descending key, ascending sec) over the next power of two
+    uint32_t p2 = 1;
+    while (p2 < m) p2 <<= 1;
+    for (uint32_t i = m + tid; i < p2; i += NT) { gc[i].key = 0; gc[i].sec = ~0ull; gc[i].idx = 0; }
+    __syncthreads();
+    for (uint32_t k = 2; k <= p2; k <<= 1) {
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t i = tid; i < p2; i += NT) {
+          const uint32_t ixj = i ^ j;
+          if (ixj > i) {
+            const GatE A = gc[i], Bv = gc[ixj];
+            const bool a_first = A.key > Bv.key || (A.key == Bv.key && A.sec < Bv.sec);
+            const bool up = (i & k) == 0;
+            if (up != a_first) { gc[i] = Bv; gc[ixj] = A; }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (tid == 0) {
+      sh.sel_key = gc[r - 1].key;
+      sh.sel_sec = gc[r - 1].sec;
+      sh.sel_found = 1;
+    }
+  }
+  __syncthreads();
+  const uint32_t ks = sh.sel_key;
+  uint32_t gt = 0, eq = 0;
+  for (uint32_t i = tid; i < m; i += NT) {
+    gt += gc[i].key > ks;
+    eq += gc[i].key == ks;
+  }
+  gt = __reduce_add_sync(0xFFFFFFFFu, gt);
+  eq = __reduce_add_sync(0xFFFFFFFFu, eq);
+  if ((tid & 31) == 0) { sh.red[tid >> 5] = gt; sh.red[16 + (tid >> 5)] = eq; }
+  __syncthreads();
+  uint64_t tgt = 0, teq = 0;
+  for (int w = 0; w < NW; ++w) { tgt += sh.red[w]; teq += sh.red[16 + w]; }
+  res.key = ks;
+  res.sec = sh.sel_sec;
+  res.n_gt = n_gt + tgt;
+  res.n_eq = teq;
+  res.r_eq = r - tgt;
+  res.all_ties = res.r_eq == teq;
+  __syncthreads();
+  return res;
 }
 
-// quant.py:59-62 in float64: floor((v - vmin)/o64 + 0.5) clipped to [0, levels].
-__device__ __forceinline__ uint32_t quant_code(uint32_t key, double vmin64, double o64, uint32_t levels) {
-  double v = (double)__uint_as_float(key);
-  double sc = __ddiv_rn(__dsub_rn(v, vmin64), o64);
-  double f = floor(__dadd_rn(sc, 0.5));
+// quant.py:59-62 in float64: floor((v - vmin)/o64 + 0.5) clipped to [0, levels].  The
+// reciprocal fast path is exact except within 1e-6 of a rounding boundary, where the
+// correctly rounded float64 division is used.
+__device__ __forceinline__ uint32_t quant_code(uint32_t key, double vmin64, double o64, double inv64,
+                                               uint32_t levels) {
+  const double v = (double)__uint_as_float(key);
+  const double dl = __dsub_rn(v, vmin64);
+  double t = __dadd_rn(__dmul_rn(dl, inv64), 0.5);
+  double f = floor(t);
+  const double fr = __dsub_rn(t, f);
+  if (fr < 1e-6 || fr > 0.999999) {
+    t = __dadd_rn(__ddiv_rn(dl, o64), 0.5);
+    f = floor(t);
+  }
   if (!(f > 0.0)) return 0u;
   return f >= (double)levels ? levels : (uint32_t)f;
 }
 
-// Load element e of an IF as fp32 bits.
 template <int DT>
 __device__ __forceinline__ uint32_t load_bits(const void* x, uint64_t e) {
   if (DT == SIF_DTYPE_F32) return __ldg(reinterpret_cast<const uint32_t*>(x) + e);
@@ -259,580 +471,620 @@ __device__ __forceinline__ uint32_t load_bits(const void* x, uint64_t e) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Streaming pass over the CTA's slice [s0, s1): counters + stable candidate compaction.
+// Phase A: stream the slice [s0, s1) once; counts + stable candidate compaction.
 struct Counts {
-  uint64_t nz, ge_lo, ge_hi, nonfinite, maxkey;
+  uint32_t ge_lo, ge_hi, maxkey;
 };
 
-template <int DT>
-__device__ void stream_pass(const void* x, uint64_t T, uint64_t s0, uint64_t s1, uint32_t lo_p, uint32_t lo_n,
-                            uint32_t lo_cnt, uint32_t hi_cnt, const List& L, Shared& sh, Counts& c) {
-  constexpr int VEC = DT == SIF_DTYPE_F32 ? 4 : 8;
-  constexpr int U = 4;
-  const uint64_t CH = (uint64_t)NT * VEC * U;
-  const uint64_t a0 = s0 - (s0 % VEC);
-  uint64_t ncand = 0;
-  for (uint64_t base = a0; base < s1; base += CH) {
-    uint32_t mask[U];
-    uint32_t bv[U][VEC];
+template <int DT, int U, int VEC>
+__device__ __forceinline__ void load_chunk(const void* x, uint64_t T, uint64_t s0, uint64_t s1, uint64_t base,
+                                           int nt, uint32_t (&bv)[U][VEC], uint32_t (&mask)[U]) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t e0 = base + ((uint64_t)u * NT + threadIdx.x) * VEC;
-      if (e0 + VEC <= T && e0 >= s0 && e0 + VEC <= s1) {
-        uint4 v = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(x) + e0 * (DT == SIF_DTYPE_F32 ? 4 : 2)));
-        if (DT == SIF_DTYPE_F32) {
-          bv[u][0] = v.x; bv[u][1] = v.y; bv[u][2] = v.z; bv[u][3] = v.w;
-        } else {
-          uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            bv[u][(2 * k) % VEC] = w[k] << 16;
-            bv[u][(2 * k + 1) % VEC] = w[k] & 0xFFFF0000u;
-          }
-        }
-        mask[u] = (1u << VEC) - 1u;
+  for (int u = 0; u < U; ++u) {
+    const uint64_t e0 = base + ((uint64_t)u * nt + threadIdx.x) * VEC;
+    if (e0 >= s0 && e0 + VEC <= s1) {
+      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(x) +
+                                                            e0 * (DT == SIF_DTYPE_F32 ? 4 : 2)));
+      if (DT == SIF_DTYPE_F32) {
+        bv[u][0] = v.x; bv[u][1 % VEC] = v.y; bv[u][2 % VEC] = v.z; bv[u][3 % VEC] = v.w;
       } else {
-        mask[u] = 0;
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) {
-          uint64_t e = e0 + j;
-          bv[u][j] = 0;
-          if (e >= s0 && e < s1 && e < T) {
-            bv[u][j] = load_bits<DT>(x, e);
-            mask[u] |= 1u << j;
-          }
+        for (int k = 0; k < 4; ++k) {
+          bv[u][(2 * k) % VEC] = w[k] << 16;
+          bv[u][(2 * k + 1) % VEC] = w[k] & 0xFFFF0000u;
+        }
+      }
+      mask[u] = (1u << VEC) - 1u;
+    } else {
+      mask[u] = 0;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        const uint64_t e = e0 + j;
+        bv[u][j] = 0;
+        if (e >= s0 && e < s1 && e < T) {
+          bv[u][j] = load_bits<DT>(x, e);
+          mask[u] |= 1u << j;
         }
       }
     }
+  }
+}
+
+// FITS: the whole slice fits in the shared-memory list (no spill branch per store).
+// ASYM: lambda > 0 thresholds differ by sign and |x| >= lo must be counted separately.
+template <int DT, int NT, bool FITS, bool ASYM>
+__device__ __noinline__ void stream_pass_t(const void* x, uint64_t T, uint64_t s0, uint64_t s1, uint32_t lo_p, uint32_t lo_n,
+                              uint32_t lo_cnt, uint32_t hi_cnt, const List& L, Shared& sh, Counts& c) {
+  constexpr int VEC = DT == SIF_DTYPE_F32 ? 4 : 8;
+  constexpr int U = DT == SIF_DTYPE_F32 ? 4 : 2;
+  const uint64_t CH = (uint64_t)NT * VEC * U;
+  const uint64_t a0 = s0 - (s0 % VEC);
+  uint32_t ncand = 0;
+  uint32_t ge_lo = 0, ge_hi = 0, mk = 0;
+  uint32_t cur[U][VEC], mcur[U];
+  if (a0 < s1) load_chunk<DT, U, VEC>(x, T, s0, s1, a0, NT, cur, mcur);
+  for (uint64_t base = a0; base < s1; base += CH) {
+    uint32_t nxt[U][VEC], mnxt[U];
+    const bool more = base + CH < s1;
+    if (more) load_chunk<DT, U, VEC>(x, T, s0, s1, base + CH, NT, nxt, mnxt);
     uint64_t packed = 0;
     uint32_t cm[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      cm[u] = 0;
+      uint32_t m = 0;
 #pragma unroll
       for (int j = 0; j < VEC; ++j) {
-        if (mask[u] & (1u << j)) {
-          uint32_t b = bv[u][j], key = b & 0x7FFFFFFFu;
-          c.nz += key != 0u;
-          c.ge_lo += key >= lo_cnt;
-          c.ge_hi += key >= hi_cnt;
-          c.nonfinite |= key >= kNonFiniteKey;
-          c.maxkey = key > c.maxkey ? key : c.maxkey;
-          if (key >= ((b >> 31) ? lo_n : lo_p)) cm[u] |= 1u << j;
+        const uint32_t b = cur[u][j], key = b & 0x7FFFFFFFu;
+        const bool in = (mcur[u] >> j) & 1u;
+        mk = in && key > mk ? key : mk;
+        ge_hi += (in && key >= hi_cnt) ? 1u : 0u;
+        if (ASYM) {
+          ge_lo += (in && key >= lo_cnt) ? 1u : 0u;
+          m |= (in && key >= ((b >> 31) ? lo_n : lo_p)) ? (1u << j) : 0u;
+        } else {
+          m |= (in && key >= lo_p) ? (1u << j) : 0u;
         }
       }
-      packed |= (uint64_t)__popc(cm[u]) << (16 * u);
+      cm[u] = m;
+      packed |= (uint64_t)__popc(m) << (16 * u);
     }
     uint64_t tot;
-    uint64_t ex = block_excl_scan_u64(packed, sh.scan, &tot);
-    uint64_t run = ncand;
+    const uint64_t ex = block_excl_scan_u64(packed, sh.scan, &tot);
+    uint32_t run = ncand;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      uint64_t off = run + ((ex >> (16 * u)) & 0xFFFFull);
-      const uint64_t e0 = base + ((uint64_t)u * NT + threadIdx.x) * VEC;
+      uint32_t off = run + (uint32_t)((ex >> (16 * u)) & 0xFFFFull);
+      const uint32_t e0 = (uint32_t)(base + ((uint64_t)u * NT + threadIdx.x) * VEC);
 #pragma unroll
       for (int j = 0; j < VEC; ++j) {
-        if (cm[u] & (1u << j)) {
-          L.set((uint32_t)off, bv[u][j], (uint32_t)(e0 + j));
+        if ((cm[u] >> j) & 1u) {
+          if (FITS) { L.sb[off] = cur[u][j]; L.si[off] = e0 + j; }
+          else {
+            const bool sm = off < L.cap;
+            uint32_t* pb = sm ? L.sb + off : L.gb + (off - L.cap);
+            uint32_t* px = sm ? L.si + off : L.gi + (off - L.cap);
+            *pb = cur[u][j];
+            *px = e0 + j;
+          }
           ++off;
         }
       }
-      run += (tot >> (16 * u)) & 0xFFFFull;
+      run += (uint32_t)((tot >> (16 * u)) & 0xFFFFull);
     }
     ncand = run;
+    if (more) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        mcur[u] = mnxt[u];
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) cur[u][j] = nxt[u][j];
+      }
+    }
   }
+  c.ge_lo = ASYM ? ge_lo : 0;
+  c.ge_hi = ge_hi;
+  c.maxkey = mk;
   if (threadIdx.x == 0) sh.n_cand = ncand;
   __syncthreads();
 }
 
-// Block-reduce the per-thread counters into the group slot (5 values).
+template <int DT, int NT>
+__device__ __forceinline__ void stream_pass(const void* x, uint64_t T, uint64_t s0, uint64_t s1, uint32_t lo_p,
+                                            uint32_t lo_n, uint32_t lo_cnt, uint32_t hi_cnt, const List& L,
+                                            Shared& sh, Counts& c, bool asym) {
+  const bool fits = s1 - s0 <= (uint64_t)L.cap;
+  if (fits) {
+    if (asym) stream_pass_t<DT, NT, true, true>(x, T, s0, s1, lo_p, lo_n, lo_cnt, hi_cnt, L, sh, c);
+    else stream_pass_t<DT, NT, true, false>(x, T, s0, s1, lo_p, lo_n, lo_cnt, hi_cnt, L, sh, c);
+  } else {
+    if (asym) stream_pass_t<DT, NT, false, true>(x, T, s0, s1, lo_p, lo_n, lo_cnt, hi_cnt, L, sh, c);
+    else stream_pass_t<DT, NT, false, false>(x, T, s0, s1, lo_p, lo_n, lo_cnt, hi_cnt, L, sh, c);
+  }
+}
+
+// Group-reduce the stream counters: sums of ge_lo / ge_hi / ncand, max of maxkey.
+template <int NT>
 __device__ void reduce_counts(Grp& g, Shared& sh, Counts& c) {
-  uint64_t v[5] = {c.nz, c.ge_lo, c.ge_hi, c.nonfinite, c.maxkey};
   uint64_t* slot = g.slot();
-  if (threadIdx.x < 5) slot[threadIdx.x] = 0;
+  if (threadIdx.x < 4) slot[threadIdx.x] = 0;
   __syncthreads();
-#pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    uint64_t x = v[k];
-    if (k == 4) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) { uint64_t y = __shfl_xor_sync(0xFFFFFFFFu, x, o); x = y > x ? y : x; }
-      if ((threadIdx.x & 31) == 0) atomicMax((unsigned long long*)&slot[k], (unsigned long long)x);
-    } else if (k == 3) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) x |= __shfl_xor_sync(0xFFFFFFFFu, x, o);
-      if ((threadIdx.x & 31) == 0 && x) atomicOr((unsigned long long*)&slot[k], 1ull);
-    } else {
-      x = warp_sum_u64(x);
-      if ((threadIdx.x & 31) == 0) atomicAdd((unsigned long long*)&slot[k], (unsigned long long)x);
-    }
+  const uint32_t glo = __reduce_add_sync(0xFFFFFFFFu, c.ge_lo), ghi = __reduce_add_sync(0xFFFFFFFFu, c.ge_hi);
+  const uint32_t mk = __reduce_max_sync(0xFFFFFFFFu, c.maxkey);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd((unsigned long long*)&slot[0], (unsigned long long)glo);
+    atomicAdd((unsigned long long*)&slot[1], (unsigned long long)ghi);
+    atomicMax((unsigned long long*)&slot[3], (unsigned long long)mk);
   }
-  // maxkey must be max-reduced over the group, not summed: the cluster path combines it
-  // through the prefix-free max below.
-  g.allsum(4, sh.vec, nullptr);
-  // group max of maxkey (slot of the previous parity still holds the local value)
-  uint64_t mk = 0;
-  {
-    uint64_t* prev = g.slots + (g.parity ^ 1) * 64;
-    if (g.size == 1) mk = prev[4];
-    else {
-      cg::cluster_group cl = cg::this_cluster();
-      for (uint32_t r = 0; r < g.size; ++r) {
-        uint64_t y = *cl.map_shared_rank(prev + 4, r);
-        mk = y > mk ? y : mk;
-      }
+  if (threadIdx.x == 0) slot[2] = sh.n_cand;
+  g.allsum(3, sh.vec, nullptr);
+  uint64_t* prev = g.slots + (g.parity ^ 1) * 64;  // this CTA's slot (still intact)
+  uint64_t m = 0;
+  if (g.size == 1) m = prev[3];
+  else {
+    cg::cluster_group cl = cg::this_cluster();
+    for (uint32_t r = 0; r < g.size; ++r) {
+      const uint64_t y = *cl.map_shared_rank(prev + 3, r);
+      m = y > m ? y : m;
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) sh.vec[4] = mk;
+  if (threadIdx.x == 0) sh.vec[3] = m;
   __syncthreads();
 }
 
 // ---------------------------------------------------------------------------------------
-template <int DT>
-__device__ void encode_one(const EncArgs& a, const sif_enc_desc& d, int ifi, Grp& g, uint8_t* dsm, Shared& sh) {
-  const uint32_t N = d.rows, K = d.cols;
-  const uint64_t T = (uint64_t)N * K;
-  const uint64_t s0 = T * g.rank / g.size, s1 = T * (g.rank + 1) / g.size;
-  const uint64_t kk = keep_count(a.s, T);
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const uint32_t cb = col_bits(K);
-  const int maxb = a.maxb;
-
-  // ---- shared memory carve-up
-  uint32_t* crctab = reinterpret_cast<uint32_t*>(dsm);
-  uint32_t* hist = crctab + 256;
-  const int nhist = (g.size > 1 ? 2 : 1) * MAXT * HB;
-  uint8_t* p = reinterpret_cast<uint8_t*>(hist + nhist);
-  uint64_t* b_sum = reinterpret_cast<uint64_t*>(p); p += 8ull * maxb;
-  uint64_t* b_pre = reinterpret_cast<uint64_t*>(p); p += 8ull * maxb;
-  uint64_t* b_N = reinterpret_cast<uint64_t*>(p); p += 8ull * maxb;
-  uint64_t* b_off = reinterpret_cast<uint64_t*>(p); p += 8ull * 4 * maxb;  // meta, rp, cols, codes
-  double* b_o64 = reinterpret_cast<double*>(p); p += 8ull * maxb;
-  double* b_or = reinterpret_cast<double*>(p); p += 8ull * maxb;
-  uint32_t* b_n = reinterpret_cast<uint32_t*>(p); p += 4ull * maxb;
-  uint32_t* b_rs = reinterpret_cast<uint32_t*>(p); p += 4ull * maxb;
-  uint32_t* b_min = reinterpret_cast<uint32_t*>(p); p += 4ull * maxb;
-  uint32_t* b_max = reinterpret_cast<uint32_t*>(p); p += 4ull * maxb;
-  uint32_t* b_q = reinterpret_cast<uint32_t*>(p); p += 4ull * maxb;
-  uint32_t* b_act = reinterpret_cast<uint32_t*>(p); p += 4ull * maxb;
-  uint32_t* cut_key = reinterpret_cast<uint32_t*>(p); p += 4ull * maxb;
-  uint32_t* cut_idx = reinterpret_cast<uint32_t*>(p); p += 4ull * maxb;
-  uint32_t* wcnt = reinterpret_cast<uint32_t*>(p); p += 4ull * NW * maxb;
-  uint32_t* woff = reinterpret_cast<uint32_t*>(p); p += 4ull * NW * maxb;
-  p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
-  const uint32_t cap = (uint32_t)a.cap;
-  uint8_t* spill = a.spill + a.spill_stride * ((uint64_t)ifi * g.size + g.rank);
-  const uint64_t slice = s1 - s0;
-  const uint64_t spill_n = slice > cap ? slice - cap : 0;
+// Per-IF encoder state, kept in shared memory so each phase (a separate, non-inlined
+// function) starts with a small live register set instead of one huge allocation.
+struct Ctx {
+  const void* x;
+  uint8_t* out;
+  uint64_t out_cap, seed;
+  uint32_t N, K, dtype, cb;
+  uint64_t T, s0, s1, kk;
+  FastDiv fk;
+  double s, lam, delta;
+  int m_plus, m_minus, q_bit, mode, atkf_only, maxb, ifi;
+  const uint8_t* fixed_q;
+  uint64_t* prof;
+  uint32_t* t4;
+  uint32_t* scratch;
+  uint64_t *b_sum, *b_pre, *b_N, *b_off;
+  double *b_o64, *b_inv;
+  uint32_t *b_n, *b_rs, *b_min, *b_max, *b_q, *b_act, *cut_key, *cut_idx, *wcnt, *woff;
   List L;
-  L.sb = reinterpret_cast<uint32_t*>(p);
-  L.si = L.sb + cap;
-  L.gb = reinterpret_cast<uint32_t*>(spill);
-  L.gi = L.gb + spill_n;
-  L.cap = cap;
   Perm M;
-  M.s = L.si + cap;
-  M.g = L.gi + spill_n;
-  M.cap = cap;
+  uint32_t lo, hi, lo_neg, maxkey, tau_key, ncand, nkept;
+  uint64_t cnt_nz, cnt_lo, cnt_hi, ck_star, h_star, kept_pre;
+  double tau, tau_p, tau_m;
+  int zero_mode, only_nonzero, keep_none, use_cls, tie_all, nonfinite;
+  uint64_t cnt_sign[2], meff[2], base[2];
+  uint32_t kmin[2], kmax[2];
+  int B, ncut0, ncut;
+  uint64_t P;
+};
 
-  for (int i = tid; i < 256; i += NT) crctab[i] = kCrcTab[i];
+__device__ __forceinline__ void phase_mark(const Ctx& c, const Grp& g, int k) {
+  if (c.prof && g.rank == 0 && threadIdx.x == 0) c.prof[(uint64_t)c.ifi * 32 + k] = gtimer();
+}
 
-  // ---- Phase S: sampled bracket [lo, hi) for tau (identical in every CTA of the group)
-  const bool zero_mode_possible = a.atkf_only != 0;
-  uint32_t lo = 1, hi = kInfKey, lo_neg = 1;
-  if (T > 16384 && kk > 0 && 2 * kk <= T) {
-    for (int i = tid; i < HB; i += NT) hist[i] = 0;
-    __syncthreads();
-    constexpr int S = 2048;
-    for (int j = tid; j < S; j += NT) {
-      uint64_t pos = (uint64_t)j * T / S + (T / (2 * S));
-      uint32_t key = load_bits<DT>(d.x, pos) & 0x7FFFFFFFu;
-      if (key && key < kNonFiniteKey) atomicAdd(&hist[key >> 20], 1u);
+// ---- Phase S: sampled bracket [lo, hi) for tau (identical in every CTA of the group)
+template <int DT, int NT>
+__device__ __noinline__ Grp phase_sample(Ctx& c, Grp g, Shared& sh) {
+  const int tid = threadIdx.x;
+  const uint64_t T = c.T, kk = c.kk;
+  uint32_t lo = 1, hi = kInfKey;
+  if (T > 32768 && kk > 0 && 2 * kk <= T) {
+    constexpr int NSECT = 512, SB = 8192;  // 512 sectors x 8 elements; 13-bit key bins
+    constexpr int PERT = (NSECT + NT - 1) / NT;
+    uint32_t* sh8k = c.scratch;
+    for (int i = tid; i < SB; i += NT) sh8k[i] = 0;
+    uint32_t sv[PERT][8];
+#pragma unroll
+    for (int k = 0; k < PERT; ++k) {
+      const int j = tid + k * NT;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) sv[k][q] = 0;
+      if (j < NSECT) {
+        // low-discrepancy (Weyl) sector positions avoid aliasing with row structure
+        const uint64_t nsec = T / 8;
+        const uint64_t frac = (uint64_t)(uint32_t)((uint32_t)j * 0x9E3779B9u);  // j * golden ratio mod 1
+        const uint64_t e = ((frac * nsec) >> 32) * 8;
+        if (DT == SIF_DTYPE_F32) {
+          const uint4* q4 = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(c.x) + e);
+          const uint4 v0 = __ldg(q4), v1 = __ldg(q4 + 1);
+          sv[k][0] = v0.x; sv[k][1] = v0.y; sv[k][2] = v0.z; sv[k][3] = v0.w;
+          sv[k][4] = v1.x; sv[k][5] = v1.y; sv[k][6] = v1.z; sv[k][7] = v1.w;
+        } else {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const unsigned short*>(c.x) + e));
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) { sv[k][2 * q] = w[q] << 16; sv[k][2 * q + 1] = w[q] & 0xFFFF0000u; }
+        }
+      }
     }
     __syncthreads();
-    const double q = (double)kk / (double)T;
-    const double sd = sqrt(q * (1.0 - q) * S);
-    const double rlo = ceil(q * S + 4.0 * sd + 4.0);
-    const double rhi = floor(q * S - 4.0 * sd - 4.0);
+#pragma unroll
+    for (int k = 0; k < PERT; ++k) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t key = sv[k][q] & 0x7FFFFFFFu;
+        if (key && key < kNonFiniteKey) atomicAdd(&sh8k[key >> 18], 1u);
+      }
+    }
+    __syncthreads();
+    const double S = NSECT * 8.0;
+    const double qf = (double)kk / (double)T;
+    const double sd = sqrt(qf * (1.0 - qf) * S);
+    const double rlo = ceil(qf * S + 3.0 * sd + 2.0);
+    const double rhi = floor(qf * S - 3.0 * sd - 2.0);
     Grp g1 = g;
-    g1.size = 1;  // local histogram only
-    find_digit(g1, sh, hist, HB, 0, (uint64_t)rlo);
-    uint32_t lo_b = sh.fd_found[0] ? sh.fd_digit[0] : 0u;
-    bool lo_ok = sh.fd_found[0] != 0;
-    uint32_t hi_b = 0;
+    g1.size = 1;
+    find_digit<NT>(g1, sh, sh8k, SB, (uint64_t)rlo);
+    const bool lo_ok = sh.fd_found != 0;
+    const uint32_t lo_b = sh.fd_digit;
     bool hi_ok = false;
+    uint32_t hi_b = 0;
     if (rhi >= 1.0) {
-      find_digit(g1, sh, hist, HB, 1, (uint64_t)rhi);
-      hi_ok = sh.fd_found[1] != 0;
-      hi_b = sh.fd_digit[1];
+      find_digit<NT>(g1, sh, sh8k, SB, (uint64_t)rhi);
+      hi_ok = sh.fd_found != 0;
+      hi_b = sh.fd_digit;
     }
-    lo = lo_ok ? (lo_b << 20) : 1u;
+    lo = lo_ok ? (lo_b << 18) : 1u;
     if (lo == 0) lo = 1;
-    hi = hi_ok ? ((hi_b + 1u) << 20) : kInfKey;
-    if (hi_ok && hi_b + 1u >= 2048u) hi = kInfKey;
+    hi = (hi_ok && hi_b + 1u < (uint32_t)SB) ? ((hi_b + 1u) << 18) : kInfKey;
   }
-  if (a.lam > 0.0 && lo > 1) {
-    double t = __dmul_rn(__dsub_rn(1.0, a.lam), (double)__uint_as_float(lo));
-    uint32_t k2 = __float_as_uint(__double2float_rd(t));
+  uint32_t lo_neg = lo;
+  if (c.lam > 0.0 && lo > 1) {
+    const double t = __dmul_rn(__dsub_rn(1.0, c.lam), (double)__uint_as_float(lo));
+    const uint32_t k2 = __float_as_uint(__double2float_rd(t));
     lo_neg = k2 > 1 ? k2 : 1u;
-  } else {
+  }
+  __syncthreads();
+  if (tid == 0) { c.lo = lo; c.hi = hi; c.lo_neg = lo_neg; }
+  __syncthreads();
+  return g;
+}
+
+// ---- Phase A: stream the slice, count, compact candidates (+ fallback re-stream)
+template <int DT, int NT>
+__device__ __noinline__ Grp phase_stream(Ctx& c, Grp g, Shared& sh) {
+  const int tid = threadIdx.x;
+  const uint64_t kk = c.kk;
+  uint32_t lo = c.lo, hi = c.hi, lo_neg = c.lo_neg;
+  const bool asym = lo_neg != lo;
+  Counts k;
+  stream_pass<DT, NT>(c.x, c.T, c.s0, c.s1, lo, lo_neg, lo, hi, c.L, sh, k, asym);
+  reduce_counts<NT>(g, sh, k);
+  // |x| >= lo count: every candidate when the thresholds are symmetric
+  uint64_t cnt_lo = asym ? sh.vec[0] : sh.vec[2], cnt_hi = sh.vec[1];
+  uint32_t maxkey = (uint32_t)sh.vec[3];
+  const int nonfinite = maxkey >= kNonFiniteKey;
+  uint64_t cnt_nz = cnt_lo;  // exact when lo <= 1, else a lower bound (only compared with kk)
+  if (!nonfinite && kk > 0 && cnt_lo < kk && lo > (c.atkf_only ? 0u : 1u)) {
+    // bracket missed (or tau == 0): re-stream keeping every nonzero (every element in
+    // ATKF-only mode); ge_lo then counts the nonzeros
+    const uint32_t new_hi = lo;
+    lo = c.atkf_only ? 0u : 1u;
     lo_neg = lo;
+    hi = new_hi;
+    stream_pass<DT, NT>(c.x, c.T, c.s0, c.s1, lo, lo_neg, 1u, hi, c.L, sh, k, true);
+    reduce_counts<NT>(g, sh, k);
+    cnt_nz = sh.vec[0];
+    cnt_lo = cnt_nz;
+    cnt_hi = sh.vec[1];
+    maxkey = (uint32_t)sh.vec[3];
   }
+  __syncthreads();
+  if (tid == 0) {
+    c.lo = lo; c.hi = hi; c.lo_neg = lo_neg;
+    c.cnt_nz = cnt_nz; c.cnt_lo = cnt_lo; c.cnt_hi = cnt_hi;
+    c.maxkey = maxkey;
+    c.nonfinite = nonfinite;
+    c.zero_mode = kk > 0 && lo == 0;
+    c.ncand = (uint32_t)sh.n_cand;
+  }
+  __syncthreads();
+  return g;
+}
 
-  // ---- Phase A: stream the slice, count, compact candidates
-  Counts c;
-  c.nz = c.ge_lo = c.ge_hi = c.nonfinite = c.maxkey = 0;
-  stream_pass<DT>(d.x, T, s0, s1, lo, lo_neg, lo, hi, L, sh, c);
-  reduce_counts(g, sh, c);
-  uint64_t cnt_nz = sh.vec[0], cnt_lo = sh.vec[1], cnt_hi = sh.vec[2];
-  const bool nonfinite = sh.vec[3] != 0;
-  const uint32_t maxkey = (uint32_t)sh.vec[4];
-  if (nonfinite) {
-    if (g.rank == 0 && tid == 0) { a.status[ifi] = SIF_ERR_NONFINITE; if (!a.atkf_only) a.out_len[ifi] = 0; }
-    return;
-  }
-  bool zero_mode = false;
-  if (kk > 0) {
-    uint32_t need_lo = lo;
-    if (cnt_nz < kk) need_lo = zero_mode_possible ? 0u : 1u;
-    else if (cnt_lo < kk) need_lo = 1u;
-    if (need_lo < lo) {
-      // bracket missed (or tau == 0): re-stream with everything nonzero (or every element)
-      uint32_t new_hi = cnt_lo < kk ? lo : hi;
-      lo = need_lo;
-      lo_neg = need_lo;
-      hi = new_hi;
-      c.nz = c.ge_lo = c.ge_hi = c.nonfinite = c.maxkey = 0;
-      stream_pass<DT>(d.x, T, s0, s1, lo, lo_neg, lo, hi, L, sh, c);
-      reduce_counts(g, sh, c);
-      cnt_nz = sh.vec[0]; cnt_lo = sh.vec[1]; cnt_hi = sh.vec[2];
-      zero_mode = (lo == 0);
-    }
-  }
-  const uint32_t ncand = (uint32_t)sh.n_cand;
-
-  // ---- tau select
+// ---- Phase B: tau, class (lambda > 0) and the tie cut (atkf.py:71-84)
+template <int NT>
+__device__ __noinline__ Grp phase_select(Ctx& c, Grp g, Shared& sh) {
+  const int tid = threadIdx.x;
+  const uint64_t kk = c.kk, seed = c.seed;
+  const uint64_t cnt_nz = c.cnt_nz, cnt_hi = c.cnt_hi;
+  const uint32_t lo = c.lo, hi = c.hi, maxkey = c.maxkey, ncand = c.ncand;
+  const bool zero_mode = c.zero_mode != 0;
+  const List L = c.L;
+  auto hash_of = [seed](uint32_t, uint32_t x) -> uint64_t { return splitmix(seed, x); };
+  auto key31 = [](uint32_t b) -> uint64_t { return b & 0x7FFFFFFFu; };
+  auto all_pred = [](uint32_t, uint32_t) { return true; };
   uint32_t tau_key = 0;
-  uint64_t n_gt = 0, n_eq = 0;
-  if (kk > 0) {
-    if (cnt_nz < kk) {
-      tau_key = 0;
-      n_gt = cnt_nz;
-      n_eq = T - cnt_nz;
+  uint64_t ck_star = 0, h_star = 0;
+  bool tie_all = true;
+  const bool keep_none = kk == 0;
+  const bool only_nonzero = kk > 0 && cnt_nz < kk && !zero_mode;  // tau == 0 in payload mode
+  if (kk > 0 && !only_nonzero) {
+    if (zero_mode && cnt_nz < kk) {
+      // tau == 0 (ATKF-only mode): every nonzero is kept; choose kk - nnz zeros by hash
+      const SelRes s = select_exact<NT>(g, sh, c.scratch, L, ncand, all_pred, key31, hash_of, 0, 1, kk - cnt_nz, false);
+      h_star = s.sec;
+      tie_all = s.all_ties;
     } else {
-      uint32_t ra, rb;
-      uint64_t r, base_gt;
-      if (cnt_hi >= kk || hi == kInfKey) { ra = (hi == kInfKey ? lo : hi); rb = kInfKey; r = kk; base_gt = 0; }
-      else { ra = lo; rb = hi; r = kk - cnt_hi; base_gt = cnt_hi; }
-      if (ra == 0) ra = 1;
-      Sel st = sel_init(r);
-      select_batch<uint32_t>(g, sh, hist, L, ncand, 1, &st,
-                             [&](int, uint32_t b, uint32_t, uint32_t& k) {
-                               k = b & 0x7FFFFFFFu;
-                               return k >= ra && k < rb;
-                             });
-      tau_key = (uint32_t)st.prefix;
-      n_gt = base_gt + st.n_gt;
-      n_eq = st.n_eq;
+      uint64_t ra, rb, r;
+      if (cnt_hi >= kk || hi == kInfKey) { ra = (hi == kInfKey ? lo : hi); rb = (uint64_t)maxkey + 1; r = kk; }
+      else { ra = lo; rb = hi; r = kk - cnt_hi; }
+      const SelRes s = select_exact<NT>(g, sh, c.scratch, L, ncand, all_pred, key31, hash_of, ra, rb, r, false);
+      tau_key = s.key;
+      ck_star = s.key;
+      h_star = s.sec;
+      tie_all = s.all_ties;
     }
   }
   const double tau = kk > 0 ? (double)__uint_as_float(tau_key) : (double)__uint_as_float(maxkey);
-  const double tau_p = __dmul_rn(__dadd_rn(1.0, a.lam), tau);
-  const double tau_m = -__dmul_rn(__dsub_rn(1.0, a.lam), tau);
-
-  // ---- lambda > 0: strict class (atkf.py:75-84)
-  const bool use_cls = a.lam > 0.0 && kk > 0 && (tau_key > 0 || zero_mode);
-  uint32_t key_star = tau_key, cls_star = 0;
-  uint64_t r_t = kk - n_gt;  // ties to take at key_star
-  auto strict_of = [&](uint32_t b) -> uint32_t {
-    double v = (double)__uint_as_float(b);
-    return (v > tau_p || v < tau_m) ? 1u : 0u;
-  };
+  const double tau_p = __dmul_rn(__dadd_rn(1.0, c.lam), tau);
+  const double tau_m = -__dmul_rn(__dsub_rn(1.0, c.lam), tau);
+  const bool use_cls = c.lam > 0.0 && kk > 0 && !only_nonzero;
   if (use_cls) {
-    uint64_t ns = 0;
-    for (uint32_t i = tid; i < ncand; i += NT) ns += strict_of(L.bits(i));
-    ns = warp_sum_u64(ns);
-    uint64_t* slot = g.slot();
-    if (tid == 0) slot[0] = 0;
-    __syncthreads();
-    if (lane == 0) atomicAdd((unsigned long long*)&slot[0], (unsigned long long)ns);
-    g.allsum(1, sh.vec, nullptr);
-    const uint64_t n_strict = sh.vec[0];
-    uint64_t r;
-    if (n_strict >= kk) { cls_star = 1; r = kk; }
-    else { cls_star = 0; r = kk - n_strict; }
-    const uint32_t cs = cls_star;
-    Sel st = sel_init(r);
-    select_batch<uint32_t>(g, sh, hist, L, ncand, 1, &st,
-                           [&](int, uint32_t b, uint32_t, uint32_t& k) {
-                             k = b & 0x7FFFFFFFu;
-                             return strict_of(b) == cs;
-                           });
-    key_star = (uint32_t)st.prefix;
-    n_eq = st.n_eq;
-    r_t = st.r;  // remaining rank inside the tie set
-  }
-  // ---- tie break by splitmix64 key (rng.py:60-68), smallest keys first
-  // tie modes: all ties kept / none / zero ties (never reach the payload) / by hash
-  bool tie_all = r_t >= n_eq;
-  bool tie_none = !tie_all && r_t == 0;
-  bool tie_skip = (!zero_mode && key_star == 0);
-  uint64_t hkey = 0;
-  if (kk > 0 && !tie_all && !tie_none && !tie_skip) {
-    const uint32_t ks = key_star, cs = cls_star;
-    const bool uc = use_cls;
-    const uint64_t seed = d.seed;
-    Sel st = sel_init(r_t);
-    select_batch<uint64_t>(g, sh, hist, L, ncand, 1, &st,
-                           [&](int, uint32_t b, uint32_t x, uint64_t& k) {
-                             if ((b & 0x7FFFFFFFu) != ks) return false;
-                             if (uc && strict_of(b) != cs) return false;
-                             k = ~splitmix(seed, x);
-                             return true;
-                           });
-    hkey = st.prefix;
-  }
-
-  // ---- kept set: stable in-place compaction of the candidate list (atkf.py:83-88)
-  uint32_t nkept = 0;
-  uint64_t cnt_sign[2] = {0, 0};
-  {
-    const uint32_t ks = key_star, cs = cls_star;
-    const bool uc = use_cls, ta = tie_all, tsk = tie_skip || tie_none;
-    const uint64_t hk = hkey, seed = d.seed;
-    auto kept_of = [&](uint32_t b, uint32_t x) -> bool {
-      if (kk == 0) return false;
-      uint32_t key = b & 0x7FFFFFFFu;
-      if (!zero_mode && key == 0) return false;
-      if (uc) {
-        uint32_t cl = strict_of(b);
-        if (cl != cs) return cl > cs;
-      }
-      if (key != ks) return key > ks;
-      if (tsk) return false;
-      if (ta) return true;
-      return ~splitmix(seed, x) >= hk;
+    // composite key (strict << 31 | |x|) selects class, magnitude and ties at once
+    auto ckey = [tau_p, tau_m](uint32_t b) -> uint64_t {
+      const double v = (double)__uint_as_float(b);
+      return ((v > tau_p || v < tau_m) ? (1ull << 31) : 0ull) | (uint64_t)(b & 0x7FFFFFFFu);
     };
-    uint32_t run = 0;
-    uint64_t sp = 0, sm = 0;
-    for (uint32_t base = 0; base < ncand; base += NT) {
-      uint32_t i = base + tid;
-      uint32_t b = 0, x = 0;
-      bool k = false;
+    const SelRes s = select_exact<NT>(g, sh, c.scratch, L, ncand, all_pred, ckey, hash_of, 0, 1ull << 32, kk, false);
+    ck_star = s.key;
+    h_star = s.sec;
+    tie_all = s.all_ties;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    c.tau_key = tau_key; c.ck_star = ck_star; c.h_star = h_star; c.tie_all = tie_all;
+    c.keep_none = keep_none; c.only_nonzero = only_nonzero; c.use_cls = use_cls;
+    c.tau = tau; c.tau_p = tau_p; c.tau_m = tau_m;
+  }
+  __syncthreads();
+  return g;
+}
+
+// ---- Phase C: kept set, stable in-place compaction (8 elements per thread per chunk)
+template <int NT>
+__device__ __noinline__ Grp phase_kept(Ctx& c, Grp g, Shared& sh) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const List L = c.L;
+  const uint32_t ncand = c.ncand;
+  const bool keep_none = c.keep_none, only_nonzero = c.only_nonzero, zero_mode = c.zero_mode;
+  const bool use_cls = c.use_cls, tie_all = c.tie_all;
+  const uint64_t ck_star = c.ck_star, h_star = c.h_star, seed = c.seed;
+  const double tau_p = c.tau_p, tau_m = c.tau_m;
+  auto kept_of = [&](uint32_t b, uint32_t x) -> bool {
+    if (keep_none) return false;
+    const uint32_t key = b & 0x7FFFFFFFu;
+    if (only_nonzero) return key != 0;
+    if (!zero_mode && key == 0) return false;
+    uint64_t ck = key;
+    if (use_cls) {
+      const double v = (double)__uint_as_float(b);
+      if (v > tau_p || v < tau_m) ck |= 1ull << 31;
+    }
+    if (ck != ck_star) return ck > ck_star;
+    return tie_all || splitmix(seed, x) <= h_star;
+  };
+  constexpr int E = 8;
+  uint32_t run = 0;
+  uint64_t sp = 0, sm = 0;
+  uint32_t mn0 = 0x7FFFFFFFu, mn1 = 0x7FFFFFFFu, mx0 = 0, mx1 = 0;
+  for (uint32_t base = 0; base < ncand; base += NT * E) {
+    uint32_t bb[E], xx[E];
+    uint32_t km = 0;
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const uint32_t i = base + tid * E + j;
+      bb[j] = 0;
+      xx[j] = 0;
       if (i < ncand) {
-        b = L.bits(i);
-        x = L.idx(i);
-        k = kept_of(b, x);
+        bb[j] = L.bits(i);
+        xx[j] = L.idx(i);
+        if (kept_of(bb[j], xx[j])) km |= 1u << j;
       }
-      uint64_t tot;
-      uint64_t ex = block_excl_scan_u64(k ? 1ull : 0ull, sh.scan, &tot);
-      if (k) {
-        L.set(run + (uint32_t)ex, b, x);
-        if ((b & 0x7FFFFFFFu) != 0) { if (b >> 31) ++sm; else ++sp; }
+    }
+    uint64_t tot;
+    const uint64_t ex = block_excl_scan_u64((uint64_t)__popc(km), sh.scan, &tot);
+    uint32_t o = run + (uint32_t)ex;
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      if (km & (1u << j)) {
+        L.set(o++, bb[j], xx[j]);
+        const uint32_t kj = bb[j] & 0x7FFFFFFFu;
+        if (kj != 0) {
+          if (bb[j] >> 31) { ++sm; mn1 = kj < mn1 ? kj : mn1; mx1 = kj > mx1 ? kj : mx1; }
+          else { ++sp; mn0 = kj < mn0 ? kj : mn0; mx0 = kj > mx0 ? kj : mx0; }
+        }
       }
-      run += (uint32_t)tot;
-      __syncthreads();
     }
-    nkept = run;
-    sp = warp_sum_u64(sp);
-    sm = warp_sum_u64(sm);
-    uint64_t* slot = g.slot();
-    if (tid < 3) slot[tid] = 0;
-    __syncthreads();
-    if (lane == 0) {
-      atomicAdd((unsigned long long*)&slot[0], (unsigned long long)sp);
-      atomicAdd((unsigned long long*)&slot[1], (unsigned long long)sm);
-    }
-    if (tid == 0) slot[2] = nkept;
-    g.allsum(3, sh.vec, sh.pre);
-    cnt_sign[0] = sh.vec[0];
-    cnt_sign[1] = sh.vec[1];
+    run += (uint32_t)tot;
   }
-  const uint64_t kept_pre = sh.pre[2];
-
-  if (a.atkf_only) {
-    int64_t* out = a.kept_out + a.kept_off[ifi] + kept_pre;
-    for (uint32_t i = tid; i < nkept; i += NT) out[i] = (int64_t)L.idx(i);
-    if (g.rank == 0 && tid == 0) {
-      a.tau3[3 * ifi + 0] = tau;
-      a.tau3[3 * ifi + 1] = tau_p;
-      a.tau3[3 * ifi + 2] = tau_m;
-      a.status[ifi] = SIF_OK;
-    }
-    return;
+  sp = warp_sum_u64(sp);
+  sm = warp_sum_u64(sm);
+  mn0 = __reduce_min_sync(0xFFFFFFFFu, mn0);
+  mn1 = __reduce_min_sync(0xFFFFFFFFu, mn1);
+  mx0 = __reduce_max_sync(0xFFFFFFFFu, mx0);
+  mx1 = __reduce_max_sync(0xFFFFFFFFu, mx1);
+  uint64_t* slot = g.slot();
+  if (tid < 7) slot[tid] = tid >= 3 && tid < 5 ? 0x7FFFFFFFull : 0ull;
+  __syncthreads();
+  if (lane == 0) {
+    atomicAdd((unsigned long long*)&slot[0], (unsigned long long)sp);
+    atomicAdd((unsigned long long*)&slot[1], (unsigned long long)sm);
+    atomicMin((unsigned long long*)&slot[3], (unsigned long long)mn0);
+    atomicMin((unsigned long long*)&slot[4], (unsigned long long)mn1);
+    atomicMax((unsigned long long*)&slot[5], (unsigned long long)mx0);
+    atomicMax((unsigned long long*)&slot[6], (unsigned long long)mx1);
   }
+  if (tid == 0) slot[2] = run;
+  g.allsum(3, sh.vec, sh.pre);
+  uint64_t* prev = g.slots + (g.parity ^ 1) * 64;
+  uint64_t k0 = 0x7FFFFFFF, k1 = 0x7FFFFFFF, k2 = 0, k3 = 0;
+  {
+    cg::cluster_group cl = cg::this_cluster();
+    for (uint32_t r = 0; r < g.size; ++r) {
+      const uint64_t* q = g.size == 1 ? prev : cl.map_shared_rank(prev, r);
+      k0 = q[3] < k0 ? q[3] : k0;
+      k1 = q[4] < k1 ? q[4] : k1;
+      k2 = q[5] > k2 ? q[5] : k2;
+      k3 = q[6] > k3 ? q[6] : k3;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    c.nkept = run;
+    c.cnt_sign[0] = sh.vec[0];
+    c.cnt_sign[1] = sh.vec[1];
+    c.kept_pre = sh.pre[2];
+    c.kmin[0] = (uint32_t)k0;
+    c.kmax[0] = (uint32_t)k2;
+    c.kmin[1] = (uint32_t)k1;
+    c.kmax[1] = (uint32_t)k3;
+  }
+  __syncthreads();
+  return g;
+}
 
-  // ---- MS: plane sizes and cut elements (msplit.py:54-80)
-  const int mcfg[2] = {a.m_plus, a.m_minus};
+// ---- Phase D: MS cut elements (msplit.py:54-80), value desc then flat idx asc
+template <int NT>
+__device__ __noinline__ Grp phase_cuts(Ctx& c, Grp g, Shared& sh) {
+  const int tid = threadIdx.x;
+  const int mcfg[2] = {c.m_plus, c.m_minus};
   uint64_t meff[2], base[2];
   for (int s = 0; s < 2; ++s) {
-    uint64_t nz = cnt_sign[s];
-    uint64_t m = (uint64_t)mcfg[s];
+    const uint64_t nz = c.cnt_sign[s], m = (uint64_t)mcfg[s];
     meff[s] = nz < m ? nz : m;
     if (meff[s] < 1) meff[s] = 1;
     base[s] = nz / meff[s];
   }
   const int B = (int)(meff[0] + meff[1]);
-  // cuts: sign s, j = 1..meff[s]-1 at 0-based rank j*base[s]; stored at cut index
-  // (s ? meff[0]-1 : 0) + j - 1
-  const int ncut = B - 2;
-  for (int c0 = 0; c0 < ncut; c0 += MAXT) {
-    const int nt = ncut - c0 < MAXT ? ncut - c0 : MAXT;
-    Sel st[MAXT];
-    uint32_t sg[MAXT];
-    uint64_t rank0[MAXT];
-    for (int t = 0; t < MAXT; ++t) {
-      int ci = c0 + t;
-      if (t < nt) {
-        int s = ci < (int)meff[0] - 1 ? 0 : 1;
-        int j = (s == 0 ? ci : ci - ((int)meff[0] - 1)) + 1;
-        sg[t] = s;
-        rank0[t] = (uint64_t)j * base[s];
-        st[t] = sel_init(rank0[t] + 1);
-      } else {
-        sg[t] = 0; rank0[t] = 0; st[t] = sel_init(1);
-      }
-    }
-    select_batch<uint32_t>(g, sh, hist, L, nkept, nt, st,
-                           [&](int t, uint32_t b, uint32_t, uint32_t& k) {
-                             k = b & 0x7FFFFFFFu;
-                             return (b >> 31) == sg[t] && k != 0;
-                           });
-    // idx resolution: the (rank0 - n_gt)-th (0-based) element, in flat order, among the
-    // kept elements of the cut's sign whose key equals the cut key (msplit.py:64 ties).
-    uint32_t ck[MAXT];
-    for (int t = 0; t < MAXT; ++t) ck[t] = (uint32_t)st[t].prefix;
-    uint64_t* slot = g.slot();
-    if (tid < MAXT) slot[tid] = 0;
-    __syncthreads();
-    {
-      uint32_t cnt[MAXT] = {0, 0, 0, 0};
-      for (uint32_t i = tid; i < nkept; i += NT) {
-        uint32_t b = L.bits(i);
-#pragma unroll
-        for (int t = 0; t < MAXT; ++t)
-          if (t < nt && (b >> 31) == sg[t] && (b & 0x7FFFFFFFu) == ck[t]) ++cnt[t];
-      }
-#pragma unroll
-      for (int t = 0; t < MAXT; ++t) {
-        uint32_t v = __reduce_add_sync(0xFFFFFFFFu, cnt[t]);
-        if (lane == 0 && v) atomicAdd((unsigned long long*)&slot[t], (unsigned long long)v);
-      }
-    }
-    g.allsum(MAXT, sh.vec, sh.pre);
-    uint64_t want[MAXT];
-    bool mine[MAXT];
-    {
-      const uint64_t* prev = g.slots + (g.parity ^ 1) * 64;  // this CTA's local counts
-      for (int t = 0; t < MAXT; ++t) {
-        const uint64_t w = rank0[t] - st[t].n_gt;
-        mine[t] = t < nt && w >= sh.pre[t] && w < sh.pre[t] + prev[t];
-        want[t] = w - sh.pre[t];
-      }
-    }
-    if (tid < MAXT) { sh.cidx_found[tid] = 0; sh.run[tid] = 0; }
-    __syncthreads();
-    for (uint32_t base2 = 0; base2 < nkept; base2 += NT) {
-      const uint32_t i = base2 + tid;
-      const uint32_t b = i < nkept ? L.bits(i) : 0u;
-      uint64_t pk = 0;
-      if (i < nkept)
-        for (int t = 0; t < MAXT; ++t)
-          if (mine[t] && (b >> 31) == sg[t] && (b & 0x7FFFFFFFu) == ck[t]) pk |= 1ull << (16 * t);
-      uint64_t tot;
-      const uint64_t ex = block_excl_scan_u64(pk, sh.scan, &tot);
-      for (int t = 0; t < MAXT; ++t)
-        if (((pk >> (16 * t)) & 1ull) && sh.run[t] + ((ex >> (16 * t)) & 0xFFFFull) == want[t]) {
-          sh.cidx_found[t] = 1;
-          cut_idx[c0 + t] = L.idx(i);
-        }
-      __syncthreads();
-      if (tid < MAXT) sh.run[tid] += (tot >> (16 * tid)) & 0xFFFFull;
-      __syncthreads();
-    }
-    uint64_t* slot2 = g.slot();
-    if (tid < MAXT) slot2[tid] = (tid < nt && sh.cidx_found[tid]) ? (uint64_t)cut_idx[c0 + tid] + 1ull : 0ull;
-    g.allsum(MAXT, sh.vec, nullptr);
-    if (tid < nt) {
-      cut_key[c0 + tid] = ck[tid];
-      cut_idx[c0 + tid] = (uint32_t)(sh.vec[tid] - 1ull);
-    }
-    __syncthreads();
-  }
   const int ncut0 = (int)meff[0] - 1;
-  auto block_of = [&](uint32_t b, uint32_t x) -> int {
-    uint32_t key = b & 0x7FFFFFFFu;
-    int s = (int)(b >> 31);
-    int c0 = s ? ncut0 : 0, cn = s ? ncut : ncut0;
-    int blk = 0;
-    for (int c = c0; c < cn; ++c) {
-      uint32_t k2 = cut_key[c];
-      if (key < k2 || (key == k2 && x >= cut_idx[c])) ++blk;
-      else break;
-    }
-    return (s ? (int)meff[0] : 0) + blk;
-  };
-
-  // ---- members per block in flat (CSR) order: warp-segmented stable walk
-  {
-    const uint32_t seg = (nkept + NW - 1) / NW;
-    const uint32_t w0 = wid * seg, w1 = (w0 + seg < nkept) ? w0 + seg : nkept;
-    for (int b = lane; b < B; b += 32) wcnt[wid * maxb + b] = 0;
-    __syncwarp();
-    for (uint32_t i = w0; i < w1; i += 32) {
-      uint32_t e = i + lane;
-      int blk = e < w1 ? block_of(L.bits(e), L.idx(e)) : -1;
-      uint32_t peers = __match_any_sync(0xFFFFFFFFu, blk);
-      if (blk >= 0 && lane == __ffs(peers) - 1) wcnt[wid * maxb + blk] += __popc(peers);
-      __syncwarp();
-    }
-    __syncthreads();
-    for (int b = tid; b < B; b += NT) {
-      uint32_t acc = 0;
-      for (int w = 0; w < NW; ++w) {
-        woff[w * maxb + b] = acc;
-        acc += wcnt[w * maxb + b];
-      }
-      b_n[b] = acc;
-    }
-    __syncthreads();
+  const int ncut = B - 2;
+  const List L = c.L;
+  const uint32_t nkept = c.nkept;
+  for (int ci = 0; ci < ncut; ++ci) {
+    const uint32_t s = ci < ncut0 ? 0u : 1u;
+    const int j = (s == 0 ? ci : ci - ncut0) + 1;
+    const uint64_t rank0 = (uint64_t)j * base[s];
+    const uint64_t klo = c.kmin[s], khi = (uint64_t)c.kmax[s] + 1;
+    const SelRes r = select_exact<NT>(g, sh, c.scratch, L, nkept, [s](uint32_t b, uint32_t) { return (b >> 31) == s; },
+                                      [](uint32_t b) -> uint64_t { return b & 0x7FFFFFFFu; },
+                                      [](uint32_t, uint32_t x) -> uint64_t { return x; }, klo, khi > klo ? khi : klo + 1,
+                                      rank0 + 1, true);
     if (tid == 0) {
-      uint32_t acc = 0;
-      for (int b = 0; b < B; ++b) { b_rs[b] = acc; acc += b_n[b]; }
-    }
-    for (int b = lane; b < B; b += 32) wcnt[wid * maxb + b] = 0;
-    __syncthreads();
-    for (uint32_t i = w0; i < w1; i += 32) {
-      uint32_t e = i + lane;
-      int blk = e < w1 ? block_of(L.bits(e), L.idx(e)) : -1;
-      uint32_t peers = __match_any_sync(0xFFFFFFFFu, blk);
-      if (blk >= 0) {
-        uint32_t rank = woff[wid * maxb + blk] + wcnt[wid * maxb + blk] + __popc(peers & ((1u << lane) - 1u));
-        M.set(b_rs[blk] + rank, e);
-      }
-      __syncwarp();
-      if (blk >= 0 && lane == __ffs(peers) - 1) wcnt[wid * maxb + blk] += __popc(peers);
-      __syncwarp();
+      c.cut_key[ci] = r.key;
+      c.cut_idx[ci] = (uint32_t)r.sec;
     }
     __syncthreads();
-    // group prefix of per-block counts + block min/max keys
-    for (int b0 = 0; b0 < B; b0 += 64) {
-      int nb = B - b0 < 64 ? B - b0 : 64;
-      uint64_t* slot = g.slot();
-      if (tid < nb) slot[tid] = b_n[b0 + tid];
-      g.allsum(nb, sh.vec, sh.pre);
-      if (tid < nb) { b_N[b0 + tid] = sh.vec[tid]; b_pre[b0 + tid] = sh.pre[tid]; }
-      __syncthreads();
-    }
   }
-  // block min / max keys (v_min, v_max of quant.py:50-51)
+  if (tid == 0) {
+    c.meff[0] = meff[0]; c.meff[1] = meff[1]; c.base[0] = base[0]; c.base[1] = base[1];
+    c.B = B; c.ncut0 = ncut0; c.ncut = ncut;
+  }
+  __syncthreads();
+  return g;
+}
+
+__device__ __forceinline__ int block_of(const uint32_t* cut_key, const uint32_t* cut_idx, int ncut0, int ncut,
+                                        int meff0, uint32_t b, uint32_t x) {
+  const uint32_t key = b & 0x7FFFFFFFu;
+  const int s = (int)(b >> 31);
+  const int c0 = s ? ncut0 : 0, cn = s ? ncut : ncut0;
+  int blk = 0;
+  for (int cc = c0; cc < cn; ++cc) {
+    const uint32_t k2 = cut_key[cc];
+    if (key < k2 || (key == k2 && x >= cut_idx[cc])) ++blk;
+    else break;
+  }
+  return (s ? meff0 : 0) + blk;
+}
+
+// ---- Phase E: members per block in flat (CSR) order: warp-segmented stable walk
+template <int NT>
+__device__ __noinline__ Grp phase_members(Ctx& c, Grp g, Shared& sh) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const List L = c.L;
+  const Perm M = c.M;
+  const uint32_t nkept = c.nkept;
+  const int B = c.B, maxb = c.maxb, ncut0 = c.ncut0, ncut = c.ncut, meff0 = (int)c.meff[0];
+  const uint32_t* cut_key = c.cut_key;
+  const uint32_t* cut_idx = c.cut_idx;
+  uint32_t* wcnt = c.wcnt;
+  uint32_t* woff = c.woff;
+  const uint32_t seg = (nkept + NW - 1) / NW;
+  const uint32_t w0 = wid * seg, w1 = (w0 + seg < nkept) ? w0 + seg : nkept;
+  for (int b = lane; b < B; b += 32) wcnt[wid * maxb + b] = 0;
+  __syncwarp();
+  for (uint32_t i = w0; i < w1; i += 32) {
+    const uint32_t e = i + lane;
+    const int blk = e < w1 ? block_of(cut_key, cut_idx, ncut0, ncut, meff0, L.bits(e), L.idx(e)) : -1;
+    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, blk);
+    if (blk >= 0 && lane == __ffs(peers) - 1) wcnt[wid * maxb + blk] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int b = tid; b < B; b += NT) {
+    uint32_t acc = 0;
+    for (int w = 0; w < NW; ++w) {
+      woff[w * maxb + b] = acc;
+      acc += wcnt[w * maxb + b];
+    }
+    c.b_n[b] = acc;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t acc = 0;
+    for (int b = 0; b < B; ++b) { c.b_rs[b] = acc; acc += c.b_n[b]; }
+  }
+  for (int b = lane; b < B; b += 32) wcnt[wid * maxb + b] = 0;
+  __syncthreads();
+  const uint32_t* b_rs = c.b_rs;
+  for (uint32_t i = w0; i < w1; i += 32) {
+    const uint32_t e = i + lane;
+    const int blk = e < w1 ? block_of(cut_key, cut_idx, ncut0, ncut, meff0, L.bits(e), L.idx(e)) : -1;
+    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, blk);
+    if (blk >= 0) {
+      const uint32_t rk = woff[wid * maxb + blk] + wcnt[wid * maxb + blk] + __popc(peers & ((1u << lane) - 1u));
+      M.set(b_rs[blk] + rk, e);
+    }
+    __syncwarp();
+    if (blk >= 0 && lane == __ffs(peers) - 1) wcnt[wid * maxb + blk] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int b0 = 0; b0 < B; b0 += 64) {
+    const int nb = B - b0 < 64 ? B - b0 : 64;
+    uint64_t* slot = g.slot();
+    if (tid < nb) slot[tid] = c.b_n[b0 + tid];
+    g.allsum(nb, sh.vec, sh.pre);
+    if (tid < nb) { c.b_N[b0 + tid] = sh.vec[tid]; c.b_pre[b0 + tid] = sh.pre[tid]; }
+    __syncthreads();
+  }
+  return g;
+}
+
+// ---- Phase F: block min / max keys (quant.py:50-51)
+template <int NT>
+__device__ __noinline__ Grp phase_minmax(Ctx& c, Grp g, Shared& sh) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int B = c.B;
+  const List L = c.L;
+  const Perm M = c.M;
+  uint32_t* b_min = c.b_min;
+  uint32_t* b_max = c.b_max;
   for (int b = tid; b < B; b += NT) { b_min[b] = 0x7FFFFFFFu; b_max[b] = 0u; }
   __syncthreads();
   for (int b = 0; b < B; ++b) {
     uint32_t mn = 0x7FFFFFFFu, mx = 0;
-    for (uint32_t i = tid; i < b_n[b]; i += NT) {
-      uint32_t k = L.bits(M.get(b_rs[b] + i)) & 0x7FFFFFFFu;
+    const uint32_t rs = c.b_rs[b], n = c.b_n[b];
+    for (uint32_t i = tid; i < n; i += NT) {
+      const uint32_t k = L.bits(M.get(rs + i)) & 0x7FFFFFFFu;
       mn = k < mn ? k : mn;
       mx = k > mx ? k : mx;
     }
@@ -842,21 +1094,19 @@ __device__ void encode_one(const EncArgs& a, const sif_enc_desc& d, int ifi, Grp
   }
   __syncthreads();
   if (g.size > 1) {
-    for (int b0 = 0; b0 < B; b0 += 32) {
-      int nb = B - b0 < 32 ? B - b0 : 32;
-      uint64_t* slot = g.slot();
-      // pack (0x7FFFFFFF - min) and max so that a single max-reduction works via sums of
-      // one-hot contributions is not possible; gather explicitly instead
-      if (tid < nb) { slot[tid] = b_min[b0 + tid]; slot[32 + tid] = b_max[b0 + tid]; }
+    for (int b0 = 0; b0 < B; b0 += 64) {
+      const int nb = B - b0 < 64 ? B - b0 : 64;
+      uint64_t* my = g.slot();
+      if (tid < nb) my[tid] = ((uint64_t)(0x7FFFFFFFu - b_min[b0 + tid]) << 32) | b_max[b0 + tid];
       g.sync();
       cg::cluster_group cl = cg::this_cluster();
       if (tid < nb) {
         uint32_t mn = 0x7FFFFFFFu, mx = 0;
         for (uint32_t r = 0; r < g.size; ++r) {
-          uint32_t a0 = (uint32_t)*cl.map_shared_rank(slot + tid, r);
-          uint32_t a1 = (uint32_t)*cl.map_shared_rank(slot + 32 + tid, r);
-          mn = a0 < mn ? a0 : mn;
-          mx = a1 > mx ? a1 : mx;
+          const uint64_t v = *cl.map_shared_rank(my + tid, r);
+          const uint32_t m0 = 0x7FFFFFFFu - (uint32_t)(v >> 32), m1 = (uint32_t)v;
+          mn = m0 < mn ? m0 : mn;
+          mx = m1 > mx ? m1 : mx;
         }
         b_min[b0 + tid] = mn;
         b_max[b0 + tid] = mx;
@@ -865,266 +1115,322 @@ __device__ void encode_one(const EncArgs& a, const sif_enc_desc& d, int ifi, Grp
       __syncthreads();
     }
   }
+  return g;
+}
 
-  // ---- ABQ (quant.py:102-115) / fixed Q (codec.py:180-181, :194-200)
+// ---- Phase G: ABQ (quant.py:102-115) / fixed Q (codec.py:180-181, :194-200)
+template <int NT>
+__device__ __noinline__ Grp phase_abq(Ctx& c, Grp g, Shared& sh) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int B = c.B, meff0 = (int)c.meff[0], q_bit = c.q_bit;
+  const List L = c.L;
+  const Perm M = c.M;
   for (int b = tid; b < B; b += NT) {
-    const int s = b < (int)meff[0] ? 0 : 1;
-    const int j = s ? b - (int)meff[0] : b;
-    const bool empty = b_N[b] == 0;
-    const bool degen = !empty && b_min[b] == b_max[b];
+    const int s = b < meff0 ? 0 : 1;
+    const int j = s ? b - meff0 : b;
+    const bool empty = c.b_N[b] == 0;
+    const bool degen = !empty && c.b_min[b] == c.b_max[b];
     uint32_t q;
-    if (a.mode == SIF_MODE_FIXED) q = a.fixed_q[(s ? a.m_plus : 0) + j];
-    else if (empty) q = (uint32_t)a.q_bit;
+    if (c.mode == SIF_MODE_FIXED) q = c.fixed_q[(s ? c.m_plus : 0) + j];
+    else if (empty) q = (uint32_t)q_bit;
     else if (degen) q = 1;
-    else q = 0;  // to be searched
-    b_q[b] = q;
-    b_act[b] = q == 0 ? 1u : 0u;
-    if (q == 0) b_q[b] = (uint32_t)a.q_bit;
-    const double vmin = (double)__uint_as_float(b_min[b]), vmax = (double)__uint_as_float(b_max[b]);
-    b_or[b] = __ddiv_rn(__dsub_rn(vmax, vmin), (double)((1u << a.q_bit) - 1u));
+    else q = 0;  // searched below
+    c.b_act[b] = q == 0 ? 1u : 0u;
+    c.b_q[b] = q == 0 ? (uint32_t)q_bit : q;
   }
   __syncthreads();
-  if (a.mode != SIF_MODE_FIXED) {
-    for (int q = a.q_bit - 1; q >= 1; --q) {
+  if (c.mode != SIF_MODE_FIXED) {
+    const uint32_t lref = (1u << q_bit) - 1u;
+    const double delta = c.delta;
+    for (int q = q_bit - 1; q >= 1; --q) {
       int any = 0;
-      for (int b = 0; b < B; ++b) any |= (int)b_act[b];
+      for (int b = 0; b < B; ++b) any |= (int)c.b_act[b];
       if (!any) break;
-      const uint32_t lv = (1u << q) - 1u, lref = (1u << a.q_bit) - 1u;
-      const int shift = a.q_bit - q;
-      for (int b = tid; b < B; b += NT) {
-        b_sum[b] = 0;
-        const double vmin = (double)__uint_as_float(b_min[b]), vmax = (double)__uint_as_float(b_max[b]);
-        b_o64[b] = __ddiv_rn(__dsub_rn(vmax, vmin), (double)lv);
-      }
-      __syncthreads();
+      const uint32_t lv = (1u << q) - 1u;
+      const int shift = q_bit - q;
       for (int b = 0; b < B; ++b) {
-        if (!b_act[b]) continue;
-        const double vmin = (double)__uint_as_float(b_min[b]);
-        const double oq = b_o64[b], orf = b_or[b];
+        if (!c.b_act[b]) continue;
+        const double vmin = (double)__uint_as_float(c.b_min[b]), vmax = (double)__uint_as_float(c.b_max[b]);
+        const double rng = __dsub_rn(vmax, vmin);
+        const double orf = __ddiv_rn(rng, (double)lref), oq = __ddiv_rn(rng, (double)lv);
+        const double irf = __drcp_rn(orf), iq = __drcp_rn(oq);
+        const uint32_t rs = c.b_rs[b], n = c.b_n[b];
         uint32_t acc = 0;
-        for (uint32_t i = tid; i < b_n[b]; i += NT) {
-          uint32_t k = L.bits(M.get(b_rs[b] + i)) & 0x7FFFFFFFu;
-          uint32_t cr = quant_code(k, vmin, orf, lref) >> shift;
-          uint32_t cq = quant_code(k, vmin, oq, lv);
+        for (uint32_t i = tid; i < n; i += NT) {
+          const uint32_t k = L.bits(M.get(rs + i)) & 0x7FFFFFFFu;
+          const uint32_t cr = quant_code(k, vmin, orf, irf, lref) >> shift;
+          const uint32_t cq = quant_code(k, vmin, oq, iq, lv);
           acc += cr > cq ? cr - cq : cq - cr;
         }
         acc = __reduce_add_sync(0xFFFFFFFFu, acc);
-        if (lane == 0 && acc) atomicAdd((unsigned long long*)&b_sum[b], (unsigned long long)acc);
+        if (lane == 0) sh.red[wid] = acc;
+        __syncthreads();
+        if (tid == 0) {
+          uint64_t t = 0;
+          for (int w = 0; w < NW; ++w) t += sh.red[w];
+          c.b_sum[b] = t;
+        }
+        __syncthreads();
       }
-      __syncthreads();
       for (int b0 = 0; b0 < B; b0 += 64) {
-        int nb = B - b0 < 64 ? B - b0 : 64;
+        const int nb = B - b0 < 64 ? B - b0 : 64;
         uint64_t* slot = g.slot();
-        if (tid < nb) slot[tid] = b_sum[b0 + tid];
+        if (tid < nb) slot[tid] = c.b_act[b0 + tid] ? c.b_sum[b0 + tid] : 0ull;
         g.allsum(nb, sh.vec, nullptr);
         if (tid < nb) {
-          int b = b0 + tid;
-          if (b_act[b]) {
-            double ds = __ddiv_rn((double)sh.vec[tid], (double)b_N[b]);
-            if (ds > a.delta) b_act[b] = 0;  // first violation stops the descent
-            else { b_q[b] = (uint32_t)q; if (q == 1) b_act[b] = 0; }
+          const int b = b0 + tid;
+          if (c.b_act[b]) {
+            const double ds = __ddiv_rn((double)sh.vec[tid], (double)c.b_N[b]);
+            if (ds > delta) c.b_act[b] = 0;  // first violation stops the descent
+            else { c.b_q[b] = (uint32_t)q; if (q == 1) c.b_act[b] = 0; }
           }
         }
         __syncthreads();
       }
     }
   }
+  return g;
+}
 
-  // ---- layout (codec.py:269-280)
+// ---- Phase H: layout (codec.py:269-280), codes in place, zero fill
+template <int NT>
+__device__ __noinline__ Grp phase_layout(Ctx& c, Grp g, Shared& sh) {
+  const int tid = threadIdx.x;
+  const int B = c.B;
   if (tid == 0) {
-    uint64_t pos = kHeaderBytes + (a.mode == SIF_MODE_FIXED ? (uint64_t)B : 0ull);
+    uint64_t pos = kHeaderBytes + (c.mode == SIF_MODE_FIXED ? (uint64_t)B : 0ull);
     for (int b = 0; b < B; ++b) {
-      b_off[4 * b + 0] = pos;
-      b_off[4 * b + 1] = pos + kBlockMetaBytes;
-      pos += kBlockMetaBytes + 4ull * ((uint64_t)N + 1ull);
-      b_off[4 * b + 2] = pos;
-      pos += (b_N[b] * cb + 7ull) / 8ull;
-      b_off[4 * b + 3] = pos;
-      pos += (b_N[b] * b_q[b] + 7ull) / 8ull;
+      c.b_off[4 * b + 0] = pos;
+      c.b_off[4 * b + 1] = pos + kBlockMetaBytes;
+      pos += kBlockMetaBytes + 4ull * ((uint64_t)c.N + 1ull);
+      c.b_off[4 * b + 2] = pos;
+      pos += (c.b_N[b] * c.cb + 7ull) / 8ull;
+      c.b_off[4 * b + 3] = pos;
+      pos += (c.b_N[b] * c.b_q[b] + 7ull) / 8ull;
     }
-    sh.total_len = pos + kCrcBytes;
+    c.P = pos + kCrcBytes;
   }
   for (int b = tid; b < B; b += NT) {
-    const double vmin = (double)__uint_as_float(b_min[b]), vmax = (double)__uint_as_float(b_max[b]);
-    const bool degen = b_N[b] == 0 || b_min[b] == b_max[b];
-    b_o64[b] = degen ? 1.0 : __ddiv_rn(__dsub_rn(vmax, vmin), (double)((1u << b_q[b]) - 1u));
+    const double vmin = (double)__uint_as_float(c.b_min[b]), vmax = (double)__uint_as_float(c.b_max[b]);
+    const bool degen = c.b_N[b] == 0 || c.b_min[b] == c.b_max[b];
+    c.b_o64[b] = degen ? 1.0 : __ddiv_rn(__dsub_rn(vmax, vmin), (double)((1u << c.b_q[b]) - 1u));
+    c.b_inv[b] = __drcp_rn(c.b_o64[b]);
   }
   __syncthreads();
-  const uint64_t P = sh.total_len;
-  if (P > d.out_cap) {
-    if (g.rank == 0 && tid == 0) { a.status[ifi] = SIF_ERR_CAPACITY; a.out_len[ifi] = P; }
-    return;
+  const uint64_t P = c.P;
+  if (P > c.out_cap) return g;
+  // codes at q* replace the value bits in the kept list (values are no longer needed)
+  const List L = c.L;
+  const Perm M = c.M;
+  for (int b = 0; b < B; ++b) {
+    const double vmin = (double)__uint_as_float(c.b_min[b]);
+    const double o64 = c.b_o64[b], inv = c.b_inv[b];
+    const uint32_t lv = (1u << c.b_q[b]) - 1u;
+    const bool degen = c.b_min[b] == c.b_max[b];
+    const uint32_t rs = c.b_rs[b], n = c.b_n[b];
+    for (uint32_t i = tid; i < n; i += NT) {
+      const uint32_t li = M.get(rs + i);
+      const uint32_t code = degen ? 0u : quant_code(L.bits(li) & 0x7FFFFFFFu, vmin, o64, inv, lv);
+      L.set_bits(li, code);
+    }
   }
-  uint8_t* out = d.out;
-  // ---- zero-fill this CTA's share of the payload
-  {
-    const uint64_t z0 = P * g.rank / g.size, z1 = P * (g.rank + 1) / g.size;
-    uint64_t za = (z0 + 15) & ~15ull, zb = z1 & ~15ull;
-    if (za > zb) { za = z1; zb = z1; }
-    for (uint64_t i = z0 + tid; i < za && i < z1; i += NT) out[i] = 0;
-    for (uint64_t i = zb + tid; i < z1; i += NT) if (i >= za) out[i] = 0;
-    uint4* o4 = reinterpret_cast<uint4*>(out);
-    for (uint64_t i = za / 16 + tid; i < zb / 16; i += NT) o4[i] = make_uint4(0, 0, 0, 0);
-  }
+  uint8_t* out = c.out;
+  const uint64_t z0 = P * g.rank / g.size, z1 = P * (g.rank + 1) / g.size;
+  uint64_t za = (z0 + 15) & ~15ull, zb = z1 & ~15ull;
+  if (za > zb) { za = z1; zb = z1; }
+  for (uint64_t i = z0 + tid; i < za && i < z1; i += NT) out[i] = 0;
+  for (uint64_t i = zb + tid; i < z1; i += NT) if (i >= za) out[i] = 0;
+  uint4* o4 = reinterpret_cast<uint4*>(out);
+  for (uint64_t i = za / 16 + tid; i < zb / 16; i += NT) o4[i] = make_uint4(0, 0, 0, 0);
   __threadfence();
   g.sync();
+  return g;
+}
 
-  // ---- header, Q vector, block meta (codec.py:285-306) by rank 0
+// ---- Phase I: header/meta, row_ptr, MSB-first word packing of cols and codes
+template <int NT>
+__device__ __noinline__ Grp phase_write(Ctx& c, Grp g, Shared& sh) {
+  const int tid = threadIdx.x;
+  const int B = c.B;
+  const uint32_t N = c.N, K = c.K, cb = c.cb;
+  uint8_t* out = c.out;
   if (g.rank == 0) {
     if (tid == 0) {
       uint8_t h[32];
       h[0] = 'S'; h[1] = 'I'; h[2] = 'F'; h[3] = '1';
       h[4] = 1; h[5] = 0;
-      uint32_t f[2] = {N, K};
-      for (int k = 0; k < 4; ++k) { h[6 + k] = (uint8_t)(f[0] >> (8 * k)); h[10 + k] = (uint8_t)(f[1] >> (8 * k)); }
-      uint32_t s32 = __float_as_uint(__double2float_rn(a.s));
-      uint32_t l32 = __float_as_uint(__double2float_rn(a.lam));
-      uint32_t d32 = __float_as_uint(__double2float_rn(a.delta));
+      for (int k = 0; k < 4; ++k) { h[6 + k] = (uint8_t)(N >> (8 * k)); h[10 + k] = (uint8_t)(K >> (8 * k)); }
+      const uint32_t s32 = __float_as_uint(__double2float_rn(c.s));
+      const uint32_t l32 = __float_as_uint(__double2float_rn(c.lam));
+      const uint32_t d32 = __float_as_uint(__double2float_rn(c.delta));
       for (int k = 0; k < 4; ++k) {
         h[14 + k] = (uint8_t)(s32 >> (8 * k));
         h[18 + k] = (uint8_t)(l32 >> (8 * k));
         h[23 + k] = (uint8_t)(d32 >> (8 * k));
       }
-      h[22] = (uint8_t)a.q_bit;
-      h[27] = (uint8_t)a.mode;
-      h[28] = (uint8_t)meff[0]; h[29] = (uint8_t)(meff[0] >> 8);
-      h[30] = (uint8_t)meff[1]; h[31] = (uint8_t)(meff[1] >> 8);
+      h[22] = (uint8_t)c.q_bit;
+      h[27] = (uint8_t)c.mode;
+      h[28] = (uint8_t)c.meff[0]; h[29] = (uint8_t)(c.meff[0] >> 8);
+      h[30] = (uint8_t)c.meff[1]; h[31] = (uint8_t)(c.meff[1] >> 8);
       for (int k = 0; k < 32; ++k) out[k] = h[k];
     }
-    if (a.mode == SIF_MODE_FIXED)
-      for (int b = tid; b < B; b += NT) out[kHeaderBytes + b] = (uint8_t)b_q[b];
+    if (c.mode == SIF_MODE_FIXED)
+      for (int b = tid; b < B; b += NT) out[kHeaderBytes + b] = (uint8_t)c.b_q[b];
     for (int b = tid; b < B; b += NT) {
-      const uint64_t o = b_off[4 * b];
-      out[o] = (uint8_t)b_q[b];
-      st_u32_le_bytes(out, o + 1, __float_as_uint(b_N[b] == 0 ? 1.0f : __double2float_rn(b_o64[b])));
-      st_u32_le_bytes(out, o + 5, b_N[b] == 0 ? 0u : b_min[b]);
-      st_u32_le_bytes(out, o + 9, (uint32_t)b_N[b]);
+      const uint64_t o = c.b_off[4 * b];
+      out[o] = (uint8_t)c.b_q[b];
+      st_u32_le_bytes(out, o + 1, __float_as_uint(c.b_N[b] == 0 ? 1.0f : __double2float_rn(c.b_o64[b])));
+      st_u32_le_bytes(out, o + 5, c.b_N[b] == 0 ? 0u : c.b_min[b]);
+      st_u32_le_bytes(out, o + 9, (uint32_t)c.b_N[b]);
     }
   }
-  // ---- row_ptr (msplit.py:97-100): rows whose start r*K lies in [s0, s1) (+ row N last)
+  phase_mark(c, g, 12);
+  const List L = c.L;
+  const Perm M = c.M;
+  const FastDiv fk = c.fk;
+  // row_ptr (msplit.py:97-100): rows whose start r*K lies in [s0, s1); entry = number of
+  // the block's members (group-wide) with flat index < r*K, by binary search
   {
-    const uint64_t r0 = (s0 + K - 1) / K;
-    uint64_t r1 = (s1 + K - 1) / K;  // exclusive
-    if (r1 > N) r1 = N;
-    const bool last = g.rank == g.size - 1;
-    const uint64_t nr = (r1 > r0 ? r1 - r0 : 0) + (last ? 1 : 0);
-    const uint64_t tot = nr * (uint64_t)B;
-    for (uint64_t w = tid; w < tot; w += NT) {
+    const uint32_t rfirst = (uint32_t)((c.s0 + K - 1) / K);
+    const uint64_t rl = (c.s1 + K - 1) / K;  // exclusive
+    const uint32_t rend = (uint32_t)(rl > N ? N : rl);
+    const uint32_t nr = rend > rfirst ? rend - rfirst : 0;
+    const uint32_t tot = nr * (uint32_t)B;
+    for (uint32_t w = tid; w < tot; w += NT) {
       const int b = (int)(w / nr);
-      const uint64_t rr = w % nr;
-      const uint64_t r = (last && rr == nr - 1) ? (uint64_t)N : r0 + rr;
-      uint32_t val;
-      if (r == N) {
-        val = (uint32_t)b_N[b];
-      } else {
-        const uint64_t bound = r * K;
-        uint32_t lo2 = 0, hi2 = b_n[b];
-        while (lo2 < hi2) {
-          uint32_t mid = (lo2 + hi2) >> 1;
-          if ((uint64_t)L.idx(M.get(b_rs[b] + mid)) < bound) lo2 = mid + 1; else hi2 = mid;
-        }
-        val = (uint32_t)(b_pre[b] + lo2);
+      const uint32_t r = rfirst + (w - (uint32_t)b * nr);
+      const uint32_t bound = r * K;
+      const uint32_t rs = c.b_rs[b];
+      uint32_t lo = 0, hi = c.b_n[b];
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (L.idx(M.get(rs + mid)) < bound) lo = mid + 1; else hi = mid;
       }
-      st_u32_le_bytes(out, b_off[4 * b + 1] + 4ull * r, val);
+      st_u32_le_bytes(out, c.b_off[4 * b + 1] + 4ull * r, (uint32_t)c.b_pre[b] + lo);
     }
+    if (g.rank == g.size - 1)
+      for (int b = tid; b < B; b += NT) st_u32_le_bytes(out, c.b_off[4 * b + 1] + 4ull * N, (uint32_t)c.b_N[b]);
   }
-  // ---- cols / codes: MSB-first bit packing with warp shuffles (bitstream.py:12-30)
+  phase_mark(c, g, 13);
+  // cols / codes (bitstream.py:12-30): each thread packs a group of 32 consecutive fields
+  // (32*w bits) MSB-first into a 64-bit window and emits payload-aligned 32-bit words;
+  // words shared with a neighbouring group/section are merged with atomicOr.
   {
     uint32_t* out32 = reinterpret_cast<uint32_t*>(out);
     for (int b = 0; b < B; ++b) {
-      const uint64_t nloc = b_n[b];
+      const uint32_t nloc = c.b_n[b];
       if (nloc == 0) continue;
-      const uint64_t pre = b_pre[b];
-      const uint64_t gfirst = pre / 32, glast = (pre + nloc - 1) / 32;
-      const double vmin = (double)__uint_as_float(b_min[b]);
-      const double o64 = b_o64[b];
-      const uint32_t qb = b_q[b], lv = (1u << qb) - 1u;
-      const bool degen = b_min[b] == b_max[b];
-      for (int sec = 0; sec < 2; ++sec) {
-        const uint32_t w = sec == 0 ? cb : qb;
-        const uint64_t secbit = 8ull * b_off[4 * b + 2 + sec];
-        const int kmax = (int)(31u / w) + 2 < 33 ? (int)(31u / w) + 2 : 33;
-        for (uint64_t gi = gfirst + wid; gi <= glast; gi += NW) {
-          const uint64_t p0 = gi * 32ull;
-          const uint64_t pp = p0 + lane;
-          const bool valid = pp >= pre && pp < pre + nloc;
-          uint32_t val = 0;
-          if (valid) {
-            uint32_t li = M.get(b_rs[b] + (uint32_t)(pp - pre));
-            if (sec == 0) val = L.idx(li) % K;
-            else val = degen ? 0u : quant_code(L.bits(li) & 0x7FFFFFFFu, vmin, o64, lv);
+      const uint64_t pre = c.b_pre[b];
+      const uint32_t rs = c.b_rs[b];
+      const uint32_t ngrp = (nloc + 31) / 32;
+      for (uint32_t job = tid; job < 2 * ngrp; job += NT) {
+        const int sec = job < ngrp ? 0 : 1;
+        const uint32_t gi = sec ? job - ngrp : job;
+        const uint32_t w = sec == 0 ? cb : c.b_q[b];
+        const uint32_t f0 = gi * 32, f1 = f0 + 32 < nloc ? f0 + 32 : nloc;
+        uint64_t bit = 8ull * c.b_off[4 * b + 2 + sec] + (pre + f0) * (uint64_t)w;  // first bit
+        const uint64_t lo_bit = bit, hi_bit = bit + (uint64_t)(f1 - f0) * w;
+        // window holds bits [wbase, wbase + nacc) MSB-aligned in acc
+        uint64_t wbase = bit & ~31ull;
+        uint64_t acc = 0;
+        uint32_t nacc = (uint32_t)(bit - wbase);
+        for (uint32_t f = f0; f < f1; ++f) {
+          const uint32_t li = M.get(rs + f);
+          const uint32_t v = sec == 0 ? fk.mod(L.idx(li)) : L.bits(li);
+          acc |= (uint64_t)v << (64u - nacc - w);
+          nacc += w;
+          if (nacc >= 32) {
+            const uint32_t word = (uint32_t)(acc >> 32);
+            const uint64_t wa = wbase >> 5;
+            if (wbase >= lo_bit) out32[wa] = bswap32(word);
+            else if (word) atomicOr(out32 + wa, bswap32(word));
+            acc <<= 32;
+            nacc -= 32;
+            wbase += 32;
           }
-          const uint64_t f_lo = (pre > p0 ? pre : p0) - p0;
-          const uint64_t f_hi = ((pre + nloc) < (p0 + 32) ? (pre + nloc) : (p0 + 32)) - p0;
-          const uint64_t Gs = secbit + p0 * w;
-          const uint64_t own_lo = Gs + f_lo * w, own_hi = Gs + f_hi * w;
-          const uint64_t a0w = own_lo >> 5, a1w = (own_hi - 1) >> 5;
-          const uint32_t nwords = (uint32_t)(a1w - a0w + 1);
-          for (uint32_t wb = 0; wb < nwords; wb += 32) {
-            const uint32_t j = wb + lane;
-            const uint64_t W = (a0w + j) * 32ull;
-            const int64_t fstart = W > Gs ? (int64_t)((W - Gs) / w) : 0;
-            uint32_t acc = 0;
-            for (int k = 0; k < kmax; ++k) {
-              const int64_t f = fstart + k;
-              const int src = f < 31 ? (int)f : 31;
-              const uint32_t fv = __shfl_sync(0xFFFFFFFFu, val, src);
-              if (j < nwords && f <= 31) {
-                const int64_t pos = (int64_t)(Gs + (uint64_t)f * w) - (int64_t)W;
-                if (pos < 32 && pos + (int64_t)w > 0) {
-                  const int sh2 = 64 - (int)w - (int)pos;
-                  const uint64_t v64 = sh2 >= 64 ? 0ull : ((uint64_t)fv << sh2);
-                  acc |= (uint32_t)(v64 >> 32);
-                }
-              }
-            }
-            if (j < nwords) {
-              const bool full = W >= own_lo && W + 32 <= own_hi;
-              if (full) out32[a0w + j] = bswap32(acc);
-              else if (acc) atomicOr(out32 + a0w + j, bswap32(acc));
-            }
-          }
+        }
+        if (nacc) {
+          const uint32_t word = (uint32_t)(acc >> 32);
+          const uint64_t wa = wbase >> 5;
+          if (wbase >= lo_bit && wbase + 32 <= hi_bit) out32[wa] = bswap32(word);
+          else if (word) atomicOr(out32 + wa, bswap32(word));
         }
       }
     }
   }
   __threadfence();
   g.sync();
+  return g;
+}
 
-  // ---- CRC-32 over bytes [4, P-4) (codec.py:316), chunked + GF(2) combine
-  {
-    const uint64_t Lc = P - 8;
-    const uint64_t c0 = 4 + Lc * g.rank / g.size, c1 = 4 + Lc * (g.rank + 1) / g.size;
-    const uint64_t n_me = c1 - c0;
-    const uint64_t t0 = c0 + n_me * tid / NT, t1 = c0 + n_me * (tid + 1) / NT;
-    uint32_t raw = crc_raw_range(out, t0, t1, crctab);
-    raw = crc_shift(raw, (P - 4) - t1);
-    raw = warp_xor(raw);
-    uint64_t* slot = g.slot();
-    if (tid == 0) slot[0] = 0;
-    __syncthreads();
-    if (lane == 0) atomicXor((unsigned long long*)&slot[0], (unsigned long long)raw);
-    // xor-combine across the group: use allsum on one-hot-free path (gather explicitly)
-    g.sync();
-    uint32_t total = 0;
-    if (g.size == 1) total = (uint32_t)slot[0];
-    else {
-      cg::cluster_group cl = cg::this_cluster();
-      for (uint32_t r = 0; r < g.size; ++r) total ^= (uint32_t)*cl.map_shared_rank(slot, r);
-    }
-    g.parity ^= 1;
-    if (g.rank == 0 && tid == 0) {
-      const uint32_t crc = crc_finish(total, Lc);
-      st_u32_le_bytes(out, P - 4, crc);
-      a.out_len[ifi] = P;
-      a.status[ifi] = SIF_OK;
-    }
+// ---- Phase J: CRC-32 over bytes [4, P-4) (codec.py:316) on rank 0
+template <int NT>
+__device__ __noinline__ void phase_crc(Ctx& c, Grp g, Shared& sh, uint64_t* out_len, int32_t* status) {
+  if (g.rank != 0) return;
+  const uint64_t P = c.P;
+  const uint32_t raw = c.L.cap * 12u >= (uint32_t)(NT * 64)
+                           ? crc_cta_staged<NT>(c.out, 4, P - 4, c.t4, sh.red, c.L.sb)
+                           : crc_cta_raw<NT>(c.out, 4, P - 4, c.t4, sh.red);
+  if (threadIdx.x == 0) {
+    st_u32_le_bytes(c.out, P - 4, crc_finish(raw, P - 8));
+    if (c.prof) c.prof[(uint64_t)c.ifi * 32 + 15] = gtimer();
+    out_len[c.ifi] = P;
+    status[c.ifi] = SIF_OK;
   }
 }
 
-__global__ void __launch_bounds__(NT, 1) sif_encode_kernel(EncArgs a) {
+// ---------------------------------------------------------------------------------------
+template <int DT, int NT>
+__device__ __forceinline__ void encode_one(const EncArgs& a, Ctx& c, Grp g, Shared& sh) {
+  phase_mark(c, g, 0);
+  g = phase_sample<DT, NT>(c, g, sh);
+  phase_mark(c, g, 1);
+  g = phase_stream<DT, NT>(c, g, sh);
+  if (c.nonfinite) {
+    if (g.rank == 0 && threadIdx.x == 0) { a.status[c.ifi] = SIF_ERR_NONFINITE; if (!a.atkf_only) a.out_len[c.ifi] = 0; }
+    return;
+  }
+  phase_mark(c, g, 2);
+  g = phase_select<NT>(c, g, sh);
+  phase_mark(c, g, 4);
+  g = phase_kept<NT>(c, g, sh);
+  if (a.atkf_only) {
+    int64_t* out = a.kept_out + a.kept_off[c.ifi] + c.kept_pre;
+    for (uint32_t i = threadIdx.x; i < c.nkept; i += NT) out[i] = (int64_t)c.L.idx(i);
+    if (g.rank == 0 && threadIdx.x == 0) {
+      a.tau3[3 * c.ifi + 0] = c.tau;
+      a.tau3[3 * c.ifi + 1] = c.tau_p;
+      a.tau3[3 * c.ifi + 2] = c.tau_m;
+      a.status[c.ifi] = SIF_OK;
+    }
+    return;
+  }
+  phase_mark(c, g, 6);
+  g = phase_cuts<NT>(c, g, sh);
+  phase_mark(c, g, 7);
+  g = phase_members<NT>(c, g, sh);
+  phase_mark(c, g, 8);
+  g = phase_minmax<NT>(c, g, sh);
+  phase_mark(c, g, 9);
+  g = phase_abq<NT>(c, g, sh);
+  phase_mark(c, g, 10);
+  g = phase_layout<NT>(c, g, sh);
+  if (c.P > c.out_cap) {
+    if (g.rank == 0 && threadIdx.x == 0) { a.status[c.ifi] = SIF_ERR_CAPACITY; a.out_len[c.ifi] = c.P; }
+    return;
+  }
+  phase_mark(c, g, 11);
+  g = phase_write<NT>(c, g, sh);
+  phase_mark(c, g, 14);
+  phase_crc<NT>(c, g, sh, a.out_len, a.status);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, (NT == 512 ? 1 : 2)) sif_encode_kernel(EncArgs a) {
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ Shared sh;
+  __shared__ Ctx c;
   __shared__ uint64_t slots[128];
   Grp g;
   {
@@ -1137,10 +1443,62 @@ __global__ void __launch_bounds__(NT, 1) sif_encode_kernel(EncArgs a) {
   g.hpar = 0;
   const int ifi = blockIdx.x / g.size;
   if (ifi >= a.n) return;
-  const sif_enc_desc d = a.descs[ifi];
-  if (d.dtype == SIF_DTYPE_BF16) encode_one<SIF_DTYPE_BF16>(a, d, ifi, g, dsm, sh);
-  else encode_one<SIF_DTYPE_F32>(a, d, ifi, g, dsm, sh);
+  if (threadIdx.x == 0) {
+    const sif_enc_desc d = a.descs[ifi];
+    c.x = d.x; c.out = d.out; c.out_cap = d.out_cap; c.seed = d.seed;
+    c.N = d.rows; c.K = d.cols; c.dtype = d.dtype; c.cb = col_bits(d.cols);
+    c.T = (uint64_t)d.rows * d.cols;
+    c.s0 = c.T * g.rank / g.size;
+    c.s1 = c.T * (g.rank + 1) / g.size;
+    c.kk = keep_count(a.s, c.T);
+    c.fk.init(d.cols);
+    c.s = a.s; c.lam = a.lam; c.delta = a.delta;
+    c.m_plus = a.m_plus; c.m_minus = a.m_minus; c.q_bit = a.q_bit; c.mode = a.mode;
+    c.atkf_only = a.atkf_only; c.maxb = a.maxb; c.ifi = ifi;
+    c.fixed_q = a.fixed_q;
+    c.prof = a.prof;
+    const int maxb = a.maxb, NW = NT / 32;
+    c.t4 = reinterpret_cast<uint32_t*>(dsm);
+    c.scratch = c.t4 + 1024;
+    uint8_t* p = reinterpret_cast<uint8_t*>(c.scratch + a.scratch_words);
+    c.b_sum = reinterpret_cast<uint64_t*>(p); p += 8ull * maxb;
+    c.b_pre = reinterpret_cast<uint64_t*>(p); p += 8ull * maxb;
+    c.b_N = reinterpret_cast<uint64_t*>(p); p += 8ull * maxb;
+    c.b_off = reinterpret_cast<uint64_t*>(p); p += 8ull * 4 * maxb;
+    c.b_o64 = reinterpret_cast<double*>(p); p += 8ull * maxb;
+    c.b_inv = reinterpret_cast<double*>(p); p += 8ull * maxb;
+    c.b_n = reinterpret_cast<uint32_t*>(p); p += 4ull * maxb;
+    c.b_rs = reinterpret_cast<uint32_t*>(p); p += 4ull * maxb;
+    c.b_min = reinterpret_cast<uint32_t*>(p); p += 4ull * maxb;
+    c.b_max = reinterpret_cast<uint32_t*>(p); p += 4ull * maxb;
+    c.b_q = reinterpret_cast<uint32_t*>(p); p += 4ull * maxb;
+    c.b_act = reinterpret_cast<uint32_t*>(p); p += 4ull * maxb;
+    c.cut_key = reinterpret_cast<uint32_t*>(p); p += 4ull * maxb;
+    c.cut_idx = reinterpret_cast<uint32_t*>(p); p += 4ull * maxb;
+    c.wcnt = reinterpret_cast<uint32_t*>(p); p += 4ull * NW * maxb;
+    c.woff = reinterpret_cast<uint32_t*>(p); p += 4ull * NW * maxb;
+    p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+    const uint32_t cap = (uint32_t)a.cap;
+    uint8_t* spill = a.spill + a.spill_stride * ((uint64_t)ifi * g.size + g.rank);
+    const uint64_t slice = c.s1 - c.s0;
+    const uint64_t spill_n = slice > cap ? slice - cap : 0;
+    c.L.sb = reinterpret_cast<uint32_t*>(p);
+    c.L.si = c.L.sb + cap;
+    c.L.gb = reinterpret_cast<uint32_t*>(spill);
+    c.L.gi = c.L.gb + spill_n;
+    c.L.cap = cap;
+    c.M.s = c.L.si + cap;
+    c.M.g = c.L.gi + spill_n;
+    c.M.cap = cap;
+  }
+  for (int i = threadIdx.x; i < 1024; i += NT) reinterpret_cast<uint32_t*>(dsm)[i] = (&kCrcTab4[0][0])[i];
+  __syncthreads();
+  if (c.dtype == SIF_DTYPE_BF16) encode_one<SIF_DTYPE_BF16, NT>(a, c, g, sh);
+  else encode_one<SIF_DTYPE_F32, NT>(a, c, g, sh);
   if (g.size > 1) cg::this_cluster().sync();  // keep DSMEM alive until all peers are done
 }
+
+template __global__ void sif_encode_kernel<256>(EncArgs);
+template __global__ void sif_encode_kernel<512>(EncArgs);
 
 }  // namespace sif

@@ -23,19 +23,34 @@ inline uint64_t up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 
 int check_cuda(cudaError_t e) { return e == cudaSuccess ? SIF_OK : SIF_ERR_CUDA; }
 
-int choose_cluster(uint64_t tmax) {
-  const char* env = getenv("SIF_CLUSTER");
-  if (env && *env) {
-    int g = atoi(env);
-    if (g == 1 || g == 2 || g == 4 || g == 8 || g == 16) return g;
+// Launch shape per size class: cluster size G (CTAs per IF) and threads per CTA.
+// Overridable with SIF_CLUSTER / SIF_NT for tuning experiments.
+void choose_shape(uint64_t tmax, int* G, int* NT) {
+  int g = 1, nt = 256;
+  if (tmax > 65536) { g = 2; nt = 512; }
+  if (tmax > (1u << 20)) { g = 8; nt = 512; }
+  const char* e1 = getenv("SIF_CLUSTER");
+  if (e1 && *e1) {
+    const int v = atoi(e1);
+    if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) g = v;
   }
-  (void)tmax;
-  return 1;
+  const char* e2 = getenv("SIF_NT");
+  if (e2 && *e2) {
+    const int v = atoi(e2);
+    if (v == 256 || v == 512) nt = v;
+  }
+  *G = g;
+  *NT = nt;
 }
 
-uint64_t enc_block_bytes(int maxb) {
-  // b_sum, b_pre, b_N, b_off x4, b_o64, b_or (u64) + 8 u32 arrays + wcnt/woff
-  return (uint64_t)maxb * (8 * 3 + 8 * 4 + 8 * 2 + 4 * 8) + 2ull * sif::NW * 4 * maxb + 64;
+uint64_t enc_block_bytes(int maxb, int nt) {
+  // 9 u64 arrays (b_sum, b_pre, b_N, b_off x4, b_o64, b_inv) + 8 u32 arrays + wcnt/woff
+  return (uint64_t)maxb * (8 * 9 + 4 * 8) + 2ull * (nt / 32) * 4 * maxb + 64;
+}
+
+uint64_t enc_scratch_words(int G) {
+  const uint64_t sel = 2ull * sif::HB + 4ull * sif::GCAP * (G > 1 ? 2 : 1);
+  return std::max<uint64_t>(8192, sel);
 }
 
 }  // namespace
@@ -115,17 +130,19 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
     tmax = std::max(tmax, T);
     kmax = std::max(kmax, sif::keep_count(c->s, T));
   }
-  const int G = choose_cluster(tmax);
+  int G, NT;
+  choose_shape(tmax, &G, &NT);
   const uint64_t kk = std::max<uint64_t>(1, kmax);
   const int maxb = (int)(std::min<uint64_t>(c->m_plus, kk) + std::min<uint64_t>(c->m_minus, kk));
-  const uint64_t fixed = 1024 + (uint64_t)(G > 1 ? 2 : 1) * sif::MAXT * sif::HB * 4 + enc_block_bytes(maxb) + 16;
-  if (fixed + 12ull * 256 > (uint64_t)kSmemBudget) return SIF_ERR_CONFIG;  // too many blocks
+  const uint64_t budget = NT == 512 ? (uint64_t)kSmemBudget : (uint64_t)(113 * 1024 - 3 * 1024);
+  const uint64_t fixed = 4096 + 4 * enc_scratch_words(G) + enc_block_bytes(maxb, NT) + 16;
+  if (fixed + 12ull * 256 > budget) return SIF_ERR_CONFIG;  // too many blocks for shared memory
   const uint64_t slice = (tmax + G - 1) / G;
-  uint64_t cap = ((uint64_t)kSmemBudget - fixed) / 12;
-  cap = std::min<uint64_t>(cap, up(slice, 32));
+  uint64_t cap = (budget - fixed) / 12;
+  cap = std::min<uint64_t>(cap, up(slice, 32)) & ~31ull;  // multiple of 32: 16-byte aligned sub-arrays
   p->n = n;
   p->cluster = G;
-  p->threads = sif::NT;
+  p->threads = NT;
   p->cap_smem = (int32_t)cap;
   p->smem_bytes = (int32_t)(fixed + 12 * cap);
   p->max_blocks = maxb;
@@ -175,23 +192,26 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   a.spill_stride = (uint64_t)p->tiles * 256;
   a.cap = p->cap_smem;
   a.maxb = p->max_blocks;
+  a.scratch_words = (int)enc_scratch_words(p->cluster);
   a.out_len = out_len;
   a.status = status;
   a.kept_out = kept;
   a.kept_off = reinterpret_cast<const uint64_t*>(w + p->ws_aux_off + up((uint64_t)c->m_plus + c->m_minus, 256));
   a.tau3 = tau3;
-  if (check_cuda(cudaFuncSetAttribute(sif::sif_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem_bytes)))
+  a.prof = reinterpret_cast<uint64_t*>(getenv("SIF_PROF_PTR") ? strtoull(getenv("SIF_PROF_PTR"), nullptr, 0) : 0ull);
+  auto kfn = p->threads == 512 ? sif::sif_encode_kernel<512> : sif::sif_encode_kernel<256>;
+  if (check_cuda(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem_bytes)))
     return SIF_ERR_CUDA;
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3((unsigned)(p->n * p->cluster));
-  cfg.blockDim = dim3(sif::NT);
+  cfg.blockDim = dim3((unsigned)p->threads);
   cfg.dynamicSmemBytes = (size_t)p->smem_bytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   if (p->cluster > 1) {
     if (p->cluster > 8)
-      cudaFuncSetAttribute(sif::sif_encode_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = (unsigned)p->cluster;
     attr[0].val.clusterDim.y = 1;
@@ -199,7 +219,7 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  if (check_cuda(cudaLaunchKernelEx(&cfg, sif::sif_encode_kernel, a))) return SIF_ERR_CUDA;
+  if (check_cuda(cudaLaunchKernelEx(&cfg, kfn, a))) return SIF_ERR_CUDA;
   return check_cuda(cudaGetLastError());
 }
 
@@ -274,6 +294,7 @@ int sif_dec_plan(const sif_dec_desc* d, int n, sif_plan* p) {
   p->ws_spill_off = off;  // tiles, then accumulators
   off += up(sizeof(sif::DecTile) * std::max<uint64_t>(ntiles, 1), 256);
   off += up(16ull * std::max(n, 1), 256);
+  off += up(4ull * std::max(n, 1), 256);  // tiles per stream
   p->ws_bytes = off;
   return SIF_OK;
 }
@@ -288,17 +309,20 @@ int sif_dec_upload(const sif_plan* p, const sif_dec_desc* d, void* ws, void* str
   if (check_cuda(cudaMemcpyAsync(w + p->ws_desc_off, d, sizeof(sif_dec_desc) * p->n, cudaMemcpyHostToDevice, s)))
     return SIF_ERR_CUDA;
   std::vector<sif::DecTile> tiles;
+  std::vector<uint32_t> per((size_t)p->n, 0);
   tiles.reserve((size_t)p->tiles);
   for (int i = 0; i < p->n; ++i) {
     const uint32_t rows = d[i].rows, cols = d[i].cols;
     if (rows == 0 || cols == 0) {
       tiles.push_back({(uint32_t)i, 0, 1, 0, 0, 0, 0, 0});
+      per[i] = 1;
       continue;
     }
     const uint32_t kc = std::min<uint32_t>(cols, kDecTileElems);
     const uint32_t r = std::max<uint32_t>(1, kDecTileElems / kc);
     const uint32_t nr = (rows + r - 1) / r, nc = (cols + kc - 1) / kc;
     const uint32_t nt = nr * nc;
+    per[i] = nt;
     uint32_t ti = 0;
     for (uint32_t a = 0; a < nr; ++a)
       for (uint32_t b = 0; b < nc; ++b, ++ti)
@@ -311,6 +335,8 @@ int sif_dec_upload(const sif_plan* p, const sif_dec_desc* d, void* ws, void* str
   if (check_cuda(cudaMemcpyAsync(tile_ptr, tiles.data(), sizeof(sif::DecTile) * tiles.size(), cudaMemcpyHostToDevice, s)))
     return SIF_ERR_CUDA;
   if (check_cuda(cudaMemsetAsync(acc_ptr, 0, 16ull * p->n, s))) return SIF_ERR_CUDA;
+  uint8_t* per_ptr = acc_ptr + up(16ull * p->n, 256);
+  if (check_cuda(cudaMemcpyAsync(per_ptr, per.data(), 4ull * p->n, cudaMemcpyHostToDevice, s))) return SIF_ERR_CUDA;
   return SIF_OK;
 }
 
@@ -332,11 +358,12 @@ int sif_dec_run(const sif_plan* p, int parse_only, void* ws, int32_t* status, vo
   a.tile_elems = kDecTileElems;
   a.rpc_cap = kDecRpcCap;
   a.status = status;
+  a.tiles_per_if = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(a.acc) + up(16ull * p->n, 256));
   sif::sif_parse_kernel<<<(p->n + 127) / 128, 128, 0, s>>>(a);
   if (check_cuda(cudaGetLastError())) return SIF_ERR_CUDA;
   if (check_cuda(cudaFuncSetAttribute(sif::sif_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem_bytes)))
     return SIF_ERR_CUDA;
-  sif::sif_scatter_kernel<<<p->tiles, sif::DNT, p->smem_bytes, s>>>(a);
+  sif::sif_scatter_kernel<<<p->tiles + p->n, sif::DNT, p->smem_bytes, s>>>(a);
   return check_cuda(cudaGetLastError());
 }
 
