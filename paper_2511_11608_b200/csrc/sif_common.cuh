@@ -64,10 +64,10 @@ __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 
 // zlib.crc32(m) = raw(m) ^ (0xFFFFFFFF * x^(8|m|)) ^ 0xFFFFFFFF.
 __device__ __forceinline__ uint32_t crc_mult(uint32_t a, uint32_t b) {
   uint32_t p = 0;
-#pragma unroll 4
+#pragma unroll
   for (int i = 31; i >= 0; --i) {
-    if ((a >> i) & 1u) p ^= b;
-    b = (b >> 1) ^ ((b & 1u) ? kCrcPoly : 0u);
+    p ^= b & (0u - ((a >> i) & 1u));
+    b = (b >> 1) ^ (kCrcPoly & (0u - (b & 1u)));
   }
   return p;
 }
@@ -159,35 +159,44 @@ __device__ uint32_t crc_cta_raw(const uint8_t* base, uint64_t b0, uint64_t b1, c
   return r;
 }
 
-// Same as crc_cta_raw but each round of 64*NT bytes is first staged into shared memory
-// with coalesced loads (one memory round trip per round); chunks are 64 bytes, so the
-// combine multipliers are x^(8*64*2^k) = kX2n[9+k].  stage: >= 16*NT u32.
+// Raw CRC of [b0, b1) by all NT threads.  Each round of 64*NT bytes (aligned to b1) is
+// staged into shared memory with coalesced loads; every thread CRCs one 64-byte chunk and
+// shifts it to the round end with one multiply by kCrcShift64[NT-1-t] (independent across
+// threads), then an XOR reduction; rounds combine with x^(8*64*NT) = kX2n[9 + log2 NT].
+// stage: >= 16*NT u32 of shared memory; red: >= NT/32 + 1 u32.
 template <int NT>
 __device__ uint32_t crc_cta_staged(const uint8_t* base, uint64_t b0, uint64_t b1, const uint32_t* t4, uint32_t* red,
                                    uint32_t* stage) {
   constexpr int NW = NT / 32;
-  constexpr int LOGNW = NW >= 16 ? 4 : NW >= 8 ? 3 : NW >= 4 ? 2 : NW >= 2 ? 1 : 0;
+  constexpr int LOGNT = NT >= 1024 ? 10 : NT >= 512 ? 9 : NT >= 256 ? 8 : NT >= 128 ? 7 : NT >= 64 ? 6 : 5;
   constexpr int64_t L = 64, SPAN = L * NT, WORDS = SPAN / 4;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint64_t n = b1 > b0 ? b1 - b0 : 0;
   const int64_t rounds = (int64_t)((n + SPAN - 1) / SPAN);
   const uint32_t* gw = reinterpret_cast<const uint32_t*>(base);
+  const uint32_t myshift = kCrcShift64[NT - 1 - tid];
   uint32_t total = 0;
   for (int64_t q = rounds - 1; q >= 0; --q) {
     const int64_t rs = (int64_t)b1 - SPAN * (q + 1);  // byte address of stage[0]
     const int64_t fl = rs >= 0 ? rs / 4 : -((-rs + 3) / 4);
     const uint32_t sh8 = (uint32_t)(rs - 4 * fl) * 8u;
-    for (int64_t j = tid; j < WORDS; j += NT) {
-      // bytes [rs + 4j, rs + 4j + 4): funnel of two aligned words; bytes before b0 are zero
+    // 16 words per thread, loads issued together (one memory round trip per round)
+    uint32_t lov[WORDS / NT], hiv[WORDS / NT];
+#pragma unroll
+    for (int k = 0; k < WORDS / NT; ++k) {
+      const int64_t j = tid + (int64_t)k * NT;
       const int64_t a = rs + 4 * j;
-      uint32_t v = 0;
-      if (a + 4 > (int64_t)b0) {
-        const int64_t w0 = fl + j;
-        const uint32_t lo = (w0 >= 0 && 4 * w0 + 4 > (int64_t)b0) ? __ldcg(gw + w0) : 0u;
-        const uint32_t hi = (sh8 && 4 * (w0 + 1) < (int64_t)b1) ? __ldcg(gw + w0 + 1) : 0u;
-        v = sh8 ? __funnelshift_r(lo, hi, sh8) : lo;
-        if (a < (int64_t)b0) v &= 0xFFFFFFFFu << (8u * (uint32_t)((int64_t)b0 - a));
-      }
+      const int64_t w0 = fl + j;
+      lov[k] = (a + 4 > (int64_t)b0 && w0 >= 0 && 4 * w0 + 4 > (int64_t)b0) ? __ldcg(gw + w0) : 0u;
+      hiv[k] = (a + 4 > (int64_t)b0 && sh8 && 4 * (w0 + 1) < (int64_t)b1) ? __ldcg(gw + w0 + 1) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < WORDS / NT; ++k) {
+      const int64_t j = tid + (int64_t)k * NT;
+      const int64_t a = rs + 4 * j;
+      uint32_t v = sh8 ? __funnelshift_r(lov[k], hiv[k], sh8) : lov[k];
+      if (a + 4 <= (int64_t)b0) v = 0;
+      else if (a < (int64_t)b0) v &= 0xFFFFFFFFu << (8u * (uint32_t)((int64_t)b0 - a));
       stage[j] = v;
     }
     __syncthreads();
@@ -198,21 +207,15 @@ __device__ uint32_t crc_cta_staged(const uint8_t* base, uint64_t b0, uint64_t b1
       const uint32_t x = w[k] ^ c;
       c = t4[768 + (x & 0xFFu)] ^ t4[512 + ((x >> 8) & 0xFFu)] ^ t4[256 + ((x >> 16) & 0xFFu)] ^ t4[x >> 24];
     }
-#pragma unroll 1
-    for (int k = 0; k < 5; ++k) {
-      const uint32_t v2 = __shfl_down_sync(0xFFFFFFFFu, c, 1 << k);
-      if ((lane & ((2 << k) - 1)) == 0) c = crc_mult(c, kX2n[9 + k]) ^ v2;
-    }
+    if (c) c = crc_mult(myshift, c);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c ^= __shfl_xor_sync(0xFFFFFFFFu, c, o);
     if (lane == 0) red[wid] = c;
     __syncthreads();
-    if (wid == 0) {
-      c = lane < NW ? red[lane] : 0u;
-#pragma unroll 1
-      for (int k = 0; k < LOGNW; ++k) {
-        const uint32_t v2 = __shfl_down_sync(0xFFFFFFFFu, c, 1 << k);
-        if ((lane & ((2 << k) - 1)) == 0) c = crc_mult(c, kX2n[14 + k]) ^ v2;
-      }
-      if (lane == 0) total = crc_mult(total, kX2n[9 + 5 + LOGNW]) ^ c;
+    if (tid == 0) {
+      uint32_t rq = 0;
+      for (int k = 0; k < NW; ++k) rq ^= red[k];
+      total = crc_mult(total, kX2n[9 + LOGNT]) ^ rq;
     }
     __syncthreads();
   }
@@ -306,6 +309,35 @@ __device__ __forceinline__ uint64_t block_excl_scan_u64(uint64_t v, uint64_t* sc
   }
   __syncthreads();
   uint64_t r = scratch[wid] + x - v;
+  *total = scratch[32];
+  __syncthreads();
+  return r;
+}
+
+// Block-wide exclusive scan of a u32; total in *total.  scratch >= 33 u32 in smem.
+__device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* scratch, uint32_t* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) scratch[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    const uint32_t t = lane < nw ? scratch[lane] : 0u;
+    uint32_t s = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < nw) scratch[lane] = s - t;
+    if (lane == 31) scratch[32] = s;
+  }
+  __syncthreads();
+  const uint32_t r = scratch[wid] + x - v;
   *total = scratch[32];
   __syncthreads();
   return r;

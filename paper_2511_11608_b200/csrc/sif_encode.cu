@@ -65,8 +65,8 @@ struct List {
   uint32_t* gb;
   uint32_t* gi;
   uint32_t cap;
-  __device__ __forceinline__ uint32_t bits(uint32_t i) const { return i < cap ? sb[i] : __ldcg(gb + (i - cap)); }
-  __device__ __forceinline__ uint32_t idx(uint32_t i) const { return i < cap ? si[i] : __ldcg(gi + (i - cap)); }
+  __device__ __forceinline__ uint32_t bits(uint32_t i) const { return *(i < cap ? sb + i : gb + (i - cap)); }
+  __device__ __forceinline__ uint32_t idx(uint32_t i) const { return *(i < cap ? si + i : gi + (i - cap)); }
   __device__ __forceinline__ void set(uint32_t i, uint32_t b, uint32_t x) const {
     if (i < cap) { sb[i] = b; si[i] = x; }
     else { __stcg(gb + (i - cap), b); __stcg(gi + (i - cap), x); }
@@ -79,7 +79,7 @@ struct Perm {
   uint32_t* s;
   uint32_t* g;
   uint32_t cap;
-  __device__ __forceinline__ uint32_t get(uint32_t i) const { return i < cap ? s[i] : __ldcg(g + (i - cap)); }
+  __device__ __forceinline__ uint32_t get(uint32_t i) const { return *(i < cap ? s + i : g + (i - cap)); }
   __device__ __forceinline__ void set(uint32_t i, uint32_t v) const {
     if (i < cap) s[i] = v; else __stcg(g + (i - cap), v);
   }
@@ -473,163 +473,163 @@ __device__ __forceinline__ uint32_t load_bits(const void* x, uint64_t e) {
 // ---------------------------------------------------------------------------------------
 // Phase A: stream the slice [s0, s1) once; counts + stable candidate compaction.
 struct Counts {
-  uint32_t ge_lo, ge_hi, maxkey;
+  uint32_t maxkey;
 };
 
-template <int DT, int U, int VEC>
-__device__ __forceinline__ void load_chunk(const void* x, uint64_t T, uint64_t s0, uint64_t s1, uint64_t base,
-                                           int nt, uint32_t (&bv)[U][VEC], uint32_t (&mask)[U]) {
+// One pass over the slice: max |x| key (NaN/Inf detection, atkf.py:49-51) and the stable
+// compaction of candidates (|x| >= lo_p for x >= 0, |x| >= lo_n for x < 0), in flat order.
+// Each thread owns 16 contiguous elements per chunk (4 x 128-bit loads for fp32, 2 for
+// bf16); the next chunk is prefetched into registers while the current one is compacted.
+// ASYM: lambda > 0 thresholds differ by sign.
+template <int DT, int NT, bool ASYM>
+__device__ __forceinline__ void classify_store(const uint32_t (&v)[16], uint32_t valid, uint32_t e0, uint32_t lo_p,
+                                               uint32_t lo_n, const List& L, uint32_t* scan, uint32_t& ncand,
+                                               uint32_t& mk) {
+  uint32_t m = 0;
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const uint64_t e0 = base + ((uint64_t)u * nt + threadIdx.x) * VEC;
-    if (e0 >= s0 && e0 + VEC <= s1) {
-      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(x) +
-                                                            e0 * (DT == SIF_DTYPE_F32 ? 4 : 2)));
-      if (DT == SIF_DTYPE_F32) {
-        bv[u][0] = v.x; bv[u][1 % VEC] = v.y; bv[u][2 % VEC] = v.z; bv[u][3 % VEC] = v.w;
-      } else {
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  for (int j = 0; j < 16; ++j) {
+    const uint32_t key = v[j] & 0x7FFFFFFFu;
+    const bool in = (valid >> j) & 1u;
+    mk = max(mk, in ? key : 0u);
+    const uint32_t thr = ASYM ? ((v[j] >> 31) ? lo_n : lo_p) : lo_p;
+    m |= (in && key >= thr) ? (1u << j) : 0u;
+  }
+  uint32_t tot;
+  const uint32_t ex = block_excl_scan_u32(__popc(m), scan, &tot);
+  uint32_t off = ncand + ex;
+  if (ncand + tot <= L.cap) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          bv[u][(2 * k) % VEC] = w[k] << 16;
-          bv[u][(2 * k + 1) % VEC] = w[k] & 0xFFFF0000u;
-        }
-      }
-      mask[u] = (1u << VEC) - 1u;
-    } else {
-      mask[u] = 0;
+    for (int j = 0; j < 16; ++j)
+      if ((m >> j) & 1u) { L.sb[off] = v[j]; L.si[off] = e0 + j; ++off; }
+  } else {
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) {
-        const uint64_t e = e0 + j;
-        bv[u][j] = 0;
-        if (e >= s0 && e < s1 && e < T) {
-          bv[u][j] = load_bits<DT>(x, e);
-          mask[u] |= 1u << j;
-        }
-      }
+    for (int j = 0; j < 16; ++j)
+      if ((m >> j) & 1u) { L.set(off, v[j], e0 + j); ++off; }
+  }
+  ncand += tot;
+}
+
+template <int DT>
+__device__ __forceinline__ void load16(const void* x, uint32_t e, uint32_t (&v)[16]) {
+  if (DT == SIF_DTYPE_F32) {
+    const uint4* p = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(x) + e);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint4 q = __ldcs(p + k);
+      v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
+    }
+  } else {
+    const uint4* p = reinterpret_cast<const uint4*>(reinterpret_cast<const unsigned short*>(x) + e);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const uint4 q = __ldcs(p + k);
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { v[8 * k + 2 * i] = w[i] << 16; v[8 * k + 2 * i + 1] = w[i] & 0xFFFF0000u; }
     }
   }
 }
 
-// FITS: the whole slice fits in the shared-memory list (no spill branch per store).
-// ASYM: lambda > 0 thresholds differ by sign and |x| >= lo must be counted separately.
-template <int DT, int NT, bool FITS, bool ASYM>
-__device__ __noinline__ void stream_pass_t(const void* x, uint64_t T, uint64_t s0, uint64_t s1, uint32_t lo_p, uint32_t lo_n,
-                              uint32_t lo_cnt, uint32_t hi_cnt, const List& L, Shared& sh, Counts& c) {
-  constexpr int VEC = DT == SIF_DTYPE_F32 ? 4 : 8;
-  constexpr int U = DT == SIF_DTYPE_F32 ? 4 : 2;
-  const uint64_t CH = (uint64_t)NT * VEC * U;
-  const uint64_t a0 = s0 - (s0 % VEC);
-  uint32_t ncand = 0;
-  uint32_t ge_lo = 0, ge_hi = 0, mk = 0;
-  uint32_t cur[U][VEC], mcur[U];
-  if (a0 < s1) load_chunk<DT, U, VEC>(x, T, s0, s1, a0, NT, cur, mcur);
-  for (uint64_t base = a0; base < s1; base += CH) {
-    uint32_t nxt[U][VEC], mnxt[U];
-    const bool more = base + CH < s1;
-    if (more) load_chunk<DT, U, VEC>(x, T, s0, s1, base + CH, NT, nxt, mnxt);
-    uint64_t packed = 0;
-    uint32_t cm[U];
+template <int DT, int NT, bool ASYM>
+__device__ __noinline__ void stream_pass_t(const void* x, uint32_t s0, uint32_t s1, uint32_t lo_p, uint32_t lo_n,
+                                           const List L, Shared& sh, Counts& c) {
+  const uint32_t tid = threadIdx.x;
+  uint32_t* scan = reinterpret_cast<uint32_t*>(sh.scan);
+  const uint32_t a0 = min(s1, (s0 + 15u) & ~15u), a1 = max(a0, s1 & ~15u);
+  uint32_t ncand = 0, mk = 0;
+  uint32_t v[16];
+  // ragged head [s0, a0): at most 15 elements, one per thread (flat order kept)
+  if (a0 > s0) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      uint32_t m = 0;
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) {
-        const uint32_t b = cur[u][j], key = b & 0x7FFFFFFFu;
-        const bool in = (mcur[u] >> j) & 1u;
-        mk = in && key > mk ? key : mk;
-        ge_hi += (in && key >= hi_cnt) ? 1u : 0u;
-        if (ASYM) {
-          ge_lo += (in && key >= lo_cnt) ? 1u : 0u;
-          m |= (in && key >= ((b >> 31) ? lo_n : lo_p)) ? (1u << j) : 0u;
-        } else {
-          m |= (in && key >= lo_p) ? (1u << j) : 0u;
-        }
-      }
-      cm[u] = m;
-      packed |= (uint64_t)__popc(m) << (16 * u);
-    }
-    uint64_t tot;
-    const uint64_t ex = block_excl_scan_u64(packed, sh.scan, &tot);
-    uint32_t run = ncand;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      uint32_t off = run + (uint32_t)((ex >> (16 * u)) & 0xFFFFull);
-      const uint32_t e0 = (uint32_t)(base + ((uint64_t)u * NT + threadIdx.x) * VEC);
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) {
-        if ((cm[u] >> j) & 1u) {
-          if (FITS) { L.sb[off] = cur[u][j]; L.si[off] = e0 + j; }
-          else {
-            const bool sm = off < L.cap;
-            uint32_t* pb = sm ? L.sb + off : L.gb + (off - L.cap);
-            uint32_t* px = sm ? L.si + off : L.gi + (off - L.cap);
-            *pb = cur[u][j];
-            *px = e0 + j;
-          }
-          ++off;
-        }
-      }
-      run += (uint32_t)((tot >> (16 * u)) & 0xFFFFull);
-    }
-    ncand = run;
+    for (int j = 0; j < 16; ++j) v[j] = 0;
+    const uint32_t e = s0 + tid;
+    uint32_t valid = 0;
+    if (e < a0) { v[0] = load_bits<DT>(x, e); valid = 1; }
+    classify_store<DT, NT, ASYM>(v, valid, e, lo_p, lo_n, L, scan, ncand, mk);
+  }
+  const uint32_t CH = NT * 16u;
+  uint32_t nx[16];
+  if (a0 < a1 && a0 + tid * 16u < a1) load16<DT>(x, a0 + tid * 16u, v);
+  for (uint32_t base = a0; base < a1; base += CH) {
+    const uint32_t e = base + tid * 16u;
+    const uint32_t en = e + CH;
+    const bool more = base + CH < a1;
+    if (more && en < a1) load16<DT>(x, en, nx);
+    classify_store<DT, NT, ASYM>(v, e < a1 ? 0xFFFFu : 0u, e, lo_p, lo_n, L, scan, ncand, mk);
     if (more) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        mcur[u] = mnxt[u];
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) cur[u][j] = nxt[u][j];
-      }
+      for (int j = 0; j < 16; ++j) v[j] = nx[j];
     }
   }
-  c.ge_lo = ASYM ? ge_lo : 0;
-  c.ge_hi = ge_hi;
+  // ragged tail [a1, s1)
+  if (s1 > a1) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = 0;
+    const uint32_t e = a1 + tid;
+    uint32_t valid = 0;
+    if (e < s1) { v[0] = load_bits<DT>(x, e); valid = 1; }
+    classify_store<DT, NT, ASYM>(v, valid, e, lo_p, lo_n, L, scan, ncand, mk);
+  }
   c.maxkey = mk;
-  if (threadIdx.x == 0) sh.n_cand = ncand;
+  if (tid == 0) sh.n_cand = ncand;
   __syncthreads();
 }
 
 template <int DT, int NT>
 __device__ __forceinline__ void stream_pass(const void* x, uint64_t T, uint64_t s0, uint64_t s1, uint32_t lo_p,
-                                            uint32_t lo_n, uint32_t lo_cnt, uint32_t hi_cnt, const List& L,
-                                            Shared& sh, Counts& c, bool asym) {
-  const bool fits = s1 - s0 <= (uint64_t)L.cap;
-  if (fits) {
-    if (asym) stream_pass_t<DT, NT, true, true>(x, T, s0, s1, lo_p, lo_n, lo_cnt, hi_cnt, L, sh, c);
-    else stream_pass_t<DT, NT, true, false>(x, T, s0, s1, lo_p, lo_n, lo_cnt, hi_cnt, L, sh, c);
-  } else {
-    if (asym) stream_pass_t<DT, NT, false, true>(x, T, s0, s1, lo_p, lo_n, lo_cnt, hi_cnt, L, sh, c);
-    else stream_pass_t<DT, NT, false, false>(x, T, s0, s1, lo_p, lo_n, lo_cnt, hi_cnt, L, sh, c);
-  }
+                                            uint32_t lo_n, const List& L, Shared& sh, Counts& c) {
+  (void)T;
+  if (lo_p != lo_n) stream_pass_t<DT, NT, true>(x, (uint32_t)s0, (uint32_t)s1, lo_p, lo_n, L, sh, c);
+  else stream_pass_t<DT, NT, false>(x, (uint32_t)s0, (uint32_t)s1, lo_p, lo_n, L, sh, c);
 }
 
-// Group-reduce the stream counters: sums of ge_lo / ge_hi / ncand, max of maxkey.
+// Group-reduce the stream pass: candidate total and max |x| key.
 template <int NT>
 __device__ void reduce_counts(Grp& g, Shared& sh, Counts& c) {
   uint64_t* slot = g.slot();
-  if (threadIdx.x < 4) slot[threadIdx.x] = 0;
+  if (threadIdx.x < 2) slot[threadIdx.x] = 0;
   __syncthreads();
-  const uint32_t glo = __reduce_add_sync(0xFFFFFFFFu, c.ge_lo), ghi = __reduce_add_sync(0xFFFFFFFFu, c.ge_hi);
   const uint32_t mk = __reduce_max_sync(0xFFFFFFFFu, c.maxkey);
-  if ((threadIdx.x & 31) == 0) {
-    atomicAdd((unsigned long long*)&slot[0], (unsigned long long)glo);
-    atomicAdd((unsigned long long*)&slot[1], (unsigned long long)ghi);
-    atomicMax((unsigned long long*)&slot[3], (unsigned long long)mk);
-  }
-  if (threadIdx.x == 0) slot[2] = sh.n_cand;
-  g.allsum(3, sh.vec, nullptr);
+  if ((threadIdx.x & 31) == 0) atomicMax((unsigned long long*)&slot[1], (unsigned long long)mk);
+  if (threadIdx.x == 0) slot[0] = sh.n_cand;
+  g.allsum(1, sh.vec, nullptr);
   uint64_t* prev = g.slots + (g.parity ^ 1) * 64;  // this CTA's slot (still intact)
   uint64_t m = 0;
-  if (g.size == 1) m = prev[3];
+  if (g.size == 1) m = prev[1];
   else {
     cg::cluster_group cl = cg::this_cluster();
     for (uint32_t r = 0; r < g.size; ++r) {
-      const uint64_t y = *cl.map_shared_rank(prev + 3, r);
+      const uint64_t y = *cl.map_shared_rank(prev + 1, r);
       m = y > m ? y : m;
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) sh.vec[3] = m;
+  if (threadIdx.x == 0) sh.vec[1] = m;
+  __syncthreads();
+}
+
+// Count candidates with key >= lo and key >= hi (group totals).
+template <int NT>
+__device__ void count_ge(Grp& g, Shared& sh, const List& L, uint32_t n, uint32_t lo, uint32_t hi, uint64_t* clo,
+                         uint64_t* chi) {
+  uint32_t a = 0, b = 0;
+  list_foreach<NT>(L, n, [&](uint32_t bits, uint32_t) {
+    const uint32_t k = bits & 0x7FFFFFFFu;
+    a += k >= lo;
+    b += k >= hi;
+  });
+  a = __reduce_add_sync(0xFFFFFFFFu, a);
+  b = __reduce_add_sync(0xFFFFFFFFu, b);
+  uint64_t* slot = g.slot();
+  if (threadIdx.x < 2) slot[threadIdx.x] = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd((unsigned long long*)&slot[0], (unsigned long long)a);
+    atomicAdd((unsigned long long*)&slot[1], (unsigned long long)b);
+  }
+  g.allsum(2, sh.vec, nullptr);
+  *clo = sh.vec[0];
+  *chi = sh.vec[1];
   __syncthreads();
 }
 
@@ -752,28 +752,26 @@ __device__ __noinline__ Grp phase_stream(Ctx& c, Grp g, Shared& sh) {
   const int tid = threadIdx.x;
   const uint64_t kk = c.kk;
   uint32_t lo = c.lo, hi = c.hi, lo_neg = c.lo_neg;
-  const bool asym = lo_neg != lo;
   Counts k;
-  stream_pass<DT, NT>(c.x, c.T, c.s0, c.s1, lo, lo_neg, lo, hi, c.L, sh, k, asym);
+  stream_pass<DT, NT>(c.x, c.T, c.s0, c.s1, lo, lo_neg, c.L, sh, k);
   reduce_counts<NT>(g, sh, k);
-  // |x| >= lo count: every candidate when the thresholds are symmetric
-  uint64_t cnt_lo = asym ? sh.vec[0] : sh.vec[2], cnt_hi = sh.vec[1];
-  uint32_t maxkey = (uint32_t)sh.vec[3];
+  uint32_t maxkey = (uint32_t)sh.vec[1];
   const int nonfinite = maxkey >= kNonFiniteKey;
+  uint64_t cnt_lo = 0, cnt_hi = 0;
+  if (!nonfinite) count_ge<NT>(g, sh, c.L, (uint32_t)sh.n_cand, lo, hi, &cnt_lo, &cnt_hi);
   uint64_t cnt_nz = cnt_lo;  // exact when lo <= 1, else a lower bound (only compared with kk)
   if (!nonfinite && kk > 0 && cnt_lo < kk && lo > (c.atkf_only ? 0u : 1u)) {
     // bracket missed (or tau == 0): re-stream keeping every nonzero (every element in
-    // ATKF-only mode); ge_lo then counts the nonzeros
+    // ATKF-only mode)
     const uint32_t new_hi = lo;
     lo = c.atkf_only ? 0u : 1u;
     lo_neg = lo;
     hi = new_hi;
-    stream_pass<DT, NT>(c.x, c.T, c.s0, c.s1, lo, lo_neg, 1u, hi, c.L, sh, k, true);
+    stream_pass<DT, NT>(c.x, c.T, c.s0, c.s1, lo, lo_neg, c.L, sh, k);
     reduce_counts<NT>(g, sh, k);
-    cnt_nz = sh.vec[0];
+    maxkey = (uint32_t)sh.vec[1];
+    count_ge<NT>(g, sh, c.L, (uint32_t)sh.n_cand, 1u, hi, &cnt_nz, &cnt_hi);
     cnt_lo = cnt_nz;
-    cnt_hi = sh.vec[1];
-    maxkey = (uint32_t)sh.vec[3];
   }
   __syncthreads();
   if (tid == 0) {
@@ -1004,9 +1002,22 @@ __device__ __forceinline__ int block_of(const uint32_t* cut_key, const uint32_t*
   return (s ? meff0 : 0) + blk;
 }
 
-// ---- Phase E: members per block in flat (CSR) order: warp-segmented stable walk
+// ---- Phase E: members per block in flat (CSR) order: warp-segmented stable walk.
+// Block ids (B <= 8) are one-hot encoded in 8-bit fields of a u64; one warp inclusive
+// scan gives every lane its rank among same-block lanes and the warp's per-block totals.
+// Lane b keeps the running count of block b in a register.  B > 8 uses match_any.
+__device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
 template <int NT>
-__device__ __noinline__ Grp phase_members(Ctx& c, Grp g, Shared& sh) {
+__device__ __noinline__ Grp phase_members(Ctx& c, Grp g, Shared& sh, int scratch_bytes) {
   constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const List L = c.L;
@@ -1017,17 +1028,58 @@ __device__ __noinline__ Grp phase_members(Ctx& c, Grp g, Shared& sh) {
   const uint32_t* cut_idx = c.cut_idx;
   uint32_t* wcnt = c.wcnt;
   uint32_t* woff = c.woff;
+  uint8_t* bid = reinterpret_cast<uint8_t*>(c.scratch);
+  const bool keep_bid = nkept <= (uint32_t)scratch_bytes && B <= 255;
+  const bool few = B <= 8;
+  const uint32_t lt = (1u << lane) - 1u;
   const uint32_t seg = (nkept + NW - 1) / NW;
   const uint32_t w0 = wid * seg, w1 = (w0 + seg < nkept) ? w0 + seg : nkept;
+  // cuts in registers (up to 4 per sign on the fast path)
+  uint32_t ck[8], cx[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) { ck[k] = 0; cx[k] = 0; }
+  const bool reg_cuts = ncut0 <= 4 && ncut - ncut0 <= 4;
+  if (reg_cuts) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < ncut0) { ck[k] = cut_key[k]; cx[k] = cut_idx[k]; }
+      if (k < ncut - ncut0) { ck[4 + k] = cut_key[ncut0 + k]; cx[4 + k] = cut_idx[ncut0 + k]; }
+    }
+  }
+  const int nc1 = ncut - ncut0;
+  auto blk_of = [&](uint32_t b, uint32_t x) -> int {
+    if (!reg_cuts) return block_of(cut_key, cut_idx, ncut0, ncut, meff0, b, x);
+    const uint32_t key = b & 0x7FFFFFFFu;
+    const bool neg = (b >> 31) != 0;
+    int blk = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t k2 = neg ? ck[4 + k] : ck[k], x2 = neg ? cx[4 + k] : cx[k];
+      const bool act = k < (neg ? nc1 : ncut0);
+      blk += (act && (key < k2 || (key == k2 && x >= x2))) ? 1 : 0;
+    }
+    return (neg ? meff0 : 0) + blk;
+  };
+  // ---- walk 1: block ids and per-warp block counts
+  uint32_t run = 0;  // lane b: running count of block b (few) in this warp
   for (int b = lane; b < B; b += 32) wcnt[wid * maxb + b] = 0;
   __syncwarp();
   for (uint32_t i = w0; i < w1; i += 32) {
     const uint32_t e = i + lane;
-    const int blk = e < w1 ? block_of(cut_key, cut_idx, ncut0, ncut, meff0, L.bits(e), L.idx(e)) : -1;
-    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, blk);
-    if (blk >= 0 && lane == __ffs(peers) - 1) wcnt[wid * maxb + blk] += __popc(peers);
-    __syncwarp();
+    const int blk = e < w1 ? blk_of(L.bits(e), L.idx(e)) : -1;
+    if (keep_bid && e < w1) bid[e] = (uint8_t)blk;
+    if (few) {
+      const uint64_t oh = blk >= 0 ? (1ull << (8 * blk)) : 0ull;
+      const uint64_t sc = warp_incl_scan_u64(oh);
+      const uint64_t tot = __shfl_sync(0xFFFFFFFFu, sc, 31);
+      if (lane < B) run += (uint32_t)((tot >> (8 * lane)) & 0xFFull);
+    } else {
+      const uint32_t peers = __match_any_sync(0xFFFFFFFFu, blk);
+      if (blk >= 0 && lane == __ffs(peers) - 1) wcnt[wid * maxb + blk] += __popc(peers);
+      __syncwarp();
+    }
   }
+  if (few && lane < B) wcnt[wid * maxb + lane] = run;
   __syncthreads();
   for (int b = tid; b < B; b += NT) {
     uint32_t acc = 0;
@@ -1042,20 +1094,32 @@ __device__ __noinline__ Grp phase_members(Ctx& c, Grp g, Shared& sh) {
     uint32_t acc = 0;
     for (int b = 0; b < B; ++b) { c.b_rs[b] = acc; acc += c.b_n[b]; }
   }
-  for (int b = lane; b < B; b += 32) wcnt[wid * maxb + b] = 0;
   __syncthreads();
-  const uint32_t* b_rs = c.b_rs;
+  for (int k = tid; k < NW * B; k += NT) {
+    const int w = k / B, b = k - w * B;
+    woff[w * maxb + b] += c.b_rs[b];
+  }
+  __syncthreads();
+  // ---- walk 2: stable positions
+  uint32_t pos = few && lane < B ? woff[wid * maxb + lane] : 0u;  // lane b: next position of block b
   for (uint32_t i = w0; i < w1; i += 32) {
     const uint32_t e = i + lane;
-    const int blk = e < w1 ? block_of(cut_key, cut_idx, ncut0, ncut, meff0, L.bits(e), L.idx(e)) : -1;
-    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, blk);
-    if (blk >= 0) {
-      const uint32_t rk = woff[wid * maxb + blk] + wcnt[wid * maxb + blk] + __popc(peers & ((1u << lane) - 1u));
-      M.set(b_rs[blk] + rk, e);
+    int blk = -1;
+    if (e < w1) blk = keep_bid ? (int)bid[e] : blk_of(L.bits(e), L.idx(e));
+    if (few) {
+      const uint64_t oh = blk >= 0 ? (1ull << (8 * blk)) : 0ull;
+      const uint64_t sc = warp_incl_scan_u64(oh);
+      const uint64_t tot = __shfl_sync(0xFFFFFFFFu, sc, 31);
+      const uint32_t basep = __shfl_sync(0xFFFFFFFFu, pos, blk >= 0 ? blk : 0);
+      if (blk >= 0) M.set(basep + (uint32_t)((sc >> (8 * blk)) & 0xFFull) - 1u, e);
+      if (lane < B) pos += (uint32_t)((tot >> (8 * lane)) & 0xFFull);
+    } else {
+      const uint32_t peers = __match_any_sync(0xFFFFFFFFu, blk);
+      if (blk >= 0) M.set(woff[wid * maxb + blk] + __popc(peers & lt), e);
+      __syncwarp();
+      if (blk >= 0 && lane == __ffs(peers) - 1) woff[wid * maxb + blk] += __popc(peers);
+      __syncwarp();
     }
-    __syncwarp();
-    if (blk >= 0 && lane == __ffs(peers) - 1) wcnt[wid * maxb + blk] += __popc(peers);
-    __syncwarp();
   }
   __syncthreads();
   for (int b0 = 0; b0 < B; b0 += 64) {
@@ -1243,8 +1307,7 @@ __device__ __noinline__ Grp phase_layout(Ctx& c, Grp g, Shared& sh) {
   for (uint64_t i = zb + tid; i < z1; i += NT) if (i >= za) out[i] = 0;
   uint4* o4 = reinterpret_cast<uint4*>(out);
   for (uint64_t i = za / 16 + tid; i < zb / 16; i += NT) o4[i] = make_uint4(0, 0, 0, 0);
-  __threadfence();
-  g.sync();
+  g.sync();  // CTA barrier / cluster barrier (release-acquire) orders the payload writes
   return g;
 }
 
@@ -1313,32 +1376,54 @@ __device__ __noinline__ Grp phase_write(Ctx& c, Grp g, Shared& sh) {
       for (int b = tid; b < B; b += NT) st_u32_le_bytes(out, c.b_off[4 * b + 1] + 4ull * N, (uint32_t)c.b_N[b]);
   }
   phase_mark(c, g, 13);
-  // cols / codes (bitstream.py:12-30): each thread packs a group of 32 consecutive fields
-  // (32*w bits) MSB-first into a 64-bit window and emits payload-aligned 32-bit words;
-  // words shared with a neighbouring group/section are merged with atomicOr.
+  // cols / codes (bitstream.py:12-30): each job packs 8 consecutive fields of one
+  // (block, section) MSB-first into a 64-bit window and emits payload-aligned 32-bit
+  // words; words shared with a neighbouring job/section are merged with atomicOr.
   {
     uint32_t* out32 = reinterpret_cast<uint32_t*>(out);
-    for (int b = 0; b < B; ++b) {
+    constexpr uint32_t FPJ = 8;
+    uint32_t* jstart = reinterpret_cast<uint32_t*>(sh.pre);  // job prefix per block batch (<= 63 blocks)
+    for (int bb0 = 0; bb0 < B; bb0 += 63) {
+    const int Bj = B - bb0 < 63 ? B - bb0 : 63;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t acc = 0;
+      for (int k = 0; k < Bj; ++k) { jstart[k] = acc; acc += 2 * ((c.b_n[bb0 + k] + FPJ - 1) / FPJ); }
+      jstart[Bj] = acc;
+    }
+    __syncthreads();
+    const uint32_t njobs = jstart[Bj];
+    for (uint32_t job = tid; job < njobs; job += NT) {
+      int bk = 0;
+      while (bk + 1 < Bj && jstart[bk + 1] <= job) ++bk;
+      const uint32_t jj = job - jstart[bk];
+      const int b = bb0 + bk;
       const uint32_t nloc = c.b_n[b];
-      if (nloc == 0) continue;
+      const uint32_t ng = (nloc + FPJ - 1) / FPJ;
+      const int sec = jj < ng ? 0 : 1;
+      const uint32_t gi = sec ? jj - ng : jj;
       const uint64_t pre = c.b_pre[b];
       const uint32_t rs = c.b_rs[b];
-      const uint32_t ngrp = (nloc + 31) / 32;
-      for (uint32_t job = tid; job < 2 * ngrp; job += NT) {
-        const int sec = job < ngrp ? 0 : 1;
-        const uint32_t gi = sec ? job - ngrp : job;
-        const uint32_t w = sec == 0 ? cb : c.b_q[b];
-        const uint32_t f0 = gi * 32, f1 = f0 + 32 < nloc ? f0 + 32 : nloc;
-        uint64_t bit = 8ull * c.b_off[4 * b + 2 + sec] + (pre + f0) * (uint64_t)w;  // first bit
-        const uint64_t lo_bit = bit, hi_bit = bit + (uint64_t)(f1 - f0) * w;
-        // window holds bits [wbase, wbase + nacc) MSB-aligned in acc
-        uint64_t wbase = bit & ~31ull;
-        uint64_t acc = 0;
-        uint32_t nacc = (uint32_t)(bit - wbase);
-        for (uint32_t f = f0; f < f1; ++f) {
-          const uint32_t li = M.get(rs + f);
-          const uint32_t v = sec == 0 ? fk.mod(L.idx(li)) : L.bits(li);
-          acc |= (uint64_t)v << (64u - nacc - w);
+      const uint32_t w = sec == 0 ? cb : c.b_q[b];
+      const uint32_t f0 = gi * FPJ, f1 = f0 + FPJ < nloc ? f0 + FPJ : nloc;
+      const uint64_t bit = 8ull * c.b_off[4 * b + 2 + sec] + (pre + f0) * (uint64_t)w;
+      const uint64_t lo_bit = bit, hi_bit = bit + (uint64_t)(f1 - f0) * w;
+      uint64_t wbase = bit & ~31ull;
+      uint64_t acc = 0;
+      uint32_t nacc = (uint32_t)(bit - wbase);
+      uint32_t vv[FPJ];
+#pragma unroll
+      for (uint32_t k = 0; k < FPJ; ++k) {
+        vv[k] = 0;
+        if (f0 + k < f1) {
+          const uint32_t li = M.get(rs + f0 + k);
+          vv[k] = sec == 0 ? fk.mod(L.idx(li)) : L.bits(li);
+        }
+      }
+#pragma unroll
+      for (uint32_t k = 0; k < FPJ; ++k) {
+        if (f0 + k < f1) {
+          acc |= (uint64_t)vv[k] << (64u - nacc - w);
           nacc += w;
           if (nacc >= 32) {
             const uint32_t word = (uint32_t)(acc >> 32);
@@ -1350,17 +1435,17 @@ __device__ __noinline__ Grp phase_write(Ctx& c, Grp g, Shared& sh) {
             wbase += 32;
           }
         }
-        if (nacc) {
-          const uint32_t word = (uint32_t)(acc >> 32);
-          const uint64_t wa = wbase >> 5;
-          if (wbase >= lo_bit && wbase + 32 <= hi_bit) out32[wa] = bswap32(word);
-          else if (word) atomicOr(out32 + wa, bswap32(word));
-        }
+      }
+      if (nacc) {
+        const uint32_t word = (uint32_t)(acc >> 32);
+        const uint64_t wa = wbase >> 5;
+        if (wbase >= lo_bit && wbase + 32 <= hi_bit) out32[wa] = bswap32(word);
+        else if (word) atomicOr(out32 + wa, bswap32(word));
       }
     }
+    }
   }
-  __threadfence();
-  g.sync();
+  g.sync();  // CTA barrier / cluster barrier (release-acquire) orders the payload writes
   return g;
 }
 
@@ -1409,7 +1494,7 @@ __device__ __forceinline__ void encode_one(const EncArgs& a, Ctx& c, Grp g, Shar
   phase_mark(c, g, 6);
   g = phase_cuts<NT>(c, g, sh);
   phase_mark(c, g, 7);
-  g = phase_members<NT>(c, g, sh);
+  g = phase_members<NT>(c, g, sh, a.scratch_words * 4);
   phase_mark(c, g, 8);
   g = phase_minmax<NT>(c, g, sh);
   phase_mark(c, g, 9);

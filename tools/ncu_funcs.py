@@ -29,3 +29,11 @@ te, ts = sum(ex), sum(st)
 for k, v in agg.most_common(40):
     name = subprocess.run(["c++filt", k], capture_output=True, text=True).stdout.strip()
     print(f"{100.0*v/te:5.1f}% exec {100.0*aggs[k]/ts:5.1f}% stall  {name[:110]}")
+
+if len(sys.argv) > 4:
+    # detail: hottest instructions (by stall samples) inside functions matching argv[4]
+    pat = sys.argv[4]
+    idx = [i for i in range(min(len(owner), len(data))) if pat in owner[i]]
+    idx.sort(key=lambda i: -st[i])
+    for i in idx[:40]:
+        print(f"  #{i:6d} stall={st[i]:6d} exec={ex[i]:9d}  {data[i][ix['Source']].strip()[:90]}")
