@@ -164,9 +164,11 @@ __device__ uint32_t crc_cta_raw(const uint8_t* base, uint64_t b0, uint64_t b1, c
 // shifts it to the round end with one multiply by kCrcShift64[NT-1-t] (independent across
 // threads), then an XOR reduction; rounds combine with x^(8*64*NT) = kX2n[9 + log2 NT].
 // stage: >= 16*NT u32 of shared memory; red: >= NT/32 + 1 u32.
+// part/nparts: this CTA handles rounds q = part, part + nparts, ... (counted from b1) and
+// returns its partial already shifted to b1; partials of all parts XOR to the raw CRC.
 template <int NT>
 __device__ uint32_t crc_cta_staged(const uint8_t* base, uint64_t b0, uint64_t b1, const uint32_t* t4, uint32_t* red,
-                                   uint32_t* stage) {
+                                   uint32_t* stage, uint32_t part = 0, uint32_t nparts = 1) {
   constexpr int NW = NT / 32;
   constexpr int LOGNT = NT >= 1024 ? 10 : NT >= 512 ? 9 : NT >= 256 ? 8 : NT >= 128 ? 7 : NT >= 64 ? 6 : 5;
   constexpr int64_t L = 64, SPAN = L * NT, WORDS = SPAN / 4;
@@ -175,8 +177,11 @@ __device__ uint32_t crc_cta_staged(const uint8_t* base, uint64_t b0, uint64_t b1
   const int64_t rounds = (int64_t)((n + SPAN - 1) / SPAN);
   const uint32_t* gw = reinterpret_cast<const uint32_t*>(base);
   const uint32_t myshift = kCrcShift64[NT - 1 - tid];
+  const int lognp = nparts >= 8 ? 3 : nparts >= 4 ? 2 : nparts >= 2 ? 1 : 0;
   uint32_t total = 0;
-  for (int64_t q = rounds - 1; q >= 0; --q) {
+  int64_t qtop = rounds - 1;
+  while (qtop >= 0 && (uint64_t)qtop % nparts != part) --qtop;
+  for (int64_t q = qtop; q >= 0; q -= nparts) {
     const int64_t rs = (int64_t)b1 - SPAN * (q + 1);  // byte address of stage[0]
     const int64_t fl = rs >= 0 ? rs / 4 : -((-rs + 3) / 4);
     const uint32_t sh8 = (uint32_t)(rs - 4 * fl) * 8u;
@@ -215,11 +220,16 @@ __device__ uint32_t crc_cta_staged(const uint8_t* base, uint64_t b0, uint64_t b1
     if (tid == 0) {
       uint32_t rq = 0;
       for (int k = 0; k < NW; ++k) rq ^= red[k];
-      total = crc_mult(total, kX2n[9 + LOGNT]) ^ rq;
+      total = crc_mult(total, kX2n[9 + LOGNT + lognp]) ^ rq;
     }
     __syncthreads();
   }
-  if (tid == 0) red[NW] = total;
+  if (tid == 0) {
+    // shift this part's rounds (q = part + k*nparts) down by part rounds
+    for (int k = 0; k < 4; ++k)
+      if ((part >> k) & 1u) total = crc_mult(total, kX2n[9 + LOGNT + k]);
+    red[NW] = total;
+  }
   __syncthreads();
   const uint32_t r = red[NW];
   __syncthreads();

@@ -152,8 +152,11 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
     const uint32_t bmw = (uint32_t)(a.tile_elems + 31) / 32;
     uint32_t* rpc = bm + 2 * bmw;
     const bool cached = (uint64_t)(R + 1) * nb <= (uint64_t)a.rpc_cap;
-    for (uint32_t k = tid; k < E; k += DNT) tile[k] = 0.0;
-    for (uint32_t k = tid; k < 2 * bmw; k += DNT) bm[k] = 0;
+    {
+      uint4* t4z = reinterpret_cast<uint4*>(tile);
+      for (uint32_t k = tid; k < (E + 1) / 2; k += DNT) t4z[k] = make_uint4(0, 0, 0, 0);
+      for (uint32_t k = tid; k < 2 * bmw; k += DNT) bm[k] = 0;
+    }
     const uint32_t cb = col_bits(K);
     uint32_t fl = 0;
     if (cached) {
@@ -207,11 +210,31 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
     }
     __syncthreads();
     float* out = d.out;
-    for (uint32_t k = tid; k < E; k += DNT) {
-      const uint32_t rr = k / Kc, cc = k % Kc;
-      const float f = __double2float_rn(tile[k]);
-      if (!isfinite(f)) fl |= FLAG_NONFINITE;
-      out[(uint64_t)(t.r0 + rr) * K + t.c0 + cc] = f;
+    const bool vec4 = (K % 4u) == 0 && (t.c0 % 4u) == 0 && (Kc % 4u) == 0 &&
+                      (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+    if (vec4) {
+      // 4 consecutive columns per thread: 2 x 16-byte smem loads, one 16-byte global store
+      const uint32_t kq = Kc / 4, nq = E / 4;
+      FastDiv fq;
+      fq.init(kq);
+      const double2* t2 = reinterpret_cast<const double2*>(tile);
+      for (uint32_t q = tid; q < nq; q += DNT) {
+        const uint32_t rr = fq.div(q), c4 = q - rr * kq;
+        const double2 a = t2[2 * q], b2 = t2[2 * q + 1];
+        const float4 f = make_float4(__double2float_rn(a.x), __double2float_rn(a.y), __double2float_rn(b2.x),
+                                     __double2float_rn(b2.y));
+        if (!(isfinite(f.x) && isfinite(f.y) && isfinite(f.z) && isfinite(f.w))) fl |= FLAG_NONFINITE;
+        *reinterpret_cast<float4*>(out + (uint64_t)(t.r0 + rr) * K + t.c0 + 4 * c4) = f;
+      }
+    } else {
+      FastDiv fc;
+      fc.init(Kc);
+      for (uint32_t k = tid; k < E; k += DNT) {
+        const uint32_t rr = fc.div(k), cc = k - rr * Kc;
+        const float f = __double2float_rn(tile[k]);
+        if (!isfinite(f)) fl |= FLAG_NONFINITE;
+        out[(uint64_t)(t.r0 + rr) * K + t.c0 + cc] = f;
+      }
     }
     fl = __reduce_or_sync(0xFFFFFFFFu, fl);
     if (lane == 0 && fl) atomicOr(&sflags, fl);

@@ -171,8 +171,26 @@ struct Shared {
 // Find digit d of a (group-summed) histogram with above(d) < r <= above(d) + h[d], from
 // the top.  Histograms of the whole group are summed through DSMEM.
 template <int NT>
-__device__ void find_digit(Grp& g, Shared& sh, const uint32_t* H, int nb, uint64_t r) {
+__device__ void find_digit(Grp& g, Shared& sh, const uint32_t* H, int nb, uint64_t r, uint32_t* stage = nullptr) {
   const int per = (nb + NT - 1) / NT;
+  if (g.size > 1 && stage) {
+    // sum the group's histograms into local smem first: independent DSMEM loads, one round trip
+    cg::cluster_group cl = cg::this_cluster();
+    for (int b = threadIdx.x; b < nb; b += NT) {
+      uint32_t v[8];
+#pragma unroll
+      for (int rr = 0; rr < 8; ++rr) v[rr] = rr < (int)g.size ? *cl.map_shared_rank(H + b, (unsigned)rr) : 0u;
+      uint32_t acc = 0;
+#pragma unroll
+      for (int rr = 0; rr < 8; ++rr) acc += v[rr];
+      stage[b] = acc;
+    }
+    __syncthreads();
+    Grp g1 = g;
+    g1.size = 1;
+    find_digit<NT>(g1, sh, stage, nb, r, nullptr);
+    return;
+  }
   cg::cluster_group cl = cg::this_cluster();
   auto bin = [&](int b) -> uint64_t {
     if (g.size == 1) return H[b];
@@ -227,7 +245,7 @@ __device__ uint64_t radix_select64(Grp& g, Shared& sh, uint32_t* hist, const Lis
       if (fn(L.bits(i), L.idx(i), k) && (k & mask) == prefix) atomicAdd(&H[(int)((k >> shf) & (uint64_t)(nb - 1))], 1u);
     }
     g.sync();
-    find_digit<NT>(g, sh, H, nb, r);
+    find_digit<NT>(g, sh, H, nb, r, hist + 2 * HB);
     prefix |= (uint64_t)sh.fd_digit << shf;
     mask |= (uint64_t)(nb - 1) << shf;
     r -= sh.fd_above;
@@ -275,7 +293,7 @@ __device__ SelRes select_exact(Grp& g, Shared& sh, uint32_t* scratch, const List
       }
     });
     g.sync();
-    find_digit<NT>(g, sh, H, nb, r);
+    find_digit<NT>(g, sh, H, nb, r, reinterpret_cast<uint32_t*>(gc));
     const uint64_t dg = sh.fd_digit;
     n_gt += sh.fd_above;
     r -= sh.fd_above;
@@ -1449,16 +1467,29 @@ __device__ __noinline__ Grp phase_write(Ctx& c, Grp g, Shared& sh) {
   return g;
 }
 
-// ---- Phase J: CRC-32 over bytes [4, P-4) (codec.py:316) on rank 0
+// ---- Phase J: CRC-32 over bytes [4, P-4) (codec.py:316); rounds interleaved over the group
 template <int NT>
 __device__ __noinline__ void phase_crc(Ctx& c, Grp g, Shared& sh, uint64_t* out_len, int32_t* status) {
-  if (g.rank != 0) return;
   const uint64_t P = c.P;
-  const uint32_t raw = c.L.cap * 12u >= (uint32_t)(NT * 64)
-                           ? crc_cta_staged<NT>(c.out, 4, P - 4, c.t4, sh.red, c.L.sb)
-                           : crc_cta_raw<NT>(c.out, 4, P - 4, c.t4, sh.red);
-  if (threadIdx.x == 0) {
-    st_u32_le_bytes(c.out, P - 4, crc_finish(raw, P - 8));
+  uint32_t part;
+  if (c.L.cap * 12u >= (uint32_t)(NT * 64))
+    part = crc_cta_staged<NT>(c.out, 4, P - 4, c.t4, sh.red, c.L.sb, g.rank, g.size);
+  else
+    part = g.rank == 0 ? crc_cta_raw<NT>(c.out, 4, P - 4, c.t4, sh.red) : 0u;
+  uint32_t total = part;
+  if (g.size > 1) {
+    uint64_t* slot = g.slot();
+    if (threadIdx.x == 0) slot[0] = part;
+    g.sync();
+    if (g.rank == 0 && threadIdx.x == 0) {
+      cg::cluster_group cl = cg::this_cluster();
+      total = 0;
+      for (uint32_t r = 0; r < g.size; ++r) total ^= (uint32_t)*cl.map_shared_rank(slot, r);
+    }
+    g.parity ^= 1;
+  }
+  if (g.rank == 0 && threadIdx.x == 0) {
+    st_u32_le_bytes(c.out, P - 4, crc_finish(total, P - 8));
     if (c.prof) c.prof[(uint64_t)c.ifi * 32 + 15] = gtimer();
     out_len[c.ifi] = P;
     status[c.ifi] = SIF_OK;
