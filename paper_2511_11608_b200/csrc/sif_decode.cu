@@ -105,7 +105,8 @@ __global__ void sif_parse_kernel(DecArgs a) {
 
 // ------------------------------------------------------------------------------- scatter
 __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
-  extern __shared__ __align__(16) uint8_t dsm[];
+  extern __shared__ __align__(16) uint8_t dsm_raw[];
+  uint8_t* dsm = dsm_raw;
   __shared__ uint32_t hdr[2 * TROW_U32];
   __shared__ uint32_t red[DNT / 32 + 2];
   __shared__ uint32_t sflags;

@@ -10,12 +10,11 @@
 
 #include "sif.h"
 #include "sif_decode.cu"
-#include "sif_encode.cu"
+#include "sif_enc.cu"
 #include "sif_synth.cu"
 
 namespace {
 
-constexpr int kSmemBudget = 227 * 1024 - 4 * 1024;  // dynamic; leaves room for static smem
 constexpr int kDecTileElems = 4096;
 constexpr int kDecRpcCap = 2048;
 
@@ -23,35 +22,54 @@ inline uint64_t up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 
 int check_cuda(cudaError_t e) { return e == cudaSuccess ? SIF_OK : SIF_ERR_CUDA; }
 
-// Launch shape per size class: cluster size G (CTAs per IF) and threads per CTA.
-// Overridable with SIF_CLUSTER / SIF_NT for tuning experiments.
-void choose_shape(uint64_t tmax, int* G, int* NT) {
-  int g = 1, nt = 256;
-  if (tmax > 65536) { g = 2; nt = 512; }
-  if (tmax > (1u << 20)) { g = 8; nt = 512; }
-  const char* e1 = getenv("SIF_CLUSTER");
-  if (e1 && *e1) {
-    const int v = atoi(e1);
-    if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) g = v;
+inline int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
   }
-  const char* e2 = getenv("SIF_NT");
-  if (e2 && *e2) {
-    const int v = atoi(e2);
-    if (v == 256 || v == 512) nt = v;
-  }
-  *G = g;
-  *NT = nt;
+  return sms;
 }
 
-uint64_t enc_block_bytes(int maxb, int nt) {
-  // 9 u64 arrays (b_sum, b_pre, b_N, b_off x4, b_o64, b_inv) + 8 u32 arrays + wcnt/woff
-  return (uint64_t)maxb * (8 * 9 + 4 * 8) + 2ull * (nt / 32) * 4 * maxb + 64;
+// Workspace sections of an encode plan (all offsets 256-byte aligned).
+struct EncWs {
+  uint64_t info, st, ch_if, ch_e0, ch_off, ch_cnt, bcnt, bpre, blast, bprev, hist, fixedq, keptoff, lists;
+};
+
+EncWs enc_ws(uint64_t n, uint64_t nch, uint64_t maxb, uint64_t nhist, uint64_t nq) {
+  EncWs w;
+  uint64_t off = 0;
+  auto take = [&](uint64_t bytes) { const uint64_t o = off; off += up(std::max<uint64_t>(bytes, 1), 256); return o; };
+  w.info = take(sizeof(sif::IfInfo) * n);
+  w.st = take(sizeof(sif::IfSt) * n);
+  w.ch_if = take(4 * nch);
+  w.ch_e0 = take(4 * nch);
+  w.ch_off = take(4 * nch);
+  w.ch_cnt = take(4 * nch);
+  w.bcnt = take(4 * nch * maxb);
+  w.bpre = take(4 * nch * maxb);
+  w.blast = take(4 * nch * maxb);
+  w.bprev = take(4 * nch * maxb);
+  w.hist = take(4ull * 2 * sif::ND * nhist);
+  w.fixedq = take(nq);
+  w.keptoff = take(8 * n);
+  w.lists = off;
+  return w;
 }
 
-uint64_t enc_scratch_words(int G) {
-  const uint64_t sel = 2ull * sif::HB + 4ull * sif::GCAP * (G > 1 ? 2 : 1);
-  return std::max<uint64_t>(8192, sel);
+// Chunk-kernel grid: persistent CTAs, as many as can be resident.
+template <class K>
+int resident_grid(K kfn, int threads, int smem, uint64_t work) {
+  int per = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, threads, smem) != cudaSuccess || per < 1) per = 1;
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>(work, (uint64_t)per * num_sms()));
 }
+
+constexpr int kSmemStream = (2 * sif::CH + 2 * sif::ND) * 4;
+constexpr int kSmemSelect = (2 * sif::ND + 2 * sif::HB + sif::GCAP * 4 + 2 * sif::GSM) * 4;
+constexpr int kSmemMembers = 4 * sif::CH * 4 + sif::CH;
+constexpr int kSmemPack = 2 * sif::CH * 4;
 
 }  // namespace
 
@@ -119,7 +137,7 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
   int st = sif_validate_cfg(c);
   if (st) return st;
   memset(p, 0, sizeof(*p));
-  uint64_t tmax = 1, kmax = 0;
+  uint64_t kmax = 0, nch = 0, nhist = 0, lists = 0;
   for (int i = 0; i < n; ++i) {
     if (d[i].rows < 1 || d[i].cols < 1) return SIF_ERR_SHAPE;  // tensor.py:27-28
     const uint64_t T = (uint64_t)d[i].rows * d[i].cols;
@@ -127,36 +145,29 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
     if (d[i].dtype != SIF_DTYPE_F32 && d[i].dtype != SIF_DTYPE_BF16) return SIF_ERR_INVALID_ARG;
     if (!d[i].x || (reinterpret_cast<uintptr_t>(d[i].x) & 15)) return SIF_ERR_INVALID_ARG;
     if (!atkf && (!d[i].out || (reinterpret_cast<uintptr_t>(d[i].out) & 15))) return SIF_ERR_INVALID_ARG;
-    tmax = std::max(tmax, T);
     kmax = std::max(kmax, sif::keep_count(c->s, T));
+    const uint64_t ch = (T + sif::CH - 1) / sif::CH;
+    nch += ch;
+    if (ch > 1) ++nhist;
+    lists += up(16 * T, 256);
   }
-  int G, NT;
-  choose_shape(tmax, &G, &NT);
+  if (nch >= (1ull << 31)) return SIF_ERR_INVALID_ARG;
   const uint64_t kk = std::max<uint64_t>(1, kmax);
   const int maxb = (int)(std::min<uint64_t>(c->m_plus, kk) + std::min<uint64_t>(c->m_minus, kk));
-  const uint64_t budget = NT == 512 ? (uint64_t)kSmemBudget : (uint64_t)(113 * 1024 - 3 * 1024);
-  const uint64_t fixed = 4096 + 4 * enc_scratch_words(G) + enc_block_bytes(maxb, NT) + 16;
-  if (fixed + 12ull * 256 > budget) return SIF_ERR_CONFIG;  // too many blocks for shared memory
-  const uint64_t slice = (tmax + G - 1) / G;
-  uint64_t cap = (budget - fixed) / 12;
-  cap = std::min<uint64_t>(cap, up(slice, 32)) & ~31ull;  // multiple of 32: 16-byte aligned sub-arrays
+  if (maxb > sif::MAXB) return SIF_ERR_CONFIG;  // more blocks than the encoder supports
+  const EncWs w = enc_ws(n, nch, maxb, nhist, (uint64_t)c->m_plus + c->m_minus);
   p->n = n;
-  p->cluster = G;
-  p->threads = NT;
-  p->cap_smem = (int32_t)cap;
-  p->smem_bytes = (int32_t)(fixed + 12 * cap);
+  p->cluster = 1;
+  p->threads = sif::CNT;
+  p->smem_bytes = kSmemSelect;
+  p->cap_smem = (int32_t)nhist;
   p->max_blocks = maxb;
+  p->tiles = (int32_t)nch;
   p->flags = atkf;
-  const uint64_t spill_cta = up(12ull * (slice > cap ? slice - cap : 0), 256);
-  uint64_t off = 0;
-  p->ws_desc_off = off;
-  off += up(sizeof(sif_enc_desc) * (uint64_t)std::max(n, 1), 256);
-  p->ws_aux_off = off;  // fixed_q bytes, then kept offsets (atkf)
-  off += up((uint64_t)c->m_plus + c->m_minus, 256) + up(8ull * std::max(n, 1), 256);
-  p->ws_spill_off = off;
-  off += spill_cta * (uint64_t)std::max(n, 1) * G;
-  p->ws_bytes = up(off, 256);
-  p->tiles = (int32_t)(spill_cta / 256);  // spill stride in 256-byte units
+  p->ws_desc_off = w.info;
+  p->ws_aux_off = w.fixedq;
+  p->ws_spill_off = w.lists;
+  p->ws_bytes = w.lists + lists;
   return SIF_OK;
 }
 
@@ -165,66 +176,121 @@ int sif_enc_plan(const sif_enc_desc* d, int n, const sif_codec_cfg* c, sif_plan*
 }
 
 int sif_enc_upload(const sif_plan* p, const sif_enc_desc* d, const sif_codec_cfg* c, void* ws, void* stream) {
-  if (!p || !ws) return SIF_ERR_INVALID_ARG;
+  if (!p || !ws || !c || (p->n > 0 && !d)) return SIF_ERR_INVALID_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  uint8_t* w = (uint8_t*)ws;
-  if (p->n > 0 && check_cuda(cudaMemcpyAsync(w + p->ws_desc_off, d, sizeof(sif_enc_desc) * p->n, cudaMemcpyHostToDevice, s)))
-    return SIF_ERR_CUDA;
+  uint8_t* wb = (uint8_t*)ws;
+  const int n = p->n;
+  const EncWs w = enc_ws(n, (uint64_t)p->tiles, p->max_blocks, (uint64_t)p->cap_smem, (uint64_t)c->m_plus + c->m_minus);
+  std::vector<sif::IfInfo> info((size_t)std::max(n, 1));
+  std::vector<uint32_t> ch_if((size_t)std::max(p->tiles, 1)), ch_e0((size_t)std::max(p->tiles, 1));
+  uint64_t ch = 0, lists = w.lists;
+  int32_t hs = 0;
+  for (int i = 0; i < n; ++i) {
+    sif::IfInfo& f = info[i];
+    memset(&f, 0, sizeof(f));
+    f.x = d[i].x;
+    f.out = d[i].out;
+    f.cap = d[i].out_cap;
+    f.seed = d[i].seed;
+    f.T = (uint64_t)d[i].rows * d[i].cols;
+    f.kk = sif::keep_count(c->s, f.T);
+    f.N = d[i].rows;
+    f.K = d[i].cols;
+    f.cb = sif::col_bits(d[i].cols);
+    f.dtype = d[i].dtype;
+    const uint64_t nc = (f.T + sif::CH - 1) / sif::CH;
+    f.ch0 = (uint32_t)ch;
+    f.nch = (uint32_t)nc;
+    f.hslot = nc > 1 ? hs++ : -1;
+    f.list_off = lists;
+    f.gat_off = lists + 8 * f.T;
+    lists += up(16 * f.T, 256);
+    for (uint64_t k = 0; k < nc; ++k) {
+      ch_if[ch + k] = (uint32_t)i;
+      ch_e0[ch + k] = (uint32_t)(k * sif::CH);
+    }
+    ch += nc;
+  }
+  if (n > 0) {
+    if (check_cuda(cudaMemcpyAsync(wb + w.info, info.data(), sizeof(sif::IfInfo) * n, cudaMemcpyHostToDevice, s)))
+      return SIF_ERR_CUDA;
+    if (check_cuda(cudaMemcpyAsync(wb + w.ch_if, ch_if.data(), 4ull * ch, cudaMemcpyHostToDevice, s)))
+      return SIF_ERR_CUDA;
+    if (check_cuda(cudaMemcpyAsync(wb + w.ch_e0, ch_e0.data(), 4ull * ch, cudaMemcpyHostToDevice, s)))
+      return SIF_ERR_CUDA;
+  }
   if (c->mode == SIF_MODE_FIXED &&
-      check_cuda(cudaMemcpyAsync(w + p->ws_aux_off, c->fixed_q, (size_t)(c->m_plus + c->m_minus), cudaMemcpyHostToDevice, s)))
+      check_cuda(cudaMemcpyAsync(wb + w.fixedq, c->fixed_q, (size_t)(c->m_plus + c->m_minus), cudaMemcpyHostToDevice, s)))
     return SIF_ERR_CUDA;
-  return SIF_OK;
+  // the uploads read host vectors: finish them before the vectors go out of scope
+  return check_cuda(cudaStreamSynchronize(s));
 }
 
 static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint64_t* out_len, int32_t* status,
                       int atkf, int64_t* kept, double* tau3, cudaStream_t s) {
   if (p->n == 0) return SIF_OK;
-  uint8_t* w = (uint8_t*)ws;
-  sif::EncArgs a;
+  uint8_t* wb = (uint8_t*)ws;
+  const EncWs w = enc_ws(p->n, (uint64_t)p->tiles, p->max_blocks, (uint64_t)p->cap_smem, (uint64_t)c->m_plus + c->m_minus);
+  sif::EArgs a;
   memset(&a, 0, sizeof(a));
-  a.descs = reinterpret_cast<const sif_enc_desc*>(w + p->ws_desc_off);
+  a.info = reinterpret_cast<const sif::IfInfo*>(wb + w.info);
+  a.st = reinterpret_cast<sif::IfSt*>(wb + w.st);
   a.n = p->n;
+  a.nch = p->tiles;
+  a.maxb = p->max_blocks;
   a.atkf_only = atkf;
+  a.ch_if = reinterpret_cast<const uint32_t*>(wb + w.ch_if);
+  a.ch_e0 = reinterpret_cast<const uint32_t*>(wb + w.ch_e0);
+  a.ch_off = reinterpret_cast<uint32_t*>(wb + w.ch_off);
+  a.ch_cnt = reinterpret_cast<uint32_t*>(wb + w.ch_cnt);
+  a.ch_bcnt = reinterpret_cast<uint32_t*>(wb + w.bcnt);
+  a.ch_bpre = reinterpret_cast<uint32_t*>(wb + w.bpre);
+  a.ch_blast = reinterpret_cast<int32_t*>(wb + w.blast);
+  a.ch_bprev = reinterpret_cast<int32_t*>(wb + w.bprev);
+  a.hist = reinterpret_cast<uint32_t*>(wb + w.hist);
+  a.ws = wb;
   a.s = c->s; a.lam = c->lam; a.delta = c->delta;
   a.m_plus = c->m_plus; a.m_minus = c->m_minus; a.q_bit = c->q_bit; a.mode = c->mode;
-  a.fixed_q = w + p->ws_aux_off;
-  a.spill = w + p->ws_spill_off;
-  a.spill_stride = (uint64_t)p->tiles * 256;
-  a.cap = p->cap_smem;
-  a.maxb = p->max_blocks;
-  a.scratch_words = (int)enc_scratch_words(p->cluster);
+  a.fixed_q = wb + w.fixedq;
   a.out_len = out_len;
   a.status = status;
   a.kept_out = kept;
-  a.kept_off = reinterpret_cast<const uint64_t*>(w + p->ws_aux_off + up((uint64_t)c->m_plus + c->m_minus, 256));
+  a.kept_off = reinterpret_cast<const uint64_t*>(wb + w.keptoff);
   a.tau3 = tau3;
-  a.prof = reinterpret_cast<uint64_t*>(getenv("SIF_PROF_PTR") ? strtoull(getenv("SIF_PROF_PTR"), nullptr, 0) : 0ull);
-  auto kfn = p->threads == 512 ? sif::sif_encode_kernel<512> : sif::sif_encode_kernel<256>;
-  if (check_cuda(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem_bytes)))
-    return SIF_ERR_CUDA;
-  cudaLaunchConfig_t cfg;
-  memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3((unsigned)(p->n * p->cluster));
-  cfg.blockDim = dim3((unsigned)p->threads);
-  cfg.dynamicSmemBytes = (size_t)p->smem_bytes;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  if (p->cluster > 1) {
-    if (p->cluster > 8)
-      cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)p->cluster;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+  static bool attrs = false;
+  if (!attrs) {
+    if (check_cuda(cudaFuncSetAttribute(sif::enc_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemStream)) ||
+        check_cuda(cudaFuncSetAttribute(sif::enc_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
+        check_cuda(cudaFuncSetAttribute(sif::enc_members, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMembers)) ||
+        check_cuda(cudaFuncSetAttribute(sif::enc_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemPack)))
+      return SIF_ERR_CUDA;
+    attrs = true;
   }
-  if (check_cuda(cudaLaunchKernelEx(&cfg, kfn, a))) return SIF_ERR_CUDA;
+  static int g_stream = 0, g_members = 0, g_abq = 0, g_pack = 0;
+  if (!g_stream) {
+    g_stream = resident_grid(sif::enc_stream, sif::CNT, kSmemStream, 1ull << 30);
+    g_members = resident_grid(sif::enc_members, sif::CNT, kSmemMembers, 1ull << 30);
+    g_abq = resident_grid(sif::enc_abq, sif::CNT, 0, 1ull << 30);
+    g_pack = resident_grid(sif::enc_pack, sif::CNT, kSmemPack, 1ull << 30);
+  }
+  const unsigned nch = (unsigned)p->tiles;
+  const unsigned n = (unsigned)p->n;
+  sif::enc_prep<<<n, 256, 0, s>>>(a);
+  sif::enc_stream<<<std::min<unsigned>(nch, g_stream), sif::CNT, kSmemStream, s>>>(a);
+  sif::enc_select<<<n, sif::SNT, kSmemSelect, s>>>(a);
+  if (!atkf) {
+    sif::enc_members<<<std::min<unsigned>(nch, g_members), sif::CNT, kSmemMembers, s>>>(a);
+    if (c->mode != SIF_MODE_FIXED) sif::enc_abq<<<std::min<unsigned>(nch, g_abq), sif::CNT, 0, s>>>(a);
+    sif::enc_layout<<<n, 256, 0, s>>>(a);
+    sif::enc_pack<<<std::min<unsigned>(nch, g_pack), sif::CNT, kSmemPack, s>>>(a);
+    sif::enc_crc<<<n, 256, 0, s>>>(a);
+  }
   return check_cuda(cudaGetLastError());
 }
 
 int sif_enc_run(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint64_t* out_len, int32_t* status, void* stream) {
   if (!p || !c || !ws || !out_len || !status) return SIF_ERR_INVALID_ARG;
+  if (p->flags) return SIF_ERR_INVALID_ARG;  // an ATKF-only plan
   return enc_launch(p, c, ws, out_len, status, 0, nullptr, nullptr, (cudaStream_t)stream);
 }
 
@@ -254,12 +320,12 @@ int sif_atkf_batched(const sif_enc_desc* d, int n, const sif_codec_cfg* c, void*
     off[i] = acc;
     acc += sif::keep_count(c->s, (uint64_t)d[i].rows * d[i].cols);
   }
-  uint8_t* w = (uint8_t*)ws;
-  if (n > 0 &&
-      check_cuda(cudaMemcpyAsync(w + p.ws_aux_off + up((uint64_t)c->m_plus + c->m_minus, 256), off.data(), 8ull * n,
-                                 cudaMemcpyHostToDevice, s)))
+  const EncWs w = enc_ws(p.n, (uint64_t)p.tiles, p.max_blocks, (uint64_t)p.cap_smem, (uint64_t)c->m_plus + c->m_minus);
+  if (n > 0 && check_cuda(cudaMemcpyAsync((uint8_t*)ws + w.keptoff, off.data(), 8ull * n, cudaMemcpyHostToDevice, s)))
     return SIF_ERR_CUDA;
-  return enc_launch(&p, c, ws, nullptr, status, 1, kept, tau3, s);
+  st = enc_launch(&p, c, ws, nullptr, status, 1, kept, tau3, s);
+  if (st) return st;
+  return check_cuda(cudaStreamSynchronize(s));
 }
 
 // ------------------------------------------------------------------ decode
