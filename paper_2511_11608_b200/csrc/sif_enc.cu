@@ -34,7 +34,10 @@
 namespace sif {
 
 constexpr int CH = 4096;           // elements per chunk
+constexpr int UNITS = 8;           // warp-streamed units per chunk
+constexpr int UE = CH / UNITS;     // elements per unit
 constexpr int CNT = 256;           // threads of chunk kernels
+constexpr int SEG = 65536;         // CRC segment bytes per CTA
 constexpr int DSH = 19;            // digit = |x| key >> 19 (12 bits)
 constexpr int ND = 4096;           // digits per sign
 constexpr int MAXB = 32;           // max blocks (M+ + M-) per IF
@@ -58,8 +61,8 @@ struct IfInfo {
   uint32_t ch0, nch;
   int32_t hslot;
   uint32_t pad;
-  uint64_t list_off;  // workspace byte offset: vals u32[T], then idx u32[T]
-  uint64_t gat_off;   // gather spill: vals u32[T], then idx u32[T]
+  uint64_t list_off;  // workspace byte offset of the candidate list: uint2[T]
+  uint64_t gat_off;   // gather spill / member slots: uint2[T]
 };
 
 // Dynamic per-IF state (device).
@@ -77,6 +80,8 @@ struct IfSt {
   double o64[MAXB], inv64[MAXB];
   uint64_t off_meta[MAXB], bit_cols[MAXB], bit_codes[MAXB];
   uint64_t P;
+  uint32_t crc_acc, seg_done;
+  uint32_t bcount[MAXB];  // block member totals (K4 atomics)
 };
 
 struct EArgs {
@@ -85,8 +90,8 @@ struct EArgs {
   int n, nch, maxb, atkf_only;
   const uint32_t* ch_if;
   const uint32_t* ch_e0;
-  uint32_t* ch_off;
-  uint32_t* ch_cnt;
+  uint32_t* u_off;     // [nch][UNITS] list offset of each unit's candidates
+  uint32_t* u_cnt;     // [nch][UNITS]
   uint32_t* ch_bcnt;   // [nch][maxb]
   uint32_t* ch_bpre;   // [nch][maxb]
   int32_t* ch_blast;   // [nch][maxb] row of the block's last member in the chunk, -1 if none
@@ -101,13 +106,16 @@ struct EArgs {
   int64_t* kept_out;
   const uint64_t* kept_off;
   double* tau3;
+  const uint32_t* seg_base;  // [n+1] prefix of CRC segments per IF
 };
 
-__device__ __forceinline__ uint32_t* lv(const EArgs& a, const IfInfo& f) {
-  return reinterpret_cast<uint32_t*>(a.ws + f.list_off);
+// candidate list of an IF: (float bits, flat index) entries
+__device__ __forceinline__ uint2* le(const EArgs& a, const IfInfo& f) {
+  return reinterpret_cast<uint2*>(a.ws + f.list_off);
 }
-__device__ __forceinline__ uint32_t* li(const EArgs& a, const IfInfo& f) {
-  return reinterpret_cast<uint32_t*>(a.ws + f.list_off) + f.T;
+// K3 gather spill, then the regrouped members (K4 output): per chunk a slot of CH entries
+__device__ __forceinline__ uint2* me(const EArgs& a, const IfInfo& f) {
+  return reinterpret_cast<uint2*>(a.ws + f.gat_off);
 }
 
 // quant.py:59-62 in float64: floor((v - vmin)/o64 + 0.5) clipped to [0, levels].  The
@@ -141,38 +149,36 @@ __device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t x) {
 // ---------------------------------------------------------------------------------------
 // List of (float bits, flat index) pairs: SMEM up to `cap` entries, global beyond.
 struct List {
-  uint32_t* sb;
-  uint32_t* si;
-  uint32_t* gb;
-  uint32_t* gi;
+  uint2* s;
+  uint2* g;
   uint32_t cap;
-  __device__ __forceinline__ uint32_t bits(uint32_t i) const { return i < cap ? sb[i] : __ldcg(gb + (i - cap)); }
-  __device__ __forceinline__ uint32_t idx(uint32_t i) const { return i < cap ? si[i] : __ldcg(gi + (i - cap)); }
   __device__ __forceinline__ void set(uint32_t i, uint32_t b, uint32_t x) const {
-    if (i < cap) { sb[i] = b; si[i] = x; }
-    else { __stcg(gb + (i - cap), b); __stcg(gi + (i - cap), x); }
+    if (i < cap) s[i] = make_uint2(b, x);
+    else __stcg(g + (i - cap), make_uint2(b, x));
   }
 };
 
-// Visit every list element (order-free).  Global parts are read 4 elements per thread per
-// step with independent loads.
+// Visit every list element (order-free).  Global parts are read 4 entries per thread per
+// step with independent 8-byte loads.
 template <int NT, class F>
 __device__ __forceinline__ void list_foreach(const List& L, uint32_t n, F f) {
   const uint32_t ns = n < L.cap ? n : L.cap;
-  for (uint32_t i = threadIdx.x; i < ns; i += NT) f(L.sb[i], L.si[i]);
+  for (uint32_t i = threadIdx.x; i < ns; i += NT) {
+    const uint2 e = L.s[i];
+    f(e.x, e.y);
+  }
   if (n > L.cap) {
     const uint32_t m = n - L.cap;
     for (uint32_t i0 = 0; i0 < m; i0 += 4 * NT) {
-      uint32_t b[4], x[4];
+      uint2 e[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint32_t i = i0 + threadIdx.x + k * NT;
-        b[k] = i < m ? __ldcg(L.gb + i) : 0u;
-        x[k] = i < m ? __ldcg(L.gi + i) : 0u;
+        e[k] = i < m ? __ldcg(L.g + i) : make_uint2(0, 0);
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (i0 + threadIdx.x + k * NT < m) f(b[k], x[k]);
+        if (i0 + threadIdx.x + k * NT < m) f(e[k].x, e[k].y);
     }
   }
 }
@@ -399,89 +405,135 @@ __device__ SelRes select_exact(SelSh& sh, uint32_t* scratch, const List& L, uint
 }
 
 // ---------------------------------------------------------------------------------------
-// Stream one chunk (n <= CH elements starting at flat index e0): candidates (|x| >= lo for
-// x >= 0, |x| >= lo_neg for x < 0) are staged per warp in flat order at sv/si[w*EW ...),
-// wcnt[w] = count.  Warp w owns elements [w*EW, (w+1)*EW) of the chunk; each lane loads V
-// consecutive elements per step (one 128-bit load).  hist (if non-null): per-sign digit
-// counts of the candidates.  Per-thread outputs: max |x| key, count of |x| >= lo, digit range.
-template <int DT, int NT>
-__device__ __forceinline__ void stream_chunk(const void* x, uint32_t e0, uint32_t n, uint32_t lo, uint32_t lo_neg,
-                                             uint32_t* sv, uint32_t* si, uint32_t* hist, uint32_t* wcnt,
-                                             uint32_t& mk, uint32_t& clo, uint32_t& dmin, uint32_t& dmax) {
-  constexpr int NW = NT / 32;
-  constexpr int EW = CH / NW;
-  constexpr int V = DT == SIF_DTYPE_F32 ? 4 : 8;
-  constexpr int IT = EW / (32 * V);
-  static_assert(IT >= 1, "chunk too small for the CTA");
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t wb = (uint32_t)w * EW;
-  uint32_t v[IT][V];
-  const bool full = wb + EW <= n;
+// A unit is UE = 512 consecutive elements of a chunk, streamed by one warp; lane l owns the
+// 16 contiguous elements [16l, 16l+16) (fp32: four 128-bit loads, bf16: two).
+struct Raw {
+  uint4 r[4];
+};
+
+__device__ __forceinline__ void load_unit(const void* xp, uint32_t dtype, uint32_t e0, uint32_t n, Raw& raw) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t b = 16u * lane;
+  if (dtype == SIF_DTYPE_F32) {
+    const uint32_t* x = reinterpret_cast<const uint32_t*>(xp) + e0 + b;
+    if (b + 16 <= n) {
 #pragma unroll
-  for (int j = 0; j < IT; ++j) {
-    const uint32_t o = wb + (uint32_t)j * 32u * V + (uint32_t)lane * V;
-    if (full) {
-      if (DT == SIF_DTYPE_F32) {
-        const uint4 q = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(x) + e0 + o));
-        v[j][0] = q.x; v[j][1] = q.y; v[j][2] = q.z; v[j][3] = q.w;
-      } else {
-        const uint4 q = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const unsigned short*>(x) + e0 + o));
-        const uint32_t ww[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) { v[j][2 * k] = ww[k] << 16; v[j][2 * k + 1] = ww[k] & 0xFFFF0000u; }
-      }
+      for (int j = 0; j < 4; ++j) raw.r[j] = __ldg(reinterpret_cast<const uint4*>(x) + j);
     } else {
 #pragma unroll
-      for (int k = 0; k < V; ++k) {
-        const uint32_t e = o + k;
-        uint32_t b = 0;
-        if (e < n) {
-          if (DT == SIF_DTYPE_F32) b = __ldcs(reinterpret_cast<const uint32_t*>(x) + e0 + e);
-          else b = (uint32_t)__ldcs(reinterpret_cast<const unsigned short*>(x) + e0 + e) << 16;
+      for (int j = 0; j < 4; ++j) {
+        uint32_t c[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) c[k] = b + 4 * j + k < n ? __ldg(x + 4 * j + k) : 0u;
+        raw.r[j] = make_uint4(c[0], c[1], c[2], c[3]);
+      }
+    }
+  } else {
+    const unsigned short* x = reinterpret_cast<const unsigned short*>(xp) + e0 + b;
+    raw.r[2] = make_uint4(0, 0, 0, 0);
+    raw.r[3] = make_uint4(0, 0, 0, 0);
+    if (b + 16 <= n) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) raw.r[j] = __ldg(reinterpret_cast<const uint4*>(x) + j);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        uint32_t c[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t e = b + 8 * j + 2 * k;
+          const uint32_t lo16 = e < n ? (uint32_t)__ldg(x + 8 * j + 2 * k) : 0u;
+          const uint32_t hi16 = e + 1 < n ? (uint32_t)__ldg(x + 8 * j + 2 * k + 1) : 0u;
+          c[k] = lo16 | (hi16 << 16);
         }
-        v[j][k] = b;
+        raw.r[j] = make_uint4(c[0], c[1], c[2], c[3]);
       }
     }
   }
-  uint32_t run = 0;
-  const uint32_t lt = (1u << lane) - 1u;
-  (void)lt;
+}
+
+__device__ __forceinline__ uint32_t u4c(const uint4& q, int k) {
+  return k == 0 ? q.x : k == 1 ? q.y : k == 2 ? q.z : q.w;
+}
+
+// Classify one unit (n valid elements from flat index e0): candidates (|x| >= lo for x >= 0,
+// |x| >= lo_neg for x < 0) are written in flat order to the warp staging `stage` as
+// (bits, flat index); returns the count (warp-uniform).  asym: lo != lo_neg, then `clo`
+// accumulates the count of |x| >= lo (otherwise that count is the candidate count).
+template <int DT>
+__device__ __forceinline__ uint32_t classify_unit(const Raw& raw, uint32_t e0, uint32_t n, uint32_t lo, uint32_t lo_neg,
+                                                  bool asym, uint2* stage, uint32_t& clo) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t b0 = 16u * lane;
+  uint32_t v[16];
 #pragma unroll
-  for (int j = 0; j < IT; ++j) {
-    const uint32_t o = wb + (uint32_t)j * 32u * V + (uint32_t)lane * V;
-    uint32_t m = 0;
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-      const uint32_t b = v[j][k];
-      const uint32_t key = b & 0x7FFFFFFFu;
-      const bool in = full || (o + k < n);
-      mk = max(mk, in ? key : 0u);
-      const uint32_t thr = (b >> 31) ? lo_neg : lo;
-      const bool c = in && key >= thr;
-      clo += (in && key >= lo) ? 1u : 0u;
-      m |= c ? (1u << k) : 0u;
-    }
-    const uint32_t cnt = __popc(m);
-    const uint32_t incl = warp_incl_scan_u32(cnt);
-    uint32_t pos = wb + run + incl - cnt;
-    run += __shfl_sync(0xFFFFFFFFu, incl, 31);
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-      if ((m >> k) & 1u) {
-        const uint32_t b = v[j][k];
-        sv[pos] = b;
-        si[pos] = e0 + o + k;
-        ++pos;
-        if (hist) {
-          const uint32_t d = (b & 0x7FFFFFFFu) >> DSH;
-          atomicAdd(&hist[((b >> 31) ? ND : 0) + d], 1u);
-          dmin = min(dmin, d);
-          dmax = max(dmax, d);
-        }
-      }
+  for (int k = 0; k < 16; ++k) {
+    if (DT == SIF_DTYPE_F32) v[k] = u4c(raw.r[k >> 2], k & 3);
+    else {
+      const uint32_t wv = u4c(raw.r[k >> 3], (k >> 1) & 3);
+      v[k] = (k & 1) ? (wv & 0xFFFF0000u) : (wv << 16);
     }
   }
-  if (lane == 0) wcnt[w] = run;
+  const uint32_t nl = n >= b0 + 16 ? 16u : (n > b0 ? n - b0 : 0u);
+  const uint32_t vmask = nl == 16 ? 0xFFFFu : ((1u << nl) - 1u);
+  uint32_t m = 0;
+  if (!asym) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) m |= ((v[k] & 0x7FFFFFFFu) >= lo ? 1u : 0u) << k;
+  } else {
+    uint32_t ml = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const uint32_t key = v[k] & 0x7FFFFFFFu;
+      m |= (key >= ((v[k] >> 31) ? lo_neg : lo) ? 1u : 0u) << k;
+      ml |= (key >= lo ? 1u : 0u) << k;
+    }
+    clo += __popc(ml & vmask);
+  }
+  m &= vmask;
+  const uint32_t cnt = __popc(m);
+  const uint32_t incl = warp_incl_scan_u32(cnt);
+  uint32_t pos = incl - cnt;
+  const uint32_t ex = e0 + b0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const bool p = (m >> k) & 1u;
+    if (p) stage[pos] = make_uint2(v[k], ex + k);
+    pos += p ? 1u : 0u;
+  }
+  return __shfl_sync(0xFFFFFFFFu, incl, 31);
+}
+
+__device__ __forceinline__ uint32_t classify_any(uint32_t dtype, const Raw& raw, uint32_t e0, uint32_t n, uint32_t lo,
+                                                 uint32_t lo_neg, bool asym, uint2* stage, uint32_t& clo) {
+  if (dtype == SIF_DTYPE_BF16) return classify_unit<SIF_DTYPE_BF16>(raw, e0, n, lo, lo_neg, asym, stage, clo);
+  return classify_unit<SIF_DTYPE_F32>(raw, e0, n, lo, lo_neg, asym, stage, clo);
+}
+
+// Copy a staged unit (cnt candidates) to the IF's list at `dst`; max key, digit histogram
+// (if hist) and digit range of the candidates.
+__device__ __forceinline__ void emit_unit(const uint2* stage, uint32_t cnt, uint2* dst, uint32_t* hist, uint32_t& mk,
+                                          uint32_t& dmin, uint32_t& dmax) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t k = lane; k < cnt; k += 32) {
+    const uint2 e = stage[k];
+    dst[k] = e;
+    const uint32_t key = e.x & 0x7FFFFFFFu;
+    mk = max(mk, key);
+    if (hist) {
+      const uint32_t d = key >> DSH;
+      atomicAdd(&hist[((e.x >> 31) ? ND : 0) + d], 1u);
+      dmin = min(dmin, d);
+      dmax = max(dmax, d);
+    }
+  }
+}
+
+// Unit geometry: flat start and valid count of unit (c, u).
+__device__ __forceinline__ void unit_span(const EArgs& a, const IfInfo& f, uint32_t c, uint32_t u, uint32_t& e0,
+                                          uint32_t& n) {
+  e0 = a.ch_e0[c] + u * (uint32_t)UE;
+  n = e0 < f.T ? (uint32_t)min((uint64_t)UE, f.T - e0) : 0u;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -489,20 +541,51 @@ __device__ __forceinline__ void stream_chunk(const void* x, uint32_t e0, uint32_
 // bracket is detected in K3 and the IF re-streamed).
 __global__ void __launch_bounds__(256) enc_prep(EArgs a) {
   constexpr int NT = 256;
-  __shared__ uint32_t sh8k[8192];
+  constexpr int EXACT_T = 8192;  // IFs up to this size get the exact tau key as lo
+  __shared__ uint32_t sh8k[8192 + 2048];
   __shared__ SelSh sh;
   const int i = blockIdx.x, tid = threadIdx.x;
   const IfInfo f = a.info[i];
   IfSt& st = a.st[i];
   for (int b = tid; b < a.maxb; b += NT) { st.bmin[b] = 0x7FFFFFFFu; st.bmax[b] = 0u; }
   for (int k = tid; k < a.maxb * 16; k += NT) st.S[k] = 0ull;
+  for (int b = tid; b < a.maxb; b += NT) st.bcount[b] = 0u;
   if (f.hslot >= 0) {
     uint4* h = reinterpret_cast<uint4*>(a.hist + (uint64_t)f.hslot * 2 * ND);
     for (int k = tid; k < 2 * ND / 4; k += NT) h[k] = make_uint4(0, 0, 0, 0);
   }
   const uint64_t T = f.T, kk = f.kk;
   uint32_t lo = 1;
-  if (T > 32768 && kk > 0 && 2 * kk <= T) {
+  if (T <= EXACT_T && kk > 0) {
+    // exact: the kk-th largest |x| key by a 3-level radix select in shared memory
+    uint32_t* keys = sh8k;
+    uint32_t* h = sh8k + 8192;
+    const uint32_t n = (uint32_t)T;
+    for (uint32_t e = tid; e < n; e += NT) {
+      const uint32_t b = f.dtype == SIF_DTYPE_F32 ? __ldg(reinterpret_cast<const uint32_t*>(f.x) + e)
+                                                  : (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(f.x) + e) << 16;
+      keys[e] = b & 0x7FFFFFFFu;
+    }
+    uint64_t r = kk;
+    uint32_t prefix = 0, mask = 0;
+    const int shifts[3] = {20, 9, 0}, widths[3] = {11, 11, 9};
+    for (int lev = 0; lev < 3; ++lev) {
+      const int shf = shifts[lev], nb = 1 << widths[lev];
+      for (int k = tid; k < nb; k += NT) h[k] = 0;
+      __syncthreads();
+      for (uint32_t e = tid; e < n; e += NT) {
+        const uint32_t key = keys[e];
+        if ((key & mask) == prefix) atomicAdd(&h[(key >> shf) & (uint32_t)(nb - 1)], 1u);
+      }
+      __syncthreads();
+      find_digit<NT>(sh, h, nb, r);
+      prefix |= sh.fd_digit << shf;
+      mask |= (uint32_t)(nb - 1) << shf;
+      r -= sh.fd_above;
+      __syncthreads();
+    }
+    lo = prefix > 0 ? prefix : 1u;  // tau == 0: every nonzero is a candidate
+  } else if (T > 32768 && kk > 0 && 2 * kk <= T) {
     constexpr int NSECT = 512, SB = 8192, PERT = NSECT / NT;
     for (int k = tid; k < SB; k += NT) sh8k[k] = 0;
     uint32_t sv[PERT][8];
@@ -555,100 +638,105 @@ __global__ void __launch_bounds__(256) enc_prep(EArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------
-// K2: stream chunks (persistent CTAs).
-template <int NT>
-__device__ __forceinline__ void stream_and_emit(const EArgs& a, uint32_t c, const IfInfo& f, uint32_t lo,
-                                                uint32_t lo_neg, uint32_t* sv, uint32_t* si, uint32_t* hist,
-                                                uint32_t* wcnt, uint32_t* misc, uint32_t* list_cursor,
-                                                bool global_reserve, IfSt* st) {
-  constexpr int NW = NT / 32;
-  constexpr int EW = CH / NW;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const uint32_t e0 = a.ch_e0[c];
-  const uint32_t n = (uint32_t)min((uint64_t)CH, f.T - e0);
-  uint32_t mk = 0, clo = 0, dmin = 0xFFFFFFFFu, dmax = 0;
-  if (f.dtype == SIF_DTYPE_BF16)
-    stream_chunk<SIF_DTYPE_BF16, NT>(f.x, e0, n, lo, lo_neg, sv, si, hist, wcnt, mk, clo, dmin, dmax);
-  else
-    stream_chunk<SIF_DTYPE_F32, NT>(f.x, e0, n, lo, lo_neg, sv, si, hist, wcnt, mk, clo, dmin, dmax);
+// K2: stream chunks.  Each CTA owns a contiguous range of chunks; warp w streams unit w of
+// every chunk (UE elements, 128-bit loads, two units prefetched), stages its candidates in
+// flat order, reserves list space with one atomic per unit and copies them out coalesced.
+// Per-IF reductions (max key, count >= lo, SMEM digit histogram) are flushed when the IF
+// changes, so the hot loop has no CTA barrier.
+__device__ __forceinline__ void flush_if_stream(const EArgs& a, uint32_t ifi, uint32_t* hist, uint32_t& mk,
+                                                uint32_t& clo, uint32_t& dmin, uint32_t& dmax, uint32_t* sdr) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  IfSt& st = a.st[ifi];
   mk = __reduce_max_sync(0xFFFFFFFFu, mk);
   clo = __reduce_add_sync(0xFFFFFFFFu, clo);
-  dmin = __reduce_min_sync(0xFFFFFFFFu, dmin);
-  dmax = __reduce_max_sync(0xFFFFFFFFu, dmax);
+  const uint32_t d0 = __reduce_min_sync(0xFFFFFFFFu, dmin), d1 = __reduce_max_sync(0xFFFFFFFFu, dmax);
   if (lane == 0) {
-    atomicMax(&misc[0], mk);
-    atomicAdd(&misc[1], clo);
-    atomicMin(&misc[2], dmin);
-    atomicMax(&misc[3], dmax);
+    atomicMax(&st.maxkey, mk);
+    if (clo) atomicAdd(&st.cnt_lo, clo);
+    atomicMin(&sdr[0], d0);
+    atomicMax(&sdr[1], d1);
   }
   __syncthreads();
-  if (tid == 0) {
-    uint32_t acc = 0;
-    for (int k = 0; k < NW; ++k) { const uint32_t t = wcnt[k]; wcnt[NW + k] = acc; acc += t; }
-    uint32_t off;
-    if (global_reserve) {
-      off = atomicAdd(&st->ncand, acc);
-      atomicMax(&st->maxkey, misc[0]);
-      atomicAdd(&st->cnt_lo, misc[1]);
-    } else {
-      off = *list_cursor;
-      *list_cursor = off + acc;
-    }
-    a.ch_off[c] = off;
-    a.ch_cnt[c] = acc;
-    misc[4] = off;
-  }
-  __syncthreads();
-  {
-    uint32_t* gv = lv(a, f);
-    uint32_t* gi = li(a, f);
-    const uint32_t base = misc[4] + wcnt[NW + w];
-    const uint32_t m = wcnt[w];
-    for (uint32_t k = lane; k < m; k += 32) {
-      gv[base + k] = sv[w * EW + k];
-      gi[base + k] = si[w * EW + k];
-    }
-  }
-  if (hist && global_reserve && misc[2] <= misc[3]) {
-    uint32_t* gh = a.hist + (uint64_t)f.hslot * 2 * ND;
-    const uint32_t d0 = misc[2], nr = misc[3] - misc[2] + 1;
-    for (uint32_t k = tid; k < 2 * nr; k += NT) {
-      const uint32_t d = (k < nr ? 0u : (uint32_t)ND) + d0 + (k < nr ? k : k - nr);
+  const int hs = a.info[ifi].hslot;
+  if (hs >= 0 && sdr[0] <= sdr[1]) {
+    uint32_t* gh = a.hist + (uint64_t)hs * 2 * ND;
+    const uint32_t lo = sdr[0], nr = sdr[1] - sdr[0] + 1;
+    for (uint32_t k = tid; k < 2 * nr; k += CNT) {
+      const uint32_t d = (k < nr ? 0u : (uint32_t)ND) + lo + (k < nr ? k : k - nr);
       const uint32_t h = hist[d];
       if (h) { atomicAdd(gh + d, h); hist[d] = 0; }
     }
   }
   __syncthreads();
-  if (tid == 0) { misc[0] = 0; misc[1] = 0; misc[2] = 0xFFFFFFFFu; misc[3] = 0; }
+  if (tid == 0) { sdr[0] = 0xFFFFFFFFu; sdr[1] = 0; }
+  mk = 0; clo = 0; dmin = 0xFFFFFFFFu; dmax = 0;
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(CNT) enc_stream(EArgs a) {
+__global__ void __launch_bounds__(CNT, 3) enc_stream(EArgs a) {
   extern __shared__ __align__(16) uint8_t dsm_raw[];
   uint32_t* dsm = reinterpret_cast<uint32_t*>(dsm_raw);
-  __shared__ uint32_t wcnt[2 * (CNT / 32)];
-  __shared__ uint32_t misc[8];
-  uint32_t* sv = dsm;
-  uint32_t* si = dsm + CH;
-  uint32_t* hist = dsm + 2 * CH;
-  for (int k = threadIdx.x; k < 2 * ND; k += CNT) hist[k] = 0;
-  if (threadIdx.x == 0) { misc[0] = 0; misc[1] = 0; misc[2] = 0xFFFFFFFFu; misc[3] = 0; }
+  __shared__ uint32_t sdr[2];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  uint2* stage = reinterpret_cast<uint2*>(dsm) + w * UE;
+  uint32_t* hist = dsm + (CNT / 32) * 2 * UE;
+  for (int k = tid; k < 2 * ND; k += CNT) hist[k] = 0;
+  if (tid == 0) { sdr[0] = 0xFFFFFFFFu; sdr[1] = 0; }
   __syncthreads();
-  for (uint32_t c = blockIdx.x; c < (uint32_t)a.nch; c += gridDim.x) {
+  const uint32_t nch = (uint32_t)a.nch;
+  const uint32_t c0 = (uint32_t)((uint64_t)nch * blockIdx.x / gridDim.x);
+  const uint32_t c1 = (uint32_t)((uint64_t)nch * (blockIdx.x + 1) / gridDim.x);
+  if (c0 >= c1) return;
+  uint32_t cur = a.ch_if[c0];
+  IfInfo f = a.info[cur];
+  uint32_t lo = a.st[cur].lo, lo_neg = a.st[cur].lo_neg;
+  uint32_t mk = 0, clo = 0, dmin = 0xFFFFFFFFu, dmax = 0;
+  Raw r0, r1;
+  auto prefetch = [&](uint32_t c, Raw& r) {
+    const IfInfo& g = a.info[a.ch_if[c]];
+    uint32_t e0, n;
+    unit_span(a, g, c, (uint32_t)w, e0, n);
+    if (n) load_unit(g.x, g.dtype, e0, n, r);
+  };
+  prefetch(c0, r0);
+  if (c0 + 1 < c1) prefetch(c0 + 1, r1);
+  for (uint32_t c = c0; c < c1; ++c) {
     const uint32_t ifi = a.ch_if[c];
-    const IfInfo f = a.info[ifi];
-    IfSt* st = a.st + ifi;
-    const uint32_t lo = st->lo, lo_neg = st->lo_neg;
-    stream_and_emit<CNT>(a, c, f, lo, lo_neg, sv, si, f.hslot >= 0 ? hist : nullptr, wcnt, misc, nullptr, true, st);
+    if (ifi != cur) {
+      flush_if_stream(a, cur, hist, mk, clo, dmin, dmax, sdr);
+      cur = ifi;
+      f = a.info[ifi];
+      lo = a.st[ifi].lo;
+      lo_neg = a.st[ifi].lo_neg;
+    }
+    Raw r2;
+    if (c + 2 < c1) prefetch(c + 2, r2);
+    uint32_t e0, n;
+    unit_span(a, f, c, (uint32_t)w, e0, n);
+    const bool asym = lo != lo_neg;
+    uint32_t cnt = 0;
+    if (n) cnt = classify_any(f.dtype, r0, e0, n, lo, lo_neg, asym, stage, clo);
+    if (!asym && lane == 0) clo += cnt;
+    uint32_t off = 0;
+    if (lane == 0) {
+      off = cnt ? atomicAdd(&a.st[ifi].ncand, cnt) : 0u;
+      a.u_off[(uint64_t)c * UNITS + w] = off;
+      a.u_cnt[(uint64_t)c * UNITS + w] = cnt;
+    }
+    off = __shfl_sync(0xFFFFFFFFu, off, 0);
+    __syncwarp();
+    emit_unit(stage, cnt, le(a, f) + off, f.hslot >= 0 ? hist : nullptr, mk, dmin, dmax);
+    __syncwarp();
+    r0 = r1;
+    r1 = r2;
   }
+  flush_if_stream(a, cur, hist, mk, clo, dmin, dmax, sdr);
 }
 
 // ---------------------------------------------------------------------------------------
 // K3: per-IF selection.
 struct K3Sh {
   SelSh s;
-  uint32_t wcnt[2 * (SNT / 32)];
-  uint32_t misc[8];
   uint32_t cursor;
   uint32_t nA, nB;
   uint32_t keptA[2];
@@ -687,10 +775,36 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
     lo = floor_lo;
     lo_neg = floor_lo;
     for (int k = tid; k < 2 * ND; k += NT) hist[k] = 0;
-    if (tid == 0) { k3.cursor = 0; k3.misc[0] = 0; k3.misc[1] = 0; k3.misc[2] = 0xFFFFFFFFu; k3.misc[3] = 0; }
+    if (tid == 0) k3.cursor = 0;
     __syncthreads();
-    for (uint32_t c = f.ch0; c < f.ch0 + f.nch; ++c)
-      stream_and_emit<NT>(a, c, f, lo, lo_neg, gbuf, gbuf + CH, hist, k3.wcnt, k3.misc, &k3.cursor, false, &st);
+    {
+      const int lane = tid & 31, w = tid >> 5;
+      if (w < UNITS) {
+        uint2* stage = reinterpret_cast<uint2*>(gbuf) + w * UE;
+        uint32_t mk = 0, clo = 0, dmin = 0, dmax = 0;
+        for (uint32_t c = f.ch0; c < f.ch0 + f.nch; ++c) {
+          uint32_t e0, n;
+          unit_span(a, f, c, (uint32_t)w, e0, n);
+          uint32_t cnt = 0;
+          if (n) {
+            Raw r;
+            load_unit(f.x, f.dtype, e0, n, r);
+            cnt = classify_any(f.dtype, r, e0, n, lo, lo_neg, lo != lo_neg, stage, clo);
+          }
+          uint32_t off = 0;
+          if (lane == 0) {
+            off = atomicAdd(&k3.cursor, cnt);
+            a.u_off[(uint64_t)c * UNITS + w] = off;
+            a.u_cnt[(uint64_t)c * UNITS + w] = cnt;
+          }
+          off = __shfl_sync(0xFFFFFFFFu, off, 0);
+          __syncwarp();
+          emit_unit(stage, cnt, le(a, f) + off, hist, mk, dmin, dmax);
+          __syncwarp();
+        }
+      }
+    }
+    __syncthreads();
     ncand = k3.cursor;
     hist_ok = true;
   } else if (f.hslot >= 0) {
@@ -699,7 +813,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
     for (int k = tid; k < 2 * ND / 4; k += NT) h4[k] = __ldcg(gh + k);
     hist_ok = true;
   }
-  const List L{nullptr, nullptr, lv(a, f), li(a, f), 0};
+  const List L{nullptr, le(a, f), 0};
   if (!hist_ok) {
     for (int k = tid; k < 2 * ND; k += NT) hist[k] = 0;
     __syncthreads();
@@ -737,8 +851,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   int dtau = -1;  // digit of tau on the fast path (-1: every candidate bin counts fully)
   const bool use_cls = a.lam > 0.0 && kk > 0 && !only_nonzero;
   const bool fast = !zero_mode && !use_cls;
-  List A{gbuf, gbuf + GSM, reinterpret_cast<uint32_t*>(a.ws + f.gat_off),
-         reinterpret_cast<uint32_t*>(a.ws + f.gat_off) + f.T, GSM};
+  List A{reinterpret_cast<uint2*>(gbuf), me(a, f), GSM};
   uint32_t nA = 0;
   if (kk > 0 && !only_nonzero) {
     if (zero_mode && cnt_nz < kk) {
@@ -810,15 +923,16 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   if (a.atkf_only) {
     int64_t* out = a.kept_out + a.kept_off[ifi];
     uint64_t run = 0;
-    for (uint32_t c = f.ch0; c < f.ch0 + f.nch; ++c) {
-      const uint32_t off = a.ch_off[c], cn = a.ch_cnt[c];
+    for (uint64_t u = (uint64_t)f.ch0 * UNITS; u < (uint64_t)(f.ch0 + f.nch) * UNITS; ++u) {
+      const uint32_t off = a.u_off[u], cn = a.u_cnt[u];
       for (uint32_t base = 0; base < cn; base += NT) {
         const uint32_t j = base + tid;
         bool kp = false;
         uint32_t x = 0;
         if (j < cn) {
-          x = __ldcg(L.gi + off + j);
-          kp = kept_of(__ldcg(L.gb + off + j), x);
+          const uint2 e = __ldcg(L.g + off + j);
+          x = e.y;
+          kp = kept_of(e.x, e.y);
         }
         uint32_t tot;
         const uint32_t ex = block_excl_scan_u32(kp ? 1u : 0u, sh.red, &tot);
@@ -1034,272 +1148,294 @@ __device__ __forceinline__ void load_kept_ctx(KeptCtx& k, const IfSt& st, uint64
 }
 
 // ---------------------------------------------------------------------------------------
-// K4: kept test, block ids, stable regroup of each chunk segment by block.
-struct K4Sh {
-  KeptCtx kc;
-  uint32_t cur_if;
-  uint32_t wcnt[CNT / 32][MAXB];
-  uint32_t wmin[CNT / 32][MAXB];
-  uint32_t wmax[CNT / 32][MAXB];
-  uint32_t wlast[CNT / 32][MAXB];
-  uint32_t wpos[CNT / 32][MAXB];
-  uint32_t bstart[MAXB];
+// Chunk-kernel work split: global warp gw of GW owns chunks [nch*gw/GW, nch*(gw+1)/GW).
+__device__ __forceinline__ void warp_range(const EArgs& a, uint32_t& c0, uint32_t& c1) {
+  const uint64_t GW = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  c0 = (uint32_t)((uint64_t)a.nch * gw / GW);
+  c1 = (uint32_t)((uint64_t)a.nch * (gw + 1) / GW);
+}
+
+// ---------------------------------------------------------------------------------------
+// K4: one warp per chunk: kept test, block id, per-block count / min / max / last row, and
+// a stable regroup of the chunk's members by block into the member slot (CSR order inside a
+// block = flat order).  Also zeroes this chunk's share of the IF's output buffer.
+struct K4W {
+  uint32_t cnt[MAXB], mn[MAXB], mx[MAXB], xl[MAXB], pos[MAXB];
 };
 
 __global__ void __launch_bounds__(CNT) enc_members(EArgs a) {
-  constexpr int NW = CNT / 32;
-  extern __shared__ __align__(16) uint8_t dsm_raw[];
-  uint32_t* dsm = reinterpret_cast<uint32_t*>(dsm_raw);
-  __shared__ K4Sh sh;
-  uint32_t* iv = dsm;
-  uint32_t* ix = dsm + CH;
-  uint32_t* ov = dsm + 2 * CH;
-  uint32_t* ox = dsm + 3 * CH;
-  int8_t* bid = reinterpret_cast<int8_t*>(dsm + 4 * CH);
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  __shared__ KeptCtx kcs[CNT / 32];
+  __shared__ K4W wst[CNT / 32];
+  __shared__ int8_t sblk[CNT / 32][CH];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t lt = (1u << lane) - 1u;
-  if (tid == 0) sh.cur_if = 0xFFFFFFFFu;
-  __syncthreads();
-  for (uint32_t c = blockIdx.x; c < (uint32_t)a.nch; c += gridDim.x) {
+  KeptCtx& kc = kcs[w];
+  K4W& ws = wst[w];
+  int8_t* bk = sblk[w];
+  uint32_t c0, c1;
+  warp_range(a, c0, c1);
+  uint32_t cur = 0xFFFFFFFFu;
+  int B = 0;
+  FastDiv fk;
+  fk.init(1);
+  for (uint32_t c = c0; c < c1; ++c) {
     const uint32_t ifi = a.ch_if[c];
     const IfInfo& f = a.info[ifi];
     IfSt& st = a.st[ifi];
     if (st.err) continue;
-    if (sh.cur_if != ifi) {
-      __syncthreads();
-      if (tid == 0) load_kept_ctx(sh.kc, st, f.seed);
-      __syncthreads();
-      if (tid == 0) sh.cur_if = ifi;
-    }
-    const int B = (int)st.B;
-    const uint32_t off = a.ch_off[c], n = a.ch_cnt[c];
-    const uint32_t K = f.K;
-    uint32_t* gv = lv(a, f);
-    uint32_t* gx = li(a, f);
-    for (uint32_t k = tid; k < n; k += CNT) { iv[k] = __ldcg(gv + off + k); ix[k] = __ldcg(gx + off + k); }
-    for (int k = tid; k < NW * MAXB; k += CNT) {
-      (&sh.wcnt[0][0])[k] = 0; (&sh.wmin[0][0])[k] = 0x7FFFFFFFu; (&sh.wmax[0][0])[k] = 0; (&sh.wlast[0][0])[k] = 0;
-    }
-    __syncthreads();
-    const uint32_t seg = (((n + NW - 1) / NW) + 31u) & ~31u;
-    const uint32_t w0 = min(n, (uint32_t)w * seg), w1 = min(n, w0 + seg);
-    // pass 1: block ids, per-warp counts, min/max keys, last member index per block
-    for (uint32_t i = w0; i < w1; i += 32) {
-      const uint32_t e = i + lane;
-      int blk = -1;
-      uint32_t key = 0, x = 0;
-      if (e < w1) {
-        const uint32_t b = iv[e];
-        x = ix[e];
-        key = b & 0x7FFFFFFFu;
-        if (sh.kc.kept(b, x)) blk = sh.kc.block_of(b, x);
-        bid[e] = (int8_t)blk;
+    if (ifi != cur) {
+      __syncwarp();
+      if (lane == 0) {
+        kc.flags = st.flags; kc.ck_star = st.ck_star; kc.h_star = st.h_star; kc.seed = f.seed;
+        kc.tau_p = st.tau_p; kc.tau_m = st.tau_m;
+        kc.ncut0 = (int)st.ncut0; kc.ncut = (int)st.ncut; kc.meff0 = (int)st.meff0;
       }
-      uint32_t pend = __ballot_sync(0xFFFFFFFFu, blk >= 0);
-      while (pend) {
-        const int ld = __ffs(pend) - 1;
-        const int bb = __shfl_sync(0xFFFFFFFFu, blk, ld);
-        const uint32_t peers = __ballot_sync(0xFFFFFFFFu, blk == bb);
-        const uint32_t mn = __reduce_min_sync(0xFFFFFFFFu, blk == bb ? key : 0x7FFFFFFFu);
-        const uint32_t mx = __reduce_max_sync(0xFFFFFFFFu, blk == bb ? key : 0u);
-        const uint32_t xl = __reduce_max_sync(0xFFFFFFFFu, blk == bb ? x + 1u : 0u);
-        if (lane == 0) {
-          sh.wcnt[w][bb] += __popc(peers);
-          sh.wmin[w][bb] = min(sh.wmin[w][bb], mn);
-          sh.wmax[w][bb] = max(sh.wmax[w][bb], mx);
-          sh.wlast[w][bb] = max(sh.wlast[w][bb], xl);
+      const int nc = (int)st.ncut;
+      if (lane < nc) { kc.ck[lane] = st.cut_key[lane]; kc.cx[lane] = st.cut_idx[lane]; }
+      __syncwarp();
+      cur = ifi;
+      B = (int)st.B;
+      fk.init(f.K);
+    }
+    // zero this chunk's share of the output (K6/K7 write into a zeroed payload)
+    {
+      const uint32_t k = c - f.ch0;
+      const uint64_t n16 = f.cap / 16;
+      const uint64_t z0 = n16 * k / f.nch, z1 = n16 * (k + 1) / f.nch;
+      uint4* o4 = reinterpret_cast<uint4*>(f.out);
+      for (uint64_t z = z0 + lane; z < z1; z += 32) o4[z] = make_uint4(0, 0, 0, 0);
+      if (k + 1 == f.nch)
+        for (uint64_t z = n16 * 16 + lane; z < f.cap; z += 32) f.out[z] = 0;
+    }
+    if (lane < B) { ws.cnt[lane] = 0; ws.mn[lane] = 0x7FFFFFFFu; ws.mx[lane] = 0; ws.xl[lane] = 0; }
+    __syncwarp();
+    const uint2* gl = le(a, f);
+    // pass 1 over the chunk's units in order: block ids (kept in SMEM), counts, min/max, last
+    uint32_t i = 0;
+    for (int u = 0; u < UNITS; ++u) {
+      const uint32_t uo = a.u_off[(uint64_t)c * UNITS + u], un = a.u_cnt[(uint64_t)c * UNITS + u];
+      for (uint32_t j0 = 0; j0 < un; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        int blk = -1;
+        uint2 e = make_uint2(0, 0);
+        if (j < un) {
+          e = __ldg(gl + uo + j);
+          if (kc.kept(e.x, e.y)) blk = kc.block_of(e.x, e.y);
+          bk[i + j] = (int8_t)blk;
         }
-        pend &= ~peers;
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, blk);
+        if (blk >= 0) {
+          const uint32_t key = e.x & 0x7FFFFFFFu;
+          atomicMin(&ws.mn[blk], key);
+          atomicMax(&ws.mx[blk], key);
+          if (lane == 31 - __clz(peers)) { ws.cnt[blk] += __popc(peers); ws.xl[blk] = max(ws.xl[blk], e.y + 1u); }
+        }
+        __syncwarp();
+      }
+      i += un;
+    }
+    const uint32_t n = i;
+    __syncwarp();
+    const uint32_t cnt = lane < B ? ws.cnt[lane] : 0u;
+    const uint32_t sinc = warp_incl_scan_u32(cnt);
+    if (lane < B) {
+      ws.pos[lane] = sinc - cnt;
+      const uint64_t ci = (uint64_t)c * a.maxb + lane;
+      a.ch_bcnt[ci] = cnt;
+      a.ch_blast[ci] = ws.xl[lane] ? (int32_t)fk.div(ws.xl[lane] - 1u) : -1;
+      if (cnt) {
+        atomicMin(&st.bmin[lane], ws.mn[lane]);
+        atomicMax(&st.bmax[lane], ws.mx[lane]);
+        atomicAdd(&st.bcount[lane], cnt);
       }
     }
-    __syncthreads();
-    // per-block totals and offsets (block runs in block order, warps in flat order)
-    if (tid < B) {
-      const int b = tid;
-      uint32_t acc = 0, mn = 0x7FFFFFFFu, mx = 0, xl = 0;
-      for (int k = 0; k < NW; ++k) {
-        sh.wpos[k][b] = acc;
-        acc += sh.wcnt[k][b];
-        mn = min(mn, sh.wmin[k][b]);
-        mx = max(mx, sh.wmax[k][b]);
-        xl = max(xl, sh.wlast[k][b]);
+    __syncwarp();
+    // pass 2: stable scatter into block runs of the member slot
+    uint2* om = me(a, f) + (uint64_t)(c - f.ch0) * CH;
+    i = 0;
+    for (int u = 0; u < UNITS; ++u) {
+      const uint32_t uo = a.u_off[(uint64_t)c * UNITS + u], un = a.u_cnt[(uint64_t)c * UNITS + u];
+      for (uint32_t j0 = 0; j0 < un; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        const int blk = j < un ? (int)bk[i + j] : -1;
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, blk);
+        if (blk >= 0) {
+          const uint32_t dst = ws.pos[blk] + __popc(peers & lt);
+          __stcg(om + dst, __ldg(gl + uo + j));
+        }
+        __syncwarp();
+        if (blk >= 0 && lane == 31 - __clz(peers)) ws.pos[blk] += __popc(peers);
+        __syncwarp();
       }
-      sh.bstart[b] = acc;  // total (turned into start below)
-      a.ch_bcnt[(uint64_t)c * a.maxb + b] = acc;
-      a.ch_blast[(uint64_t)c * a.maxb + b] = xl ? (int32_t)((xl - 1u) / K) : -1;
-      if (acc) { atomicMin(&st.bmin[b], mn); atomicMax(&st.bmax[b], mx); }
+      i += un;
     }
-    __syncthreads();
-    if (tid == 0) {
-      uint32_t acc = 0;
-      for (int b = 0; b < B; ++b) { const uint32_t t = sh.bstart[b]; sh.bstart[b] = acc; acc += t; }
-    }
-    __syncthreads();
-    for (int k = tid; k < NW * B; k += CNT) {
-      const int ww = k / B, b = k - ww * B;
-      sh.wpos[ww][b] += sh.bstart[b];
-    }
-    __syncthreads();
-    // pass 2: stable scatter into block runs
-    for (uint32_t i = w0; i < w1; i += 32) {
-      const uint32_t e = i + lane;
-      const int blk = e < w1 ? (int)bid[e] : -1;
-      const uint32_t peers = __match_any_sync(0xFFFFFFFFu, blk);
-      if (blk >= 0) {
-        const uint32_t dst = sh.wpos[w][blk] + __popc(peers & lt);
-        ov[dst] = iv[e];
-        ox[dst] = ix[e];
-      }
-      __syncwarp();
-      if (blk >= 0 && lane == __ffs(peers) - 1) sh.wpos[w][blk] += __popc(peers);
-      __syncwarp();
-    }
-    __syncthreads();
-    uint32_t tot = 0;
-    for (int b = 0; b < B; ++b) tot += a.ch_bcnt[(uint64_t)c * a.maxb + b];
-    for (uint32_t k = tid; k < tot; k += CNT) { __stcg(gv + off + k, ov[k]); __stcg(gx + off + k, ox[k]); }
-    __syncthreads();
+    (void)n;
   }
 }
 
 // ---------------------------------------------------------------------------------------
-// K5: ABQ distortion sums: S[b][q] = sum |code_qbit >> (qbit - q) - code_q| (quant.py:88-99)
-struct K5Sh {
-  uint32_t cur_if;
-  double vmin[MAXB];
-  double o[MAXB][17];
-  double inv[MAXB][17];
-  uint32_t act[MAXB];
-  uint32_t red[CNT / 32][17];
+// K5: ABQ distortion sums S[b][q] = sum |code_qbit >> (qbit - q) - code_q| (quant.py:88-99),
+// one warp per chunk, over block runs.  Pass A (first_pass=1) computes q = q_bit-1 only,
+// which decides most blocks (the descent stops at the first violation, quant.py:110-115);
+// pass B computes every q < q_bit-1 for the blocks whose q_bit-1 distortion is within
+// delta.  Per-warp accumulators in SMEM are flushed when the warp moves to another IF.
+struct AbqPar {
+  double vmin;
+  double o[17];
+  double inv[17];
+  uint32_t act;
 };
 
+template <int FIRST>
 __global__ void __launch_bounds__(CNT) enc_abq(EArgs a) {
-  constexpr int NW = CNT / 32;
-  __shared__ K5Sh sh;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int qb = a.q_bit;
-  if (tid == 0) sh.cur_if = 0xFFFFFFFFu;
-  __syncthreads();
-  for (uint32_t c = blockIdx.x; c < (uint32_t)a.nch; c += gridDim.x) {
+  extern __shared__ __align__(16) uint8_t dsm_raw[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int maxb = a.maxb, qb = a.q_bit;
+  if (qb < (FIRST ? 2 : 3)) return;
+  AbqPar* par = reinterpret_cast<AbqPar*>(dsm_raw) + (size_t)w * maxb;
+  uint64_t* acc_s = reinterpret_cast<uint64_t*>(reinterpret_cast<AbqPar*>(dsm_raw) + (size_t)(CNT / 32) * maxb) +
+                    (size_t)w * maxb * 16;
+  uint32_t c0, c1;
+  warp_range(a, c0, c1);
+  uint32_t cur = 0xFFFFFFFFu;
+  int B = 0;
+  auto flush = [&]() {
+    __syncwarp();
+    if (cur != 0xFFFFFFFFu) {
+      IfSt& st = a.st[cur];
+      for (int k = lane; k < B * 16; k += 32)
+        if (acc_s[k]) atomicAdd((unsigned long long*)&st.S[k], (unsigned long long)acc_s[k]);
+    }
+    __syncwarp();
+  };
+  for (uint32_t c = c0; c < c1; ++c) {
     const uint32_t ifi = a.ch_if[c];
     const IfInfo& f = a.info[ifi];
     IfSt& st = a.st[ifi];
     if (st.err) continue;
-    const int B = (int)st.B;
-    if (sh.cur_if != ifi) {
-      __syncthreads();
-      for (int k = tid; k < B * 16; k += CNT) {
+    if (ifi != cur) {
+      flush();
+      B = (int)st.B;
+      for (int k = lane; k < B * 16; k += 32) acc_s[k] = 0;
+      for (int k = lane; k < B * 16; k += 32) {
         const int b = k >> 4, q = (k & 15) + 1;
-        const uint32_t mn = st.bmin[b], mx = st.bmax[b];
-        const double vmin = (double)__uint_as_float(mn), vmax = (double)__uint_as_float(mx);
+        const uint32_t m0 = st.bmin[b], m1 = st.bmax[b];
+        const double vmin = (double)__uint_as_float(m0), vmax = (double)__uint_as_float(m1);
         if (q <= qb) {
           const double o = __ddiv_rn(__dsub_rn(vmax, vmin), (double)((1u << q) - 1u));
-          sh.o[b][q] = o;
-          sh.inv[b][q] = __drcp_rn(o);
+          par[b].o[q] = o;
+          par[b].inv[q] = __drcp_rn(o);
         }
-        if (q == 1) { sh.vmin[b] = vmin; sh.act[b] = mn < mx ? 1u : 0u; }
+        if (q == 1) {
+          bool act = m0 < m1;
+          if (!FIRST && act) {
+            // descend past q_bit - 1 only if that level is within delta
+            const double ds = __ddiv_rn((double)st.S[b * 16 + qb - 1], (double)st.bcount[b]);
+            act = !(ds > a.delta);
+          }
+          par[b].vmin = vmin;
+          par[b].act = act ? 1u : 0u;
+        }
       }
-      __syncthreads();
-      if (tid == 0) sh.cur_if = ifi;
+      cur = ifi;
+      __syncwarp();
     }
-    const uint32_t off = a.ch_off[c];
-    const uint32_t* gv = lv(a, f) + off;
-    uint32_t rs = 0;
+    const uint32_t bcnt = lane < B ? a.ch_bcnt[(uint64_t)c * maxb + lane] : 0u;
+    const uint32_t binc = warp_incl_scan_u32(bcnt);
+    const uint2* gm = me(a, f) + (uint64_t)(c - f.ch0) * CH;
+    const uint32_t lref = (1u << qb) - 1u;
     for (int b = 0; b < B; ++b) {
-      const uint32_t nb = a.ch_bcnt[(uint64_t)c * a.maxb + b];
-      if (nb == 0 || !sh.act[b]) { rs += nb; continue; }
-      uint32_t acc[16];
+      const uint32_t nb = __shfl_sync(0xFFFFFFFFu, bcnt, b);
+      if (nb == 0 || !par[b].act) continue;
+      const uint32_t rs = __shfl_sync(0xFFFFFFFFu, binc, b) - nb;
+      const double vmin = par[b].vmin;
+      const double oref = par[b].o[qb], iref = par[b].inv[qb];
+      if (FIRST) {
+        const int q = qb - 1;
+        const double oq = par[b].o[q], iq = par[b].inv[q];
+        uint32_t acc = 0;
+        for (uint32_t i = lane; i < nb; i += 32) {
+          const uint32_t key = __ldg(&gm[rs + i].x) & 0x7FFFFFFFu;
+          const uint32_t r = quant_code(key, vmin, oref, iref, lref) >> 1;
+          const uint32_t cq = quant_code(key, vmin, oq, iq, (1u << q) - 1u);
+          acc += r > cq ? r - cq : cq - r;
+        }
+        const uint32_t v = __reduce_add_sync(0xFFFFFFFFu, acc);
+        if (lane == 0) acc_s[b * 16 + q] += v;
+      } else {
+        uint32_t acc[16];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) acc[q] = 0;
-      const double vmin = sh.vmin[b];
-      const uint32_t lref = (1u << qb) - 1u;
-      for (uint32_t k = tid; k < nb; k += CNT) {
-        const uint32_t key = __ldcg(gv + rs + k) & 0x7FFFFFFFu;
-        const uint32_t cr = quant_code(key, vmin, sh.o[b][qb], sh.inv[b][qb], lref);
+        for (int q = 0; q < 16; ++q) acc[q] = 0;
+        for (uint32_t i = lane; i < nb; i += 32) {
+          const uint32_t key = __ldg(&gm[rs + i].x) & 0x7FFFFFFFu;
+          const uint32_t cr = quant_code(key, vmin, oref, iref, lref);
 #pragma unroll
-        for (int q = 1; q < 16; ++q) {
-          if (q < qb) {
-            const uint32_t cq = quant_code(key, vmin, sh.o[b][q], sh.inv[b][q], (1u << q) - 1u);
-            const uint32_t r = cr >> (qb - q);
-            acc[q] += r > cq ? r - cq : cq - r;
+          for (int q = 1; q < 15; ++q) {
+            if (q < qb - 1) {
+              const uint32_t cq = quant_code(key, vmin, par[b].o[q], par[b].inv[q], (1u << q) - 1u);
+              const uint32_t r = cr >> (qb - q);
+              acc[q] += r > cq ? r - cq : cq - r;
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 1; q < 15; ++q) {
+          if (q < qb - 1) {
+            const uint32_t v = __reduce_add_sync(0xFFFFFFFFu, acc[q]);
+            if (lane == q) acc_s[b * 16 + q] += v;
           }
         }
       }
-#pragma unroll
-      for (int q = 1; q < 16; ++q) {
-        if (q < qb) {
-          const uint32_t v = __reduce_add_sync(0xFFFFFFFFu, acc[q]);
-          if (lane == 0) sh.red[w][q] = v;
-        }
-      }
-      __syncthreads();
-      if (tid >= 1 && tid < qb) {
-        uint64_t t = 0;
-        for (int k = 0; k < NW; ++k) t += sh.red[k][tid];
-        if (t) atomicAdd((unsigned long long*)&st.S[b * 16 + tid], (unsigned long long)t);
-      }
-      __syncthreads();
-      rs += nb;
     }
   }
+  flush();
 }
 
 // ---------------------------------------------------------------------------------------
-// K6: per-IF q*, layout, header, chunk prefixes, row_ptr tails.
+// K6: per-IF q*, layout, header/meta, chunk prefixes (one warp per block), row_ptr tails.
 __device__ __forceinline__ void st_u32_le(uint8_t* base, uint64_t off, uint32_t v) { st_u32_le_bytes(base, off, v); }
 
 __global__ void __launch_bounds__(256) enc_layout(EArgs a) {
   constexpr int NT = 256;
-  __shared__ uint32_t scan32[40];
-  __shared__ uint64_t scan64[40];
   __shared__ uint64_t s_bn[MAXB];
   __shared__ int32_t s_last[MAXB];
   __shared__ uint32_t s_q[MAXB];
   __shared__ uint64_t s_P;
-  const int ifi = blockIdx.x, tid = threadIdx.x;
+  const int ifi = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const IfInfo f = a.info[ifi];
   IfSt& st = a.st[ifi];
   if (st.err) return;
   const int B = (int)st.B;
   const uint32_t ch0 = f.ch0, nch = f.nch;
-  // chunk prefixes per block: member offsets and the row of the previous member
-  for (int b = 0; b < B; ++b) {
+  // chunk prefixes of block b (warp b % 8): member offsets and the last row before the chunk
+  for (int b = w; b < B; b += NT / 32) {
     uint32_t run = 0;
     int32_t lastp = -1;
-    for (uint32_t t0 = 0; t0 < nch; t0 += NT) {
-      const uint32_t k = t0 + tid;
+    for (uint32_t t0 = 0; t0 < nch; t0 += 32) {
+      const uint32_t k = t0 + lane;
       const uint64_t ci = (uint64_t)(ch0 + k) * a.maxb + b;
       const uint32_t v = k < nch ? a.ch_bcnt[ci] : 0u;
       const int32_t l = k < nch ? a.ch_blast[ci] : -1;
-      uint32_t tot;
-      const uint32_t ex = block_excl_scan_u32(v, scan32, &tot);
-      // exclusive max-scan of last rows (rows grow with the chunk index)
+      const uint32_t inc = warp_incl_scan_u32(v);
       int32_t m = l;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int32_t y = __shfl_up_sync(0xFFFFFFFFu, m, o);
-        if ((tid & 31) >= o) m = max(m, y);
+        if (lane >= o) m = max(m, y);
       }
-      if ((tid & 31) == 31) scan64[tid >> 5] = (uint64_t)(int64_t)m;
-      __syncthreads();
-      int32_t wpre = lastp;
-      for (int w = 0; w < (tid >> 5); ++w) wpre = max(wpre, (int32_t)(int64_t)scan64[w]);
-      const int32_t me_ex = __shfl_up_sync(0xFFFFFFFFu, m, 1);
-      const int32_t prev = max(wpre, (tid & 31) ? me_ex : -1);
+      const int32_t mex = __shfl_up_sync(0xFFFFFFFFu, m, 1);
       if (k < nch) {
-        a.ch_bpre[ci] = run + ex;
-        a.ch_bprev[ci] = prev;
+        a.ch_bpre[ci] = run + inc - v;
+        a.ch_bprev[ci] = max(lastp, lane ? mex : -1);
       }
-      int32_t tl = lastp;
-      for (int w = 0; w < NT / 32; ++w) tl = max(tl, (int32_t)(int64_t)scan64[w]);
-      __syncthreads();
-      run += tot;
-      lastp = tl;
+      run += __shfl_sync(0xFFFFFFFFu, inc, 31);
+      lastp = max(lastp, __shfl_sync(0xFFFFFFFFu, m, 31));
     }
-    if (tid == 0) { s_bn[b] = run; s_last[b] = lastp; }
-    __syncthreads();
+    if (lane == 0) { s_bn[b] = run; s_last[b] = lastp; }
   }
-  // q* per block
+  __syncthreads();
+  // q* per block (quant.py:102-115; codec.py:176-181, :194-200)
   if (tid < B) {
     const int b = tid;
     const int s = b < (int)st.meff0 ? 0 : 1;
@@ -1315,7 +1451,7 @@ __global__ void __launch_bounds__(256) enc_layout(EArgs a) {
       q = (uint32_t)a.q_bit;
       for (int qq = a.q_bit - 1; qq >= 1; --qq) {
         const double ds = __ddiv_rn((double)st.S[b * 16 + qq], (double)n);
-        if (ds > a.delta) break;  // first violation stops the descent (quant.py:110-115)
+        if (ds > a.delta) break;  // first violation stops the descent
         q = (uint32_t)qq;
       }
     }
@@ -1341,19 +1477,14 @@ __global__ void __launch_bounds__(256) enc_layout(EArgs a) {
     const uint64_t P = pos + kCrcBytes;
     st.P = P;
     s_P = P;
+    st.crc_acc = 0;
+    st.seg_done = 0;
     if (P > f.cap) st.err = E_CAPACITY;
   }
   __syncthreads();
   const uint64_t P = s_P;
   if (P > f.cap) return;
   uint8_t* out = f.out;
-  {
-    uint4* o4 = reinterpret_cast<uint4*>(out);
-    const uint64_t n16 = P / 16;
-    for (uint64_t k = tid; k < n16; k += NT) o4[k] = make_uint4(0, 0, 0, 0);
-    for (uint64_t k = n16 * 16 + tid; k < P; k += NT) out[k] = 0;
-  }
-  __syncthreads();
   if (tid == 0) {
     uint8_t h[32];
     h[0] = 'S'; h[1] = 'I'; h[2] = 'F'; h[3] = '1';
@@ -1393,143 +1524,183 @@ __global__ void __launch_bounds__(256) enc_layout(EArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------
-// K7: codes, row_ptr transitions and MSB-first word assembly (chunk kernel).
-struct K7Sh {
-  uint32_t cur_if;
-  int B;
-  double vmin[MAXB], o64[MAXB], inv[MAXB];
-  uint32_t q[MAXB], degen[MAXB];
-  uint64_t rp[MAXB], bc[MAXB], bq[MAXB];
-  uint32_t bcnt[MAXB], bpre[MAXB], rs[MAXB + 1];
-  int32_t bprev[MAXB];
+// K7: one warp per chunk: codes at q* (quant.py:59-62), row_ptr transitions and MSB-first
+// packing of cols and codes (bitstream.py:6-30).  32 consecutive fields of a block run are
+// assembled into 32-bit words with shuffles; a word cut by the window end is carried into
+// the next window, words at run edges are merged with atomicOr, all others stored.
+struct PackPar {
+  double vmin, o64, inv;
+  uint64_t rp, bc, bq;
+  uint32_t q, degen;
 };
 
-__device__ __forceinline__ void pack_words(uint32_t* out32, const uint32_t* vals, uint32_t n, uint32_t w,
-                                           uint64_t b0) {
-  if (n == 0) return;
-  const uint64_t b1 = b0 + (uint64_t)n * w;
-  const uint64_t W0 = b0 >> 5, W1 = (b1 - 1) >> 5;
-  for (uint64_t W = W0 + threadIdx.x; W <= W1; W += CNT) {
-    const uint64_t lo = max(W << 5, b0), hi = min((W << 5) + 32, b1);
-    const uint32_t j0 = (uint32_t)(lo - b0) / w, j1 = (uint32_t)(hi - 1 - b0) / w;
-    uint32_t wv = 0;
-    for (uint32_t j = j0; j <= j1; ++j) {
-      const int64_t t = (int64_t)(b0 + (uint64_t)j * w) - (int64_t)(W << 5);
-      const int sh = 32 - (int)t - (int)w;
-      const uint64_t v = vals[j];
-      wv |= (uint32_t)(sh >= 0 ? (v << sh) : (v >> (-sh)));
-    }
-    const uint32_t le = bswap32(wv);
-    if (lo == (W << 5) && hi == (W << 5) + 32) out32[W] = le;
-    else if (wv) atomicOr(out32 + W, le);
+struct Carry {
+  uint32_t W;
+  uint32_t v;
+};
+
+// Pack the window of fields j0 .. j0+nv-1 (lane l holds field j0+l) of a run spanning
+// payload bits [Rs, Re), width w, MSB-first (bitstream.py:12-20).  Fields are OR-ed into a
+// per-warp shared-memory word buffer; words wholly inside the run are stored, words at run
+// edges merged with atomicOr, and the word cut by the window end carried (cy) into the next.
+__device__ __forceinline__ void pack_window(uint32_t* out32, uint32_t* buf, uint32_t val, bool valid, uint32_t w,
+                                            uint32_t Rs, uint32_t Re, uint32_t j0, uint32_t nv, Carry& cy) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t P = Rs + j0 * w, E = P + nv * w;
+  const bool last = E == Re;
+  const uint32_t W0 = P >> 5, W1 = (E - 1) >> 5;
+  const uint32_t nw = W1 - W0 + 1;
+  if (lane < nw) buf[lane] = (lane == 0 && cy.W == W0) ? cy.v : 0u;
+  __syncwarp();
+  if (valid) {
+    const uint32_t pb = P + lane * w - (W0 << 5);
+    const uint32_t wi = pb >> 5, sh = pb & 31u;
+    const uint64_t x = (uint64_t)val << (64u - w - sh);
+    atomicOr(&buf[wi], (uint32_t)(x >> 32));
+    if (sh + w > 32u) atomicOr(&buf[wi + 1], (uint32_t)x);
   }
+  __syncwarp();
+  const bool cut_last = ((W1 << 5) + 32 > E) && !last;  // last word continues in the next window
+  const uint32_t cv = buf[nw - 1];
+  if (lane < nw && !(cut_last && lane == nw - 1)) {
+    const uint32_t W = W0 + lane;
+    const uint32_t wv = buf[lane];
+    const bool edge = (W << 5) < Rs || (W << 5) + 32 > Re;
+    if (edge) { if (wv) atomicOr(out32 + W, bswap32(wv)); }
+    else out32[W] = bswap32(wv);
+  }
+  cy.W = cut_last ? W1 : 0xFFFFFFFFu;
+  cy.v = cut_last ? cv : 0u;
+  __syncwarp();
 }
 
 __global__ void __launch_bounds__(CNT) enc_pack(EArgs a) {
   extern __shared__ __align__(16) uint8_t dsm_raw[];
-  uint32_t* dsm = reinterpret_cast<uint32_t*>(dsm_raw);
-  __shared__ K7Sh sh;
-  uint32_t* sv = dsm;       // codes (in place of values)
-  uint32_t* sx = dsm + CH;  // flat indices, then cols
-  const int tid = threadIdx.x;
-  if (tid == 0) sh.cur_if = 0xFFFFFFFFu;
-  __syncthreads();
-  for (uint32_t c = blockIdx.x; c < (uint32_t)a.nch; c += gridDim.x) {
+  __shared__ uint32_t pbuf[CNT / 32][2][40];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int maxb = a.maxb;
+  PackPar* par = reinterpret_cast<PackPar*>(dsm_raw) + (size_t)w * maxb;
+  uint32_t c0, c1;
+  warp_range(a, c0, c1);
+  uint32_t cur = 0xFFFFFFFFu;
+  int B = 0;
+  FastDiv fk;
+  fk.init(1);
+  for (uint32_t c = c0; c < c1; ++c) {
     const uint32_t ifi = a.ch_if[c];
     const IfInfo& f = a.info[ifi];
     IfSt& st = a.st[ifi];
     if (st.err) continue;
-    if (sh.cur_if != ifi) {
-      __syncthreads();
-      const int B = (int)st.B;
-      if (tid < B) {
-        const int b = tid;
-        sh.vmin[b] = (double)__uint_as_float(st.bmin[b]);
-        sh.o64[b] = st.o64[b];
-        sh.inv[b] = st.inv64[b];
-        sh.q[b] = st.q[b];
-        sh.degen[b] = st.bmin[b] == st.bmax[b] ? 1u : 0u;
-        sh.rp[b] = st.off_meta[b] + kBlockMetaBytes;
-        sh.bc[b] = st.bit_cols[b];
-        sh.bq[b] = st.bit_codes[b];
+    if (ifi != cur) {
+      __syncwarp();
+      B = (int)st.B;
+      if (lane < B) {
+        PackPar& p = par[lane];
+        p.vmin = (double)__uint_as_float(st.bmin[lane]);
+        p.o64 = st.o64[lane];
+        p.inv = st.inv64[lane];
+        p.rp = st.off_meta[lane] + kBlockMetaBytes;
+        p.bc = st.bit_cols[lane];
+        p.bq = st.bit_codes[lane];
+        p.q = st.q[lane];
+        p.degen = st.bmin[lane] == st.bmax[lane] ? 1u : 0u;
       }
-      if (tid == 0) { sh.B = B; sh.cur_if = ifi; }
-      __syncthreads();
+      __syncwarp();
+      cur = ifi;
+      fk.init(f.K);
     }
-    const int B = sh.B;
-    if (tid < B) {
-      const uint64_t ci = (uint64_t)c * a.maxb + tid;
-      sh.bcnt[tid] = a.ch_bcnt[ci];
-      sh.bpre[tid] = a.ch_bpre[ci];
-      sh.bprev[tid] = a.ch_bprev[ci];
-    }
-    __syncthreads();
-    if (tid == 0) {
-      uint32_t acc = 0;
-      for (int b = 0; b < B; ++b) { sh.rs[b] = acc; acc += sh.bcnt[b]; }
-      sh.rs[B] = acc;
-    }
-    __syncthreads();
-    const uint32_t total = sh.rs[B];
-    const uint32_t off = a.ch_off[c];
-    const uint32_t* gv = lv(a, f) + off;
-    const uint32_t* gx = li(a, f) + off;
-    const FastDiv fk = [&] { FastDiv d; d.init(f.K); return d; }();
-    // load members; codes at q* (quant.py:59-62)
-    for (uint32_t k = tid; k < total; k += CNT) {
-      int b = 0;
-      while (b + 1 < B && sh.rs[b + 1] <= k) ++b;
-      const uint32_t key = __ldcg(gv + k) & 0x7FFFFFFFu;
-      const uint32_t x = __ldcg(gx + k);
-      sv[k] = sh.degen[b] ? 0u : quant_code(key, sh.vmin[b], sh.o64[b], sh.inv[b], (1u << sh.q[b]) - 1u);
-      sx[k] = x;
-    }
-    __syncthreads();
+    const uint64_t ci = (uint64_t)c * maxb + lane;
+    const uint32_t bcnt = lane < B ? a.ch_bcnt[ci] : 0u;
+    const uint32_t bpre = lane < B ? a.ch_bpre[ci] : 0u;
+    const int32_t bprev = lane < B ? a.ch_bprev[ci] : -1;
+    const uint32_t binc = warp_incl_scan_u32(bcnt);
+    const uint2* gm = me(a, f) + (uint64_t)(c - f.ch0) * CH;
     uint8_t* out = f.out;
-    // row_ptr transitions: row_ptr[r] = position of the first member with row >= r
+    uint32_t* out32 = reinterpret_cast<uint32_t*>(out);
+    const uint32_t cb = f.cb;
     for (int b = 0; b < B; ++b) {
-      const uint32_t n = sh.bcnt[b], r0 = sh.rs[b], p0 = sh.bpre[b];
-      for (uint32_t j = tid; j < n; j += CNT) {
-        const uint32_t rj = fk.div(sx[r0 + j]);
-        const int32_t rprev = j ? (int32_t)fk.div(sx[r0 + j - 1]) : sh.bprev[b];
-        for (int32_t r = rprev + 1; r <= (int32_t)rj; ++r) st_u32_le(out, sh.rp[b] + 4ull * (uint32_t)r, p0 + j);
+      const uint32_t n = __shfl_sync(0xFFFFFFFFu, bcnt, b);
+      if (n == 0) continue;
+      const uint32_t rs = __shfl_sync(0xFFFFFFFFu, binc, b) - n;
+      const uint32_t p0 = __shfl_sync(0xFFFFFFFFu, bpre, b);
+      int32_t rprev = __shfl_sync(0xFFFFFFFFu, bprev, b);
+      const PackPar p = par[b];
+      const uint32_t lv_ = (1u << p.q) - 1u;
+      const uint32_t Rc = (uint32_t)p.bc + p0 * cb, Rq = (uint32_t)p.bq + p0 * p.q;
+      const uint32_t Ec = Rc + n * cb, Eq = Rq + n * p.q;
+      Carry cyc{0xFFFFFFFFu, 0u}, cyq{0xFFFFFFFFu, 0u};
+      for (uint32_t j0 = 0; j0 < n; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        const uint32_t nv = min(32u, n - j0);
+        const bool valid = j < n;
+        const uint2 e = valid ? __ldg(gm + rs + j) : make_uint2(0, 0);
+        const uint32_t key = e.x & 0x7FFFFFFFu;
+        const uint32_t x = e.y;
+        const uint32_t code = (valid && !p.degen) ? quant_code(key, p.vmin, p.o64, p.inv, lv_) : 0u;
+        const uint32_t row = fk.div(x);
+        const uint32_t col = x - row * f.K;
+        const int32_t rup = __shfl_up_sync(0xFFFFFFFFu, (int32_t)row, 1);
+        const int32_t rp = lane ? rup : rprev;
+        if (valid)
+          for (int32_t r = rp + 1; r <= (int32_t)row; ++r) st_u32_le(out, p.rp + 4ull * (uint32_t)r, p0 + j);
+        rprev = __shfl_sync(0xFFFFFFFFu, (int32_t)row, (int)nv - 1);
+        pack_window(out32, pbuf[w][0], col, valid, cb, Rc, Ec, j0, nv, cyc);
+        pack_window(out32, pbuf[w][1], code, valid, p.q, Rq, Eq, j0, nv, cyq);
       }
     }
-    __syncthreads();
-    for (uint32_t k = tid; k < total; k += CNT) sx[k] = fk.mod(sx[k]);
-    __syncthreads();
-    uint32_t* out32 = reinterpret_cast<uint32_t*>(out);
-    for (int b = 0; b < B; ++b) {
-      const uint32_t n = sh.bcnt[b], r0 = sh.rs[b], p0 = sh.bpre[b];
-      pack_words(out32, sx + r0, n, f.cb, sh.bc[b] + (uint64_t)p0 * f.cb);
-      pack_words(out32, sv + r0, n, sh.q[b], sh.bq[b] + (uint64_t)p0 * sh.q[b]);
-    }
-    __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------------------------------
-// K8: CRC-32 (codec.py:316), lengths and status.
+// K8: CRC-32 over bytes [4, P-4) (codec.py:316).  The payload is cut into SEG-byte segments
+// (one CTA each, grid sized from the capacity); each CTA computes its segment's raw CRC
+// shifted to the end of the range; the XOR of all segments is the raw CRC (GF(2)
+// linearity).  The last CTA of an IF finishes it and writes CRC, length and status.
 __global__ void __launch_bounds__(256) enc_crc(EArgs a) {
   constexpr int NT = 256;
   __shared__ uint32_t t4[1024];
   __shared__ uint32_t stage[16 * NT];
   __shared__ uint32_t red[NT / 32 + 2];
-  const int ifi = blockIdx.x, tid = threadIdx.x;
+  __shared__ uint32_t s_last;
+  const int tid = threadIdx.x;
+  // locate (IF, segment) of this CTA: the per-IF segment counts are a prefix in seg_base
+  const uint32_t gb = blockIdx.x;
+  int lo = 0, hi = a.n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.seg_base[mid] <= gb) lo = mid; else hi = mid - 1;
+  }
+  const int ifi = lo;
+  const uint32_t seg = gb - a.seg_base[ifi];
+  const uint32_t nseg = a.seg_base[ifi + 1] - a.seg_base[ifi];
   const IfInfo& f = a.info[ifi];
   IfSt& st = a.st[ifi];
   if (st.err) {
-    if (tid == 0) {
+    if (tid == 0 && seg == 0) {
       if (st.err == E_NONFINITE) { a.status[ifi] = SIF_ERR_NONFINITE; a.out_len[ifi] = 0; }
       else { a.status[ifi] = SIF_ERR_CAPACITY; a.out_len[ifi] = st.P; }
     }
     return;
   }
-  for (int k = tid; k < 1024; k += NT) t4[k] = (&kCrcTab4[0][0])[k];
-  __syncthreads();
   const uint64_t P = st.P;
-  const uint32_t raw = crc_cta_staged<NT>(f.out, 4, P - 4, t4, red, stage);
+  const uint64_t b0 = 4, b1 = P - 4;
+  const uint64_t s0 = b0 + (uint64_t)seg * SEG, s1 = min(b1, s0 + SEG);
+  uint32_t part = 0;
+  if (s0 < s1) {
+    for (int k = tid; k < 1024; k += NT) t4[k] = (&kCrcTab4[0][0])[k];
+    __syncthreads();
+    const uint32_t raw = crc_cta_staged<NT>(f.out, s0, s1, t4, red, stage);
+    if (tid == 0) part = crc_shift(raw, b1 - s1);
+  }
   if (tid == 0) {
+    if (part) atomicXor(&st.crc_acc, part);
+    __threadfence();
+    s_last = atomicAdd(&st.seg_done, 1u) + 1 == nseg;
+  }
+  __syncthreads();
+  if (s_last && tid == 0) {
+    __threadfence();
+    const uint32_t raw = atomicXor(&st.crc_acc, 0u);
     st_u32_le_bytes(f.out, P - 4, crc_finish(raw, P - 8));
     a.out_len[ifi] = P;
     a.status[ifi] = SIF_OK;

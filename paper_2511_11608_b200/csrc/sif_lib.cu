@@ -34,7 +34,7 @@ inline int num_sms() {
 
 // Workspace sections of an encode plan (all offsets 256-byte aligned).
 struct EncWs {
-  uint64_t info, st, ch_if, ch_e0, ch_off, ch_cnt, bcnt, bpre, blast, bprev, hist, fixedq, keptoff, lists;
+  uint64_t info, st, ch_if, ch_e0, u_off, u_cnt, bcnt, bpre, blast, bprev, hist, fixedq, keptoff, segbase, lists;
 };
 
 EncWs enc_ws(uint64_t n, uint64_t nch, uint64_t maxb, uint64_t nhist, uint64_t nq) {
@@ -45,8 +45,8 @@ EncWs enc_ws(uint64_t n, uint64_t nch, uint64_t maxb, uint64_t nhist, uint64_t n
   w.st = take(sizeof(sif::IfSt) * n);
   w.ch_if = take(4 * nch);
   w.ch_e0 = take(4 * nch);
-  w.ch_off = take(4 * nch);
-  w.ch_cnt = take(4 * nch);
+  w.u_off = take(4 * nch * sif::UNITS);
+  w.u_cnt = take(4 * nch * sif::UNITS);
   w.bcnt = take(4 * nch * maxb);
   w.bpre = take(4 * nch * maxb);
   w.blast = take(4 * nch * maxb);
@@ -54,6 +54,7 @@ EncWs enc_ws(uint64_t n, uint64_t nch, uint64_t maxb, uint64_t nhist, uint64_t n
   w.hist = take(4ull * 2 * sif::ND * nhist);
   w.fixedq = take(nq);
   w.keptoff = take(8 * n);
+  w.segbase = take(4 * (n + 1));
   w.lists = off;
   return w;
 }
@@ -68,8 +69,9 @@ int resident_grid(K kfn, int threads, int smem, uint64_t work) {
 
 constexpr int kSmemStream = (2 * sif::CH + 2 * sif::ND) * 4;
 constexpr int kSmemSelect = (2 * sif::ND + 2 * sif::HB + sif::GCAP * 4 + 2 * sif::GSM) * 4;
-constexpr int kSmemMembers = 4 * sif::CH * 4 + sif::CH;
-constexpr int kSmemPack = 2 * sif::CH * 4;
+inline int smem_abq(int maxb) { return (sif::CNT / 32) * maxb * (int)(sizeof(sif::AbqPar) + 16 * 8); }
+inline int smem_pack(int maxb) { return (sif::CNT / 32) * maxb * (int)sizeof(sif::PackPar); }
+inline uint32_t crc_segments(uint64_t cap) { return (uint32_t)std::max<uint64_t>(1, (cap + sif::SEG - 1) / sif::SEG); }
 
 }  // namespace
 
@@ -137,7 +139,7 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
   int st = sif_validate_cfg(c);
   if (st) return st;
   memset(p, 0, sizeof(*p));
-  uint64_t kmax = 0, nch = 0, nhist = 0, lists = 0;
+  uint64_t kmax = 0, nch = 0, nhist = 0, lists = 0, nseg = 0;
   for (int i = 0; i < n; ++i) {
     if (d[i].rows < 1 || d[i].cols < 1) return SIF_ERR_SHAPE;  // tensor.py:27-28
     const uint64_t T = (uint64_t)d[i].rows * d[i].cols;
@@ -146,18 +148,20 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
     if (!d[i].x || (reinterpret_cast<uintptr_t>(d[i].x) & 15)) return SIF_ERR_INVALID_ARG;
     if (!atkf && (!d[i].out || (reinterpret_cast<uintptr_t>(d[i].out) & 15))) return SIF_ERR_INVALID_ARG;
     kmax = std::max(kmax, sif::keep_count(c->s, T));
+    if (sif_max_payload_bytes(d[i].rows, d[i].cols, c) >= (1ull << 29)) return SIF_ERR_INVALID_ARG;  // u32 bit offsets
     const uint64_t ch = (T + sif::CH - 1) / sif::CH;
     nch += ch;
     if (ch > 1) ++nhist;
     lists += up(16 * T, 256);
+    nseg += crc_segments(d[i].out_cap);
   }
-  if (nch >= (1ull << 31)) return SIF_ERR_INVALID_ARG;
+  if (nch >= (1ull << 31) || nseg >= (1ull << 31)) return SIF_ERR_INVALID_ARG;
   const uint64_t kk = std::max<uint64_t>(1, kmax);
   const int maxb = (int)(std::min<uint64_t>(c->m_plus, kk) + std::min<uint64_t>(c->m_minus, kk));
   if (maxb > sif::MAXB) return SIF_ERR_CONFIG;  // more blocks than the encoder supports
   const EncWs w = enc_ws(n, nch, maxb, nhist, (uint64_t)c->m_plus + c->m_minus);
   p->n = n;
-  p->cluster = 1;
+  p->cluster = (int32_t)nseg;  // encode plans: CRC segments (grid of enc_crc)
   p->threads = sif::CNT;
   p->smem_bytes = kSmemSelect;
   p->cap_smem = (int32_t)nhist;
@@ -183,6 +187,7 @@ int sif_enc_upload(const sif_plan* p, const sif_enc_desc* d, const sif_codec_cfg
   const EncWs w = enc_ws(n, (uint64_t)p->tiles, p->max_blocks, (uint64_t)p->cap_smem, (uint64_t)c->m_plus + c->m_minus);
   std::vector<sif::IfInfo> info((size_t)std::max(n, 1));
   std::vector<uint32_t> ch_if((size_t)std::max(p->tiles, 1)), ch_e0((size_t)std::max(p->tiles, 1));
+  std::vector<uint32_t> seg((size_t)n + 1, 0);
   uint64_t ch = 0, lists = w.lists;
   int32_t hs = 0;
   for (int i = 0; i < n; ++i) {
@@ -190,7 +195,8 @@ int sif_enc_upload(const sif_plan* p, const sif_enc_desc* d, const sif_codec_cfg
     memset(&f, 0, sizeof(f));
     f.x = d[i].x;
     f.out = d[i].out;
-    f.cap = d[i].out_cap;
+    // bytes past the largest possible payload are never touched (zeroing in enc_members)
+    f.cap = std::min<uint64_t>(d[i].out_cap, sif_max_payload_bytes(d[i].rows, d[i].cols, c));
     f.seed = d[i].seed;
     f.T = (uint64_t)d[i].rows * d[i].cols;
     f.kk = sif::keep_count(c->s, f.T);
@@ -205,6 +211,7 @@ int sif_enc_upload(const sif_plan* p, const sif_enc_desc* d, const sif_codec_cfg
     f.list_off = lists;
     f.gat_off = lists + 8 * f.T;
     lists += up(16 * f.T, 256);
+    seg[i + 1] = seg[i] + crc_segments(f.cap);
     for (uint64_t k = 0; k < nc; ++k) {
       ch_if[ch + k] = (uint32_t)i;
       ch_e0[ch + k] = (uint32_t)(k * sif::CH);
@@ -217,6 +224,8 @@ int sif_enc_upload(const sif_plan* p, const sif_enc_desc* d, const sif_codec_cfg
     if (check_cuda(cudaMemcpyAsync(wb + w.ch_if, ch_if.data(), 4ull * ch, cudaMemcpyHostToDevice, s)))
       return SIF_ERR_CUDA;
     if (check_cuda(cudaMemcpyAsync(wb + w.ch_e0, ch_e0.data(), 4ull * ch, cudaMemcpyHostToDevice, s)))
+      return SIF_ERR_CUDA;
+    if (check_cuda(cudaMemcpyAsync(wb + w.segbase, seg.data(), 4ull * (n + 1), cudaMemcpyHostToDevice, s)))
       return SIF_ERR_CUDA;
   }
   if (c->mode == SIF_MODE_FIXED &&
@@ -241,8 +250,9 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   a.atkf_only = atkf;
   a.ch_if = reinterpret_cast<const uint32_t*>(wb + w.ch_if);
   a.ch_e0 = reinterpret_cast<const uint32_t*>(wb + w.ch_e0);
-  a.ch_off = reinterpret_cast<uint32_t*>(wb + w.ch_off);
-  a.ch_cnt = reinterpret_cast<uint32_t*>(wb + w.ch_cnt);
+  a.u_off = reinterpret_cast<uint32_t*>(wb + w.u_off);
+  a.u_cnt = reinterpret_cast<uint32_t*>(wb + w.u_cnt);
+  a.seg_base = reinterpret_cast<const uint32_t*>(wb + w.segbase);
   a.ch_bcnt = reinterpret_cast<uint32_t*>(wb + w.bcnt);
   a.ch_bpre = reinterpret_cast<uint32_t*>(wb + w.bpre);
   a.ch_blast = reinterpret_cast<int32_t*>(wb + w.blast);
@@ -261,29 +271,38 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   if (!attrs) {
     if (check_cuda(cudaFuncSetAttribute(sif::enc_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemStream)) ||
         check_cuda(cudaFuncSetAttribute(sif::enc_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
-        check_cuda(cudaFuncSetAttribute(sif::enc_members, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMembers)) ||
-        check_cuda(cudaFuncSetAttribute(sif::enc_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemPack)))
+        check_cuda(cudaFuncSetAttribute(sif::enc_abq<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_abq(sif::MAXB))) ||
+        check_cuda(cudaFuncSetAttribute(sif::enc_abq<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_abq(sif::MAXB))) ||
+        check_cuda(cudaFuncSetAttribute(sif::enc_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pack(sif::MAXB))))
       return SIF_ERR_CUDA;
     attrs = true;
   }
-  static int g_stream = 0, g_members = 0, g_abq = 0, g_pack = 0;
+  const int maxb = p->max_blocks;
+  static int g_stream = 0, g_members = 0, g_abq = 0, g_pack = 0, g_maxb = -1;
   if (!g_stream) {
     g_stream = resident_grid(sif::enc_stream, sif::CNT, kSmemStream, 1ull << 30);
-    g_members = resident_grid(sif::enc_members, sif::CNT, kSmemMembers, 1ull << 30);
-    g_abq = resident_grid(sif::enc_abq, sif::CNT, 0, 1ull << 30);
-    g_pack = resident_grid(sif::enc_pack, sif::CNT, kSmemPack, 1ull << 30);
+    g_members = resident_grid(sif::enc_members, sif::CNT, 0, 1ull << 30);
+  }
+  if (g_maxb != maxb) {
+    g_abq = resident_grid(sif::enc_abq<1>, sif::CNT, smem_abq(maxb), 1ull << 30);
+    g_pack = resident_grid(sif::enc_pack, sif::CNT, smem_pack(maxb), 1ull << 30);
+    g_maxb = maxb;
   }
   const unsigned nch = (unsigned)p->tiles;
   const unsigned n = (unsigned)p->n;
+  const unsigned wgrid = std::max(1u, (nch + sif::CNT / 32 - 1) / (sif::CNT / 32));  // >= 1 chunk per warp
   sif::enc_prep<<<n, 256, 0, s>>>(a);
   sif::enc_stream<<<std::min<unsigned>(nch, g_stream), sif::CNT, kSmemStream, s>>>(a);
   sif::enc_select<<<n, sif::SNT, kSmemSelect, s>>>(a);
   if (!atkf) {
-    sif::enc_members<<<std::min<unsigned>(nch, g_members), sif::CNT, kSmemMembers, s>>>(a);
-    if (c->mode != SIF_MODE_FIXED) sif::enc_abq<<<std::min<unsigned>(nch, g_abq), sif::CNT, 0, s>>>(a);
+    sif::enc_members<<<std::min<unsigned>(wgrid, g_members), sif::CNT, 0, s>>>(a);
+    if (c->mode != SIF_MODE_FIXED) {
+      sif::enc_abq<1><<<std::min<unsigned>(wgrid, g_abq), sif::CNT, smem_abq(maxb), s>>>(a);
+      sif::enc_abq<0><<<std::min<unsigned>(wgrid, g_abq), sif::CNT, smem_abq(maxb), s>>>(a);
+    }
     sif::enc_layout<<<n, 256, 0, s>>>(a);
-    sif::enc_pack<<<std::min<unsigned>(nch, g_pack), sif::CNT, kSmemPack, s>>>(a);
-    sif::enc_crc<<<n, 256, 0, s>>>(a);
+    sif::enc_pack<<<std::min<unsigned>(wgrid, g_pack), sif::CNT, smem_pack(maxb), s>>>(a);
+    sif::enc_crc<<<(unsigned)p->cluster, 256, 0, s>>>(a);
   }
   return check_cuda(cudaGetLastError());
 }

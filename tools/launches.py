@@ -11,7 +11,7 @@ for r in rows[h + 1:]:
     name = r[ix['Kernel Name']].split('(')[0]
     v = float(r[ix['Metric Value']].replace(',', ''))
     unit = r[ix['Metric Unit']]
-    v = v / 1000.0 if unit == 'nsecond' else (v * 1000.0 if unit == 'msecond' else v)
+    v = v / 1000.0 if unit in ('nsecond', 'ns') else (v * 1000.0 if unit in ('msecond', 'ms') else v)
     d.setdefault(name, []).append(v)
 tot = 0.0
 for k, v in d.items():
