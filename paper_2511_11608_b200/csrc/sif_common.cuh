@@ -282,6 +282,16 @@ __device__ __forceinline__ void st_u32_le_bytes(uint8_t* base, uint64_t off, uin
 }
 
 // ---------------------------------------------------------------- reductions
+__device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);

@@ -1,14 +1,14 @@
 // sif_decode.cu -- B200 (sm_100a) decoder for the SLICER .sif wire format.
 //
-// Two launches per batch:
+// Four launches per batch:
 //   sif_parse_kernel   one thread per stream walks the header/block framing exactly in the
 //                      order of deserialize (codec.py:320-385) and writes a block table.
-//   sif_scatter_kernel one CTA per (stream, row slab): CRC-32 of a payload chunk (combined
-//                      with GF(2) shifts), row_ptr/cols validation (codec.py:235-251),
-//                      fused unpack + float64 dequantize (quant.py:67-73) + scatter-add
-//                      into a float64 shared-memory tile, rounded to fp32 (codec.py:266)
-//                      and written once with coalesced stores.  The last CTA of a stream
-//                      folds CRC, framing and validation flags into the reference's error
+//   sif_dcrc_kernel    one CTA per 64 KiB CRC-32 segment of a stream (GF(2)-combined).
+//   sif_scatter_kernel one warp per (row, column segment): row_ptr/cols validation
+//                      (codec.py:235-251), fused unpack + float64 dequantize
+//                      (quant.py:67-73) + scatter into a float64 shared-memory row buffer,
+//                      rounded to fp32 (codec.py:266) and written once with 16-byte stores.
+//   sif_dfinal_kernel  folds CRC, framing and validation flags into the reference's error
 //                      precedence and resets the per-stream accumulators.
 
 #include <stdint.h>
@@ -21,24 +21,20 @@ constexpr int DNT = 256;
 constexpr int TROW_U32 = 16;  // table row: 16 x u32 = 64 bytes
 constexpr uint32_t FLAG_CORRUPT = 1u, FLAG_NONFINITE = 2u;
 
-struct DecTile {
-  uint32_t ifi, ti, nt, r0, r1, c0, c1, pad;
-};
-
 struct DecArgs {
   const sif_dec_desc* descs;
   int n;
   uint32_t* table;        // per IF: (2 + maxb) rows of TROW_U32
   uint64_t table_stride;  // in u32
   uint32_t* acc;          // per IF: {crc, flags, count, pad}
-  const DecTile* tiles;
-  int ntiles;
   int parse_only;
-  int tile_elems;
-  int rpc_cap;
   int32_t* status;
-  const uint32_t* tiles_per_if;
+  const uint32_t* seg_base;    // [n+1] prefix of CRC segments per stream
+  const uint64_t* item_base;   // [n+1] prefix of (row, column segment) work items per stream
+  int segw;                    // columns per work item (<= 1024, multiple of 4)
 };
+
+constexpr uint64_t SEGD = 65536;  // CRC segment bytes per CTA
 
 // ------------------------------------------------------------------------------- parse
 __device__ __forceinline__ uint32_t rd_u32(const uint8_t* p, uint64_t o) {
@@ -103,169 +99,245 @@ __global__ void sif_parse_kernel(DecArgs a) {
   tab[TROW_U32 + 3] = (uint32_t)(len >> 32);
 }
 
-// ------------------------------------------------------------------------------- scatter
-__global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
-  extern __shared__ __align__(16) uint8_t dsm_raw[];
-  uint8_t* dsm = dsm_raw;
-  __shared__ uint32_t hdr[2 * TROW_U32];
+// ------------------------------------------------------------------------------- CRC
+// One CTA per CRC-32 segment of a stream: raw CRC of [s0, s1) shifted to the end of the
+// range [4, len-4) and XOR-combined into the stream's accumulator (GF(2) linearity).
+__global__ void __launch_bounds__(DNT) sif_dcrc_kernel(DecArgs a) {
+  __shared__ uint32_t t4[1024];
+  __shared__ uint32_t stage[16 * DNT];
   __shared__ uint32_t red[DNT / 32 + 2];
-  __shared__ uint32_t sflags;
-  __shared__ int s_last;
-  const int tid = threadIdx.x, lane = tid & 31;
-  // CTAs past the tile list compute one stream's CRC-32 each (codec.py:325-327)
-  const bool crc_cta = (int)blockIdx.x >= a.ntiles;
-  DecTile t;
-  if (crc_cta) {
-    t.ifi = blockIdx.x - a.ntiles;
-    t.ti = 0; t.nt = 0; t.r0 = t.r1 = t.c0 = t.c1 = 0;
-  } else {
-    t = a.tiles[blockIdx.x];
+  const int tid = threadIdx.x;
+  const uint32_t gs = blockIdx.x;
+  int lo = 0, hi = a.n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.seg_base[mid] <= gs) lo = mid; else hi = mid - 1;
   }
-  const sif_dec_desc d = a.descs[t.ifi];
-  const uint32_t* tab = a.table + (uint64_t)t.ifi * a.table_stride;
-  if (tid < 2 * TROW_U32) hdr[tid] = tab[tid];
-  if (tid == 0) sflags = 0;
-  __syncthreads();
-  const uint32_t walk = hdr[0], N = hdr[1], K = hdr[2], mp = hdr[3], nb = hdr[7];
-  const uint32_t pre = hdr[TROW_U32 + 0];
+  const int ifi = lo;
+  const uint32_t seg = gs - a.seg_base[lo];
+  const uint32_t* tab = a.table + (uint64_t)ifi * a.table_stride;
+  if (tab[TROW_U32 + 0]) return;  // length / magic failure: no CRC
+  const sif_dec_desc d = a.descs[ifi];
   const uint64_t len = d.in_len;
-  const uint8_t* in = d.in;
-  // number of CTAs that report to this stream's accumulator: its tiles + the CRC CTA
-  uint32_t ntiles_if = t.nt;
-
-  if (crc_cta) {
-    uint32_t* t4 = reinterpret_cast<uint32_t*>(dsm);
-    for (int k = tid; k < 1024; k += DNT) t4[k] = (&kCrcTab4[0][0])[k];
-    __syncthreads();
-    if (!pre) {
-      const uint32_t raw = crc_cta_staged<DNT>(in, 4, len - 4, t4, red, t4 + 1024);
-      if (tid == 0) a.acc[4ull * t.ifi + 0] = raw;
-    }
-    ntiles_if = a.tiles_per_if[t.ifi];
+  const uint64_t s0 = 4 + (uint64_t)seg * SEGD, s1 = min(len - 4, s0 + SEGD);
+  if (s0 >= s1) return;
+  for (int k = tid; k < 1024; k += DNT) t4[k] = (&kCrcTab4[0][0])[k];
+  __syncthreads();
+  const uint32_t raw = crc_cta_staged<DNT>(d.in, s0, s1, t4, red, stage);
+  if (tid == 0) {
+    const uint32_t part = crc_shift(raw, (len - 4) - s1);
+    if (part) atomicXor(a.acc + 4ull * ifi + 0, part);
   }
-  // ---- validate + dequantize + scatter this row slab
-  const bool shape_ok = a.parse_only || (N == d.rows && K == d.cols);
-  if (!crc_cta && !a.parse_only && !pre && !walk && shape_ok) {
-    const uint32_t R = t.r1 - t.r0, Kc = t.c1 - t.c0;
-    const uint32_t E = R * Kc;
-    double* tile = reinterpret_cast<double*>(dsm);
-    uint32_t* bm = reinterpret_cast<uint32_t*>(tile + a.tile_elems);
-    const uint32_t bmw = (uint32_t)(a.tile_elems + 31) / 32;
-    uint32_t* rpc = bm + 2 * bmw;
-    const bool cached = (uint64_t)(R + 1) * nb <= (uint64_t)a.rpc_cap;
-    {
-      uint4* t4z = reinterpret_cast<uint4*>(tile);
-      for (uint32_t k = tid; k < (E + 1) / 2; k += DNT) t4z[k] = make_uint4(0, 0, 0, 0);
-      for (uint32_t k = tid; k < 2 * bmw; k += DNT) bm[k] = 0;
+}
+
+// ------------------------------------------------------------------------------- scatter
+// Work item = (stream, row group, column segment): R = max(1, segw / K) consecutive rows of
+// at most segw columns; a warp owns a contiguous range of items.  Lanes hold one (block,
+// row) pair each (pairs block-major, in groups of 32 that never span both planes): block
+// metadata and the row's entry range.  The pairs' entries are unpacked 32 at a time
+// (cols, codes), validated (codec.py:238-250), dequantized in float64 (quant.py:67-73)
+// into a per-warp float64 buffer (plus plane stored, minus plane subtracted: positions are
+// unique within a valid plane, so this is the reference's f64 scatter-add,
+// codec.py:257-266), then rounded to fp32 and stored with 16-byte stores.
+__global__ void __launch_bounds__(DNT) sif_scatter_kernel(DecArgs a) {
+  extern __shared__ __align__(16) uint8_t dsm_raw[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t segw = (uint32_t)a.segw;
+  const uint32_t bmw = (segw + 31) / 32;
+  double* buf = reinterpret_cast<double*>(dsm_raw) + (size_t)w * segw;
+  uint32_t* bm = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(dsm_raw) + (size_t)(DNT / 32) * segw) +
+                 (size_t)w * 2 * bmw;
+  const uint64_t GW = (uint64_t)gridDim.x * (DNT / 32);
+  const uint64_t gw = (uint64_t)blockIdx.x * (DNT / 32) + w;
+  const uint64_t nitems = a.item_base[a.n];
+  const uint64_t i0 = nitems * gw / GW, i1 = nitems * (gw + 1) / GW;
+  int cur = -1;
+  uint32_t N = 0, K = 0, mp = 0, nb = 0, nsegr = 1, cb = 1, R = 1;
+  bool ok = false;
+  const uint32_t* tab = nullptr;
+  const uint8_t* in = nullptr;
+  float* out = nullptr;
+  uint32_t fl = 0;
+  for (uint64_t it = i0; it < i1; ++it) {
+    if (cur < 0 || it >= a.item_base[cur + 1]) {
+      if (cur >= 0) {
+        fl = __reduce_or_sync(0xFFFFFFFFu, fl);
+        if (lane == 0 && fl) atomicOr(a.acc + 4ull * cur + 1, fl);
+      }
+      fl = 0;
+      int lo = cur < 0 ? 0 : cur, hi = a.n - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a.item_base[mid] <= it) lo = mid; else hi = mid - 1;
+      }
+      cur = lo;
+      const sif_dec_desc d = a.descs[cur];
+      tab = a.table + (uint64_t)cur * a.table_stride;
+      const uint32_t walk = tab[0], pre = tab[TROW_U32 + 0];
+      N = tab[1]; K = tab[2]; mp = tab[3]; nb = tab[7];
+      ok = !pre && !walk && N == d.rows && K == d.cols && !a.parse_only;
+      in = d.in;
+      out = d.out;
+      nsegr = (d.cols + segw - 1) / segw;
+      R = d.cols <= segw ? segw / d.cols : 1u;
+      cb = col_bits(K);
     }
-    const uint32_t cb = col_bits(K);
-    uint32_t fl = 0;
-    if (cached) {
-      for (uint64_t k = tid; k < (uint64_t)(R + 1) * nb; k += DNT) {
-        const uint32_t b = (uint32_t)(k / (R + 1)), rr = (uint32_t)(k % (R + 1));
+    if (!ok) continue;
+    const uint64_t li = it - a.item_base[cur];
+    const uint32_t rg = (uint32_t)(li / nsegr), sg = (uint32_t)(li - (uint64_t)rg * nsegr);
+    const uint32_t r0 = rg * R, nr = min(R, N - r0);
+    const uint32_t c0 = sg * segw, c1 = min(K, c0 + segw), W = c1 - c0;
+    const uint32_t span = nr * W;  // buffer elements (rows are contiguous when nsegr == 1)
+    for (uint32_t k = 2 * lane; k < span; k += 64) *reinterpret_cast<double2*>(buf + k) = make_double2(0.0, 0.0);
+    for (uint32_t k = lane; k < 2 * bmw; k += 32) bm[k] = 0;
+    __syncwarp();
+    const uint32_t np = nb * nr;       // (block, row) pairs, block-major
+    const uint32_t npp = mp * nr;      // plus-plane pairs
+    for (uint32_t g0 = 0; g0 < np;) {
+      uint32_t g1 = min(np, g0 + 32u);
+      if (g0 < npp && g1 > npp) g1 = npp;  // a group never spans both planes
+      const int plane = g0 < npp ? 0 : 1;
+      const uint32_t pi = g0 + lane;
+      const bool has = pi < g1;
+      uint32_t q = 1, lo = 0, hi = 0, rs0 = 0, ri = 0;
+      double o = 1.0, vmin = 0.0;
+      uint64_t cbit = 0, qbit = 0;
+      if (has) {
+        const uint32_t b = pi / nr;
+        ri = pi - b * nr;
+        const uint32_t r = r0 + ri;
         const uint32_t* row = tab + (2ull + b) * TROW_U32;
+        q = row[0];
+        const uint32_t nnz = row[1];
+        o = (double)__uint_as_float(row[2]);
+        vmin = (double)__uint_as_float(row[3]);
         const uint64_t rpo = (uint64_t)row[4] | ((uint64_t)row[5] << 32);
-        rpc[k] = ld_u32_le(in, rpo + 4ull * (t.r0 + rr));
-      }
-    }
-    __syncthreads();
-    for (uint32_t b = 0; b < nb; ++b) {
-      const uint32_t* row = tab + (2ull + b) * TROW_U32;
-      const uint32_t q = row[0], nnz = row[1];
-      const double o = (double)__uint_as_float(row[2]), vmin = (double)__uint_as_float(row[3]);
-      const uint64_t rpo = (uint64_t)row[4] | ((uint64_t)row[5] << 32);
-      const uint64_t cbit = 8ull * ((uint64_t)row[6] | ((uint64_t)row[7] << 32));
-      const uint64_t qbit = 8ull * ((uint64_t)row[8] | ((uint64_t)row[9] << 32));
-      const int plane = b < mp ? 0 : 1;
-      auto rp = [&](uint32_t rr) -> uint32_t {
-        return cached ? rpc[(uint64_t)b * (R + 1) + rr] : ld_u32_le(in, rpo + 4ull * (t.r0 + rr));
-      };
-      // row pointer checks (codec.py:238-241)
-      for (uint32_t rr = tid; rr < R; rr += DNT)
-        if (rp(rr + 1) < rp(rr)) fl |= FLAG_CORRUPT;
-      if (tid == 0) {
-        if (t.r0 == 0 && rp(0) != 0) fl |= FLAG_CORRUPT;
-        if (t.r1 == N && rp(R) != nnz) fl |= FLAG_CORRUPT;
-      }
-      const uint32_t elo = rp(0) < nnz ? rp(0) : nnz;
-      const uint32_t ehi = rp(R) < nnz ? rp(R) : nnz;
-      for (uint32_t e = elo + tid; e < ehi; e += DNT) {
-        // row of entry e: last rr with rp(rr) <= e
-        uint32_t lo = 0, hi = R - 1;  // answer in [0, R-1]
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi + 1) >> 1;
-          if (rp(mid) <= e) lo = mid; else hi = mid - 1;
+        cbit = 8ull * ((uint64_t)row[6] | ((uint64_t)row[7] << 32));
+        qbit = 8ull * ((uint64_t)row[8] | ((uint64_t)row[9] << 32));
+        const uint32_t p0 = ld_u32_le(in, rpo + 4ull * r), p1 = ld_u32_le(in, rpo + 4ull * (r + 1));
+        if (sg == 0) {
+          if (p1 < p0) fl |= FLAG_CORRUPT;  // codec.py:238-241
+          if (r == 0 && p0 != 0) fl |= FLAG_CORRUPT;
+          if (r + 1 == N && p1 != nnz) fl |= FLAG_CORRUPT;
         }
-        const uint32_t rr = lo;
-        const uint32_t col = ld_field(in, cbit + (uint64_t)e * cb, cb);
-        if (col >= K) { fl |= FLAG_CORRUPT; continue; }  // codec.py:242-243
-        if (e > rp(rr) && ld_field(in, cbit + (uint64_t)(e - 1) * cb, cb) >= col) fl |= FLAG_CORRUPT;  // :244-247
-        if (col < t.c0 || col >= t.c1) continue;
-        const uint32_t pos = rr * Kc + (col - t.c0);
-        const uint32_t old = atomicOr(bm + plane * bmw + (pos >> 5), 1u << (pos & 31));
-        if (old & (1u << (pos & 31))) fl |= FLAG_CORRUPT;  // codec.py:248-250 (overlap)
-        const uint32_t code = ld_field(in, qbit + (uint64_t)e * q, q);
-        const double v = __dadd_rn(__dmul_rn((double)code, o), vmin);
-        atomicAdd(tile + pos, plane ? -v : v);
+        lo = min(p0, nnz);
+        hi = max(lo, min(p1, nnz));
+        rs0 = lo;
+        if (nsegr > 1) {
+          // entries of this column segment: lower bounds of c0 and c1 among the row's cols
+          auto lb = [&](uint32_t cv) {
+            uint32_t a0 = lo, a1 = hi;
+            while (a0 < a1) {
+              const uint32_t m = (a0 + a1) >> 1;
+              if (ld_field(in, cbit + (uint64_t)m * cb, cb) < cv) a0 = m + 1; else a1 = m;
+            }
+            return a0;
+          };
+          const uint32_t l0 = sg == 0 ? lo : lb(c0);
+          const uint32_t l1 = sg + 1 == nsegr ? hi : lb(c1);
+          lo = l0;
+          hi = max(l0, l1);
+        }
       }
+      const uint32_t cnt = hi - lo;
+      const uint32_t inc = warp_incl_scan_u32(cnt);
+      const uint32_t M = __shfl_sync(0xFFFFFFFFu, inc, 31);
+      const uint32_t exc = inc - cnt;
+      const uint32_t ng = g1 - g0;
+      for (uint32_t m0 = 0; m0 < M; m0 += 32) {
+        const uint32_t m = m0 + lane;
+        // pair of entry m: last pair whose exclusive prefix is <= m (binary search via shuffles)
+        uint32_t jl = 0;
+        {
+          uint32_t a0 = 0, a1 = ng - 1;
+#pragma unroll
+          for (int step = 0; step < 5; ++step) {
+            const uint32_t mid = (a0 + a1 + 1) >> 1;
+            const uint32_t v = __shfl_sync(0xFFFFFFFFu, exc, (int)mid);
+            if (a0 < a1) { if (v <= m) a0 = mid; else a1 = mid - 1; }
+          }
+          jl = a0;
+        }
+        const uint32_t e = __shfl_sync(0xFFFFFFFFu, lo, (int)jl) + (m - __shfl_sync(0xFFFFFFFFu, exc, (int)jl));
+        const uint64_t cbj = __shfl_sync(0xFFFFFFFFu, cbit, (int)jl);
+        const uint64_t qbj = __shfl_sync(0xFFFFFFFFu, qbit, (int)jl);
+        const uint32_t qj = __shfl_sync(0xFFFFFFFFu, q, (int)jl);
+        const double oj = __shfl_sync(0xFFFFFFFFu, o, (int)jl), vj = __shfl_sync(0xFFFFFFFFu, vmin, (int)jl);
+        const uint32_t rsj = __shfl_sync(0xFFFFFFFFu, rs0, (int)jl);
+        const uint32_t rij = __shfl_sync(0xFFFFFFFFu, ri, (int)jl);
+        if (m < M) {
+          const uint32_t col = ld_field(in, cbj + (uint64_t)e * cb, cb);
+          if (col >= K) fl |= FLAG_CORRUPT;  // codec.py:242-243
+          else {
+            // strictly increasing within the row (codec.py:244-247)
+            if (e > rsj && ld_field(in, cbj + (uint64_t)(e - 1) * cb, cb) >= col) fl |= FLAG_CORRUPT;
+            if (col >= c0 && col < c1) {
+              const uint32_t pos = rij * W + (col - c0);
+              const uint32_t old = atomicOr(bm + plane * bmw + (pos >> 5), 1u << (pos & 31));
+              if (old & (1u << (pos & 31))) fl |= FLAG_CORRUPT;  // codec.py:248-250 (overlap)
+              const uint32_t code = ld_field(in, qbj + (uint64_t)e * qj, qj);
+              const double v = __dadd_rn(__dmul_rn((double)code, oj), vj);
+              if (plane == 0) buf[pos] = v;
+              else buf[pos] = __dsub_rn(buf[pos], v);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      g0 = g1;
     }
-    __syncthreads();
-    float* out = d.out;
-    const bool vec4 = (K % 4u) == 0 && (t.c0 % 4u) == 0 && (Kc % 4u) == 0 &&
-                      (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
-    if (vec4) {
-      // 4 consecutive columns per thread: 2 x 16-byte smem loads, one 16-byte global store
-      const uint32_t kq = Kc / 4, nq = E / 4;
-      FastDiv fq;
-      fq.init(kq);
-      const double2* t2 = reinterpret_cast<const double2*>(tile);
-      for (uint32_t q = tid; q < nq; q += DNT) {
-        const uint32_t rr = fq.div(q), c4 = q - rr * kq;
-        const double2 a = t2[2 * q], b2 = t2[2 * q + 1];
-        const float4 f = make_float4(__double2float_rn(a.x), __double2float_rn(a.y), __double2float_rn(b2.x),
-                                     __double2float_rn(b2.y));
-        if (!(isfinite(f.x) && isfinite(f.y) && isfinite(f.z) && isfinite(f.w))) fl |= FLAG_NONFINITE;
-        *reinterpret_cast<float4*>(out + (uint64_t)(t.r0 + rr) * K + t.c0 + 4 * c4) = f;
+    // round to fp32 and store (nr full rows, or one row segment)
+    float* dst = out + (uint64_t)r0 * K + c0;
+    uint32_t bad = 0;
+    if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && (span & 3u) == 0) {
+      for (uint32_t k = 4 * lane; k < span; k += 128) {
+        const double2 x0 = *reinterpret_cast<const double2*>(buf + k), x1 = *reinterpret_cast<const double2*>(buf + k + 2);
+        const float4 f = make_float4(__double2float_rn(x0.x), __double2float_rn(x0.y), __double2float_rn(x1.x),
+                                     __double2float_rn(x1.y));
+        bad |= ((__float_as_uint(f.x) & 0x7F800000u) == 0x7F800000u) | ((__float_as_uint(f.y) & 0x7F800000u) == 0x7F800000u) |
+               ((__float_as_uint(f.z) & 0x7F800000u) == 0x7F800000u) | ((__float_as_uint(f.w) & 0x7F800000u) == 0x7F800000u);
+        __stcs(reinterpret_cast<float4*>(dst + k), f);
       }
     } else {
-      FastDiv fc;
-      fc.init(Kc);
-      for (uint32_t k = tid; k < E; k += DNT) {
-        const uint32_t rr = fc.div(k), cc = k - rr * Kc;
-        const float f = __double2float_rn(tile[k]);
-        if (!isfinite(f)) fl |= FLAG_NONFINITE;
-        out[(uint64_t)(t.r0 + rr) * K + t.c0 + cc] = f;
+      for (uint32_t k = lane; k < span; k += 32) {
+        const float f = __double2float_rn(buf[k]);
+        bad |= (__float_as_uint(f) & 0x7F800000u) == 0x7F800000u;
+        __stcs(dst + k, f);
       }
     }
+    if (bad) fl |= FLAG_NONFINITE;
+    __syncwarp();
+  }
+  if (cur >= 0) {
     fl = __reduce_or_sync(0xFFFFFFFFu, fl);
-    if (lane == 0 && fl) atomicOr(&sflags, fl);
-    __syncthreads();
-    if (tid == 0 && sflags) atomicOr(a.acc + 4ull * t.ifi + 1, sflags);
+    if (lane == 0 && fl) atomicOr(a.acc + 4ull * cur + 1, fl);
   }
+}
 
-  // ---- last CTA of this stream folds everything into the reference error precedence
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) s_last = atomicAdd(a.acc + 4ull * t.ifi + 2, 1u) == ntiles_if;  // tiles + CRC CTA
-  __syncthreads();
-  if (s_last && tid == 0) {
-    __threadfence();
-    uint32_t* acc = a.acc + 4ull * t.ifi;
-    const uint32_t crc_raw = *((volatile uint32_t*)(acc + 0));
-    const uint32_t flags = atomicAdd(acc + 1, 0u);
-    int st = SIF_OK;
-    if (pre) st = (int)pre;
-    else if (crc_finish(crc_raw, len - 8) != hdr[TROW_U32 + 1]) st = SIF_ERR_STREAM_FORMAT;  // :325-327
-    else if (walk) st = (int)walk;
-    else if (!shape_ok) st = SIF_ERR_CAPACITY;
-    else if (!a.parse_only) {
-      if (flags & FLAG_CORRUPT) st = SIF_ERR_CORRUPT_STREAM;
-      else if (N < 1 || K < 1) st = SIF_ERR_SHAPE;  // tensor.py:27-28
-      else if (flags & FLAG_NONFINITE) st = SIF_ERR_NONFINITE;  // tensor.py:35-36
-    }
-    a.status[t.ifi] = st;
-    acc[0] = 0; acc[1] = 0; acc[2] = 0;
+// ------------------------------------------------------------------------------- finalize
+// One thread per stream: the reference's error precedence (codec.py:320-385, :235-252,
+// tensor.py:27-36) from framing, CRC and validation flags; resets the accumulators.
+__global__ void sif_dfinal_kernel(DecArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  const uint32_t* tab = a.table + (uint64_t)i * a.table_stride;
+  const sif_dec_desc d = a.descs[i];
+  uint32_t* acc = a.acc + 4ull * i;
+  const uint32_t walk = tab[0], N = tab[1], K = tab[2], pre = tab[TROW_U32 + 0];
+  const uint32_t crc_raw = acc[0], flags = acc[1];
+  const bool shape_ok = a.parse_only || (N == d.rows && K == d.cols);
+  int st = SIF_OK;
+  if (pre) st = (int)pre;
+  else if (crc_finish(crc_raw, d.in_len - 8) != tab[TROW_U32 + 1]) st = SIF_ERR_STREAM_FORMAT;  // :325-327
+  else if (walk) st = (int)walk;
+  else if (!shape_ok) st = SIF_ERR_CAPACITY;
+  else if (!a.parse_only) {
+    if (flags & FLAG_CORRUPT) st = SIF_ERR_CORRUPT_STREAM;
+    else if (N < 1 || K < 1) st = SIF_ERR_SHAPE;
+    else if (flags & FLAG_NONFINITE) st = SIF_ERR_NONFINITE;
   }
+  a.status[i] = st;
+  acc[0] = 0; acc[1] = 0; acc[2] = 0;
 }
 
 }  // namespace sif

@@ -136,15 +136,6 @@ __device__ __forceinline__ uint32_t quant_code(uint32_t key, double vmin64, doub
   return f >= (double)levels ? levels : (uint32_t)f;
 }
 
-__device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t x) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-    if (lane >= o) x += y;
-  }
-  return x;
-}
 
 // ---------------------------------------------------------------------------------------
 // List of (float bits, flat index) pairs: SMEM up to `cap` entries, global beyond.

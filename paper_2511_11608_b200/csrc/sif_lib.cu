@@ -15,8 +15,6 @@
 
 namespace {
 
-constexpr int kDecTileElems = 4096;
-constexpr int kDecRpcCap = 2048;
 
 inline uint64_t up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 
@@ -348,39 +346,58 @@ int sif_atkf_batched(const sif_enc_desc* d, int n, const sif_codec_cfg* c, void*
 }
 
 // ------------------------------------------------------------------ decode
+static uint32_t dec_segments(uint64_t len) {
+  const uint64_t body = len > 8 ? len - 8 : 0;  // CRC range [4, len - 4)
+  return (uint32_t)std::max<uint64_t>(1, (body + sif::SEGD - 1) / sif::SEGD);
+}
+
+struct DecWs {
+  uint64_t desc, table, acc, segbase, itembase, total;
+};
+
+static DecWs dec_ws(uint64_t n, uint64_t maxrows) {
+  DecWs w;
+  uint64_t off = 0;
+  auto take = [&](uint64_t bytes) { const uint64_t o = off; off += up(std::max<uint64_t>(bytes, 1), 256); return o; };
+  w.desc = take(sizeof(sif_dec_desc) * n);
+  w.table = take((2 + maxrows) * 64ull * n);
+  w.acc = take(16ull * n);
+  w.segbase = take(4ull * (n + 1));
+  w.itembase = take(8ull * (n + 1));
+  w.total = off;
+  return w;
+}
+
+// Elements per decode work item (a group of whole rows, or a segment of one long row).
+static uint32_t dec_segw(const sif_dec_desc* d, int n) {
+  (void)d;
+  (void)n;
+  return 1024;
+}
+
 int sif_dec_plan(const sif_dec_desc* d, int n, sif_plan* p) {
   if (!p || (n > 0 && !d) || n < 0) return SIF_ERR_INVALID_ARG;
   memset(p, 0, sizeof(*p));
-  uint64_t ntiles = 0, maxrows = 0;
+  uint64_t maxrows = 0, nseg = 0;
   for (int i = 0; i < n; ++i) {
     if (!d[i].in || (reinterpret_cast<uintptr_t>(d[i].in) & 3)) return SIF_ERR_INVALID_ARG;
-    const uint64_t rows = d[i].rows, cols = d[i].cols;
-    uint64_t tiles = 1;
-    if (rows > 0 && cols > 0) {
-      const uint64_t kc = std::min<uint64_t>(cols, kDecTileElems);
-      const uint64_t r = std::max<uint64_t>(1, kDecTileElems / kc);
-      tiles = ((rows + r - 1) / r) * ((cols + kc - 1) / kc);
-    }
-    ntiles += tiles;
     const uint64_t blk = d[i].in_len > 32 ? (d[i].in_len - 32) / 17 + 1 : 1;
     maxrows = std::max(maxrows, blk);
+    nseg += dec_segments(d[i].in_len);
   }
-  if (ntiles >= (1ull << 31)) return SIF_ERR_INVALID_ARG;
+  if (nseg >= (1ull << 31)) return SIF_ERR_INVALID_ARG;
+  const uint32_t segw = dec_segw(d, n);
   p->n = n;
   p->threads = sif::DNT;
-  p->tiles = (int32_t)ntiles;
+  p->tiles = (int32_t)segw;    // decode plans: columns per work item
+  p->cluster = (int32_t)nseg;  // decode plans: CRC segment CTAs
   p->max_blocks = (int32_t)std::min<uint64_t>(maxrows, 1u << 30);
-  p->smem_bytes = kDecTileElems * 8 + 2 * ((kDecTileElems + 31) / 32) * 4 + kDecRpcCap * 4;
-  uint64_t off = 0;
-  p->ws_desc_off = off;
-  off += up(sizeof(sif_dec_desc) * (uint64_t)std::max(n, 1), 256);
-  p->ws_aux_off = off;  // tables
-  off += up((2 + maxrows) * 64ull * std::max(n, 1), 256);
-  p->ws_spill_off = off;  // tiles, then accumulators
-  off += up(sizeof(sif::DecTile) * std::max<uint64_t>(ntiles, 1), 256);
-  off += up(16ull * std::max(n, 1), 256);
-  off += up(4ull * std::max(n, 1), 256);  // tiles per stream
-  p->ws_bytes = off;
+  p->smem_bytes = (sif::DNT / 32) * (int)(segw * 8 + 2 * ((segw + 31) / 32) * 4);
+  const DecWs w = dec_ws(std::max(n, 1), maxrows);
+  p->ws_desc_off = w.desc;
+  p->ws_aux_off = w.table;
+  p->ws_spill_off = w.acc;
+  p->ws_bytes = w.total;
   return SIF_OK;
 }
 
@@ -389,66 +406,62 @@ uint64_t sif_dec_table_stride(const sif_plan* p) { return p ? (2ull + (uint64_t)
 int sif_dec_upload(const sif_plan* p, const sif_dec_desc* d, void* ws, void* stream) {
   if (!p || !ws) return SIF_ERR_INVALID_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  uint8_t* w = (uint8_t*)ws;
+  uint8_t* wb = (uint8_t*)ws;
   if (p->n == 0) return SIF_OK;
-  if (check_cuda(cudaMemcpyAsync(w + p->ws_desc_off, d, sizeof(sif_dec_desc) * p->n, cudaMemcpyHostToDevice, s)))
+  const DecWs w = dec_ws(p->n, p->max_blocks);
+  if (check_cuda(cudaMemcpyAsync(wb + w.desc, d, sizeof(sif_dec_desc) * p->n, cudaMemcpyHostToDevice, s)))
     return SIF_ERR_CUDA;
-  std::vector<sif::DecTile> tiles;
-  std::vector<uint32_t> per((size_t)p->n, 0);
-  tiles.reserve((size_t)p->tiles);
+  const uint32_t segw = (uint32_t)p->tiles;
+  std::vector<uint32_t> seg((size_t)p->n + 1, 0);
+  std::vector<uint64_t> items((size_t)p->n + 1, 0);
   for (int i = 0; i < p->n; ++i) {
-    const uint32_t rows = d[i].rows, cols = d[i].cols;
-    if (rows == 0 || cols == 0) {
-      tiles.push_back({(uint32_t)i, 0, 1, 0, 0, 0, 0, 0});
-      per[i] = 1;
-      continue;
-    }
-    const uint32_t kc = std::min<uint32_t>(cols, kDecTileElems);
-    const uint32_t r = std::max<uint32_t>(1, kDecTileElems / kc);
-    const uint32_t nr = (rows + r - 1) / r, nc = (cols + kc - 1) / kc;
-    const uint32_t nt = nr * nc;
-    per[i] = nt;
-    uint32_t ti = 0;
-    for (uint32_t a = 0; a < nr; ++a)
-      for (uint32_t b = 0; b < nc; ++b, ++ti)
-        tiles.push_back({(uint32_t)i, ti, nt, a * r, std::min(rows, (a + 1) * r), b * kc, std::min(cols, (b + 1) * kc), 0});
+    seg[i + 1] = seg[i] + dec_segments(d[i].in_len);
+    const uint32_t R = d[i].cols <= segw && d[i].cols ? segw / d[i].cols : 1u;  // rows per item
+    items[i + 1] = items[i] + (uint64_t)((d[i].rows + R - 1) / R) * ((d[i].cols + segw - 1) / segw);
   }
-  const uint64_t tab_bytes = up((2 + (uint64_t)p->max_blocks) * 64ull * p->n, 256);
-  uint8_t* tile_ptr = w + p->ws_spill_off;
-  uint8_t* acc_ptr = tile_ptr + up(sizeof(sif::DecTile) * std::max<uint64_t>(tiles.size(), 1), 256);
-  (void)tab_bytes;
-  if (check_cuda(cudaMemcpyAsync(tile_ptr, tiles.data(), sizeof(sif::DecTile) * tiles.size(), cudaMemcpyHostToDevice, s)))
+  if (check_cuda(cudaMemsetAsync(wb + w.acc, 0, 16ull * p->n, s))) return SIF_ERR_CUDA;
+  if (check_cuda(cudaMemcpyAsync(wb + w.segbase, seg.data(), 4ull * (p->n + 1), cudaMemcpyHostToDevice, s)))
     return SIF_ERR_CUDA;
-  if (check_cuda(cudaMemsetAsync(acc_ptr, 0, 16ull * p->n, s))) return SIF_ERR_CUDA;
-  uint8_t* per_ptr = acc_ptr + up(16ull * p->n, 256);
-  if (check_cuda(cudaMemcpyAsync(per_ptr, per.data(), 4ull * p->n, cudaMemcpyHostToDevice, s))) return SIF_ERR_CUDA;
-  return SIF_OK;
+  if (check_cuda(cudaMemcpyAsync(wb + w.itembase, items.data(), 8ull * (p->n + 1), cudaMemcpyHostToDevice, s)))
+    return SIF_ERR_CUDA;
+  return check_cuda(cudaStreamSynchronize(s));
 }
 
 int sif_dec_run(const sif_plan* p, int parse_only, void* ws, int32_t* status, void* stream) {
   if (!p || !ws || !status) return SIF_ERR_INVALID_ARG;
   if (p->n == 0) return SIF_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  uint8_t* w = (uint8_t*)ws;
+  uint8_t* wb = (uint8_t*)ws;
+  const DecWs w = dec_ws(p->n, p->max_blocks);
   sif::DecArgs a;
   memset(&a, 0, sizeof(a));
-  a.descs = reinterpret_cast<const sif_dec_desc*>(w + p->ws_desc_off);
+  a.descs = reinterpret_cast<const sif_dec_desc*>(wb + w.desc);
   a.n = p->n;
-  a.table = reinterpret_cast<uint32_t*>(w + p->ws_aux_off);
+  a.table = reinterpret_cast<uint32_t*>(wb + w.table);
   a.table_stride = (2ull + (uint64_t)p->max_blocks) * sif::TROW_U32;
-  a.tiles = reinterpret_cast<const sif::DecTile*>(w + p->ws_spill_off);
-  a.acc = reinterpret_cast<uint32_t*>(w + p->ws_spill_off + up(sizeof(sif::DecTile) * std::max<int>(p->tiles, 1), 256));
-  a.ntiles = p->tiles;
+  a.acc = reinterpret_cast<uint32_t*>(wb + w.acc);
   a.parse_only = parse_only;
-  a.tile_elems = kDecTileElems;
-  a.rpc_cap = kDecRpcCap;
   a.status = status;
-  a.tiles_per_if = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(a.acc) + up(16ull * p->n, 256));
+  a.seg_base = reinterpret_cast<const uint32_t*>(wb + w.segbase);
+  a.item_base = reinterpret_cast<const uint64_t*>(wb + w.itembase);
+  a.segw = p->tiles;
   sif::sif_parse_kernel<<<(p->n + 127) / 128, 128, 0, s>>>(a);
-  if (check_cuda(cudaGetLastError())) return SIF_ERR_CUDA;
-  if (check_cuda(cudaFuncSetAttribute(sif::sif_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem_bytes)))
-    return SIF_ERR_CUDA;
-  sif::sif_scatter_kernel<<<p->tiles + p->n, sif::DNT, p->smem_bytes, s>>>(a);
+  sif::sif_dcrc_kernel<<<(unsigned)p->cluster, sif::DNT, 0, s>>>(a);
+  if (!parse_only) {
+    static int attr_bytes = 0;
+    if (p->smem_bytes > attr_bytes) {
+      if (check_cuda(cudaFuncSetAttribute(sif::sif_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          std::max(p->smem_bytes, 1))))
+        return SIF_ERR_CUDA;
+      attr_bytes = p->smem_bytes;
+    }
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sif::sif_scatter_kernel, sif::DNT, p->smem_bytes) != cudaSuccess ||
+        per < 1)
+      per = 1;
+    sif::sif_scatter_kernel<<<(unsigned)(per * num_sms()), sif::DNT, p->smem_bytes, s>>>(a);
+  }
+  sif::sif_dfinal_kernel<<<(p->n + 127) / 128, 128, 0, s>>>(a);
   return check_cuda(cudaGetLastError());
 }
 
