@@ -16,7 +16,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import time
 
@@ -59,48 +58,64 @@ def _ncu_traffic(config: str):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled with NVML every ~1 ms while the
+    timed region runs (a background thread; nvidia-smi's 50 ms period is too coarse for a
+    sub-second region)."""
+
+    NAMES = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+             0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.proc = None
-        self.path = f"/tmp/sif_clocks_{os.getpid()}.csv"
+        self.samples = []
+        self.max_mhz = None
+        self._stop = None
+        self._thr = None
+
+    def _run(self):
+        import pynvml
+
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+        get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), int(get_reasons(h))))
+            except Exception:  # noqa: BLE001
+                break
+            time.sleep(0.001)
 
     def __enter__(self):
+        import threading
+
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu),
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except OSError:
-            self.proc = None
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self._stop = threading.Event()
+            self._thr = threading.Thread(target=self._run, daemon=True)
+            self._thr.start()
+        except Exception:  # noqa: BLE001
+            self._thr = None
         return self
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        if self._thr is not None:
+            self._stop.set()
+            self._thr.join(timeout=2)
 
     def summary(self):
-        try:
-            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
-        except OSError:
+        if not self.samples:
             return None
-        if not rows:
-            return None
-        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 3 + i and "Active" in r[3 + i]
-                          and "Not" not in r[3 + i]})
-        return dict(sm_mhz=statistics.median(sm) if sm else None, sm_max_mhz=max(mx) if mx else None,
-                    reasons=reasons, samples=len(rows))
+        mhz = [m for m, _ in self.samples]
+        bits = 0
+        for _, r in self.samples:
+            bits |= r
+        reasons = sorted(n for b, n in self.NAMES.items() if bits & b)
+        return dict(sm_mhz=statistics.median(mhz), sm_max_mhz=self.max_mhz, reasons=reasons, samples=len(mhz),
+                    source="nvml, 1 ms period")
 
 
 # ------------------------------------------------------------------------- CPU arm
@@ -160,8 +175,38 @@ def run_reference(args, conf, rank):
 
 
 # ------------------------------------------------------------------------- GPU arm
+# Algorithmic bytes per launch of the kernels that carry the path's compulsory traffic
+# (B_alg = T*b_in + P + P + T*b_out per IF); the other kernels of the
+# pipeline move only intermediate data and count 0.
+def _alg_bytes(name, raw, payload, dense_out):
+    return {"enc_stream": raw, "enc_pack": payload, "enc_crc": payload, "sif_dcrc_kernel": payload,
+            "sif_scatter_kernel": dense_out + payload}.get(name, 0)
+
+
+def _kernel_profile(sif, step, steps):
+    """Per-kernel average launch durations: the same steps again with every library kernel
+    bracketed by CUDA events on its stream (sif_profile_enable)."""
+    import ctypes
+
+    import torch
+
+    L = sif._lib.load()
+    L.sif_profile_enable(1)
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+    L.sif_profile_enable(0)
+    ms = (ctypes.c_double * 32)()
+    cnt = (ctypes.c_int32 * 32)()
+    nk = L.sif_profile_read(ms, cnt, 32)
+    out = {}
+    for k in range(max(0, nk)):
+        if cnt[k]:
+            out[L.sif_profile_kernel_name(k).decode()] = dict(ms_total=ms[k], launches=int(cnt[k]))
+    return out
+
+
 def run_ours(args, conf, rank, world, local_rank):
-    import numpy as np
     import torch
 
     import paper_2511_11608_b200 as sif
@@ -191,8 +236,9 @@ def run_ours(args, conf, rank, world, local_rank):
     torch.cuda.synchronize()
     payload_total = int(lens.sum())
     raw_bytes = B * N * K * b_in
+    dense_out = B * N * K * 4
     alg_enc = raw_bytes + payload_total
-    alg_dec = payload_total + B * N * K * 4
+    alg_dec = payload_total + dense_out
     stream = torch.cuda.current_stream()
 
     def step():
@@ -225,13 +271,15 @@ def run_ours(args, conf, rank, world, local_rank):
     enc_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps
     dec_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps
     st_ms = total_ms / args.steps
-    # status after timing (must all be OK)
-    enc.check()
+    enc.check()  # status after timing (must all be OK)
     dec.check()
     if pg:
         t = torch.tensor([st_ms, enc_ms, dec_ms], dtype=torch.float64, device=dev)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         st_ms, enc_ms, dec_ms = [float(v) for v in t.cpu().numpy()]
+
+    # per-kernel durations (instrumented repeat of the same steps, after the timed region)
+    kprof = _kernel_profile(sif, step, args.steps)
 
     # ---- e2e through the public API with host buffers (pinned), copies inside the timing
     x_host = xs.cpu().pin_memory()
@@ -282,34 +330,50 @@ def run_ours(args, conf, rank, world, local_rank):
     if rank == 0:
         hbm, peak_kind = _peaks()
         value = world * raw_bytes / (st_ms * 1e-3) / 1e9
-        enc_gbs = alg_enc / (enc_ms * 1e-3) / 1e9
-        dec_gbs = alg_dec / (dec_ms * 1e-3) / 1e9
         step_gbs = (alg_enc + alg_dec) / (st_ms * 1e-3) / 1e9
-        dominant = "sif_encode_kernel" if enc_ms >= dec_ms else "sif_scatter_kernel"
-        dom_ach = enc_gbs if enc_ms >= dec_ms else dec_gbs
-        traffic = _ncu_traffic(args.config)
+        kernels = {}
+        prof_ms = sum(v["ms_total"] for v in kprof.values()) or 1.0
+        for name, v in kprof.items():
+            per = v["ms_total"] / v["launches"]
+            alg = _alg_bytes(name, raw_bytes, payload_total, dense_out)
+            kernels[name] = dict(us_per_launch=round(per * 1e3, 2), launches_per_step=v["launches"] // args.steps,
+                                 share=round(v["ms_total"] / prof_ms, 4), alg_bytes_per_launch=alg,
+                                 alg_gbs=round(alg / (per * 1e-3) / 1e9, 1) if alg else 0.0)
+        # dominant kernel: the longest one that carries compulsory (algorithmic) traffic
+        cand = [k for k, v in kernels.items() if v["alg_bytes_per_launch"]]
+        dom = max(cand, key=lambda k: kernels[k]["us_per_launch"]) if cand else None
+        traffic = (_ncu_traffic(args.config) or {}).get(dom) if dom else None
+        roof = None
+        if dom:
+            kd = kernels[dom]
+            roof = dict(bound="hbm", kernel=dom, achieved=kd["alg_gbs"], peak=hbm, unit="GB/s",
+                        frac=round(kd["alg_gbs"] / hbm, 4), traffic=traffic, peak_source=peak_kind,
+                        algorithmic_bytes_per_launch=kd["alg_bytes_per_launch"], us_per_launch=kd["us_per_launch"],
+                        share_of_step=kd["share"],
+                        note="per-launch duration from CUDA events around each library kernel in an instrumented "
+                             "repeat of the timed steps")
         line = dict(
             metric=METRIC, value=round(value, 3), unit="GB/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
             ms_per_step=round(st_ms, 5), higher_is_better=True, scaling="weak", vs_baseline=None,
             dtype=conf["dtype"], data="synthetic (integer-exact device generator, SURVEY.md §8(d))",
             config=dict(workload=conf["workload"], codec=CODEC, if_shape=[N, K], batch_per_gpu=B,
                         parallelism=f"dp{world} (independent IF streams per GPU, no collectives)",
-                        l2="per-step inputs %.0f MB/GPU exceed the 126 MB L2; no flush" % (raw_bytes / 1e6)),
-            roofline=dict(bound="hbm", kernel=dominant, achieved=round(dom_ach, 2), peak=hbm, unit="GB/s",
-                          frac=round(dom_ach / hbm, 4), traffic=(traffic or {}).get(dominant),
-                          peak_source=peak_kind,
-                          algorithmic_bytes_per_launch=alg_enc if dominant == "sif_encode_kernel" else alg_dec),
-            roofline_step=dict(achieved=round(step_gbs, 2), frac=round(step_gbs / hbm, 4),
+                        l2="per-step inputs %.0f MB/GPU %s the 126 MB L2; no flush" %
+                           (raw_bytes / 1e6, "exceed" if raw_bytes > 126e6 else "fit in")),
+            roofline=roof,
+            roofline_step=dict(achieved=round(step_gbs, 2), frac=round(step_gbs / hbm, 4), unit="GB/s",
                                algorithmic_bytes_per_step=alg_enc + alg_dec,
                                encode_ms=round(enc_ms, 5), decode_ms=round(dec_ms, 5),
-                               encode_gbs=round(enc_gbs, 2), decode_gbs=round(dec_gbs, 2)),
+                               encode_gbs=round(alg_enc / (enc_ms * 1e-3) / 1e9, 2),
+                               decode_gbs=round(alg_dec / (dec_ms * 1e-3) / 1e9, 2)),
+            kernels=kernels,
             bits_per_element=round(8.0 * payload_total / (B * N * K), 6),
             raw_gbs_per_gpu=round(raw_bytes / (st_ms * 1e-3) / 1e9, 3),
             e2e=dict(value=round(world * raw_bytes / (e2e_ms * 1e-3) / 1e9, 3), unit="GB/s",
                      h2d_bytes_per_step=int(x_host.numel() * x_host.element_size() + pay_host.numel()),
                      d2h_bytes_per_step=int(pay_host.numel() + y_host.numel() * 4),
                      ms_per_step=round(e2e_ms, 4)),
-            gpu_launches=3 * args.steps,
+            gpu_launches=sum(v["launches"] for v in kprof.values()),
             clocks=clk.summary(),
             cpu_baseline=cpu,
         )

@@ -139,6 +139,16 @@ int sif_decode_batched(const sif_dec_desc* descs, int n, int parse_only, void* d
  * row holds {status, rows, cols, m_plus, m_minus, mode, q_bit, nblocks}. */
 uint64_t sif_dec_table_stride(const sif_plan* plan);
 
+/* ---- per-kernel timing (diagnostics) ----
+ * While enabled, every kernel launched by sif_enc_run / sif_dec_run is bracketed by CUDA
+ * events on its stream.  sif_profile_read synchronizes those events, fills ms[k] (total
+ * milliseconds) and count[k] (launches) for kernel kinds k < maxk, clears the record and
+ * returns the number of kernel kinds (or -status on failure); sif_profile_kernel_name(k)
+ * names kind k. */
+int sif_profile_enable(int on);
+int sif_profile_read(double* ms, int32_t* count, int maxk);
+const char* sif_profile_kernel_name(int k);
+
 /* ---- device synthetic IF generator (bench/tests) ---- */
 int sif_gen_synthetic(void* d_x, uint32_t rows, uint32_t cols, uint32_t dtype, uint32_t kind,
                       uint64_t sid, void* stream);

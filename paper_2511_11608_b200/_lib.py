@@ -57,6 +57,9 @@ EXPORTS = {
     "sif_decode_batched": (c_int, [POINTER(DecDesc), c_int, c_int, c_void_p, c_size_t, c_void_p, c_void_p]),
     "sif_dec_table_stride": (c_uint64, [POINTER(Plan)]),
     "sif_gen_synthetic": (c_int, [c_void_p, c_uint32, c_uint32, c_uint32, c_uint32, c_uint64, c_void_p]),
+    "sif_profile_enable": (c_int, [c_int]),
+    "sif_profile_read": (c_int, [POINTER(c_double), POINTER(c_int32), c_int]),
+    "sif_profile_kernel_name": (ctypes.c_char_p, [c_int]),
 }
 
 _lib = None

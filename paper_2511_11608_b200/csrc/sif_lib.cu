@@ -20,6 +20,32 @@ inline uint64_t up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 
 int check_cuda(cudaError_t e) { return e == cudaSuccess ? SIF_OK : SIF_ERR_CUDA; }
 
+// ---- optional per-kernel timing (diagnostics; sif_profile_enable)
+enum { KP_PREP, KP_STREAM, KP_SELECT, KP_MEMBERS, KP_ABQ1, KP_ABQ2, KP_LAYOUT, KP_PACK, KP_CRC, KP_PARSE, KP_DCRC,
+       KP_SCATTER, KP_DFINAL, KP_N };
+const char* kKpNames[KP_N] = {"enc_prep", "enc_stream", "enc_select", "enc_members", "enc_abq<1>", "enc_abq<0>",
+                              "enc_layout", "enc_pack", "enc_crc", "sif_parse_kernel", "sif_dcrc_kernel",
+                              "sif_scatter_kernel", "sif_dfinal_kernel"};
+struct ProfRec { int k; cudaEvent_t a, b; };
+bool g_prof = false;
+std::vector<ProfRec> g_recs;
+struct ProfScope {
+  int k;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+  ProfScope(int kk, cudaStream_t ss) : k(kk), s(ss) {
+    if (!g_prof) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+  }
+  ~ProfScope() {
+    if (!g_prof || !a) return;
+    cudaEventRecord(b, s);
+    g_recs.push_back({k, a, b});
+  }
+};
+
 inline int num_sms() {
   static int sms = 0;
   if (!sms) {
@@ -76,6 +102,28 @@ inline uint32_t crc_segments(uint64_t cap) { return (uint32_t)std::max<uint64_t>
 extern "C" {
 
 int sif_version(void) { return 1; }
+
+int sif_profile_enable(int on) {
+  g_prof = on != 0;
+  return SIF_OK;
+}
+
+int sif_profile_read(double* ms, int32_t* count, int maxk) {
+  if (!ms || !count || maxk < 0) return SIF_ERR_INVALID_ARG;
+  for (int k = 0; k < maxk; ++k) { ms[k] = 0.0; count[k] = 0; }
+  int st = SIF_OK;
+  for (const ProfRec& r : g_recs) {
+    float t = 0.f;
+    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) st = SIF_ERR_CUDA;
+    if (r.k < maxk) { ms[r.k] += t; count[r.k] += 1; }
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_recs.clear();
+  return st ? -st : KP_N;
+}
+
+const char* sif_profile_kernel_name(int k) { return k >= 0 && k < KP_N ? kKpNames[k] : ""; }
 
 uint64_t sif_keep_count(double s, uint64_t t) { return sif::keep_count(s, t); }
 
@@ -289,18 +337,18 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   const unsigned nch = (unsigned)p->tiles;
   const unsigned n = (unsigned)p->n;
   const unsigned wgrid = std::max(1u, (nch + sif::CNT / 32 - 1) / (sif::CNT / 32));  // >= 1 chunk per warp
-  sif::enc_prep<<<n, 256, 0, s>>>(a);
-  sif::enc_stream<<<std::min<unsigned>(nch, g_stream), sif::CNT, kSmemStream, s>>>(a);
-  sif::enc_select<<<n, sif::SNT, kSmemSelect, s>>>(a);
+  { ProfScope ps(KP_PREP, s); sif::enc_prep<<<n, 256, 0, s>>>(a); }
+  { ProfScope ps(KP_STREAM, s); sif::enc_stream<<<std::min<unsigned>(nch, g_stream), sif::CNT, kSmemStream, s>>>(a); }
+  { ProfScope ps(KP_SELECT, s); sif::enc_select<<<n, sif::SNT, kSmemSelect, s>>>(a); }
   if (!atkf) {
-    sif::enc_members<<<std::min<unsigned>(wgrid, g_members), sif::CNT, 0, s>>>(a);
+    { ProfScope ps(KP_MEMBERS, s); sif::enc_members<<<std::min<unsigned>(wgrid, g_members), sif::CNT, 0, s>>>(a); }
     if (c->mode != SIF_MODE_FIXED) {
-      sif::enc_abq<1><<<std::min<unsigned>(wgrid, g_abq), sif::CNT, smem_abq(maxb), s>>>(a);
-      sif::enc_abq<0><<<std::min<unsigned>(wgrid, g_abq), sif::CNT, smem_abq(maxb), s>>>(a);
+      { ProfScope ps(KP_ABQ1, s); sif::enc_abq<1><<<std::min<unsigned>(wgrid, g_abq), sif::CNT, smem_abq(maxb), s>>>(a); }
+      { ProfScope ps(KP_ABQ2, s); sif::enc_abq<0><<<std::min<unsigned>(wgrid, g_abq), sif::CNT, smem_abq(maxb), s>>>(a); }
     }
-    sif::enc_layout<<<n, 256, 0, s>>>(a);
-    sif::enc_pack<<<std::min<unsigned>(wgrid, g_pack), sif::CNT, smem_pack(maxb), s>>>(a);
-    sif::enc_crc<<<(unsigned)p->cluster, 256, 0, s>>>(a);
+    { ProfScope ps(KP_LAYOUT, s); sif::enc_layout<<<n, 256, 0, s>>>(a); }
+    { ProfScope ps(KP_PACK, s); sif::enc_pack<<<std::min<unsigned>(wgrid, g_pack), sif::CNT, smem_pack(maxb), s>>>(a); }
+    { ProfScope ps(KP_CRC, s); sif::enc_crc<<<(unsigned)p->cluster, 256, 0, s>>>(a); }
   }
   return check_cuda(cudaGetLastError());
 }
@@ -445,8 +493,8 @@ int sif_dec_run(const sif_plan* p, int parse_only, void* ws, int32_t* status, vo
   a.seg_base = reinterpret_cast<const uint32_t*>(wb + w.segbase);
   a.item_base = reinterpret_cast<const uint64_t*>(wb + w.itembase);
   a.segw = p->tiles;
-  sif::sif_parse_kernel<<<(p->n + 127) / 128, 128, 0, s>>>(a);
-  sif::sif_dcrc_kernel<<<(unsigned)p->cluster, sif::DNT, 0, s>>>(a);
+  { ProfScope ps(KP_PARSE, s); sif::sif_parse_kernel<<<(p->n + 127) / 128, 128, 0, s>>>(a); }
+  { ProfScope ps(KP_DCRC, s); sif::sif_dcrc_kernel<<<(unsigned)p->cluster, sif::DNT, 0, s>>>(a); }
   if (!parse_only) {
     static int attr_bytes = 0;
     if (p->smem_bytes > attr_bytes) {
@@ -459,9 +507,10 @@ int sif_dec_run(const sif_plan* p, int parse_only, void* ws, int32_t* status, vo
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sif::sif_scatter_kernel, sif::DNT, p->smem_bytes) != cudaSuccess ||
         per < 1)
       per = 1;
+    ProfScope ps(KP_SCATTER, s);
     sif::sif_scatter_kernel<<<(unsigned)(per * num_sms()), sif::DNT, p->smem_bytes, s>>>(a);
   }
-  sif::sif_dfinal_kernel<<<(p->n + 127) / 128, 128, 0, s>>>(a);
+  { ProfScope ps(KP_DFINAL, s); sif::sif_dfinal_kernel<<<(p->n + 127) / 128, 128, 0, s>>>(a); }
   return check_cuda(cudaGetLastError());
 }
 

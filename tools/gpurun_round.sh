@@ -1,9 +1,21 @@
-set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/r1_smi.txt 2>&1
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/r1_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r1_pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r1_smoke.log 2>&1
-for c in c2 c3 c4; do timeout 600 python bench.py --config $c --steps 20 --warmup 5 > gpurun_out/r1_bench_$c.json 2> gpurun_out/r1_bench_$c.err; done
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/r1_launches_c2.csv python bench.py --config c2 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/r1_ncu_launch.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:sif_encode_kernel -s 3 -c 1 -o gpurun_out/r1_enc_c2 python bench.py --config c2 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/r1_ncu_enc.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:sif_scatter_kernel -s 3 -c 1 -o gpurun_out/r1_dec_c2 python bench.py --config c2 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/r1_ncu_dec.log 2>&1
-ls -la gpurun_out
+# Full round evidence: GPU tests, smoke, 1-GPU bench of c2/c3/c4 (with CPU baseline),
+# launch lists and ncu --set full captures of one encode+decode step per config.
+# usage: bash tools/gpurun_round.sh TAG
+TAG=${1:-r1}
+O=gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv > $O/${TAG}_smi.txt 2>&1
+timeout 900 python -m pytest tests -x -q -m gpu > $O/${TAG}_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/${TAG}_pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/${TAG}_smoke.log 2>&1; echo "smoke rc=$?" >> $O/${TAG}_smoke.log
+for c in c2 c3 c4; do timeout 600 python bench.py --config $c --steps 20 --warmup 5 > $O/${TAG}_bench_$c.json 2> $O/${TAG}_bench_$c.err; done
+timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > $O/${TAG}_bench_ref_c2.json 2> $O/${TAG}_bench_ref_c2.err
+KRE='regex:enc_|sif_(parse|dcrc|scatter|dfinal)'
+for c in c2 c3 c4; do
+  timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KRE" -c 26 --csv --log-file $O/${TAG}_launches_$c.csv python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k "$KRE" -s 13 -c 13 -o $O/${TAG}_full_$c python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+done
+
+# summarise on the box (reports are too large to bring back together), keep the c2 report
+python tools/make_profiles.py ${TAG} c2:$O/${TAG}_full_c2.ncu-rep c3:$O/${TAG}_full_c3.ncu-rep c4:$O/${TAG}_full_c4.ncu-rep > $O/${TAG}_profiles.log 2>&1
+mkdir -p $O/profiles && cp profiles/${TAG}_*_ncu.txt profiles/ncu_traffic.json $O/profiles/ 2>/dev/null
+rm -f $O/${TAG}_full_c3.ncu-rep $O/${TAG}_full_c4.ncu-rep
+du -sh $O
