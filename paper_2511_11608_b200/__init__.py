@@ -13,6 +13,7 @@ from .codec import (
     AtkfResult,
     BatchDecoder,
     BatchEncoder,
+    ListEncoder,
     CodecConfig,
     Payload,
     atkf_filter,
@@ -20,15 +21,18 @@ from .codec import (
     col_bits,
     decode,
     decode_batch,
+    decode_list,
     deserialize,
     encode,
     encode_batch,
+    encode_list,
     keep_count,
     max_payload_bytes,
     payload_bits_exact,
     serialize,
     synthetic,
 )
+from . import shard
 from .errors import (
     CapacityError,
     ConfigError,

@@ -244,6 +244,55 @@ class BatchEncoder:
         return [Payload(self.out[i], int(lens[i]), self.rows, self.cols) for i in range(self.B)]
 
 
+class ListEncoder:
+    """Plan + descriptors for a list of IFs of arbitrary shapes and dtypes (e.g. the mixed
+    vision/LLM streams of one GPU's shard), encoded by one launch sequence.  Payloads are
+    written into one flat device buffer at 16-byte aligned offsets."""
+
+    def __init__(self, xs: list, cfg: CodecConfig, seeds, stream=None):
+        if not isinstance(cfg, CodecConfig):
+            raise ConfigError("cfg must be a CodecConfig")
+        ts = [_as_if(x) for x in xs]
+        self.xs = [t for t, _ in ts]
+        self.cfg = cfg
+        self.B = len(self.xs)
+        self.shapes = [tuple(t.shape) for t in self.xs]
+        self.caps = [max_payload_bytes(r, c, cfg) for r, c in self.shapes]
+        self.offs, acc = [], 0
+        for cap in self.caps:
+            self.offs.append(acc)
+            acc += cap
+        dev = torch.device("cuda")
+        self.out = torch.zeros(max(16, acc), dtype=torch.uint8, device=dev)
+        self.out_len = torch.zeros(max(1, self.B), dtype=torch.int64, device=dev)
+        self.status = torch.full((max(1, self.B),), -1, dtype=torch.int32, device=dev)
+        self.seeds = [_check_seed(sd) for sd in seeds]
+        outs = [self.out.data_ptr() + o for o in self.offs]
+        self._descs = _enc_descs(self.xs, outs, self.caps, self.seeds, [d for _, d in ts])
+        self._cfg_c, self._keep = cfg._c()
+        self.plan = _lib.Plan()
+        raise_for(_L().sif_enc_plan(self._descs, self.B, ctypes.byref(self._cfg_c), ctypes.byref(self.plan)),
+                  "sif_enc_plan")
+        self.ws = torch.empty(max(1, self.plan.ws_bytes), dtype=torch.uint8, device=dev)
+        raise_for(_L().sif_enc_upload(ctypes.byref(self.plan), self._descs, ctypes.byref(self._cfg_c),
+                                      ctypes.c_void_p(self.ws.data_ptr()), _stream()), "sif_enc_upload")
+
+    run = BatchEncoder.run
+    check = BatchEncoder.check
+
+    def payloads(self) -> list:
+        lens = self.out_len.cpu().numpy()
+        return [Payload(self.out[o:o + cap], int(lens[i]), r, c)
+                for i, (o, cap, (r, c)) in enumerate(zip(self.offs, self.caps, self.shapes))]
+
+
+def encode_list(xs: list, cfg: CodecConfig, seeds) -> list:
+    """encode() of a list of IFs with arbitrary shapes/dtypes in one launch sequence."""
+    enc = ListEncoder(xs, cfg, list(seeds))
+    enc.run().check()
+    return enc.payloads()
+
+
 def encode(x, cfg: CodecConfig, seed: int = 0) -> Payload:
     """serialize(encode(x, cfg, seed)) of the reference, computed on the GPU."""
     if not isinstance(cfg, CodecConfig):
@@ -271,24 +320,38 @@ def payload_bits_exact(p: Payload) -> int:
 
 # ---------------------------------------------------------------------------- decode
 class BatchDecoder:
-    """Plan + descriptors for decoding B streams into a (B, rows, cols) fp32 tensor."""
+    """Plan + descriptors for decoding B streams into a (B, rows, cols) fp32 tensor, or, with
+    `shapes` (one (rows, cols) per stream), into per-stream tensors `self.outs` (views of one
+    flat buffer)."""
 
-    def __init__(self, bufs, lens, rows: int, cols: int, out: torch.Tensor | None = None,
-                 parse_only: bool = False):
+    def __init__(self, bufs, lens, rows: int = 0, cols: int = 0, out: torch.Tensor | None = None,
+                 parse_only: bool = False, shapes=None):
         self.B = len(lens)
-        self.rows, self.cols = int(rows), int(cols)
         dev = torch.device("cuda")
-        self.out = out if out is not None else torch.empty((self.B, self.rows, self.cols), dtype=torch.float32,
-                                                            device=dev)
+        if shapes is None:
+            shapes = [(int(rows), int(cols))] * self.B
+            self.rows, self.cols = int(rows), int(cols)
+            self.out = out if out is not None else torch.empty((self.B, self.rows, self.cols), dtype=torch.float32,
+                                                                device=dev)
+            offs = [i * self.rows * self.cols for i in range(self.B)]
+            self.outs = [self.out[i] for i in range(self.B)] if self.out.numel() else []
+        else:
+            shapes = [(int(r), int(c)) for r, c in shapes]
+            offs, acc = [], 0
+            for r, c in shapes:
+                offs.append(acc)
+                acc += (r * c + 3) // 4 * 4  # 16-byte aligned starts
+            self.out = torch.empty(max(1, acc), dtype=torch.float32, device=dev)
+            self.outs = [self.out[o:o + r * c].view(r, c) for o, (r, c) in zip(offs, shapes)]
         self.status = torch.full((self.B,), -1, dtype=torch.int32, device=dev)
         self.parse_only = 1 if parse_only else 0
         arr = (_lib.DecDesc * max(1, self.B))()
         for i in range(self.B):
             arr[i].inp = bufs[i]
             arr[i].in_len = int(lens[i])
-            arr[i].out = self.out.data_ptr() + i * self.rows * self.cols * 4
-            arr[i].rows = self.rows
-            arr[i].cols = self.cols
+            arr[i].out = self.out.data_ptr() + offs[i] * 4
+            arr[i].rows = shapes[i][0]
+            arr[i].cols = shapes[i][1]
         self._descs = arr
         self.plan = _lib.Plan()
         raise_for(_L().sif_dec_plan(arr, self.B, ctypes.byref(self.plan)), "sif_dec_plan")
@@ -368,6 +431,16 @@ def decode_batch(payloads: list, out: torch.Tensor | None = None) -> torch.Tenso
     dec = BatchDecoder([p.buf.data_ptr() for p in payloads], [p.nbytes for p in payloads], rows, cols, out=out)
     dec.run().check()
     return dec.out
+
+
+def decode_list(payloads: list) -> list:
+    """decode() of payloads with arbitrary shapes in one launch sequence; fp32 tensors."""
+    if not payloads:
+        return []
+    dec = BatchDecoder([p.buf.data_ptr() for p in payloads], [p.nbytes for p in payloads],
+                       shapes=[(p.rows, p.cols) for p in payloads])
+    dec.run().check()
+    return dec.outs
 
 
 def _parse_table(p: Payload) -> list:
