@@ -84,6 +84,13 @@ __device__ __forceinline__ uint32_t crc_x8n(uint64_t nbytes) {
 __device__ __forceinline__ uint32_t crc_shift(uint32_t c, uint64_t nbytes) {
   return c ? crc_mult(crc_x8n(nbytes), c) : 0u;
 }
+// kSegShift[j] = x^(8 * CRC_SEG * j) mod P: shifts a segment's raw CRC over j whole
+// segments (segments are aligned to the end of the CRC range).  Filled by the host
+// (sif_lib.cu, crc_tables_init) before the first CRC launch.
+constexpr uint64_t CRC_SEG = 16384;
+constexpr int CRC_SEG_MAX = 8192;  // payloads up to 128 MiB per CTA-segment table
+__device__ uint32_t kSegShift[CRC_SEG_MAX];
+
 __device__ __forceinline__ uint32_t crc_finish(uint32_t raw_total, uint64_t len) {
   return raw_total ^ crc_mult(crc_x8n(len), 0xFFFFFFFFu) ^ 0xFFFFFFFFu;
 }

@@ -34,7 +34,7 @@ struct DecArgs {
   int segw;                    // columns per work item (<= 1024, multiple of 4)
 };
 
-constexpr uint64_t SEGD = 65536;  // CRC segment bytes per CTA
+constexpr uint64_t SEGD = CRC_SEG;  // CRC segment bytes per CTA
 
 // ------------------------------------------------------------------------------- parse
 __device__ __forceinline__ uint32_t rd_u32(const uint8_t* p, uint64_t o) {
@@ -119,13 +119,16 @@ __global__ void __launch_bounds__(DNT) sif_dcrc_kernel(DecArgs a) {
   if (tab[TROW_U32 + 0]) return;  // length / magic failure: no CRC
   const sif_dec_desc d = a.descs[ifi];
   const uint64_t len = d.in_len;
-  const uint64_t s0 = 4 + (uint64_t)seg * SEGD, s1 = min(len - 4, s0 + SEGD);
-  if (s0 >= s1) return;
+  const uint64_t b0 = 4, b1 = len - 4;
+  // segment `seg` covers [b1 - (seg+1)*SEGD, b1 - seg*SEGD) clipped to [b0, b1)
+  const uint64_t e1 = seg * SEGD < b1 - b0 ? b1 - seg * SEGD : b0;
+  const uint64_t e0 = e1 - b0 > SEGD ? e1 - SEGD : b0;
+  if (e0 >= e1) return;
   for (int k = tid; k < 1024; k += DNT) t4[k] = (&kCrcTab4[0][0])[k];
   __syncthreads();
-  const uint32_t raw = crc_cta_staged<DNT>(d.in, s0, s1, t4, red, stage);
+  const uint32_t raw = crc_cta_staged<DNT>(d.in, e0, e1, t4, red, stage);
   if (tid == 0) {
-    const uint32_t part = crc_shift(raw, (len - 4) - s1);
+    const uint32_t part = raw ? crc_mult(kSegShift[seg], raw) : 0u;
     if (part) atomicXor(a.acc + 4ull * ifi + 0, part);
   }
 }

@@ -37,7 +37,7 @@ constexpr int CH = 4096;           // elements per chunk
 constexpr int UNITS = 8;           // warp-streamed units per chunk
 constexpr int UE = CH / UNITS;     // elements per unit
 constexpr int CNT = 256;           // threads of chunk kernels
-constexpr int SEG = 65536;         // CRC segment bytes per CTA
+constexpr int SEG = (int)CRC_SEG;  // CRC segment bytes per CTA
 constexpr int DSH = 19;            // digit = |x| key >> 19 (12 bits)
 constexpr int ND = 4096;           // digits per sign
 constexpr int MAXB = 32;           // max blocks (M+ + M-) per IF
@@ -225,15 +225,15 @@ __device__ void find_digit(SelSh& sh, const uint32_t* H, int nb, uint64_t r) {
   __syncthreads();
 }
 
-// Multi-level radix select on 64-bit keys ("r-th largest") over list elements accepted by
-// fn(bits, idx, &key).  Used for huge single-value tie sets.
+// Multi-level radix select ("r-th largest") on keys of `nbits` bits (64 or <= 33) over list
+// elements accepted by fn(bits, idx, &key).  Used for huge single-value tie sets.
 template <int NT, class KeyFn>
-__device__ uint64_t radix_select64(SelSh& sh, uint32_t* hist, const List& L, uint32_t n, uint64_t r, KeyFn fn) {
-  const int shifts[6] = {53, 42, 31, 20, 9, 0};
-  const int widths[6] = {11, 11, 11, 11, 11, 9};
+__device__ uint64_t radix_select64(SelSh& sh, uint32_t* hist, const List& L, uint32_t n, uint64_t r, KeyFn fn,
+                                   int nbits = 64) {
   uint64_t prefix = 0, mask = 0;
-  for (int lev = 0; lev < 6; ++lev) {
-    const int shf = shifts[lev], nb = 1 << widths[lev];
+  for (int hi = nbits; hi > 0;) {
+    const int wdt = hi >= 11 ? 11 : hi;
+    const int shf = hi - wdt, nb = 1 << wdt;
     for (int i = threadIdx.x; i < nb; i += NT) hist[i] = 0;
     __syncthreads();
     list_foreach<NT>(L, n, [&](uint32_t b, uint32_t x) {
@@ -246,6 +246,7 @@ __device__ uint64_t radix_select64(SelSh& sh, uint32_t* hist, const List& L, uin
     mask |= (uint64_t)(nb - 1) << shf;
     r -= sh.fd_above;
     __syncthreads();
+    hi = shf;
   }
   return prefix;
 }
@@ -265,7 +266,7 @@ struct SelRes {
 // select on the secondary key.  scratch: 2*HB u32 + GCAP GatE.
 template <int NT, class Pred, class KeyF, class SecF>
 __device__ SelRes select_exact(SelSh& sh, uint32_t* scratch, const List& L, uint32_t n, Pred pred, KeyF keyf,
-                               SecF secf, uint64_t klo, uint64_t khi, uint64_t r) {
+                               SecF secf, uint64_t klo, uint64_t khi, uint64_t r, int sec_bits = 64) {
   constexpr int NW = NT / 32;
   uint32_t* hist = scratch;
   GatE* gl = reinterpret_cast<GatE*>(scratch + 2 * HB);
@@ -306,12 +307,14 @@ __device__ SelRes select_exact(SelSh& sh, uint32_t* scratch, const List& L, uint
     res.sec = 0;
     if (!res.all_ties) {
       const uint32_t kk = (uint32_t)klo;
+      // smallest secondary keys first: select the r-th largest of (2^sec_bits - 1 - sec)
+      const uint64_t smax = sec_bits >= 64 ? ~0ull : ((1ull << sec_bits) - 1ull);
       const uint64_t top = radix_select64<NT>(sh, hist, L, n, r, [&](uint32_t b, uint32_t x, uint64_t& k) {
         if (!pred(b, x) || keyf(b) != kk) return false;
-        k = ~secf(b, x);
+        k = smax - secf(b, x);
         return true;
-      });
-      res.sec = ~top;
+      }, sec_bits);
+      res.sec = smax - top;
     }
     return res;
   }
@@ -733,7 +736,8 @@ struct K3Sh {
   uint32_t keptA[2];
   uint64_t cnt_nz;
   uint32_t pend_n;
-  uint32_t pend_s[MAXB], pend_d[MAXB], pend_r[MAXB], pend_ci[MAXB];
+  uint32_t pend_s[MAXB], pend_d[MAXB], pend_r[MAXB], pend_ci[MAXB], pend_reg[MAXB];
+  uint32_t reg_off[MAXB], reg_cnt[MAXB];
 };
 
 __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
@@ -1016,7 +1020,8 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
       if ((int)dc == dtau) {
         const SelRes r = select_exact<NT>(
             sh, scratch, A, nA, [&](uint32_t b, uint32_t x) { return (b >> 31) == s && kept_of(b, x); }, key31,
-            [](uint32_t, uint32_t x) -> uint64_t { return x; }, (uint64_t)dc << DSH, (uint64_t)(dc + 1) << DSH, rc);
+            [](uint32_t, uint32_t x) -> uint64_t { return x; }, (uint64_t)dc << DSH, (uint64_t)(dc + 1) << DSH, rc,
+            31);
         if (tid == 0) { st.cut_key[ci] = r.key; st.cut_idx[ci] = (uint32_t)r.sec; }
       } else if (tid == 0) {
         const uint32_t p = k3.pend_n++;
@@ -1026,33 +1031,46 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
     }
     const uint32_t np = k3.pend_n;
     if (np > 0) {
-      // gather every pending cut bin in one pass (B reuses A's storage)
-      uint32_t* pm = scratch;  // bitmap of pending (sign, digit): 2*ND bits
+      // gather every pending cut bin in one pass, each (sign, digit) into its own region
+      // of the gather area (sizes from the histogram); A is no longer needed
+      uint32_t* pm = scratch;                                         // 2*ND bits
+      uint8_t* pslot = reinterpret_cast<uint8_t*>(scratch + 2 * ND / 32);  // (sign,digit) -> region
       for (int k = tid; k < 2 * ND / 32; k += NT) pm[k] = 0;
       __syncthreads();
-      if (tid < (int)np) {
-        const uint32_t d = k3.pend_s[tid] * ND + k3.pend_d[tid];
-        atomicOr(&pm[d >> 5], 1u << (d & 31));
+      if (tid == 0) {
+        uint32_t nreg = 0, off = 0;
+        for (uint32_t p = 0; p < np; ++p) {
+          const uint32_t d = k3.pend_s[p] * ND + k3.pend_d[p];
+          if (!((pm[d >> 5] >> (d & 31)) & 1u)) {
+            pm[d >> 5] |= 1u << (d & 31);
+            pslot[d] = (uint8_t)nreg;
+            k3.reg_off[nreg] = off;
+            k3.reg_cnt[nreg] = 0;
+            off += hist[d];
+            ++nreg;
+          }
+          k3.pend_reg[p] = pslot[d];
+        }
       }
-      if (tid == 0) k3.nB = 0;
       __syncthreads();
-      List Bl = A;
+      uint2* gat = me(a, f);
       list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t x) {
         const uint32_t d = ((b >> 31) ? ND : 0) + ((b & 0x7FFFFFFFu) >> DSH);
         if ((pm[d >> 5] >> (d & 31)) & 1u) {
-          const uint32_t p = atomicAdd(&k3.nB, 1u);
-          Bl.set(p, b, x);
+          const uint32_t g = pslot[d];
+          const uint32_t p = atomicAdd(&k3.reg_cnt[g], 1u);
+          __stcg(gat + k3.reg_off[g] + p, make_uint2(b, x));
         }
       });
       __syncthreads();
-      const uint32_t nB = k3.nB;
       for (uint32_t p = 0; p < np; ++p) {
-        const uint32_t s = k3.pend_s[p], dc = k3.pend_d[p];
+        const uint32_t g = k3.pend_reg[p];
+        const List Bp{nullptr, gat + k3.reg_off[g], 0};
+        const uint32_t dc = k3.pend_d[p];
         const SelRes r = select_exact<NT>(
-            sh, scratch, Bl, nB,
-            [&](uint32_t b, uint32_t) { return (b >> 31) == s && ((b & 0x7FFFFFFFu) >> DSH) == dc; }, key31,
+            sh, scratch, Bp, k3.reg_cnt[g], [](uint32_t, uint32_t) { return true; }, key31,
             [](uint32_t, uint32_t x) -> uint64_t { return x; }, (uint64_t)dc << DSH, (uint64_t)(dc + 1) << DSH,
-            k3.pend_r[p]);
+            k3.pend_r[p], 31);
         if (tid == 0) { st.cut_key[k3.pend_ci[p]] = r.key; st.cut_idx[k3.pend_ci[p]] = (uint32_t)r.sec; }
         __syncthreads();
       }
@@ -1065,7 +1083,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
       const SelRes r = select_exact<NT>(
           sh, scratch, L, ncand,
           [&](uint32_t b, uint32_t x) { return (b >> 31) == s && (b & 0x7FFFFFFFu) != 0 && kept_of(b, x); }, key31,
-          [](uint32_t, uint32_t x) -> uint64_t { return x; }, 1, 1ull << 31, rank0 + 1);
+          [](uint32_t, uint32_t x) -> uint64_t { return x; }, 1, 1ull << 31, rank0 + 1, 31);
       if (tid == 0) { st.cut_key[ci] = r.key; st.cut_idx[ci] = (uint32_t)r.sec; }
       __syncthreads();
     }
@@ -1675,13 +1693,15 @@ __global__ void __launch_bounds__(256) enc_crc(EArgs a) {
   }
   const uint64_t P = st.P;
   const uint64_t b0 = 4, b1 = P - 4;
-  const uint64_t s0 = b0 + (uint64_t)seg * SEG, s1 = min(b1, s0 + SEG);
+  // segment `seg` covers [b1 - (seg+1)*SEG, b1 - seg*SEG) clipped to [b0, b1)
+  const uint64_t e1 = (uint64_t)seg * SEG < b1 - b0 ? b1 - (uint64_t)seg * SEG : b0;
+  const uint64_t e0 = e1 - b0 > (uint64_t)SEG ? e1 - SEG : b0;
   uint32_t part = 0;
-  if (s0 < s1) {
+  if (e0 < e1) {
     for (int k = tid; k < 1024; k += NT) t4[k] = (&kCrcTab4[0][0])[k];
     __syncthreads();
-    const uint32_t raw = crc_cta_staged<NT>(f.out, s0, s1, t4, red, stage);
-    if (tid == 0) part = crc_shift(raw, b1 - s1);
+    const uint32_t raw = crc_cta_staged<NT>(f.out, e0, e1, t4, red, stage);
+    if (tid == 0) part = raw ? crc_mult(kSegShift[seg], raw) : 0u;
   }
   if (tid == 0) {
     if (part) atomicXor(&st.crc_acc, part);

@@ -46,6 +46,40 @@ struct ProfScope {
   }
 };
 
+// Host GF(2) arithmetic for the CRC-32 segment shift table (same as sif_common.cuh).
+uint32_t h_crc_mult(uint32_t a, uint32_t b) {
+  uint32_t p = 0;
+  for (int i = 31; i >= 0; --i) {
+    p ^= b & (0u - ((a >> i) & 1u));
+    b = (b >> 1) ^ (0xEDB88320u & (0u - (b & 1u)));
+  }
+  return p;
+}
+uint32_t h_x8n(uint64_t nbytes) {  // x^(8 n) mod P, reflected
+  uint32_t x2n[64];
+  x2n[0] = 1u << 30;  // x^1
+  for (int k = 1; k < 64; ++k) x2n[k] = h_crc_mult(x2n[k - 1], x2n[k - 1]);
+  uint32_t p = 1u << 31;  // x^0
+  int k = 3;
+  while (nbytes) {
+    if (nbytes & 1ull) p = h_crc_mult(x2n[k & 63], p);
+    nbytes >>= 1;
+    ++k;
+  }
+  return p;
+}
+int crc_tables_init() {
+  static int done = 0;
+  if (done) return SIF_OK;
+  std::vector<uint32_t> t(sif::CRC_SEG_MAX);
+  const uint32_t step = h_x8n(sif::CRC_SEG);
+  t[0] = 1u << 31;
+  for (int j = 1; j < sif::CRC_SEG_MAX; ++j) t[j] = h_crc_mult(step, t[j - 1]);
+  if (cudaMemcpyToSymbol(sif::kSegShift, t.data(), 4ull * sif::CRC_SEG_MAX) != cudaSuccess) return SIF_ERR_CUDA;
+  done = 1;
+  return SIF_OK;
+}
+
 inline int num_sms() {
   static int sms = 0;
   if (!sms) {
@@ -200,6 +234,7 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
     if (ch > 1) ++nhist;
     lists += up(16 * T, 256);
     nseg += crc_segments(d[i].out_cap);
+    if (crc_segments(d[i].out_cap) > (uint64_t)sif::CRC_SEG_MAX) return SIF_ERR_INVALID_ARG;
   }
   if (nch >= (1ull << 31) || nseg >= (1ull << 31)) return SIF_ERR_INVALID_ARG;
   const uint64_t kk = std::max<uint64_t>(1, kmax);
@@ -227,6 +262,7 @@ int sif_enc_plan(const sif_enc_desc* d, int n, const sif_codec_cfg* c, sif_plan*
 
 int sif_enc_upload(const sif_plan* p, const sif_enc_desc* d, const sif_codec_cfg* c, void* ws, void* stream) {
   if (!p || !ws || !c || (p->n > 0 && !d)) return SIF_ERR_INVALID_ARG;
+  if (crc_tables_init()) return SIF_ERR_CUDA;
   cudaStream_t s = (cudaStream_t)stream;
   uint8_t* wb = (uint8_t*)ws;
   const int n = p->n;
@@ -432,6 +468,7 @@ int sif_dec_plan(const sif_dec_desc* d, int n, sif_plan* p) {
     const uint64_t blk = d[i].in_len > 32 ? (d[i].in_len - 32) / 17 + 1 : 1;
     maxrows = std::max(maxrows, blk);
     nseg += dec_segments(d[i].in_len);
+    if (dec_segments(d[i].in_len) > (uint32_t)sif::CRC_SEG_MAX) return SIF_ERR_INVALID_ARG;
   }
   if (nseg >= (1ull << 31)) return SIF_ERR_INVALID_ARG;
   const uint32_t segw = dec_segw(d, n);
@@ -453,6 +490,7 @@ uint64_t sif_dec_table_stride(const sif_plan* p) { return p ? (2ull + (uint64_t)
 
 int sif_dec_upload(const sif_plan* p, const sif_dec_desc* d, void* ws, void* stream) {
   if (!p || !ws) return SIF_ERR_INVALID_ARG;
+  if (crc_tables_init()) return SIF_ERR_CUDA;
   cudaStream_t s = (cudaStream_t)stream;
   uint8_t* wb = (uint8_t*)ws;
   if (p->n == 0) return SIF_OK;
