@@ -245,8 +245,17 @@ def run_ours(args, conf, rank, world, local_rank):
         enc.run()
         dec.run()
 
+    # one CUDA graph per half-step (encode, decode): the 13 library kernels of a step are
+    # issued with two graph launches; events between them split encode and decode time
+    if args.graph:
+        g_enc = sif.capture_graph(enc.run)
+        g_dec = sif.capture_graph(dec.run)
+        run_enc, run_dec = g_enc.replay, g_dec.replay
+    else:
+        run_enc, run_dec = enc.run, dec.run
     for _ in range(args.warmup):
-        step()
+        run_enc()
+        run_dec()
     torch.cuda.synchronize()
     if pg:
         pg.barrier()
@@ -259,9 +268,9 @@ def run_ours(args, conf, rank, world, local_rank):
         t_start.record(stream)
         for i in range(args.steps):
             ev[i][0].record(stream)
-            enc.run()
+            run_enc()
             ev[i][1].record(stream)
-            dec.run()
+            run_dec()
             ev[i][2].record(stream)
         t_end.record(stream)
         torch.cuda.synchronize()
@@ -358,6 +367,7 @@ def run_ours(args, conf, rank, world, local_rank):
             dtype=conf["dtype"], data="synthetic (integer-exact device generator, SURVEY.md §8(d))",
             config=dict(workload=conf["workload"], codec=CODEC, if_shape=[N, K], batch_per_gpu=B,
                         parallelism=f"dp{world} (independent IF streams per GPU, no collectives)",
+                        launch="CUDA graph replay (encode graph + decode graph)" if args.graph else "direct launches",
                         l2="per-step inputs %.0f MB/GPU %s the 126 MB L2; no flush" %
                            (raw_bytes / 1e6, "exceed" if raw_bytes > 126e6 else "fit in")),
             roofline=roof,
@@ -390,6 +400,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="launch the kernels directly instead of replaying CUDA graphs")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank = int(os.environ.get("RANK", 0))

@@ -18,6 +18,7 @@ from .codec import (
     Payload,
     atkf_filter,
     broadcast_q,
+    capture_graph,
     col_bits,
     decode,
     decode_batch,

@@ -507,6 +507,23 @@ def atkf_filter(x, s: float, lam: float, seed: int) -> AtkfResult:
     return AtkfResult(kept[:k], float(t[0]), float(t[1]), float(t[2]), k, k == 0, xt)
 
 
+# ---------------------------------------------------------------------------- graphs
+def capture_graph(fn, warmup: int = 1):
+    """Capture `fn()` -- launches through the C ABI (e.g. `enc.run(); dec.run()`) on the
+    current stream -- into a CUDA graph; `g.replay()` then issues the whole encode/decode
+    pipeline with one launch.  Plans/uploads must be done before capture."""
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(warmup):
+            fn()
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    return g
+
+
 # ---------------------------------------------------------------------------- synthetic
 def synthetic(kind: int, rows: int, cols: int, sid: int, dtype=torch.float32, out: torch.Tensor | None = None):
     """Integer-exact synthetic IF generated on the device."""
