@@ -107,7 +107,16 @@ struct EArgs {
   const uint64_t* kept_off;
   double* tau3;
   const uint32_t* seg_base;  // [n+1] prefix of CRC segments per IF
+  uint64_t* prof;            // optional phase timestamps of enc_select (16 per IF, debug)
 };
+
+__device__ __forceinline__ void prof_mark(const EArgs& a, int ifi, int k) {
+  if (a.prof && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.prof[(uint64_t)ifi * 16 + k] = t;
+  }
+}
 
 // candidate list of an IF: (float bits, flat index) entries
 __device__ __forceinline__ uint2* le(const EArgs& a, const IfInfo& f) {
@@ -149,14 +158,14 @@ struct List {
   }
 };
 
-// Visit every list element (order-free).  Global parts are read 4 entries per thread per
-// step with independent 8-byte loads.
+// Visit every list element (order-free) as f(bits, idx, true).  Global parts are read 4
+// entries per thread per step with independent 8-byte loads.
 template <int NT, class F>
 __device__ __forceinline__ void list_foreach(const List& L, uint32_t n, F f) {
   const uint32_t ns = n < L.cap ? n : L.cap;
   for (uint32_t i = threadIdx.x; i < ns; i += NT) {
     const uint2 e = L.s[i];
-    f(e.x, e.y);
+    f(e.x, e.y, true);
   }
   if (n > L.cap) {
     const uint32_t m = n - L.cap;
@@ -169,7 +178,7 @@ __device__ __forceinline__ void list_foreach(const List& L, uint32_t n, F f) {
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (i0 + threadIdx.x + k * NT < m) f(e[k].x, e[k].y);
+        if (i0 + threadIdx.x + k * NT < m) f(e[k].x, e[k].y, true);
     }
   }
 }
@@ -226,27 +235,57 @@ __device__ void find_digit(SelSh& sh, const uint32_t* H, int nb, uint64_t r) {
 }
 
 // Multi-level radix select ("r-th largest") on keys of `nbits` bits (64 or <= 33) over list
-// elements accepted by fn(bits, idx, &key).  Used for huge single-value tie sets.
+// elements accepted by fn(bits, idx, &key); keys must be distinct (splitmix64 hashes and
+// flat indices are).  As soon as the bin holding rank r has <= GCAP elements they are
+// gathered and ranked directly.  Used for huge single-value tie sets.
+struct GatE;
 template <int NT, class KeyFn>
 __device__ uint64_t radix_select64(SelSh& sh, uint32_t* hist, const List& L, uint32_t n, uint64_t r, KeyFn fn,
-                                   int nbits = 64) {
+                                   int nbits = 64);
+
+template <int NT, class KeyFn>
+__device__ uint64_t radix_select64(SelSh& sh, uint32_t* hist, const List& L, uint32_t n, uint64_t r, KeyFn fn,
+                                   int nbits) {
+  GatE* gl = reinterpret_cast<GatE*>(hist + 2 * HB);
   uint64_t prefix = 0, mask = 0;
   for (int hi = nbits; hi > 0;) {
     const int wdt = hi >= 11 ? 11 : hi;
     const int shf = hi - wdt, nb = 1 << wdt;
     for (int i = threadIdx.x; i < nb; i += NT) hist[i] = 0;
     __syncthreads();
-    list_foreach<NT>(L, n, [&](uint32_t b, uint32_t x) {
-      uint64_t k;
-      if (fn(b, x, k) && (k & mask) == prefix) atomicAdd(&hist[(int)((k >> shf) & (uint64_t)(nb - 1))], 1u);
+    list_foreach<NT>(L, n, [&](uint32_t b, uint32_t x, bool v) {
+      uint64_t k = 0;
+      if (v && fn(b, x, k) && (k & mask) == prefix) atomicAdd(&hist[(int)((k >> shf) & (uint64_t)(nb - 1))], 1u);
     });
     __syncthreads();
     find_digit<NT>(sh, hist, nb, r);
     prefix |= (uint64_t)sh.fd_digit << shf;
     mask |= (uint64_t)(nb - 1) << shf;
     r -= sh.fd_above;
+    const uint64_t cnt = sh.fd_eq;
     __syncthreads();
     hi = shf;
+    if (hi > 0 && cnt <= GCAP) {
+      // small bin: gather its keys and take the r-th largest directly
+      if (threadIdx.x == 0) sh.gcount = 0;
+      __syncthreads();
+      list_foreach<NT>(L, n, [&](uint32_t b, uint32_t x, bool v) {
+        uint64_t k = 0;
+        if (v && fn(b, x, k) && (k & mask) == prefix) gl[atomicAdd(&sh.gcount, 1u)].sec = k;
+      });
+      __syncthreads();
+      const uint32_t m = sh.gcount;
+      for (uint32_t i = threadIdx.x; i < m; i += NT) {
+        const uint64_t ki = gl[i].sec;
+        uint32_t rank = 0;
+        for (uint32_t j = 0; j < m; ++j) rank += gl[j].sec > ki;
+        if (rank == r - 1) sh.sel_sec = ki;
+      }
+      __syncthreads();
+      const uint64_t res = sh.sel_sec;
+      __syncthreads();
+      return res;
+    }
   }
   return prefix;
 }
@@ -279,8 +318,8 @@ __device__ SelRes select_exact(SelSh& sh, uint32_t* scratch, const List& L, uint
     const int nb = (int)(((span - 1) >> shf) + 1);
     for (int i = tid; i < nb; i += NT) hist[i] = 0;
     __syncthreads();
-    list_foreach<NT>(L, n, [&](uint32_t b, uint32_t x) {
-      if (pred(b, x)) {
+    list_foreach<NT>(L, n, [&](uint32_t b, uint32_t x, bool v) {
+      if (v && pred(b, x)) {
         const uint64_t k = keyf(b);
         if (k >= klo && k < khi) atomicAdd(&hist[(int)((k - klo) >> shf)], 1u);
       }
@@ -320,15 +359,15 @@ __device__ SelRes select_exact(SelSh& sh, uint32_t* scratch, const List& L, uint
   }
   if (tid == 0) sh.gcount = 0;
   __syncthreads();
-  list_foreach<NT>(L, n, [&](uint32_t b, uint32_t x) {
-    if (pred(b, x)) {
-      const uint64_t k = keyf(b);
-      if (k >= klo && k < khi) {
-        const uint32_t p = atomicAdd(&sh.gcount, 1u);
-        gl[p].key = (uint32_t)k;
-        gl[p].idx = x;
-        gl[p].sec = secf(b, x);
-      }
+  list_foreach<NT>(L, n, [&](uint32_t b, uint32_t x, bool v) {
+    bool in = v && pred(b, x);
+    const uint64_t k = in ? keyf(b) : 0;
+    in = in && k >= klo && k < khi;
+    if (in) {
+      const uint32_t p = atomicAdd(&sh.gcount, 1u);
+      gl[p].key = (uint32_t)k;
+      gl[p].idx = x;
+      gl[p].sec = secf(b, x);
     }
   });
   __syncthreads();
@@ -764,6 +803,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   const uint32_t floor_lo = a.atkf_only ? 0u : 1u;
   uint32_t ncand = st.ncand;
   bool hist_ok = false;
+  prof_mark(a, ifi, 0);
   if (kk > 0 && st.cnt_lo < kk && lo > floor_lo) {
     // bracket missed (or tau == 0): re-stream keeping every nonzero (every element in
     // ATKF-only mode); this CTA writes the list in chunk order and the histogram in SMEM
@@ -812,19 +852,20 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   if (!hist_ok) {
     for (int k = tid; k < 2 * ND; k += NT) hist[k] = 0;
     __syncthreads();
-    list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t) {
-      atomicAdd(&hist[((b >> 31) ? ND : 0) + ((b & 0x7FFFFFFFu) >> DSH)], 1u);
+    list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t, bool v) {
+      if (v) atomicAdd(&hist[((b >> 31) ? ND : 0) + ((b & 0x7FFFFFFFu) >> DSH)], 1u);
     });
   }
   __syncthreads();
+  prof_mark(a, ifi, 1);
   // candidates with key != 0 (only lo == 0 admits zeros)
   uint64_t cnt_nz = ncand;
   if (lo == 0) {
     cnt_nz = (uint64_t)ncand - hist[0] - hist[ND];  // digit 0 holds zeros and tiny values
     uint32_t tiny = 0;
-    list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t) {
+    list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t, bool v) {
       const uint32_t key = b & 0x7FFFFFFFu;
-      tiny += (key != 0 && (key >> DSH) == 0) ? 1u : 0u;
+      tiny += (v && key != 0 && (key >> DSH) == 0) ? 1u : 0u;
     });
     tiny = __reduce_add_sync(0xFFFFFFFFu, tiny);
     if (tid == 0) k3.cnt_nz = 0;
@@ -863,6 +904,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
       h_star = s.sec;
       tie_all = s.all_ties;
     } else {
+      prof_mark(a, ifi, 2);
       // digit of tau over both signs, then the bin's elements -> exact select
       uint32_t* comb = scratch;
       for (int k = tid; k < ND; k += NT) comb[k] = hist[k] + hist[ND + k];
@@ -872,11 +914,8 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
       const uint64_t rt = kk - sh.fd_above;
       if (tid == 0) k3.nA = 0;
       __syncthreads();
-      list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t x) {
-        if (((b & 0x7FFFFFFFu) >> DSH) == (uint32_t)dtau) {
-          const uint32_t p = atomicAdd(&k3.nA, 1u);
-          A.set(p, b, x);
-        }
+      list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t x, bool v) {
+        if (v && ((b & 0x7FFFFFFFu) >> DSH) == (uint32_t)dtau) A.set(atomicAdd(&k3.nA, 1u), b, x);
       });
       __syncthreads();
       nA = k3.nA;
@@ -888,6 +927,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
       tie_all = s.all_ties;
     }
   }
+  prof_mark(a, ifi, 3);
   const double tau = kk > 0 ? (double)__uint_as_float(tau_key) : (double)__uint_as_float(st.maxkey);
   const double tau_p = __dmul_rn(__dadd_rn(1.0, a.lam), tau);
   const double tau_m = -__dmul_rn(__dsub_rn(1.0, a.lam), tau);
@@ -943,6 +983,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
     }
     return;
   }
+  prof_mark(a, ifi, 4);
   // ---- kept nonzeros per sign
   uint64_t nnz[2] = {0, 0};
   if (fast) {
@@ -950,8 +991,8 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
     __syncthreads();
     if (dtau >= 0) {
       uint32_t c0 = 0, c1 = 0;
-      list_foreach<NT>(A, nA, [&](uint32_t b, uint32_t x) {
-        if (kept_of(b, x)) { if (b >> 31) ++c1; else ++c0; }
+      list_foreach<NT>(A, nA, [&](uint32_t b, uint32_t x, bool v) {
+        if (v && kept_of(b, x)) { if (b >> 31) ++c1; else ++c0; }
       });
       c0 = __reduce_add_sync(0xFFFFFFFFu, c0);
       c1 = __reduce_add_sync(0xFFFFFFFFu, c1);
@@ -981,8 +1022,8 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
     if (keep_none) { nnz[0] = 0; nnz[1] = 0; }
   } else {
     uint32_t c0 = 0, c1 = 0;
-    list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t x) {
-      if ((b & 0x7FFFFFFFu) != 0 && kept_of(b, x)) { if (b >> 31) ++c1; else ++c0; }
+    list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t x, bool v) {
+      if (v && (b & 0x7FFFFFFFu) != 0 && kept_of(b, x)) { if (b >> 31) ++c1; else ++c0; }
     });
     c0 = __reduce_add_sync(0xFFFFFFFFu, c0);
     c1 = __reduce_add_sync(0xFFFFFFFFu, c1);
@@ -994,6 +1035,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
     nnz[1] = k3.s.cnt[1];
     __syncthreads();
   }
+  prof_mark(a, ifi, 5);
   // ---- MS cuts (msplit.py:68-80): element at rank j*base of each sign plane
   const int mcfg[2] = {a.m_plus, a.m_minus};
   uint64_t meff[2], base[2];
@@ -1029,6 +1071,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
       }
       __syncthreads();
     }
+    prof_mark(a, ifi, 6);
     const uint32_t np = k3.pend_n;
     if (np > 0) {
       // gather every pending cut bin in one pass, each (sign, digit) into its own region
@@ -1054,16 +1097,16 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
       }
       __syncthreads();
       uint2* gat = me(a, f);
-      list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t x) {
+      list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t x, bool v) {
         const uint32_t d = ((b >> 31) ? ND : 0) + ((b & 0x7FFFFFFFu) >> DSH);
-        if ((pm[d >> 5] >> (d & 31)) & 1u) {
+        if (v && ((pm[d >> 5] >> (d & 31)) & 1u)) {
           const uint32_t g = pslot[d];
-          const uint32_t p = atomicAdd(&k3.reg_cnt[g], 1u);
-          __stcg(gat + k3.reg_off[g] + p, make_uint2(b, x));
+          __stcg(gat + k3.reg_off[g] + atomicAdd(&k3.reg_cnt[g], 1u), make_uint2(b, x));
         }
       });
       __syncthreads();
       for (uint32_t p = 0; p < np; ++p) {
+        if (p == 0) prof_mark(a, ifi, 7);
         const uint32_t g = k3.pend_reg[p];
         const List Bp{nullptr, gat + k3.reg_off[g], 0};
         const uint32_t dc = k3.pend_d[p];
@@ -1088,6 +1131,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
       __syncthreads();
     }
   }
+  prof_mark(a, ifi, 8);
   if (tid == 0) {
     uint32_t fl = 0;
     if (keep_none) fl |= F_KEEP_NONE;
@@ -1209,13 +1253,13 @@ __global__ void __launch_bounds__(CNT) enc_members(EArgs a) {
     }
     // zero this chunk's share of the output (K6/K7 write into a zeroed payload)
     {
+      // chunk k of the IF zeroes the 512-byte stripes k, k + nch, k + 2*nch, ... of the output
       const uint32_t k = c - f.ch0;
-      const uint64_t n16 = f.cap / 16;
-      const uint64_t z0 = n16 * k / f.nch, z1 = n16 * (k + 1) / f.nch;
+      const uint32_t n16 = (uint32_t)(f.cap / 16);
       uint4* o4 = reinterpret_cast<uint4*>(f.out);
-      for (uint64_t z = z0 + lane; z < z1; z += 32) o4[z] = make_uint4(0, 0, 0, 0);
+      for (uint32_t z = k * 32u + lane; z < n16; z += 32u * f.nch) o4[z] = make_uint4(0, 0, 0, 0);
       if (k + 1 == f.nch)
-        for (uint64_t z = n16 * 16 + lane; z < f.cap; z += 32) f.out[z] = 0;
+        for (uint64_t z = (uint64_t)n16 * 16 + lane; z < f.cap; z += 32) f.out[z] = 0;
     }
     if (lane < B) { ws.cnt[lane] = 0; ws.mn[lane] = 0x7FFFFFFFu; ws.mx[lane] = 0; ws.xl[lane] = 0; }
     __syncwarp();
@@ -1224,23 +1268,32 @@ __global__ void __launch_bounds__(CNT) enc_members(EArgs a) {
     uint32_t i = 0;
     for (int u = 0; u < UNITS; ++u) {
       const uint32_t uo = a.u_off[(uint64_t)c * UNITS + u], un = a.u_cnt[(uint64_t)c * UNITS + u];
-      for (uint32_t j0 = 0; j0 < un; j0 += 32) {
-        const uint32_t j = j0 + lane;
-        int blk = -1;
-        uint2 e = make_uint2(0, 0);
-        if (j < un) {
-          e = __ldg(gl + uo + j);
-          if (kc.kept(e.x, e.y)) blk = kc.block_of(e.x, e.y);
-          bk[i + j] = (int8_t)blk;
+      for (uint32_t j0 = 0; j0 < un; j0 += 64) {
+        // two windows in flight: both loads issued before either is used
+        uint2 ev[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t j = j0 + 32 * h + lane;
+          ev[h] = j < un ? __ldg(gl + uo + j) : make_uint2(0, 0);
         }
-        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, blk);
-        if (blk >= 0) {
-          const uint32_t key = e.x & 0x7FFFFFFFu;
-          atomicMin(&ws.mn[blk], key);
-          atomicMax(&ws.mx[blk], key);
-          if (lane == 31 - __clz(peers)) { ws.cnt[blk] += __popc(peers); ws.xl[blk] = max(ws.xl[blk], e.y + 1u); }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t j = j0 + 32 * h + lane;
+          const uint2 e = ev[h];
+          int blk = -1;
+          if (j < un) {
+            if (kc.kept(e.x, e.y)) blk = kc.block_of(e.x, e.y);
+            bk[i + j] = (int8_t)blk;
+          }
+          const uint32_t peers = __match_any_sync(0xFFFFFFFFu, blk);
+          if (blk >= 0) {
+            const uint32_t key = e.x & 0x7FFFFFFFu;
+            atomicMin(&ws.mn[blk], key);
+            atomicMax(&ws.mx[blk], key);
+            if (lane == 31 - __clz(peers)) { ws.cnt[blk] += __popc(peers); ws.xl[blk] = max(ws.xl[blk], e.y + 1u); }
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
       i += un;
     }
@@ -1265,17 +1318,27 @@ __global__ void __launch_bounds__(CNT) enc_members(EArgs a) {
     i = 0;
     for (int u = 0; u < UNITS; ++u) {
       const uint32_t uo = a.u_off[(uint64_t)c * UNITS + u], un = a.u_cnt[(uint64_t)c * UNITS + u];
-      for (uint32_t j0 = 0; j0 < un; j0 += 32) {
-        const uint32_t j = j0 + lane;
-        const int blk = j < un ? (int)bk[i + j] : -1;
-        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, blk);
-        if (blk >= 0) {
-          const uint32_t dst = ws.pos[blk] + __popc(peers & lt);
-          __stcg(om + dst, __ldg(gl + uo + j));
+      for (uint32_t j0 = 0; j0 < un; j0 += 64) {
+        uint2 ev[2];
+        int bv[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t j = j0 + 32 * h + lane;
+          bv[h] = j < un ? (int)bk[i + j] : -1;
+          ev[h] = bv[h] >= 0 ? __ldg(gl + uo + j) : make_uint2(0, 0);
         }
-        __syncwarp();
-        if (blk >= 0 && lane == 31 - __clz(peers)) ws.pos[blk] += __popc(peers);
-        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int blk = bv[h];
+          const uint32_t peers = __match_any_sync(0xFFFFFFFFu, blk);
+          if (blk >= 0) {
+            const uint32_t dst = ws.pos[blk] + __popc(peers & lt);
+            __stcg(om + dst, ev[h]);
+          }
+          __syncwarp();
+          if (blk >= 0 && lane == 31 - __clz(peers)) ws.pos[blk] += __popc(peers);
+          __syncwarp();
+        }
       }
       i += un;
     }
@@ -1364,11 +1427,21 @@ __global__ void __launch_bounds__(CNT) enc_abq(EArgs a) {
         const int q = qb - 1;
         const double oq = par[b].o[q], iq = par[b].inv[q];
         uint32_t acc = 0;
-        for (uint32_t i = lane; i < nb; i += 32) {
-          const uint32_t key = __ldg(&gm[rs + i].x) & 0x7FFFFFFFu;
-          const uint32_t r = quant_code(key, vmin, oref, iref, lref) >> 1;
-          const uint32_t cq = quant_code(key, vmin, oq, iq, (1u << q) - 1u);
-          acc += r > cq ? r - cq : cq - r;
+        for (uint32_t i0 = 0; i0 < nb; i0 += 64) {
+          uint32_t kv[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t i = i0 + 32 * h + lane;
+            kv[h] = i < nb ? __ldg(&gm[rs + i].x) & 0x7FFFFFFFu : 0xFFFFFFFFu;
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (kv[h] != 0xFFFFFFFFu) {
+              const uint32_t r = quant_code(kv[h], vmin, oref, iref, lref) >> 1;
+              const uint32_t cq = quant_code(kv[h], vmin, oq, iq, (1u << q) - 1u);
+              acc += r > cq ? r - cq : cq - r;
+            }
+          }
         }
         const uint32_t v = __reduce_add_sync(0xFFFFFFFFu, acc);
         if (lane == 0) acc_s[b * 16 + q] += v;
@@ -1638,11 +1711,13 @@ __global__ void __launch_bounds__(CNT) enc_pack(EArgs a) {
       const uint32_t Rc = (uint32_t)p.bc + p0 * cb, Rq = (uint32_t)p.bq + p0 * p.q;
       const uint32_t Ec = Rc + n * cb, Eq = Rq + n * p.q;
       Carry cyc{0xFFFFFFFFu, 0u}, cyq{0xFFFFFFFFu, 0u};
+      uint2 enext = lane < n ? __ldg(gm + rs + lane) : make_uint2(0, 0);
       for (uint32_t j0 = 0; j0 < n; j0 += 32) {
         const uint32_t j = j0 + lane;
         const uint32_t nv = min(32u, n - j0);
         const bool valid = j < n;
-        const uint2 e = valid ? __ldg(gm + rs + j) : make_uint2(0, 0);
+        const uint2 e = enext;  // prefetched; the next window's entry is requested now
+        if (j0 + 32 < n) enext = j + 32 < n ? __ldg(gm + rs + j + 32) : make_uint2(0, 0);
         const uint32_t key = e.x & 0x7FFFFFFFu;
         const uint32_t x = e.y;
         const uint32_t code = (valid && !p.degen) ? quant_code(key, p.vmin, p.o64, p.inv, lv_) : 0u;

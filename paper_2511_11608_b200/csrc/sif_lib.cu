@@ -349,6 +349,7 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   a.kept_out = kept;
   a.kept_off = reinterpret_cast<const uint64_t*>(wb + w.keptoff);
   a.tau3 = tau3;
+  a.prof = reinterpret_cast<uint64_t*>(getenv("SIF_PROF_PTR") ? strtoull(getenv("SIF_PROF_PTR"), nullptr, 0) : 0ull);
   static bool attrs = false;
   if (!attrs) {
     if (check_cuda(cudaFuncSetAttribute(sif::enc_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemStream)) ||
