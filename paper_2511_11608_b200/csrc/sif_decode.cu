@@ -133,22 +133,50 @@ __global__ void __launch_bounds__(DNT) sif_dcrc_kernel(DecArgs a) {
   }
 }
 
+// Float64 value of the plus-plane entry at (row, col), 0 if none (slow path for elements
+// present in both planes).  Plus blocks are 0 .. mp-1; cols are ascending within a row.
+__device__ __noinline__ double plus_value(const uint32_t* tab, const uint8_t* in, uint32_t mp, uint32_t r,
+                                          uint32_t col, uint32_t cb) {
+  double v = 0.0;
+  for (uint32_t b = 0; b < mp; ++b) {
+    const uint32_t* row = tab + (2ull + b) * TROW_U32;
+    const uint32_t q = row[0], nnz = row[1];
+    const uint64_t rpo = (uint64_t)row[4] | ((uint64_t)row[5] << 32);
+    const uint64_t cbit = 8ull * ((uint64_t)row[6] | ((uint64_t)row[7] << 32));
+    const uint64_t qbit = 8ull * ((uint64_t)row[8] | ((uint64_t)row[9] << 32));
+    uint32_t lo = min(ld_u32_le(in, rpo + 4ull * r), nnz), hi = min(ld_u32_le(in, rpo + 4ull * (r + 1)), nnz);
+    while (lo < hi) {
+      const uint32_t m = (lo + hi) >> 1;
+      const uint32_t cm = ld_field(in, cbit + (uint64_t)m * cb, cb);
+      if (cm == col) {
+        const uint32_t code = ld_field(in, qbit + (uint64_t)m * q, q);
+        v = __dadd_rn(v, __dadd_rn(__dmul_rn((double)code, (double)__uint_as_float(row[2])),
+                                   (double)__uint_as_float(row[3])));
+        break;
+      }
+      if (cm < col) lo = m + 1; else hi = m;
+    }
+  }
+  return v;
+}
+
 // ------------------------------------------------------------------------------- scatter
 // Work item = (stream, row group, column segment): R = max(1, segw / K) consecutive rows of
 // at most segw columns; a warp owns a contiguous range of items.  Lanes hold one (block,
 // row) pair each (pairs block-major, in groups of 32 that never span both planes): block
 // metadata and the row's entry range.  The pairs' entries are unpacked 32 at a time
 // (cols, codes), validated (codec.py:238-250), dequantized in float64 (quant.py:67-73)
-// into a per-warp float64 buffer (plus plane stored, minus plane subtracted: positions are
-// unique within a valid plane, so this is the reference's f64 scatter-add,
-// codec.py:257-266), then rounded to fp32 and stored with 16-byte stores.
+// into a per-warp fp32 buffer: an element held by one plane is f32(0 +/- v), exactly the
+// reference's f64 scatter-add rounded to fp32 (codec.py:257-266); an element held by both
+// planes is summed in float64 (plus value recovered from its block).  Stored with 16-byte
+// stores.
 __global__ void __launch_bounds__(DNT) sif_scatter_kernel(DecArgs a) {
   extern __shared__ __align__(16) uint8_t dsm_raw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t segw = (uint32_t)a.segw;
   const uint32_t bmw = (segw + 31) / 32;
-  double* buf = reinterpret_cast<double*>(dsm_raw) + (size_t)w * segw;
-  uint32_t* bm = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(dsm_raw) + (size_t)(DNT / 32) * segw) +
+  float* buf = reinterpret_cast<float*>(dsm_raw) + (size_t)w * segw;
+  uint32_t* bm = reinterpret_cast<uint32_t*>(reinterpret_cast<float*>(dsm_raw) + (size_t)(DNT / 32) * segw) +
                  (size_t)w * 2 * bmw;
   const uint64_t GW = (uint64_t)gridDim.x * (DNT / 32);
   const uint64_t gw = (uint64_t)blockIdx.x * (DNT / 32) + w;
@@ -191,7 +219,7 @@ __global__ void __launch_bounds__(DNT) sif_scatter_kernel(DecArgs a) {
     const uint32_t r0 = rg * R, nr = min(R, N - r0);
     const uint32_t c0 = sg * segw, c1 = min(K, c0 + segw), W = c1 - c0;
     const uint32_t span = nr * W;  // buffer elements (rows are contiguous when nsegr == 1)
-    for (uint32_t k = 2 * lane; k < span; k += 64) *reinterpret_cast<double2*>(buf + k) = make_double2(0.0, 0.0);
+    for (uint32_t k = 4 * lane; k < span; k += 128) *reinterpret_cast<float4*>(buf + k) = make_float4(0.f, 0.f, 0.f, 0.f);
     for (uint32_t k = lane; k < 2 * bmw; k += 32) bm[k] = 0;
     __syncwarp();
     const uint32_t np = nb * nr;       // (block, row) pairs, block-major
@@ -268,20 +296,34 @@ __global__ void __launch_bounds__(DNT) sif_scatter_kernel(DecArgs a) {
         const double oj = __shfl_sync(0xFFFFFFFFu, o, (int)jl), vj = __shfl_sync(0xFFFFFFFFu, vmin, (int)jl);
         const uint32_t rsj = __shfl_sync(0xFFFFFFFFu, rs0, (int)jl);
         const uint32_t rij = __shfl_sync(0xFFFFFFFFu, ri, (int)jl);
+        const uint32_t col = m < M ? ld_field(in, cbj + (uint64_t)e * cb, cb) : 0u;
+        // the previous entry e-1 of the same pair sits in the previous lane of this window
+        const uint32_t colp = __shfl_up_sync(0xFFFFFFFFu, col, 1);
+        const uint32_t jlp = __shfl_up_sync(0xFFFFFFFFu, jl, 1);
         if (m < M) {
-          const uint32_t col = ld_field(in, cbj + (uint64_t)e * cb, cb);
           if (col >= K) fl |= FLAG_CORRUPT;  // codec.py:242-243
           else {
             // strictly increasing within the row (codec.py:244-247)
-            if (e > rsj && ld_field(in, cbj + (uint64_t)(e - 1) * cb, cb) >= col) fl |= FLAG_CORRUPT;
+            if (e > rsj) {
+              const uint32_t prev = (lane > 0 && jlp == jl) ? colp : ld_field(in, cbj + (uint64_t)(e - 1) * cb, cb);
+              if (prev >= col) fl |= FLAG_CORRUPT;
+            }
             if (col >= c0 && col < c1) {
               const uint32_t pos = rij * W + (col - c0);
               const uint32_t old = atomicOr(bm + plane * bmw + (pos >> 5), 1u << (pos & 31));
               if (old & (1u << (pos & 31))) fl |= FLAG_CORRUPT;  // codec.py:248-250 (overlap)
               const uint32_t code = ld_field(in, qbj + (uint64_t)e * qj, qj);
               const double v = __dadd_rn(__dmul_rn((double)code, oj), vj);
-              if (plane == 0) buf[pos] = v;
-              else buf[pos] = __dsub_rn(buf[pos], v);
+              if (plane == 0) {
+                buf[pos] = __double2float_rn(v);  // f32(0 + v)
+              } else if ((bm[pos >> 5] >> (pos & 31)) & 1u) {
+                // both planes hold this element: the reference sums them in float64
+                // (codec.py:257-266); recover the plus value from its plus block entry
+                const double pv = plus_value(tab, in, mp, r0 + rij, col, cb);
+                buf[pos] = __double2float_rn(__dsub_rn(pv, v));
+              } else {
+                buf[pos] = __double2float_rn(-v);  // f32(0 - v)
+              }
             }
           }
         }
@@ -294,16 +336,14 @@ __global__ void __launch_bounds__(DNT) sif_scatter_kernel(DecArgs a) {
     uint32_t bad = 0;
     if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && (span & 3u) == 0) {
       for (uint32_t k = 4 * lane; k < span; k += 128) {
-        const double2 x0 = *reinterpret_cast<const double2*>(buf + k), x1 = *reinterpret_cast<const double2*>(buf + k + 2);
-        const float4 f = make_float4(__double2float_rn(x0.x), __double2float_rn(x0.y), __double2float_rn(x1.x),
-                                     __double2float_rn(x1.y));
+        const float4 f = *reinterpret_cast<const float4*>(buf + k);
         bad |= ((__float_as_uint(f.x) & 0x7F800000u) == 0x7F800000u) | ((__float_as_uint(f.y) & 0x7F800000u) == 0x7F800000u) |
                ((__float_as_uint(f.z) & 0x7F800000u) == 0x7F800000u) | ((__float_as_uint(f.w) & 0x7F800000u) == 0x7F800000u);
         __stcs(reinterpret_cast<float4*>(dst + k), f);
       }
     } else {
       for (uint32_t k = lane; k < span; k += 32) {
-        const float f = __double2float_rn(buf[k]);
+        const float f = buf[k];
         bad |= (__float_as_uint(f) & 0x7F800000u) == 0x7F800000u;
         __stcs(dst + k, f);
       }

@@ -478,7 +478,7 @@ int sif_dec_plan(const sif_dec_desc* d, int n, sif_plan* p) {
   p->tiles = (int32_t)segw;    // decode plans: columns per work item
   p->cluster = (int32_t)nseg;  // decode plans: CRC segment CTAs
   p->max_blocks = (int32_t)std::min<uint64_t>(maxrows, 1u << 30);
-  p->smem_bytes = (sif::DNT / 32) * (int)(segw * 8 + 2 * ((segw + 31) / 32) * 4);
+  p->smem_bytes = (sif::DNT / 32) * (int)(segw * 4 + 2 * ((segw + 31) / 32) * 4);
   const DecWs w = dec_ws(std::max(n, 1), maxrows);
   p->ws_desc_off = w.desc;
   p->ws_aux_off = w.table;

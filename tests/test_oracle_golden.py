@@ -65,3 +65,24 @@ def test_pack_unpack_roundtrip():
     for w in range(1, 33):
         v = rng.integers(0, 2 ** w, size=37, dtype=np.uint64).astype(np.uint32)
         assert np.array_equal(O.unpack_bits(O.pack_bits(v, w), 37, w), v)
+
+
+def _structural():
+    import os
+    d = np.load(os.path.join(os.path.dirname(__file__), "golden", "structural.npz"))
+    return d, [str(n) for n in d["names"]]
+
+
+def test_oracle_structural_streams():
+    """Hand-built streams (cross-plane overlap, corrupt CSR) decoded by the reference."""
+    d, names = _structural()
+    for n in names:
+        data = d[f"{n}_blob"].tobytes()
+        err = d[f"{n}_err"].tobytes().decode()
+        _, kind = O.status_of(O.decode_bytes, data)
+        if err:
+            assert kind == err, n
+        else:
+            assert kind is None, (n, kind)
+            y = O.decode_bytes(data)
+            assert np.array_equal(y.reshape(-1).view(np.uint32), d[f"{n}_dec"].reshape(-1).view(np.uint32)), n
