@@ -15,6 +15,7 @@ from .codec import (
     BatchEncoder,
     ListEncoder,
     CodecConfig,
+    HostRoundTrip,
     Payload,
     atkf_filter,
     broadcast_q,

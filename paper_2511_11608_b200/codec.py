@@ -507,6 +507,100 @@ def atkf_filter(x, s: float, lam: float, seed: int) -> AtkfResult:
     return AtkfResult(kept[:k], float(t[0]), float(t[1]), float(t[2]), k, k == 0, xt)
 
 
+# ---------------------------------------------------------------------------- host round trip
+class HostRoundTrip:
+    """encode -> .sif -> decode of a batch that lives in pinned HOST memory, pipelined over
+    sub-batches: the host->device copy of sub-batch i+1 and the device->host copy of the
+    decoded sub-batch i-1 run on their own streams while sub-batch i is encoded and
+    decoded, so PCIe traffic in both directions overlaps the kernels.  The .sif payloads
+    stay in device memory between encode and decode (`payloads(i)` exposes them).
+
+    x_host: pinned (B, rows, cols) fp32/bf16 tensor; y_host: pinned (B, rows, cols) fp32."""
+
+    def __init__(self, x_host: torch.Tensor, cfg: CodecConfig, seeds, y_host: torch.Tensor | None = None,
+                 parts: int = 8):
+        if x_host.dim() != 3:
+            raise ShapeError("batch must be (B, rows, cols)")
+        self.x_host = x_host
+        self.B, self.rows, self.cols = x_host.shape
+        self.y_host = y_host if y_host is not None else torch.empty((self.B, self.rows, self.cols),
+                                                                   dtype=torch.float32).pin_memory()
+        seeds = list(seeds)
+        parts = max(1, min(parts, self.B))
+        bounds = [self.B * i // parts for i in range(parts + 1)]
+        self.parts = []
+        dev = torch.device("cuda")
+        for i in range(parts):
+            b0, b1 = bounds[i], bounds[i + 1]
+            xs = torch.empty((b1 - b0, self.rows, self.cols), dtype=x_host.dtype, device=dev)
+            enc = BatchEncoder(xs, cfg, seeds[b0:b1])
+            ys = torch.empty((b1 - b0, self.rows, self.cols), dtype=torch.float32, device=dev)
+            self.parts.append(dict(b0=b0, b1=b1, xs=xs, enc=enc, ys=ys, dec=None))
+        self.s_in, self.s_run, self.s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        self._lens_known = False
+
+    def _decoders(self):
+        # payload lengths are data dependent: plan the decoders once, after a first encode
+        for p in self.parts:
+            lens = p["enc"].out_len.cpu().numpy()
+            cap = p["enc"].cap
+            p["dec"] = BatchDecoder([p["enc"].out.data_ptr() + i * cap for i in range(len(lens))], lens, self.rows,
+                                    self.cols, out=p["ys"])
+        self._lens_known = True
+
+    def run(self):
+        """One pipelined pass over the whole batch (stream-ordered; synchronize to read)."""
+        if not self._lens_known:
+            for p in self.parts:
+                p["xs"].copy_(self.x_host[p["b0"]:p["b1"]])
+                p["enc"].run()
+            torch.cuda.synchronize()
+            self._decoders()
+        cur = torch.cuda.current_stream()
+        for st in (self.s_in, self.s_run, self.s_out):
+            st.wait_stream(cur)
+        ev_in, ev_run = [], []
+        for p in self.parts:  # all uploads, in order, on the input copy stream
+            with torch.cuda.stream(self.s_in):
+                p["xs"].copy_(self.x_host[p["b0"]:p["b1"]], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(self.s_in)
+                ev_in.append(e)
+        for p, e in zip(self.parts, ev_in):
+            with torch.cuda.stream(self.s_run):
+                self.s_run.wait_event(e)
+                p["enc"].run()
+                p["dec"].run()
+                e2 = torch.cuda.Event()
+                e2.record(self.s_run)
+                ev_run.append(e2)
+        for p, e in zip(self.parts, ev_run):
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(e)
+                self.y_host[p["b0"]:p["b1"]].copy_(p["ys"], non_blocking=True)
+        for st in (self.s_in, self.s_run, self.s_out):
+            cur.wait_stream(st)
+        return self
+
+    def check(self):
+        for p in self.parts:
+            p["enc"].check()
+            p["dec"].check()
+        return self
+
+    def payloads(self, i: int) -> list:
+        """The .sif payloads of sub-batch i (device memory), after run()."""
+        return self.parts[i]["enc"].payloads()
+
+    @property
+    def h2d_bytes(self) -> int:
+        return int(self.x_host.numel() * self.x_host.element_size())
+
+    @property
+    def d2h_bytes(self) -> int:
+        return int(self.y_host.numel() * 4)
+
+
 # ---------------------------------------------------------------------------- graphs
 def capture_graph(fn, warmup: int = 1):
     """Capture `fn()` -- launches through the C ABI (e.g. `enc.run(); dec.run()`) on the

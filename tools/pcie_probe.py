@@ -1,0 +1,16 @@
+import torch, time
+n = 200 * 1024 * 1024
+h1 = torch.empty(n, dtype=torch.uint8).pin_memory(); h2 = torch.empty(n, dtype=torch.uint8).pin_memory()
+d1 = torch.empty(n, dtype=torch.uint8, device='cuda'); d2 = torch.empty(n, dtype=torch.uint8, device='cuda')
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+def t(fn, k=5):
+    fn(); torch.cuda.synchronize(); t0=time.perf_counter()
+    for _ in range(k): fn()
+    torch.cuda.synchronize(); return (time.perf_counter()-t0)/k
+h2d = t(lambda: d1.copy_(h1, non_blocking=True)); d2h = t(lambda: h2.copy_(d2, non_blocking=True))
+def both():
+    with torch.cuda.stream(s1): d1.copy_(h1, non_blocking=True)
+    with torch.cuda.stream(s2): h2.copy_(d2, non_blocking=True)
+    torch.cuda.current_stream().wait_stream(s1); torch.cuda.current_stream().wait_stream(s2)
+bt = t(both)
+print(f"H2D {n/h2d/1e9:.1f} GB/s, D2H {n/d2h/1e9:.1f} GB/s, both concurrently: {2*n/bt/1e9:.1f} GB/s total ({bt*1e3:.2f} ms vs serial {(h2d+d2h)*1e3:.2f})")
