@@ -84,12 +84,50 @@ __device__ __forceinline__ uint32_t crc_x8n(uint64_t nbytes) {
 __device__ __forceinline__ uint32_t crc_shift(uint32_t c, uint64_t nbytes) {
   return c ? crc_mult(crc_x8n(nbytes), c) : 0u;
 }
-// kSegShift[j] = x^(8 * CRC_SEG * j) mod P: shifts a segment's raw CRC over j whole
-// segments (segments are aligned to the end of the CRC range).  Filled by the host
+// kPieceShift[j] = x^(8 * CRC_PIECE * j) mod P: shifts a piece's raw CRC over j whole
+// pieces (pieces are aligned to the end of the CRC range).  Filled by the host
 // (sif_lib.cu, crc_tables_init) before the first CRC launch.
-constexpr uint64_t CRC_SEG = 16384;
-constexpr int CRC_SEG_MAX = 8192;  // payloads up to 128 MiB per CTA-segment table
-__device__ uint32_t kSegShift[CRC_SEG_MAX];
+constexpr uint64_t CRC_PIECE = 2048;      // bytes per warp-level CRC piece (64 per lane)
+constexpr int CRC_PIECES_MAX = 65536;     // payloads up to 128 MiB
+__device__ uint32_t kPieceShift[CRC_PIECES_MAX];
+
+// Raw CRC-32 of bytes [e0, e1) (0 < e1 - e0 <= CRC_PIECE) of a 4-byte aligned buffer,
+// shifted to e1, computed by one warp (all lanes call; result in every lane).  Lane l
+// owns the 64 bytes ending 64*(31-l) bytes before e1; bytes before e0 are taken as zero
+// (leading zeros do not change a raw CRC).  stage: >= 544 words of this warp's shared
+// memory; t4: kCrcTab4 in shared memory.
+__device__ __forceinline__ uint32_t crc_piece_warp(const uint8_t* base, uint64_t e0, uint64_t e1, const uint32_t* t4,
+                                                   uint32_t* stage) {
+  const int lane = threadIdx.x & 31;
+  const int64_t rs = (int64_t)e1 - (int64_t)CRC_PIECE;  // byte address of the piece start
+  const int64_t fl = rs >= 0 ? rs / 4 : -((-rs + 3) / 4);
+  const uint32_t sh8 = (uint32_t)(rs - 4 * fl) * 8u;
+  const uint32_t* gw = reinterpret_cast<const uint32_t*>(base);
+  const int64_t w_lo = (int64_t)(e0 / 4), w_hi = (int64_t)((e1 + 3) / 4);  // words holding [e0, e1)
+#pragma unroll
+  for (int k = 0; k < 17; ++k) {
+    const int j = lane + 32 * k;
+    const int64_t wi = fl + j;
+    stage[j] = (wi >= w_lo && wi < w_hi) ? __ldcg(gw + wi) : 0u;
+  }
+  __syncwarp();
+  uint32_t c = 0;
+#pragma unroll 4
+  for (int k = 0; k < 16; ++k) {
+    const int j = 16 * lane + k;
+    uint32_t v = sh8 ? __funnelshift_r(stage[j], stage[j + 1], sh8) : stage[j];
+    const int64_t a = rs + 4 * (int64_t)j;
+    if (a + 4 <= (int64_t)e0) v = 0;
+    else if (a < (int64_t)e0) v &= 0xFFFFFFFFu << (8u * (uint32_t)((int64_t)e0 - a));
+    const uint32_t x = v ^ c;
+    c = t4[768 + (x & 0xFFu)] ^ t4[512 + ((x >> 8) & 0xFFu)] ^ t4[256 + ((x >> 16) & 0xFFu)] ^ t4[x >> 24];
+  }
+  __syncwarp();
+  if (c) c = crc_mult(kCrcShift64[31 - lane], c);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c ^= __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  return c;
+}
 
 __device__ __forceinline__ uint32_t crc_finish(uint32_t raw_total, uint64_t len) {
   return raw_total ^ crc_mult(crc_x8n(len), 0xFFFFFFFFu) ^ 0xFFFFFFFFu;

@@ -34,7 +34,7 @@ struct DecArgs {
   int segw;                    // columns per work item (<= 1024, multiple of 4)
 };
 
-constexpr uint64_t SEGD = CRC_SEG;  // CRC segment bytes per CTA
+constexpr uint64_t SEGD = CRC_PIECE;  // CRC bytes per warp piece
 
 // ------------------------------------------------------------------------------- parse
 __device__ __forceinline__ uint32_t rd_u32(const uint8_t* p, uint64_t o) {
@@ -100,36 +100,34 @@ __global__ void sif_parse_kernel(DecArgs a) {
 }
 
 // ------------------------------------------------------------------------------- CRC
-// One CTA per CRC-32 segment of a stream: raw CRC of [s0, s1) shifted to the end of the
-// range [4, len-4) and XOR-combined into the stream's accumulator (GF(2) linearity).
+// One warp per 2 KiB CRC-32 piece of a stream (pieces aligned to the end of [4, len-4)):
+// raw piece CRC shifted over the pieces after it (kPieceShift) and XOR-combined into the
+// stream's accumulator (GF(2) linearity).
 __global__ void __launch_bounds__(DNT) sif_dcrc_kernel(DecArgs a) {
   __shared__ uint32_t t4[1024];
-  __shared__ uint32_t stage[16 * DNT];
-  __shared__ uint32_t red[DNT / 32 + 2];
-  const int tid = threadIdx.x;
-  const uint32_t gs = blockIdx.x;
-  int lo = 0, hi = a.n - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (a.seg_base[mid] <= gs) lo = mid; else hi = mid - 1;
-  }
-  const int ifi = lo;
-  const uint32_t seg = gs - a.seg_base[lo];
-  const uint32_t* tab = a.table + (uint64_t)ifi * a.table_stride;
-  if (tab[TROW_U32 + 0]) return;  // length / magic failure: no CRC
-  const sif_dec_desc d = a.descs[ifi];
-  const uint64_t len = d.in_len;
-  const uint64_t b0 = 4, b1 = len - 4;
-  // segment `seg` covers [b1 - (seg+1)*SEGD, b1 - seg*SEGD) clipped to [b0, b1)
-  const uint64_t e1 = seg * SEGD < b1 - b0 ? b1 - seg * SEGD : b0;
-  const uint64_t e0 = e1 - b0 > SEGD ? e1 - SEGD : b0;
-  if (e0 >= e1) return;
-  for (int k = tid; k < 1024; k += DNT) t4[k] = (&kCrcTab4[0][0])[k];
+  __shared__ uint32_t stage[DNT / 32][544];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < 1024; k += DNT) t4[k] = (&kCrcTab4[0][0])[k];
   __syncthreads();
-  const uint32_t raw = crc_cta_staged<DNT>(d.in, e0, e1, t4, red, stage);
-  if (tid == 0) {
-    const uint32_t part = raw ? crc_mult(kSegShift[seg], raw) : 0u;
-    if (part) atomicXor(a.acc + 4ull * ifi + 0, part);
+  const uint64_t GW = (uint64_t)gridDim.x * (DNT / 32);
+  const uint64_t total = a.seg_base[a.n];
+  for (uint64_t gp = (uint64_t)blockIdx.x * (DNT / 32) + w; gp < total; gp += GW) {
+    int lo = 0, hi = a.n - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.seg_base[mid] <= gp) lo = mid; else hi = mid - 1;
+    }
+    const int ifi = lo;
+    const uint32_t piece = (uint32_t)(gp - a.seg_base[lo]);
+    const uint32_t* tab = a.table + (uint64_t)ifi * a.table_stride;
+    if (tab[TROW_U32 + 0]) continue;  // length / magic failure: no CRC
+    const sif_dec_desc d = a.descs[ifi];
+    const uint64_t b0 = 4, b1 = d.in_len - 4;
+    const uint64_t e1 = (uint64_t)piece * SEGD < b1 - b0 ? b1 - (uint64_t)piece * SEGD : b0;
+    const uint64_t e0 = e1 - b0 > SEGD ? e1 - SEGD : b0;
+    if (e0 >= e1) continue;
+    const uint32_t raw = crc_piece_warp(d.in, e0, e1, t4, stage[w]);
+    if (lane == 0 && raw) atomicXor(a.acc + 4ull * ifi + 0, crc_mult(kPieceShift[piece], raw));
   }
 }
 
@@ -170,7 +168,7 @@ __device__ __noinline__ double plus_value(const uint32_t* tab, const uint8_t* in
 // reference's f64 scatter-add rounded to fp32 (codec.py:257-266); an element held by both
 // planes is summed in float64 (plus value recovered from its block).  Stored with 16-byte
 // stores.
-__global__ void __launch_bounds__(DNT) sif_scatter_kernel(DecArgs a) {
+__global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
   extern __shared__ __align__(16) uint8_t dsm_raw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t segw = (uint32_t)a.segw;

@@ -37,7 +37,6 @@ constexpr int CH = 4096;           // elements per chunk
 constexpr int UNITS = 8;           // warp-streamed units per chunk
 constexpr int UE = CH / UNITS;     // elements per unit
 constexpr int CNT = 256;           // threads of chunk kernels
-constexpr int SEG = (int)CRC_SEG;  // CRC segment bytes per CTA
 constexpr int DSH = 19;            // digit = |x| key >> 19 (12 bits)
 constexpr int ND = 4096;           // digits per sign
 constexpr int MAXB = 32;           // max blocks (M+ + M-) per IF
@@ -572,8 +571,8 @@ __device__ __forceinline__ void unit_span(const EArgs& a, const IfInfo& f, uint3
 // ---------------------------------------------------------------------------------------
 // K1: per-IF setup: accumulators and the sampled bracket lo (speculation only: a missed
 // bracket is detected in K3 and the IF re-streamed).
-__global__ void __launch_bounds__(256) enc_prep(EArgs a) {
-  constexpr int NT = 256;
+__global__ void __launch_bounds__(512) enc_prep(EArgs a) {
+  constexpr int NT = 512;
   constexpr int EXACT_T = 8192;  // IFs up to this size get the exact tau key as lo
   __shared__ uint32_t sh8k[8192 + 2048];
   __shared__ SelSh sh;
@@ -583,10 +582,8 @@ __global__ void __launch_bounds__(256) enc_prep(EArgs a) {
   for (int b = tid; b < a.maxb; b += NT) { st.bmin[b] = 0x7FFFFFFFu; st.bmax[b] = 0u; }
   for (int k = tid; k < a.maxb * 16; k += NT) st.S[k] = 0ull;
   for (int b = tid; b < a.maxb; b += NT) st.bcount[b] = 0u;
-  if (f.hslot >= 0) {
-    uint4* h = reinterpret_cast<uint4*>(a.hist + (uint64_t)f.hslot * 2 * ND);
-    for (int k = tid; k < 2 * ND / 4; k += NT) h[k] = make_uint4(0, 0, 0, 0);
-  }
+  // (the IF's digit histogram is zeroed by enc_select after it has read it, and by
+  //  sif_enc_upload before the first run)
   const uint64_t T = f.T, kk = f.kk;
   uint32_t lo = 1;
   if (T <= EXACT_T && kk > 0) {
@@ -666,7 +663,7 @@ __global__ void __launch_bounds__(256) enc_prep(EArgs a) {
   }
   if (tid == 0) {
     st.lo = lo; st.lo_neg = lo_neg; st.ncand = 0; st.maxkey = 0; st.cnt_lo = 0; st.err = E_NONE; st.flags = 0;
-    st.P = 0;
+    st.P = 0; st.crc_acc = 0; st.seg_done = 0;
   }
 }
 
@@ -766,6 +763,14 @@ __global__ void __launch_bounds__(CNT, 3) enc_stream(EArgs a) {
   flush_if_stream(a, cur, hist, mk, clo, dmin, dmax, sdr);
 }
 
+// The IF's digit histogram is dead once enc_select has read it: zero it for the next run
+// (plain stores at the end of the kernel, so nothing waits on them).
+__device__ __forceinline__ void zero_hist(const EArgs& a, const IfInfo& f) {
+  if (f.hslot < 0) return;
+  uint4* gh = reinterpret_cast<uint4*>(a.hist + (uint64_t)f.hslot * 2 * ND);
+  for (int k = threadIdx.x; k < 2 * ND / 4; k += blockDim.x) gh[k] = make_uint4(0, 0, 0, 0);
+}
+
 // ---------------------------------------------------------------------------------------
 // K3: per-IF selection.
 struct K3Sh {
@@ -793,6 +798,10 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   IfSt& st = a.st[ifi];
   const uint64_t kk = f.kk, seed = f.seed;
   if (st.maxkey >= kNonFiniteKey) {
+    if (f.hslot >= 0) {
+      uint4* gh = reinterpret_cast<uint4*>(a.hist + (uint64_t)f.hslot * 2 * ND);
+      for (int k = tid; k < 2 * ND / 4; k += NT) gh[k] = make_uint4(0, 0, 0, 0);
+    }
     if (tid == 0) {
       st.err = E_NONFINITE;
       if (a.atkf_only) a.status[ifi] = SIF_ERR_NONFINITE;
@@ -810,6 +819,10 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
     lo = floor_lo;
     lo_neg = floor_lo;
     for (int k = tid; k < 2 * ND; k += NT) hist[k] = 0;
+    if (f.hslot >= 0) {  // the global histogram of the first pass is discarded: zero it for the next run
+      uint4* gh = reinterpret_cast<uint4*>(a.hist + (uint64_t)f.hslot * 2 * ND);
+      for (int k = tid; k < 2 * ND / 4; k += NT) gh[k] = make_uint4(0, 0, 0, 0);
+    }
     if (tid == 0) k3.cursor = 0;
     __syncthreads();
     {
@@ -975,6 +988,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
         run += tot;
       }
     }
+    zero_hist(a, f);
     if (tid == 0) {
       a.tau3[3 * ifi + 0] = tau;
       a.tau3[3 * ifi + 1] = tau_p;
@@ -1132,6 +1146,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
     }
   }
   prof_mark(a, ifi, 8);
+  zero_hist(a, f);
   if (tid == 0) {
     uint32_t fl = 0;
     if (keep_none) fl |= F_KEEP_NONE;
@@ -1360,7 +1375,7 @@ struct AbqPar {
 };
 
 template <int FIRST>
-__global__ void __launch_bounds__(CNT) enc_abq(EArgs a) {
+__global__ void __launch_bounds__(CNT, 4) enc_abq(EArgs a) {
   extern __shared__ __align__(16) uint8_t dsm_raw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int maxb = a.maxb, qb = a.q_bit;
@@ -1559,8 +1574,6 @@ __global__ void __launch_bounds__(256) enc_layout(EArgs a) {
     const uint64_t P = pos + kCrcBytes;
     st.P = P;
     s_P = P;
-    st.crc_acc = 0;
-    st.seg_done = 0;
     if (P > f.cap) st.err = E_CAPACITY;
   }
   __syncthreads();
@@ -1656,7 +1669,7 @@ __device__ __forceinline__ void pack_window(uint32_t* out32, uint32_t* buf, uint
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(CNT) enc_pack(EArgs a) {
+__global__ void __launch_bounds__(CNT, 4) enc_pack(EArgs a) {
   extern __shared__ __align__(16) uint8_t dsm_raw[];
   __shared__ uint32_t pbuf[CNT / 32][2][40];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1736,60 +1749,57 @@ __global__ void __launch_bounds__(CNT) enc_pack(EArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------
-// K8: CRC-32 over bytes [4, P-4) (codec.py:316).  The payload is cut into SEG-byte segments
-// (one CTA each, grid sized from the capacity); each CTA computes its segment's raw CRC
-// shifted to the end of the range; the XOR of all segments is the raw CRC (GF(2)
-// linearity).  The last CTA of an IF finishes it and writes CRC, length and status.
-__global__ void __launch_bounds__(256) enc_crc(EArgs a) {
-  constexpr int NT = 256;
+// K8: CRC-32 over bytes [4, P-4) (codec.py:316).  The range is cut into 2 KiB pieces
+// aligned to its end; one warp computes a piece's raw CRC (crc_piece_warp), shifts it over
+// the pieces after it with one multiply (kPieceShift) and XORs it into the IF's
+// accumulator (GF(2) linearity).  Piece slots are sized from the capacity; the warp that
+// completes an IF's last slot writes the CRC, the length and the status.
+__global__ void __launch_bounds__(CNT) enc_crc(EArgs a) {
   __shared__ uint32_t t4[1024];
-  __shared__ uint32_t stage[16 * NT];
-  __shared__ uint32_t red[NT / 32 + 2];
-  __shared__ uint32_t s_last;
-  const int tid = threadIdx.x;
-  // locate (IF, segment) of this CTA: the per-IF segment counts are a prefix in seg_base
-  const uint32_t gb = blockIdx.x;
-  int lo = 0, hi = a.n - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (a.seg_base[mid] <= gb) lo = mid; else hi = mid - 1;
-  }
-  const int ifi = lo;
-  const uint32_t seg = gb - a.seg_base[ifi];
-  const uint32_t nseg = a.seg_base[ifi + 1] - a.seg_base[ifi];
-  const IfInfo& f = a.info[ifi];
-  IfSt& st = a.st[ifi];
-  if (st.err) {
-    if (tid == 0 && seg == 0) {
-      if (st.err == E_NONFINITE) { a.status[ifi] = SIF_ERR_NONFINITE; a.out_len[ifi] = 0; }
-      else { a.status[ifi] = SIF_ERR_CAPACITY; a.out_len[ifi] = st.P; }
-    }
-    return;
-  }
-  const uint64_t P = st.P;
-  const uint64_t b0 = 4, b1 = P - 4;
-  // segment `seg` covers [b1 - (seg+1)*SEG, b1 - seg*SEG) clipped to [b0, b1)
-  const uint64_t e1 = (uint64_t)seg * SEG < b1 - b0 ? b1 - (uint64_t)seg * SEG : b0;
-  const uint64_t e0 = e1 - b0 > (uint64_t)SEG ? e1 - SEG : b0;
-  uint32_t part = 0;
-  if (e0 < e1) {
-    for (int k = tid; k < 1024; k += NT) t4[k] = (&kCrcTab4[0][0])[k];
-    __syncthreads();
-    const uint32_t raw = crc_cta_staged<NT>(f.out, e0, e1, t4, red, stage);
-    if (tid == 0) part = raw ? crc_mult(kSegShift[seg], raw) : 0u;
-  }
-  if (tid == 0) {
-    if (part) atomicXor(&st.crc_acc, part);
-    __threadfence();
-    s_last = atomicAdd(&st.seg_done, 1u) + 1 == nseg;
-  }
+  __shared__ uint32_t stage[CNT / 32][544];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < 1024; k += CNT) t4[k] = (&kCrcTab4[0][0])[k];
   __syncthreads();
-  if (s_last && tid == 0) {
-    __threadfence();
-    const uint32_t raw = atomicXor(&st.crc_acc, 0u);
-    st_u32_le_bytes(f.out, P - 4, crc_finish(raw, P - 8));
-    a.out_len[ifi] = P;
-    a.status[ifi] = SIF_OK;
+  const uint64_t GW = (uint64_t)gridDim.x * (CNT / 32);
+  const uint64_t total = a.seg_base[a.n];
+  for (uint64_t gp = (uint64_t)blockIdx.x * (CNT / 32) + w; gp < total; gp += GW) {
+    int lo = 0, hi = a.n - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.seg_base[mid] <= gp) lo = mid; else hi = mid - 1;
+    }
+    const int ifi = lo;
+    const uint32_t piece = (uint32_t)(gp - a.seg_base[ifi]);
+    const uint32_t npieces = a.seg_base[ifi + 1] - a.seg_base[ifi];
+    const IfInfo& f = a.info[ifi];
+    IfSt& st = a.st[ifi];
+    const uint32_t err = st.err;
+    uint32_t part = 0;
+    if (!err) {
+      const uint64_t b0 = 4, b1 = st.P - 4;
+      const uint64_t e1 = (uint64_t)piece * CRC_PIECE < b1 - b0 ? b1 - (uint64_t)piece * CRC_PIECE : b0;
+      const uint64_t e0 = e1 - b0 > CRC_PIECE ? e1 - CRC_PIECE : b0;
+      if (e0 < e1) {
+        const uint32_t raw = crc_piece_warp(f.out, e0, e1, t4, stage[w]);
+        part = raw ? crc_mult(kPieceShift[piece], raw) : 0u;
+      }
+    }
+    if (lane == 0) {
+      if (part) atomicXor(&st.crc_acc, part);
+      __threadfence();
+      if (atomicAdd(&st.seg_done, 1u) + 1 == npieces) {
+        __threadfence();
+        if (err == E_NONFINITE) { a.status[ifi] = SIF_ERR_NONFINITE; a.out_len[ifi] = 0; }
+        else if (err) { a.status[ifi] = SIF_ERR_CAPACITY; a.out_len[ifi] = st.P; }
+        else {
+          const uint64_t P = st.P;
+          st_u32_le_bytes(f.out, P - 4, crc_finish(atomicXor(&st.crc_acc, 0u), P - 8));
+          a.out_len[ifi] = P;
+          a.status[ifi] = SIF_OK;
+        }
+      }
+    }
+    __syncwarp();
   }
 }
 

@@ -71,11 +71,11 @@ uint32_t h_x8n(uint64_t nbytes) {  // x^(8 n) mod P, reflected
 int crc_tables_init() {
   static int done = 0;
   if (done) return SIF_OK;
-  std::vector<uint32_t> t(sif::CRC_SEG_MAX);
-  const uint32_t step = h_x8n(sif::CRC_SEG);
+  std::vector<uint32_t> t(sif::CRC_PIECES_MAX);
+  const uint32_t step = h_x8n(sif::CRC_PIECE);
   t[0] = 1u << 31;
-  for (int j = 1; j < sif::CRC_SEG_MAX; ++j) t[j] = h_crc_mult(step, t[j - 1]);
-  if (cudaMemcpyToSymbol(sif::kSegShift, t.data(), 4ull * sif::CRC_SEG_MAX) != cudaSuccess) return SIF_ERR_CUDA;
+  for (int j = 1; j < sif::CRC_PIECES_MAX; ++j) t[j] = h_crc_mult(step, t[j - 1]);
+  if (cudaMemcpyToSymbol(sif::kPieceShift, t.data(), 4ull * sif::CRC_PIECES_MAX) != cudaSuccess) return SIF_ERR_CUDA;
   done = 1;
   return SIF_OK;
 }
@@ -129,7 +129,7 @@ constexpr int kSmemStream = (2 * sif::CH + 2 * sif::ND) * 4;
 constexpr int kSmemSelect = (2 * sif::ND + 2 * sif::HB + sif::GCAP * 4 + 2 * sif::GSM) * 4;
 inline int smem_abq(int maxb) { return (sif::CNT / 32) * maxb * (int)(sizeof(sif::AbqPar) + 16 * 8); }
 inline int smem_pack(int maxb) { return (sif::CNT / 32) * maxb * (int)sizeof(sif::PackPar); }
-inline uint32_t crc_segments(uint64_t cap) { return (uint32_t)std::max<uint64_t>(1, (cap + sif::SEG - 1) / sif::SEG); }
+inline uint32_t crc_segments(uint64_t cap) { return (uint32_t)std::max<uint64_t>(1, (cap + sif::CRC_PIECE - 1) / sif::CRC_PIECE); }
 
 }  // namespace
 
@@ -234,7 +234,7 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
     if (ch > 1) ++nhist;
     lists += up(16 * T, 256);
     nseg += crc_segments(d[i].out_cap);
-    if (crc_segments(d[i].out_cap) > (uint64_t)sif::CRC_SEG_MAX) return SIF_ERR_INVALID_ARG;
+    if (crc_segments(d[i].out_cap) > (uint64_t)sif::CRC_PIECES_MAX) return SIF_ERR_INVALID_ARG;
   }
   if (nch >= (1ull << 31) || nseg >= (1ull << 31)) return SIF_ERR_INVALID_ARG;
   const uint64_t kk = std::max<uint64_t>(1, kmax);
@@ -313,6 +313,10 @@ int sif_enc_upload(const sif_plan* p, const sif_enc_desc* d, const sif_codec_cfg
   if (c->mode == SIF_MODE_FIXED &&
       check_cuda(cudaMemcpyAsync(wb + w.fixedq, c->fixed_q, (size_t)(c->m_plus + c->m_minus), cudaMemcpyHostToDevice, s)))
     return SIF_ERR_CUDA;
+  // digit histograms start zeroed; enc_select re-zeroes each one after reading it
+  if (p->cap_smem > 0 &&
+      check_cuda(cudaMemsetAsync(wb + w.hist, 0, 4ull * 2 * sif::ND * (uint64_t)p->cap_smem, s)))
+    return SIF_ERR_CUDA;
   // the uploads read host vectors: finish them before the vectors go out of scope
   return check_cuda(cudaStreamSynchronize(s));
 }
@@ -361,8 +365,9 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
     attrs = true;
   }
   const int maxb = p->max_blocks;
-  static int g_stream = 0, g_members = 0, g_abq = 0, g_pack = 0, g_maxb = -1;
+  static int g_stream = 0, g_members = 0, g_abq = 0, g_pack = 0, g_maxb = -1, g_crc = 0;
   if (!g_stream) {
+    g_crc = (int)std::max<uint64_t>(1, (uint64_t)resident_grid(sif::enc_crc, sif::CNT, 0, 1ull << 30));
     g_stream = resident_grid(sif::enc_stream, sif::CNT, kSmemStream, 1ull << 30);
     g_members = resident_grid(sif::enc_members, sif::CNT, 0, 1ull << 30);
   }
@@ -374,7 +379,7 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   const unsigned nch = (unsigned)p->tiles;
   const unsigned n = (unsigned)p->n;
   const unsigned wgrid = std::max(1u, (nch + sif::CNT / 32 - 1) / (sif::CNT / 32));  // >= 1 chunk per warp
-  { ProfScope ps(KP_PREP, s); sif::enc_prep<<<n, 256, 0, s>>>(a); }
+  { ProfScope ps(KP_PREP, s); sif::enc_prep<<<n, 512, 0, s>>>(a); }
   { ProfScope ps(KP_STREAM, s); sif::enc_stream<<<std::min<unsigned>(nch, g_stream), sif::CNT, kSmemStream, s>>>(a); }
   { ProfScope ps(KP_SELECT, s); sif::enc_select<<<n, sif::SNT, kSmemSelect, s>>>(a); }
   if (!atkf) {
@@ -385,7 +390,7 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
     }
     { ProfScope ps(KP_LAYOUT, s); sif::enc_layout<<<n, 256, 0, s>>>(a); }
     { ProfScope ps(KP_PACK, s); sif::enc_pack<<<std::min<unsigned>(wgrid, g_pack), sif::CNT, smem_pack(maxb), s>>>(a); }
-    { ProfScope ps(KP_CRC, s); sif::enc_crc<<<(unsigned)p->cluster, 256, 0, s>>>(a); }
+    { ProfScope ps(KP_CRC, s); sif::enc_crc<<<std::min<unsigned>((unsigned)p->cluster, g_crc), sif::CNT, 0, s>>>(a); }
   }
   return check_cuda(cudaGetLastError());
 }
@@ -469,7 +474,7 @@ int sif_dec_plan(const sif_dec_desc* d, int n, sif_plan* p) {
     const uint64_t blk = d[i].in_len > 32 ? (d[i].in_len - 32) / 17 + 1 : 1;
     maxrows = std::max(maxrows, blk);
     nseg += dec_segments(d[i].in_len);
-    if (dec_segments(d[i].in_len) > (uint32_t)sif::CRC_SEG_MAX) return SIF_ERR_INVALID_ARG;
+    if (dec_segments(d[i].in_len) > (uint32_t)sif::CRC_PIECES_MAX) return SIF_ERR_INVALID_ARG;
   }
   if (nseg >= (1ull << 31)) return SIF_ERR_INVALID_ARG;
   const uint32_t segw = dec_segw(d, n);
@@ -533,7 +538,13 @@ int sif_dec_run(const sif_plan* p, int parse_only, void* ws, int32_t* status, vo
   a.item_base = reinterpret_cast<const uint64_t*>(wb + w.itembase);
   a.segw = p->tiles;
   { ProfScope ps(KP_PARSE, s); sif::sif_parse_kernel<<<(p->n + 127) / 128, 128, 0, s>>>(a); }
-  { ProfScope ps(KP_DCRC, s); sif::sif_dcrc_kernel<<<(unsigned)p->cluster, sif::DNT, 0, s>>>(a); }
+  {
+    static int g_dcrc = 0;
+    if (!g_dcrc) g_dcrc = resident_grid(sif::sif_dcrc_kernel, sif::DNT, 0, 1ull << 30);
+    const unsigned warps = (unsigned)p->cluster, grid = std::min<unsigned>((warps + sif::DNT / 32 - 1) / (sif::DNT / 32), g_dcrc);
+    ProfScope ps(KP_DCRC, s);
+    sif::sif_dcrc_kernel<<<std::max(1u, grid), sif::DNT, 0, s>>>(a);
+  }
   if (!parse_only) {
     static int attr_bytes = 0;
     if (p->smem_bytes > attr_bytes) {
