@@ -13,6 +13,7 @@ from .codec import (
     AtkfResult,
     BatchDecoder,
     BatchEncoder,
+    BatchPipeline,
     ListEncoder,
     CodecConfig,
     HostRoundTrip,

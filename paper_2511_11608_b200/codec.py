@@ -507,6 +507,68 @@ def atkf_filter(x, s: float, lam: float, seed: int) -> AtkfResult:
     return AtkfResult(kept[:k], float(t[0]), float(t[1]), float(t[2]), k, k == 0, xt)
 
 
+# ---------------------------------------------------------------------------- pipelined steps
+class BatchPipeline:
+    """Serving loop for a fixed batch layout: `depth` (encoder, decoder) pairs with their
+    own payload buffers, each captured as one CUDA graph on its own stream.  Consecutive
+    `step()`s rotate over the slots, so the decode of batch i overlaps the encode of batch
+    i+1 (the kernels are latency-bound and leave SM resources free for each other).
+    `xs` is the device input batch read by every step (refill it between steps in a real
+    server); `ys(slot)` is the decoded output of a slot."""
+
+    def __init__(self, xs: torch.Tensor, cfg: CodecConfig, seeds, depth: int = 2, graphs: bool = True):
+        self.xs = xs
+        self.B, self.rows, self.cols = xs.shape
+        seeds = list(seeds)
+        self.slots = []
+        for _ in range(max(1, depth)):
+            enc = BatchEncoder(xs, cfg, seeds)
+            enc.run().check()
+            lens = enc.out_len.cpu().numpy()
+            dec = BatchDecoder([enc.out.data_ptr() + i * enc.cap for i in range(self.B)], lens, self.rows, self.cols)
+            dec.run().check()
+            st = torch.cuda.Stream()
+            fn = (lambda e=enc, d=dec: (e.run(), d.run()))
+            g = None
+            if graphs:
+                with torch.cuda.stream(st):
+                    g = capture_graph(fn)
+            self.slots.append(dict(enc=enc, dec=dec, stream=st, graph=g, fn=fn))
+        self.i = 0
+        torch.cuda.synchronize()
+
+    def begin(self):
+        """Order the slot streams after the current stream (call before a burst of steps)."""
+        cur = torch.cuda.current_stream()
+        for sl in self.slots:
+            sl["stream"].wait_stream(cur)
+
+    def step(self):
+        sl = self.slots[self.i % len(self.slots)]
+        self.i += 1
+        with torch.cuda.stream(sl["stream"]):
+            if sl["graph"] is not None:
+                sl["graph"].replay()
+            else:
+                sl["fn"]()
+        return self
+
+    def end(self):
+        """Make the current stream wait for every slot (call after a burst of steps)."""
+        cur = torch.cuda.current_stream()
+        for sl in self.slots:
+            cur.wait_stream(sl["stream"])
+
+    def check(self):
+        for sl in self.slots:
+            sl["enc"].check()
+            sl["dec"].check()
+        return self
+
+    def ys(self, slot: int = 0) -> torch.Tensor:
+        return self.slots[slot]["dec"].out
+
+
 # ---------------------------------------------------------------------------- host round trip
 class HostRoundTrip:
     """encode -> .sif -> decode of a batch that lives in pinned HOST memory, pipelined over
