@@ -400,7 +400,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch the kernels directly instead of replaying CUDA graphs")
-    ap.add_argument("--depth", type=int, default=2,
+    ap.add_argument("--depth", type=int, default=3,
                     help="pipeline slots: consecutive steps overlap on this many streams (1 = sequential)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

@@ -93,6 +93,7 @@ struct EArgs {
   uint32_t* u_cnt;     // [nch][UNITS]
   uint32_t* ch_bcnt;   // [nch][maxb]
   uint32_t* ch_bpre;   // [nch][maxb]
+  uint32_t* ch_brs;    // [nch][maxb] start of the block's run inside the chunk's member slot
   int32_t* ch_blast;   // [nch][maxb] row of the block's last member in the chunk, -1 if none
   int32_t* ch_bprev;   // [nch][maxb] row of the block's last member in earlier chunks
   uint32_t* hist;      // [nhist][2][ND]
@@ -1279,10 +1280,17 @@ __global__ void __launch_bounds__(CNT) enc_members(EArgs a) {
     if (lane < B) { ws.cnt[lane] = 0; ws.mn[lane] = 0x7FFFFFFFu; ws.mx[lane] = 0; ws.xl[lane] = 0; }
     __syncwarp();
     const uint2* gl = le(a, f);
-    // pass 1 over the chunk's units in order: block ids (kept in SMEM), counts, min/max, last
+    uint2* om = me(a, f) + (uint64_t)(c - f.ch0) * CH;
+    const uint32_t my_uo = lane < UNITS ? a.u_off[(uint64_t)c * UNITS + lane] : 0u;
+    const uint32_t my_un = lane < UNITS ? a.u_cnt[(uint64_t)c * UNITS + lane] : 0u;
+    const uint32_t n = __reduce_add_sync(0xFFFFFFFFu, my_un);
+    // one pass when every block fits a run of capacity n (B*n <= slot): block b's run starts
+    // at b*n; otherwise block ids are kept and a second pass scatters into prefix runs
+    const uint64_t slot = min((uint64_t)CH, f.T - (uint64_t)(c - f.ch0) * CH);  // member slot capacity
+    const bool one = (uint64_t)B * n <= slot;
     uint32_t i = 0;
     for (int u = 0; u < UNITS; ++u) {
-      const uint32_t uo = a.u_off[(uint64_t)c * UNITS + u], un = a.u_cnt[(uint64_t)c * UNITS + u];
+      const uint32_t uo = __shfl_sync(0xFFFFFFFFu, my_uo, u), un = __shfl_sync(0xFFFFFFFFu, my_un, u);
       for (uint32_t j0 = 0; j0 < un; j0 += 64) {
         // two windows in flight: both loads issued before either is used
         uint2 ev[2];
@@ -1298,28 +1306,31 @@ __global__ void __launch_bounds__(CNT) enc_members(EArgs a) {
           int blk = -1;
           if (j < un) {
             if (kc.kept(e.x, e.y)) blk = kc.block_of(e.x, e.y);
-            bk[i + j] = (int8_t)blk;
+            if (!one) bk[i + j] = (int8_t)blk;
           }
           const uint32_t peers = __match_any_sync(0xFFFFFFFFu, blk);
+          const bool last = blk >= 0 && lane == 31 - __clz(peers);
           if (blk >= 0) {
             const uint32_t key = e.x & 0x7FFFFFFFu;
             atomicMin(&ws.mn[blk], key);
             atomicMax(&ws.mx[blk], key);
-            if (lane == 31 - __clz(peers)) { ws.cnt[blk] += __popc(peers); ws.xl[blk] = max(ws.xl[blk], e.y + 1u); }
+            if (one) __stcg(om + (uint32_t)blk * n + ws.cnt[blk] + __popc(peers & lt), e);
           }
+          __syncwarp();
+          if (last) { ws.cnt[blk] += __popc(peers); ws.xl[blk] = max(ws.xl[blk], e.y + 1u); }
           __syncwarp();
         }
       }
       i += un;
     }
-    const uint32_t n = i;
-    __syncwarp();
     const uint32_t cnt = lane < B ? ws.cnt[lane] : 0u;
     const uint32_t sinc = warp_incl_scan_u32(cnt);
     if (lane < B) {
-      ws.pos[lane] = sinc - cnt;
+      const uint32_t rs = one ? (uint32_t)lane * n : sinc - cnt;
+      ws.pos[lane] = rs;
       const uint64_t ci = (uint64_t)c * a.maxb + lane;
       a.ch_bcnt[ci] = cnt;
+      a.ch_brs[ci] = rs;
       a.ch_blast[ci] = ws.xl[lane] ? (int32_t)fk.div(ws.xl[lane] - 1u) : -1;
       if (cnt) {
         atomicMin(&st.bmin[lane], ws.mn[lane]);
@@ -1328,11 +1339,11 @@ __global__ void __launch_bounds__(CNT) enc_members(EArgs a) {
       }
     }
     __syncwarp();
+    if (one) continue;
     // pass 2: stable scatter into block runs of the member slot
-    uint2* om = me(a, f) + (uint64_t)(c - f.ch0) * CH;
     i = 0;
     for (int u = 0; u < UNITS; ++u) {
-      const uint32_t uo = a.u_off[(uint64_t)c * UNITS + u], un = a.u_cnt[(uint64_t)c * UNITS + u];
+      const uint32_t uo = __shfl_sync(0xFFFFFFFFu, my_uo, u), un = __shfl_sync(0xFFFFFFFFu, my_un, u);
       for (uint32_t j0 = 0; j0 < un; j0 += 64) {
         uint2 ev[2];
         int bv[2];
@@ -1357,7 +1368,6 @@ __global__ void __launch_bounds__(CNT) enc_members(EArgs a) {
       }
       i += un;
     }
-    (void)n;
   }
 }
 
@@ -1429,13 +1439,13 @@ __global__ void __launch_bounds__(CNT, 4) enc_abq(EArgs a) {
       __syncwarp();
     }
     const uint32_t bcnt = lane < B ? a.ch_bcnt[(uint64_t)c * maxb + lane] : 0u;
-    const uint32_t binc = warp_incl_scan_u32(bcnt);
+    const uint32_t brs = lane < B ? a.ch_brs[(uint64_t)c * maxb + lane] : 0u;
     const uint2* gm = me(a, f) + (uint64_t)(c - f.ch0) * CH;
     const uint32_t lref = (1u << qb) - 1u;
     for (int b = 0; b < B; ++b) {
       const uint32_t nb = __shfl_sync(0xFFFFFFFFu, bcnt, b);
       if (nb == 0 || !par[b].act) continue;
-      const uint32_t rs = __shfl_sync(0xFFFFFFFFu, binc, b) - nb;
+      const uint32_t rs = __shfl_sync(0xFFFFFFFFu, brs, b);
       const double vmin = par[b].vmin;
       const double oref = par[b].o[qb], iref = par[b].inv[qb];
       if (FIRST) {
@@ -1708,7 +1718,7 @@ __global__ void __launch_bounds__(CNT, 4) enc_pack(EArgs a) {
     const uint32_t bcnt = lane < B ? a.ch_bcnt[ci] : 0u;
     const uint32_t bpre = lane < B ? a.ch_bpre[ci] : 0u;
     const int32_t bprev = lane < B ? a.ch_bprev[ci] : -1;
-    const uint32_t binc = warp_incl_scan_u32(bcnt);
+    const uint32_t brs = lane < B ? a.ch_brs[ci] : 0u;
     const uint2* gm = me(a, f) + (uint64_t)(c - f.ch0) * CH;
     uint8_t* out = f.out;
     uint32_t* out32 = reinterpret_cast<uint32_t*>(out);
@@ -1716,7 +1726,7 @@ __global__ void __launch_bounds__(CNT, 4) enc_pack(EArgs a) {
     for (int b = 0; b < B; ++b) {
       const uint32_t n = __shfl_sync(0xFFFFFFFFu, bcnt, b);
       if (n == 0) continue;
-      const uint32_t rs = __shfl_sync(0xFFFFFFFFu, binc, b) - n;
+      const uint32_t rs = __shfl_sync(0xFFFFFFFFu, brs, b);
       const uint32_t p0 = __shfl_sync(0xFFFFFFFFu, bpre, b);
       int32_t rprev = __shfl_sync(0xFFFFFFFFu, bprev, b);
       const PackPar p = par[b];

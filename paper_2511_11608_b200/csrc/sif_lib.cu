@@ -92,7 +92,7 @@ inline int num_sms() {
 
 // Workspace sections of an encode plan (all offsets 256-byte aligned).
 struct EncWs {
-  uint64_t info, st, ch_if, ch_e0, u_off, u_cnt, bcnt, bpre, blast, bprev, hist, fixedq, keptoff, segbase, lists;
+  uint64_t info, st, ch_if, ch_e0, u_off, u_cnt, bcnt, bpre, brs, blast, bprev, hist, fixedq, keptoff, segbase, lists;
 };
 
 EncWs enc_ws(uint64_t n, uint64_t nch, uint64_t maxb, uint64_t nhist, uint64_t nq) {
@@ -107,6 +107,7 @@ EncWs enc_ws(uint64_t n, uint64_t nch, uint64_t maxb, uint64_t nhist, uint64_t n
   w.u_cnt = take(4 * nch * sif::UNITS);
   w.bcnt = take(4 * nch * maxb);
   w.bpre = take(4 * nch * maxb);
+  w.brs = take(4 * nch * maxb);
   w.blast = take(4 * nch * maxb);
   w.bprev = take(4 * nch * maxb);
   w.hist = take(4ull * 2 * sif::ND * nhist);
@@ -341,6 +342,7 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   a.seg_base = reinterpret_cast<const uint32_t*>(wb + w.segbase);
   a.ch_bcnt = reinterpret_cast<uint32_t*>(wb + w.bcnt);
   a.ch_bpre = reinterpret_cast<uint32_t*>(wb + w.bpre);
+  a.ch_brs = reinterpret_cast<uint32_t*>(wb + w.brs);
   a.ch_blast = reinterpret_cast<int32_t*>(wb + w.blast);
   a.ch_bprev = reinterpret_cast<int32_t*>(wb + w.bprev);
   a.hist = reinterpret_cast<uint32_t*>(wb + w.hist);
