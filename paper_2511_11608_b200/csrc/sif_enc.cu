@@ -81,6 +81,13 @@ struct IfSt {
   uint64_t P;
   uint32_t crc_acc, seg_done;
   uint32_t bcount[MAXB];  // block member totals (K4 atomics)
+  // multi-kernel select state (enc_select<1|2>, enc_gather<1|2>)
+  uint32_t sel_phase;     // 0 done, 1 needs the tau-bin gather, 2 needs the cut-bin gather
+  int32_t dtau;
+  uint64_t rt, cnt_nz;
+  uint32_t nA, pend_n, nreg, sel_lo;
+  uint32_t pend_s[MAXB], pend_d[MAXB], pend_r[MAXB], pend_ci[MAXB], pend_reg[MAXB];
+  uint32_t reg_off[MAXB], reg_cnt[MAXB], reg_key[MAXB];
 };
 
 struct EArgs {
@@ -108,6 +115,7 @@ struct EArgs {
   double* tau3;
   const uint32_t* seg_base;  // [n+1] prefix of CRC segments per IF
   uint64_t* prof;            // optional phase timestamps of enc_select (16 per IF, debug)
+  uint32_t big_ncand;        // IFs with more candidates use the multi-kernel select (0: never)
 };
 
 __device__ __forceinline__ void prof_mark(const EArgs& a, int ifi, int k) {
@@ -664,7 +672,7 @@ __global__ void __launch_bounds__(512) enc_prep(EArgs a) {
   }
   if (tid == 0) {
     st.lo = lo; st.lo_neg = lo_neg; st.ncand = 0; st.maxkey = 0; st.cnt_lo = 0; st.err = E_NONE; st.flags = 0;
-    st.P = 0; st.crc_acc = 0; st.seg_done = 0;
+    st.P = 0; st.crc_acc = 0; st.seg_done = 0; st.sel_phase = 0;
   }
 }
 
@@ -785,6 +793,12 @@ struct K3Sh {
   uint32_t reg_off[MAXB], reg_cnt[MAXB];
 };
 
+// Three launches: PH 0 resolves everything for the uncommon paths (lambda > 0, tau == 0,
+// k == 0, tiny plane counts) and, on the common path, only the digit of tau; the tau bin is
+// then gathered by all SMs (enc_gather<1>), PH 1 selects tau inside it, counts the kept
+// elements, finds every MS cut's digit and resolves the cuts inside tau's bin; the other
+// cut bins are gathered by all SMs (enc_gather<2>) and PH 2 resolves those cuts.
+template <int PH>
 __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   constexpr int NT = SNT;
   extern __shared__ __align__(16) uint8_t dsm_raw[];
@@ -798,7 +812,29 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   const IfInfo f = a.info[ifi];
   IfSt& st = a.st[ifi];
   const uint64_t kk = f.kk, seed = f.seed;
-  if (st.maxkey >= kNonFiniteKey) {
+  if (PH > 0) {
+    if (st.sel_phase != (uint32_t)PH) return;
+    if (PH == 2) {
+      // cut bins gathered into their regions of the gather area: exact selects
+      auto key31 = [](uint32_t b) -> uint64_t { return b & 0x7FFFFFFFu; };
+      const uint32_t np = st.pend_n;
+      uint2* gat = me(a, f);
+      for (uint32_t p = 0; p < np; ++p) {
+        const uint32_t g = st.pend_reg[p];
+        const List Bp{nullptr, gat + st.reg_off[g], 0};
+        const uint32_t dc = st.pend_d[p];
+        const SelRes r = select_exact<NT>(
+            sh, scratch, Bp, st.reg_cnt[g], [](uint32_t, uint32_t) { return true; }, key31,
+            [](uint32_t, uint32_t x) -> uint64_t { return x; }, (uint64_t)dc << DSH, (uint64_t)(dc + 1) << DSH,
+            st.pend_r[p], 31);
+        if (tid == 0) { st.cut_key[st.pend_ci[p]] = r.key; st.cut_idx[st.pend_ci[p]] = (uint32_t)r.sec; }
+        __syncthreads();
+      }
+      if (tid == 0) st.sel_phase = 0;
+      return;
+    }
+  }
+  if (PH == 0 && st.maxkey >= kNonFiniteKey) {
     if (f.hslot >= 0) {
       uint4* gh = reinterpret_cast<uint4*>(a.hist + (uint64_t)f.hslot * 2 * ND);
       for (int k = tid; k < 2 * ND / 4; k += NT) gh[k] = make_uint4(0, 0, 0, 0);
@@ -809,12 +845,12 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
     }
     return;
   }
-  uint32_t lo = st.lo, lo_neg = st.lo_neg;
+  uint32_t lo = PH == 0 ? st.lo : st.sel_lo, lo_neg = st.lo_neg;
   const uint32_t floor_lo = a.atkf_only ? 0u : 1u;
   uint32_t ncand = st.ncand;
   bool hist_ok = false;
   prof_mark(a, ifi, 0);
-  if (kk > 0 && st.cnt_lo < kk && lo > floor_lo) {
+  if (PH == 0 && kk > 0 && st.cnt_lo < kk && lo > floor_lo) {
     // bracket missed (or tau == 0): re-stream keeping every nonzero (every element in
     // ATKF-only mode); this CTA writes the list in chunk order and the histogram in SMEM
     lo = floor_lo;
@@ -856,6 +892,11 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
     __syncthreads();
     ncand = k3.cursor;
     hist_ok = true;
+    if (f.hslot >= 0) {  // later phases reload the histogram of the re-streamed list
+      uint4* gh = reinterpret_cast<uint4*>(a.hist + (uint64_t)f.hslot * 2 * ND);
+      const uint4* h4 = reinterpret_cast<const uint4*>(hist);
+      for (int k = tid; k < 2 * ND / 4; k += NT) gh[k] = h4[k];
+    }
   } else if (f.hslot >= 0) {
     const uint4* gh = reinterpret_cast<const uint4*>(a.hist + (uint64_t)f.hslot * 2 * ND);
     uint4* h4 = reinterpret_cast<uint4*>(hist);
@@ -874,7 +915,8 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   prof_mark(a, ifi, 1);
   // candidates with key != 0 (only lo == 0 admits zeros)
   uint64_t cnt_nz = ncand;
-  if (lo == 0) {
+  if (PH == 1) cnt_nz = st.cnt_nz;
+  else if (lo == 0) {
     cnt_nz = (uint64_t)ncand - hist[0] - hist[ND];  // digit 0 holds zeros and tiny values
     uint32_t tiny = 0;
     list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t, bool v) {
@@ -919,20 +961,51 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
       tie_all = s.all_ties;
     } else {
       prof_mark(a, ifi, 2);
-      // digit of tau over both signs, then the bin's elements -> exact select
-      uint32_t* comb = scratch;
-      for (int k = tid; k < ND; k += NT) comb[k] = hist[k] + hist[ND + k];
-      __syncthreads();
-      find_digit<NT>(sh, comb, ND, kk);
-      dtau = (int)sh.fd_digit;
-      const uint64_t rt = kk - sh.fd_above;
-      if (tid == 0) k3.nA = 0;
-      __syncthreads();
-      list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t x, bool v) {
-        if (v && ((b & 0x7FFFFFFFu) >> DSH) == (uint32_t)dtau) A.set(atomicAdd(&k3.nA, 1u), b, x);
-      });
-      __syncthreads();
-      nA = k3.nA;
+      if (PH == 0 && a.big_ncand && ncand > a.big_ncand) {
+        // digit of tau over both signs; its bin is gathered by enc_gather<1> (all SMs)
+        uint32_t* comb = scratch;
+        for (int k = tid; k < ND; k += NT) comb[k] = hist[k] + hist[ND + k];
+        __syncthreads();
+        find_digit<NT>(sh, comb, ND, kk);
+        if (tid == 0) {
+          st.dtau = (int32_t)sh.fd_digit;
+          st.rt = kk - sh.fd_above;
+          st.nA = 0;
+          st.sel_lo = lo;
+          st.ncand = ncand;
+          st.cnt_nz = cnt_nz;
+          st.sel_phase = 1;
+        }
+        return;
+      }
+      uint64_t rt;
+      if (PH == 1) {
+        dtau = st.dtau;
+        rt = st.rt;
+        nA = st.nA;
+        // the gathered bin: first GSM entries in shared memory, the rest read from global
+        const uint2* gsrc = me(a, f);
+        uint2* sdst = reinterpret_cast<uint2*>(gbuf);
+        const uint32_t ns = nA < (uint32_t)GSM ? nA : (uint32_t)GSM;
+        for (uint32_t k = tid; k < ns; k += NT) sdst[k] = __ldcg(gsrc + k);
+        A.g = me(a, f) + GSM;
+        __syncthreads();
+      } else {
+        // small IF: digit of tau and its bin gathered by this CTA
+        uint32_t* comb = scratch;
+        for (int k = tid; k < ND; k += NT) comb[k] = hist[k] + hist[ND + k];
+        __syncthreads();
+        find_digit<NT>(sh, comb, ND, kk);
+        dtau = (int)sh.fd_digit;
+        rt = kk - sh.fd_above;
+        if (tid == 0) k3.nA = 0;
+        __syncthreads();
+        list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t x, bool v) {
+          if (v && ((b & 0x7FFFFFFFu) >> DSH) == (uint32_t)dtau) A.set(atomicAdd(&k3.nA, 1u), b, x);
+        });
+        __syncthreads();
+        nA = k3.nA;
+      }
       const SelRes s = select_exact<NT>(sh, scratch, A, nA, all_pred, key31, hash_of, (uint64_t)dtau << DSH,
                                         (uint64_t)(dtau + 1) << DSH, rt);
       tau_key = s.key;
@@ -991,6 +1064,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
     }
     zero_hist(a, f);
     if (tid == 0) {
+      st.sel_phase = 0;
       a.tau3[3 * ifi + 0] = tau;
       a.tau3[3 * ifi + 1] = tau_p;
       a.tau3[3 * ifi + 2] = tau_m;
@@ -1088,7 +1162,29 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
     }
     prof_mark(a, ifi, 6);
     const uint32_t np = k3.pend_n;
-    if (np > 0) {
+    if (PH == 1 && np > 0) {
+      // regions of the gather area for the pending cut bins (sizes from the histogram);
+      // enc_gather<2> fills them with all SMs, enc_select<2> resolves the cuts
+      if (tid == 0) {
+        uint32_t nreg = 0, off = 0;
+        for (uint32_t p = 0; p < np; ++p) {
+          const uint32_t d = k3.pend_s[p] * ND + k3.pend_d[p];
+          uint32_t g = 0;
+          while (g < nreg && st.reg_key[g] != d) ++g;
+          if (g == nreg) {
+            st.reg_key[g] = d;
+            st.reg_off[g] = off;
+            st.reg_cnt[g] = 0;
+            off += hist[d];
+            ++nreg;
+          }
+          st.pend_s[p] = k3.pend_s[p]; st.pend_d[p] = k3.pend_d[p]; st.pend_r[p] = k3.pend_r[p];
+          st.pend_ci[p] = k3.pend_ci[p]; st.pend_reg[p] = g;
+        }
+        st.nreg = nreg;
+        st.pend_n = np;
+      }
+    } else if (np > 0) {
       // gather every pending cut bin in one pass, each (sign, digit) into its own region
       // of the gather area (sizes from the histogram); A is no longer needed
       uint32_t* pm = scratch;                                         // 2*ND bits
@@ -1149,6 +1245,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   prof_mark(a, ifi, 8);
   zero_hist(a, f);
   if (tid == 0) {
+    st.sel_phase = (PH == 1 && k3.pend_n > 0 && fast) ? 2u : 0u;
     uint32_t fl = 0;
     if (keep_none) fl |= F_KEEP_NONE;
     if (only_nonzero) fl |= F_ONLY_NONZERO;
@@ -1167,6 +1264,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
     st.ncand = ncand;
   }
 }
+
 
 // ---------------------------------------------------------------------------------------
 // Per-IF kept test and block id, evaluated by the chunk kernels from IfSt.
@@ -1224,6 +1322,83 @@ __device__ __forceinline__ void warp_range(const EArgs& a, uint32_t& c0, uint32_
   c0 = (uint32_t)((uint64_t)a.nch * gw / GW);
   c1 = (uint32_t)((uint64_t)a.nch * (gw + 1) / GW);
 }
+
+// ---------------------------------------------------------------------------------------
+// Chunk-parallel gathers for enc_select (one warp per chunk, all SMs): G = 1 copies the
+// candidates in tau's digit (either sign) to the IF's gather area, G = 2 copies the
+// candidates of every pending (sign, digit) cut bin to its region.  Appends are
+// warp-aggregated (one atomic per region per window).
+template <int G>
+__global__ void __launch_bounds__(CNT) enc_gather(EArgs a) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t c0, c1;
+  warp_range(a, c0, c1);
+  uint32_t cur = 0xFFFFFFFFu, dtau = 0, nreg = 0, rkey = 0xFFFFFFFFu, roff = 0;
+  for (uint32_t c = c0; c < c1; ++c) {
+    const uint32_t ifi = a.ch_if[c];
+    IfSt& st = a.st[ifi];
+    if (st.sel_phase != (uint32_t)G) continue;
+    const IfInfo& f = a.info[ifi];
+    if (ifi != cur) {
+      cur = ifi;
+      if (G == 1) dtau = (uint32_t)st.dtau;
+      else {
+        nreg = st.nreg;
+        rkey = lane < (int)nreg ? st.reg_key[lane] : 0xFFFFFFFFu;
+        roff = lane < (int)nreg ? st.reg_off[lane] : 0u;
+      }
+    }
+    const uint2* gl = le(a, f);
+    uint2* gat = me(a, f);
+    const uint32_t my_uo = lane < UNITS ? a.u_off[(uint64_t)c * UNITS + lane] : 0u;
+    const uint32_t my_un = lane < UNITS ? a.u_cnt[(uint64_t)c * UNITS + lane] : 0u;
+    for (int u = 0; u < UNITS; ++u) {
+      const uint32_t uo = __shfl_sync(0xFFFFFFFFu, my_uo, u), un = __shfl_sync(0xFFFFFFFFu, my_un, u);
+      for (uint32_t j0 = 0; j0 < un; j0 += 64) {
+        uint2 ev[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t j = j0 + 32 * h + lane;
+          ev[h] = j < un ? __ldg(gl + uo + j) : make_uint2(0, 0);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t j = j0 + 32 * h + lane;
+          const uint2 e = ev[h];
+          const uint32_t dig = (e.x & 0x7FFFFFFFu) >> DSH;
+          int g = -1;
+          if (G == 1) {
+            if (j < un && dig == dtau) g = 0;
+          } else {
+            const uint32_t key = j < un ? ((e.x >> 31) ? (uint32_t)ND : 0u) + dig : 0xFFFFFFFEu;
+            for (uint32_t k = 0; k < nreg; ++k)
+              if (__shfl_sync(0xFFFFFFFFu, rkey, (int)k) == key) g = (int)k;
+          }
+          if (G == 1) {
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, g >= 0);
+            if (bal) {
+              const uint32_t ld = (uint32_t)(__ffs(bal) - 1);
+              uint32_t base = 0;
+              if (lane == ld) base = atomicAdd(&st.nA, (uint32_t)__popc(bal));
+              base = __shfl_sync(0xFFFFFFFFu, base, (int)ld);
+              if (g >= 0) __stcg(gat + base + __popc(bal & lt), e);
+            }
+          } else {
+            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, g);
+            const uint32_t ld = (uint32_t)(__ffs(peers) - 1);
+            uint32_t base = 0;
+            if (g >= 0 && lane == ld) base = atomicAdd(&st.reg_cnt[g], (uint32_t)__popc(peers));
+            base = __shfl_sync(0xFFFFFFFFu, base, (int)ld);
+            const uint32_t off = __shfl_sync(0xFFFFFFFFu, roff, g >= 0 ? g : 0);
+            if (g >= 0) __stcg(gat + off + base + __popc(peers & lt), e);
+          }
+        }
+      }
+    }
+  }
+}
+
 
 // ---------------------------------------------------------------------------------------
 // K4: one warp per chunk: kept test, block id, per-block count / min / max / last row, and

@@ -119,13 +119,27 @@ EncWs enc_ws(uint64_t n, uint64_t nch, uint64_t maxb, uint64_t nhist, uint64_t n
 }
 
 // Chunk-kernel grid: persistent CTAs, as many as can be resident.
+// Fraction of the resident CTA slots a persistent kernel takes (SIF_GRID_FRAC, default 1):
+// below 1 leaves room for kernels of other in-flight batches on other streams.
+double grid_frac() {
+  static double f = -1.0;
+  if (f < 0.0) {
+    const char* e = getenv("SIF_GRID_FRAC");
+    f = e && *e ? atof(e) : 1.0;
+    if (!(f > 0.0 && f <= 1.0)) f = 1.0;
+  }
+  return f;
+}
+
 template <class K>
 int resident_grid(K kfn, int threads, int smem, uint64_t work) {
   int per = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, threads, smem) != cudaSuccess || per < 1) per = 1;
-  return (int)std::max<uint64_t>(1, std::min<uint64_t>(work, (uint64_t)per * num_sms()));
+  const uint64_t slots = std::max<uint64_t>(1, (uint64_t)(per * num_sms() * grid_frac()));
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>(work, slots));
 }
 
+constexpr uint32_t kBigNcand = 131072;  // candidates above which an IF uses the multi-kernel select
 constexpr int kSmemStream = (2 * sif::CH + 2 * sif::ND) * 4;
 constexpr int kSmemSelect = (2 * sif::ND + 2 * sif::HB + sif::GCAP * 4 + 2 * sif::GSM) * 4;
 inline int smem_abq(int maxb) { return (sif::CNT / 32) * maxb * (int)(sizeof(sif::AbqPar) + 16 * 8); }
@@ -249,7 +263,7 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
   p->cap_smem = (int32_t)nhist;
   p->max_blocks = maxb;
   p->tiles = (int32_t)nch;
-  p->flags = atkf;
+  p->flags = atkf | (kmax * 2 > (uint64_t)kBigNcand ? 2 : 0);  // bit 0: ATKF-only, bit 1: multi-kernel select
   p->ws_desc_off = w.info;
   p->ws_aux_off = w.fixedq;
   p->ws_spill_off = w.lists;
@@ -355,11 +369,16 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   a.kept_out = kept;
   a.kept_off = reinterpret_cast<const uint64_t*>(wb + w.keptoff);
   a.tau3 = tau3;
+  // multi-kernel select for IFs with many candidates (one CTA per IF would scan them
+  // alone); enabled when the batch holds an IF whose keep count exceeds half the cut-off
+  a.big_ncand = (p->flags & 2) ? kBigNcand : 0u;
   a.prof = reinterpret_cast<uint64_t*>(getenv("SIF_PROF_PTR") ? strtoull(getenv("SIF_PROF_PTR"), nullptr, 0) : 0ull);
   static bool attrs = false;
   if (!attrs) {
     if (check_cuda(cudaFuncSetAttribute(sif::enc_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemStream)) ||
-        check_cuda(cudaFuncSetAttribute(sif::enc_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
+        check_cuda(cudaFuncSetAttribute(sif::enc_select<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
+        check_cuda(cudaFuncSetAttribute(sif::enc_select<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
+        check_cuda(cudaFuncSetAttribute(sif::enc_select<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
         check_cuda(cudaFuncSetAttribute(sif::enc_abq<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_abq(sif::MAXB))) ||
         check_cuda(cudaFuncSetAttribute(sif::enc_abq<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_abq(sif::MAXB))) ||
         check_cuda(cudaFuncSetAttribute(sif::enc_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pack(sif::MAXB))))
@@ -367,8 +386,9 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
     attrs = true;
   }
   const int maxb = p->max_blocks;
-  static int g_stream = 0, g_members = 0, g_abq = 0, g_pack = 0, g_maxb = -1, g_crc = 0;
+  static int g_stream = 0, g_members = 0, g_abq = 0, g_pack = 0, g_maxb = -1, g_crc = 0, g_gather = 0;
   if (!g_stream) {
+    g_gather = resident_grid(sif::enc_gather<1>, sif::CNT, 0, 1ull << 30);
     g_crc = (int)std::max<uint64_t>(1, (uint64_t)resident_grid(sif::enc_crc, sif::CNT, 0, 1ull << 30));
     g_stream = resident_grid(sif::enc_stream, sif::CNT, kSmemStream, 1ull << 30);
     g_members = resident_grid(sif::enc_members, sif::CNT, 0, 1ull << 30);
@@ -383,7 +403,18 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   const unsigned wgrid = std::max(1u, (nch + sif::CNT / 32 - 1) / (sif::CNT / 32));  // >= 1 chunk per warp
   { ProfScope ps(KP_PREP, s); sif::enc_prep<<<n, 512, 0, s>>>(a); }
   { ProfScope ps(KP_STREAM, s); sif::enc_stream<<<std::min<unsigned>(nch, g_stream), sif::CNT, kSmemStream, s>>>(a); }
-  { ProfScope ps(KP_SELECT, s); sif::enc_select<<<n, sif::SNT, kSmemSelect, s>>>(a); }
+  {
+    ProfScope ps(KP_SELECT, s);
+    sif::enc_select<0><<<n, sif::SNT, kSmemSelect, s>>>(a);
+    if (a.big_ncand) {  // some IF is large enough for the multi-kernel select
+      sif::enc_gather<1><<<std::min<unsigned>(wgrid, g_gather), sif::CNT, 0, s>>>(a);
+      sif::enc_select<1><<<n, sif::SNT, kSmemSelect, s>>>(a);
+      if (!atkf) {
+        sif::enc_gather<2><<<std::min<unsigned>(wgrid, g_gather), sif::CNT, 0, s>>>(a);
+        sif::enc_select<2><<<n, sif::SNT, kSmemSelect, s>>>(a);
+      }
+    }
+  }
   if (!atkf) {
     { ProfScope ps(KP_MEMBERS, s); sif::enc_members<<<std::min<unsigned>(wgrid, g_members), sif::CNT, 0, s>>>(a); }
     if (c->mode != SIF_MODE_FIXED) {
@@ -399,7 +430,7 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
 
 int sif_enc_run(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint64_t* out_len, int32_t* status, void* stream) {
   if (!p || !c || !ws || !out_len || !status) return SIF_ERR_INVALID_ARG;
-  if (p->flags) return SIF_ERR_INVALID_ARG;  // an ATKF-only plan
+  if (p->flags & 1) return SIF_ERR_INVALID_ARG;  // an ATKF-only plan
   return enc_launch(p, c, ws, out_len, status, 0, nullptr, nullptr, (cudaStream_t)stream);
 }
 
