@@ -170,6 +170,9 @@ __device__ __noinline__ double plus_value(const uint32_t* tab, const uint8_t* in
 // stores.
 __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
   extern __shared__ __align__(16) uint8_t dsm_raw[];
+  __shared__ uint4 pa[DNT / 32][32], pb[DNT / 32][32];
+  __shared__ uint2 pc[DNT / 32][32];
+  __shared__ uint8_t own[DNT / 32][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t segw = (uint32_t)a.segw;
   const uint32_t bmw = (segw + 31) / 32;
@@ -229,7 +232,7 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
       const uint32_t pi = g0 + lane;
       const bool has = pi < g1;
       uint32_t q = 1, lo = 0, hi = 0, rs0 = 0, ri = 0;
-      double o = 1.0, vmin = 0.0;
+      float o = 1.0f, vmin = 0.0f;
       uint64_t cbit = 0, qbit = 0;
       if (has) {
         const uint32_t b = pi / nr;
@@ -238,8 +241,8 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
         const uint32_t* row = tab + (2ull + b) * TROW_U32;
         q = row[0];
         const uint32_t nnz = row[1];
-        o = (double)__uint_as_float(row[2]);
-        vmin = (double)__uint_as_float(row[3]);
+        o = __uint_as_float(row[2]);
+        vmin = __uint_as_float(row[3]);
         const uint64_t rpo = (uint64_t)row[4] | ((uint64_t)row[5] << 32);
         cbit = 8ull * ((uint64_t)row[6] | ((uint64_t)row[7] << 32));
         qbit = 8ull * ((uint64_t)row[8] | ((uint64_t)row[9] << 32));
@@ -272,28 +275,30 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
       const uint32_t inc = warp_incl_scan_u32(cnt);
       const uint32_t M = __shfl_sync(0xFFFFFFFFu, inc, 31);
       const uint32_t exc = inc - cnt;
-      const uint32_t ng = g1 - g0;
+      // pair parameters staged in shared memory: one LDS.128 pair per entry instead of a
+      // dozen shuffles (and no registers held across the entry windows)
+      pa[w][lane] = make_uint4((uint32_t)cbit, (uint32_t)(cbit >> 32), (uint32_t)qbit, (uint32_t)(qbit >> 32));
+      pb[w][lane] = make_uint4(lo - exc, q, __float_as_uint(o), __float_as_uint(vmin));
+      pc[w][lane] = make_uint2(rs0, ri);
       for (uint32_t m0 = 0; m0 < M; m0 += 32) {
         const uint32_t m = m0 + lane;
-        // pair of entry m: last pair whose exclusive prefix is <= m (binary search via shuffles)
-        uint32_t jl = 0;
-        {
-          uint32_t a0 = 0, a1 = ng - 1;
-#pragma unroll
-          for (int step = 0; step < 5; ++step) {
-            const uint32_t mid = (a0 + a1 + 1) >> 1;
-            const uint32_t v = __shfl_sync(0xFFFFFFFFu, exc, (int)mid);
-            if (a0 < a1) { if (v <= m) a0 = mid; else a1 = mid - 1; }
-          }
-          jl = a0;
-        }
-        const uint32_t e = __shfl_sync(0xFFFFFFFFu, lo, (int)jl) + (m - __shfl_sync(0xFFFFFFFFu, exc, (int)jl));
-        const uint64_t cbj = __shfl_sync(0xFFFFFFFFu, cbit, (int)jl);
-        const uint64_t qbj = __shfl_sync(0xFFFFFFFFu, qbit, (int)jl);
-        const uint32_t qj = __shfl_sync(0xFFFFFFFFu, q, (int)jl);
-        const double oj = __shfl_sync(0xFFFFFFFFu, o, (int)jl), vj = __shfl_sync(0xFFFFFFFFu, vmin, (int)jl);
-        const uint32_t rsj = __shfl_sync(0xFFFFFFFFu, rs0, (int)jl);
-        const uint32_t rij = __shfl_sync(0xFFFFFFFFu, ri, (int)jl);
+        // owner of entry m: the last pair (with entries) starting at or before m in this
+        // window; window position 0 is owned by the pair covering m0
+        const uint32_t st0 = max(exc, m0);
+        const bool starts = cnt != 0 && st0 < inc && st0 < m0 + 32u;
+        if (starts) own[w][st0 - m0] = (uint8_t)lane;
+        const uint32_t smask = __reduce_or_sync(0xFFFFFFFFu, starts ? 1u << (st0 - m0) : 0u);
+        __syncwarp();
+        const uint32_t src = 31u - __clz(smask & (0xFFFFFFFFu >> (31 - lane)));
+        const uint32_t jl = own[w][src];
+        const uint4 A = pa[w][jl];
+        const uint4 B = pb[w][jl];
+        const uint2 C = pc[w][jl];
+        const uint64_t cbj = (uint64_t)A.x | ((uint64_t)A.y << 32);
+        const uint64_t qbj = (uint64_t)A.z | ((uint64_t)A.w << 32);
+        const uint32_t e = B.x + m;
+        const uint32_t qj = B.y;
+        const uint32_t rsj = C.x, rij = C.y;
         const uint32_t col = m < M ? ld_field(in, cbj + (uint64_t)e * cb, cb) : 0u;
         // the previous entry e-1 of the same pair sits in the previous lane of this window
         const uint32_t colp = __shfl_up_sync(0xFFFFFFFFu, col, 1);
@@ -311,7 +316,8 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
               const uint32_t old = atomicOr(bm + plane * bmw + (pos >> 5), 1u << (pos & 31));
               if (old & (1u << (pos & 31))) fl |= FLAG_CORRUPT;  // codec.py:248-250 (overlap)
               const uint32_t code = ld_field(in, qbj + (uint64_t)e * qj, qj);
-              const double v = __dadd_rn(__dmul_rn((double)code, oj), vj);
+              const double v = __dadd_rn(__dmul_rn((double)code, (double)__uint_as_float(B.z)),
+                                         (double)__uint_as_float(B.w));
               if (plane == 0) {
                 buf[pos] = __double2float_rn(v);  // f32(0 + v)
               } else if ((bm[pos >> 5] >> (pos & 31)) & 1u) {
@@ -325,6 +331,7 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
             }
           }
         }
+        __syncwarp();
       }
       __syncwarp();
       g0 = g1;
