@@ -161,13 +161,14 @@ __device__ __noinline__ double plus_value(const uint32_t* tab, const uint8_t* in
 // ------------------------------------------------------------------------------- scatter
 // Work item = (stream, row group, column segment): R = max(1, segw / K) consecutive rows of
 // at most segw columns; a warp owns a contiguous range of items.  Lanes hold one (block,
-// row) pair each (pairs block-major, in groups of 32 that never span both planes): block
-// metadata and the row's entry range.  The pairs' entries are unpacked 32 at a time
-// (cols, codes), validated (codec.py:238-250), dequantized in float64 (quant.py:67-73)
-// into a per-warp fp32 buffer: an element held by one plane is f32(0 +/- v), exactly the
-// reference's f64 scatter-add rounded to fp32 (codec.py:257-266); an element held by both
-// planes is summed in float64 (plus value recovered from its block).  Stored with 16-byte
-// stores.
+// row) pair each (pairs block-major, plus blocks first, in groups of 32): block metadata
+// and the row's entry range, staged in shared memory.  The pairs' entries are unpacked 32
+// at a time (cols, codes), validated (codec.py:238-250), dequantized in float64
+// (quant.py:67-73) into a per-warp fp32 buffer: an element held by one plane is
+// f32(0 +/- v), exactly the reference's f64 scatter-add rounded to fp32 (codec.py:257-266);
+// an element held by both planes is summed in float64 (plus value recovered from its
+// block).  Within a window plus entries are written before minus entries.  The buffer is
+// stored with 16-byte streaming stores and re-zeroed in the same pass.
 __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
   extern __shared__ __align__(16) uint8_t dsm_raw[];
   __shared__ uint4 pa[DNT / 32][32], pb[DNT / 32][32];
@@ -179,19 +180,21 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
   float* buf = reinterpret_cast<float*>(dsm_raw) + (size_t)w * segw;
   uint32_t* bm = reinterpret_cast<uint32_t*>(reinterpret_cast<float*>(dsm_raw) + (size_t)(DNT / 32) * segw) +
                  (size_t)w * 2 * bmw;
+  for (uint32_t k = 4 * lane; k < segw; k += 128) *reinterpret_cast<float4*>(buf + k) = make_float4(0.f, 0.f, 0.f, 0.f);
   const uint64_t GW = (uint64_t)gridDim.x * (DNT / 32);
   const uint64_t gw = (uint64_t)blockIdx.x * (DNT / 32) + w;
   const uint64_t nitems = a.item_base[a.n];
   const uint64_t i0 = nitems * gw / GW, i1 = nitems * (gw + 1) / GW;
   int cur = -1;
   uint32_t N = 0, K = 0, mp = 0, nb = 0, nsegr = 1, cb = 1, R = 1;
+  uint64_t ib0 = 0, ib1 = 0;
   bool ok = false;
   const uint32_t* tab = nullptr;
   const uint8_t* in = nullptr;
   float* out = nullptr;
   uint32_t fl = 0;
   for (uint64_t it = i0; it < i1; ++it) {
-    if (cur < 0 || it >= a.item_base[cur + 1]) {
+    if (cur < 0 || it >= ib1) {
       if (cur >= 0) {
         fl = __reduce_or_sync(0xFFFFFFFFu, fl);
         if (lane == 0 && fl) atomicOr(a.acc + 4ull * cur + 1, fl);
@@ -203,6 +206,8 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
         if (a.item_base[mid] <= it) lo = mid; else hi = mid - 1;
       }
       cur = lo;
+      ib0 = a.item_base[cur];
+      ib1 = a.item_base[cur + 1];
       const sif_dec_desc d = a.descs[cur];
       tab = a.table + (uint64_t)cur * a.table_stride;
       const uint32_t walk = tab[0], pre = tab[TROW_U32 + 0];
@@ -215,46 +220,40 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
       cb = col_bits(K);
     }
     if (!ok) continue;
-    const uint64_t li = it - a.item_base[cur];
-    const uint32_t rg = (uint32_t)(li / nsegr), sg = (uint32_t)(li - (uint64_t)rg * nsegr);
+    const uint64_t li = it - ib0;
+    uint32_t rg, sg;
+    if (nsegr == 1) { rg = (uint32_t)li; sg = 0; }
+    else { rg = (uint32_t)(li / nsegr); sg = (uint32_t)(li - (uint64_t)rg * nsegr); }
     const uint32_t r0 = rg * R, nr = min(R, N - r0);
     const uint32_t c0 = sg * segw, c1 = min(K, c0 + segw), W = c1 - c0;
     const uint32_t span = nr * W;  // buffer elements (rows are contiguous when nsegr == 1)
-    for (uint32_t k = 4 * lane; k < span; k += 128) *reinterpret_cast<float4*>(buf + k) = make_float4(0.f, 0.f, 0.f, 0.f);
     for (uint32_t k = lane; k < 2 * bmw; k += 32) bm[k] = 0;
     __syncwarp();
+    bool nf0 = false;  // a plus-plane value rounded to a non-finite fp32 (re-checked at the store)
     const uint32_t np = nb * nr;       // (block, row) pairs, block-major
-    const uint32_t npp = mp * nr;      // plus-plane pairs
-    for (uint32_t g0 = 0; g0 < np;) {
-      uint32_t g1 = min(np, g0 + 32u);
-      if (g0 < npp && g1 > npp) g1 = npp;  // a group never spans both planes
-      const int plane = g0 < npp ? 0 : 1;
+    for (uint32_t g0 = 0; g0 < np; g0 += 32) {
+      const uint32_t g1 = min(np, g0 + 32u);
       const uint32_t pi = g0 + lane;
-      const bool has = pi < g1;
-      uint32_t q = 1, lo = 0, hi = 0, rs0 = 0, ri = 0;
-      float o = 1.0f, vmin = 0.0f;
-      uint64_t cbit = 0, qbit = 0;
-      if (has) {
+      uint32_t cnt = 0;
+      if (pi < g1) {
         const uint32_t b = pi / nr;
-        ri = pi - b * nr;
+        const uint32_t ri = pi - b * nr;
         const uint32_t r = r0 + ri;
-        const uint32_t* row = tab + (2ull + b) * TROW_U32;
-        q = row[0];
-        const uint32_t nnz = row[1];
-        o = __uint_as_float(row[2]);
-        vmin = __uint_as_float(row[3]);
-        const uint64_t rpo = (uint64_t)row[4] | ((uint64_t)row[5] << 32);
-        cbit = 8ull * ((uint64_t)row[6] | ((uint64_t)row[7] << 32));
-        qbit = 8ull * ((uint64_t)row[8] | ((uint64_t)row[9] << 32));
+        const uint4* row4 = reinterpret_cast<const uint4*>(tab + (2ull + b) * TROW_U32);
+        const uint4 m0v = row4[0], m1v = row4[1];
+        const uint32_t q = m0v.x, nnz = m0v.y;
+        const uint64_t rpo = (uint64_t)m1v.x | ((uint64_t)m1v.y << 32);
+        const uint64_t cbit = 8ull * ((uint64_t)m1v.z | ((uint64_t)m1v.w << 32));
+        const uint2 m2v = *reinterpret_cast<const uint2*>(tab + (2ull + b) * TROW_U32 + 8);
+        const uint64_t qbit = 8ull * ((uint64_t)m2v.x | ((uint64_t)m2v.y << 32));
         const uint32_t p0 = ld_u32_le(in, rpo + 4ull * r), p1 = ld_u32_le(in, rpo + 4ull * (r + 1));
         if (sg == 0) {
           if (p1 < p0) fl |= FLAG_CORRUPT;  // codec.py:238-241
           if (r == 0 && p0 != 0) fl |= FLAG_CORRUPT;
           if (r + 1 == N && p1 != nnz) fl |= FLAG_CORRUPT;
         }
-        lo = min(p0, nnz);
-        hi = max(lo, min(p1, nnz));
-        rs0 = lo;
+        uint32_t lo = min(p0, nnz), hi = max(lo, min(p1, nnz));
+        const uint32_t rs0 = lo;
         if (nsegr > 1) {
           // entries of this column segment: lower bounds of c0 and c1 among the row's cols
           auto lb = [&](uint32_t cv) {
@@ -270,16 +269,16 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
           lo = l0;
           hi = max(l0, l1);
         }
+        cnt = hi - lo;
+        // pair parameters in shared memory (entry base stored as lo - exclusive prefix)
+        pa[w][lane] = make_uint4((uint32_t)cbit, (uint32_t)(cbit >> 32), (uint32_t)qbit, (uint32_t)(qbit >> 32));
+        pb[w][lane] = make_uint4(lo, q, m0v.z, m0v.w);
+        pc[w][lane] = make_uint2(rs0, ri | (b >= mp ? 0x80000000u : 0u));
       }
-      const uint32_t cnt = hi - lo;
       const uint32_t inc = warp_incl_scan_u32(cnt);
       const uint32_t M = __shfl_sync(0xFFFFFFFFu, inc, 31);
       const uint32_t exc = inc - cnt;
-      // pair parameters staged in shared memory: one LDS.128 pair per entry instead of a
-      // dozen shuffles (and no registers held across the entry windows)
-      pa[w][lane] = make_uint4((uint32_t)cbit, (uint32_t)(cbit >> 32), (uint32_t)qbit, (uint32_t)(qbit >> 32));
-      pb[w][lane] = make_uint4(lo - exc, q, __float_as_uint(o), __float_as_uint(vmin));
-      pc[w][lane] = make_uint2(rs0, ri);
+      if (pi < g1) pb[w][lane].x -= exc;
       for (uint32_t m0 = 0; m0 < M; m0 += 32) {
         const uint32_t m = m0 + lane;
         // owner of entry m: the last pair (with entries) starting at or before m in this
@@ -295,61 +294,76 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
         const uint4 B = pb[w][jl];
         const uint2 C = pc[w][jl];
         const uint64_t cbj = (uint64_t)A.x | ((uint64_t)A.y << 32);
-        const uint64_t qbj = (uint64_t)A.z | ((uint64_t)A.w << 32);
         const uint32_t e = B.x + m;
-        const uint32_t qj = B.y;
-        const uint32_t rsj = C.x, rij = C.y;
+        const uint32_t rij = C.y & 0x7FFFFFFFu;
+        const bool minus = (C.y >> 31) != 0;
         const uint32_t col = m < M ? ld_field(in, cbj + (uint64_t)e * cb, cb) : 0u;
         // the previous entry e-1 of the same pair sits in the previous lane of this window
         const uint32_t colp = __shfl_up_sync(0xFFFFFFFFu, col, 1);
         const uint32_t jlp = __shfl_up_sync(0xFFFFFFFFu, jl, 1);
+        bool wr = false;
+        uint32_t pos = 0;
+        double v = 0.0;
         if (m < M) {
           if (col >= K) fl |= FLAG_CORRUPT;  // codec.py:242-243
           else {
             // strictly increasing within the row (codec.py:244-247)
-            if (e > rsj) {
+            if (e > C.x) {
               const uint32_t prev = (lane > 0 && jlp == jl) ? colp : ld_field(in, cbj + (uint64_t)(e - 1) * cb, cb);
               if (prev >= col) fl |= FLAG_CORRUPT;
             }
             if (col >= c0 && col < c1) {
-              const uint32_t pos = rij * W + (col - c0);
-              const uint32_t old = atomicOr(bm + plane * bmw + (pos >> 5), 1u << (pos & 31));
+              wr = true;
+              pos = rij * W + (col - c0);
+              const uint32_t old = atomicOr(bm + (minus ? bmw : 0u) + (pos >> 5), 1u << (pos & 31));
               if (old & (1u << (pos & 31))) fl |= FLAG_CORRUPT;  // codec.py:248-250 (overlap)
-              const uint32_t code = ld_field(in, qbj + (uint64_t)e * qj, qj);
-              const double v = __dadd_rn(__dmul_rn((double)code, (double)__uint_as_float(B.z)),
-                                         (double)__uint_as_float(B.w));
-              if (plane == 0) {
-                buf[pos] = __double2float_rn(v);  // f32(0 + v)
-              } else if ((bm[pos >> 5] >> (pos & 31)) & 1u) {
-                // both planes hold this element: the reference sums them in float64
-                // (codec.py:257-266); recover the plus value from its plus block entry
-                const double pv = plus_value(tab, in, mp, r0 + rij, col, cb);
-                buf[pos] = __double2float_rn(__dsub_rn(pv, v));
-              } else {
-                buf[pos] = __double2float_rn(-v);  // f32(0 - v)
+              const uint64_t qbj = (uint64_t)A.z | ((uint64_t)A.w << 32);
+              const uint32_t code = ld_field(in, qbj + (uint64_t)e * B.y, B.y);
+              v = __dadd_rn(__dmul_rn((double)code, (double)__uint_as_float(B.z)), (double)__uint_as_float(B.w));
+              if (!minus) {
+                const float f = __double2float_rn(v);  // f32(0 + v)
+                buf[pos] = f;
+                nf0 |= (__float_as_uint(f) & 0x7F800000u) == 0x7F800000u;
               }
             }
           }
         }
+        __syncwarp();  // plus entries of this window land before the minus entries read them
+        if (wr && minus) {
+          float f;
+          if ((bm[pos >> 5] >> (pos & 31)) & 1u) {
+            // both planes hold this element: the reference sums them in float64
+            // (codec.py:257-266); recover the plus value from its plus block entry
+            const double pv = plus_value(tab, in, mp, r0 + rij, col, cb);
+            f = __double2float_rn(__dsub_rn(pv, v));
+          } else {
+            f = __double2float_rn(-v);  // f32(0 - v)
+          }
+          buf[pos] = f;
+          if ((__float_as_uint(f) & 0x7F800000u) == 0x7F800000u) fl |= FLAG_NONFINITE;
+        }
         __syncwarp();
       }
-      __syncwarp();
-      g0 = g1;
     }
-    // round to fp32 and store (nr full rows, or one row segment)
+    // store (nr full rows, or one row segment) and re-zero the buffer
+    const bool chk = __any_sync(0xFFFFFFFFu, nf0);
     float* dst = out + (uint64_t)r0 * K + c0;
     uint32_t bad = 0;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
     if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && (span & 3u) == 0) {
       for (uint32_t k = 4 * lane; k < span; k += 128) {
         const float4 f = *reinterpret_cast<const float4*>(buf + k);
-        bad |= ((__float_as_uint(f.x) & 0x7F800000u) == 0x7F800000u) | ((__float_as_uint(f.y) & 0x7F800000u) == 0x7F800000u) |
-               ((__float_as_uint(f.z) & 0x7F800000u) == 0x7F800000u) | ((__float_as_uint(f.w) & 0x7F800000u) == 0x7F800000u);
+        *reinterpret_cast<float4*>(buf + k) = z4;
+        if (chk)
+          bad |= ((__float_as_uint(f.x) & 0x7F800000u) == 0x7F800000u) | ((__float_as_uint(f.y) & 0x7F800000u) == 0x7F800000u) |
+                 ((__float_as_uint(f.z) & 0x7F800000u) == 0x7F800000u) | ((__float_as_uint(f.w) & 0x7F800000u) == 0x7F800000u);
         __stcs(reinterpret_cast<float4*>(dst + k), f);
       }
     } else {
       for (uint32_t k = lane; k < span; k += 32) {
         const float f = buf[k];
-        bad |= (__float_as_uint(f) & 0x7F800000u) == 0x7F800000u;
+        buf[k] = 0.f;
+        if (chk) bad |= (__float_as_uint(f) & 0x7F800000u) == 0x7F800000u;
         __stcs(dst + k, f);
       }
     }

@@ -33,6 +33,50 @@ def cif(rows, cols, plus, minus):
                         blocks_minus=tuple(minus))
 
 
+def _random_cif(rows, cols, mp, mm, dens, seed, break_at=None):
+    """Random planes with cross-plane overlaps; break_at swaps two cols around that column
+    of one minus row (non-increasing -> CorruptStreamError)."""
+    rng = np.random.default_rng(seed)
+
+    def plane(m, minus):
+        out = []
+        for bi in range(m):
+            q = int(rng.integers(1, 17))
+            rp, cs, codes = [0], [], []
+            for r in range(rows):
+                cc = np.sort(rng.choice(cols, size=int(rng.binomial(cols, dens / m)), replace=False))
+                if minus and break_at is not None and bi == 0 and r == 1 and len(cc) > 2:
+                    j = int(np.searchsorted(cc, break_at))
+                    j = min(max(j, 1), len(cc) - 1)
+                    cc[j - 1], cc[j] = cc[j], cc[j - 1]
+                cs += [int(c) for c in cc]
+                codes += [int(x) for x in rng.integers(0, 1 << q, size=len(cc))]
+                rp.append(len(cs))
+            out.append(blk(q, float(rng.uniform(0.01, 2)), float(rng.uniform(0, 3)), rp, cs, codes))
+        return out
+
+    # blocks of a plane must not overlap each other: carve one plane's columns per block
+    def disjoint(m, minus):
+        bl = plane(m, minus)
+        seen = [set() for _ in range(rows)]
+        fixed = []
+        for b in bl:
+            rp, cs, codes = [0], [], []
+            for r in range(rows):
+                for k in range(int(b.row_ptr[r]), int(b.row_ptr[r + 1])):
+                    c = int(b.cols[k])
+                    if c in seen[r] and not (break_at is not None and minus):
+                        continue
+                    seen[r].add(c)
+                    cs.append(c)
+                    codes.append(int(b.codes[k]))
+                rp.append(len(cs))
+            fixed.append(blk(b.q, b.o, b.v_min, rp, cs, codes))
+        return fixed
+
+    return cif(rows, cols, disjoint(mp, False), disjoint(mm, True))
+
+
 CASES = {
     # plus and minus planes share (0,1) and (2,3): float64 sums, not an error
     "cross_plane_overlap": cif(3, 5, [blk(8, 0.0123, 0.5, [0, 2, 2, 3], [1, 4, 3], [200, 7, 255])],
@@ -46,6 +90,15 @@ CASES = {
     "cols_not_increasing": cif(2, 8, [blk(4, 0.25, 0.0, [0, 2, 2], [5, 3], [1, 2])], [blk(8, 1.0, 0.0, [0, 0, 0], [], [])]),
     "cols_equal": cif(1, 8, [blk(4, 0.25, 0.0, [0, 2], [4, 4], [1, 2])], [blk(8, 1.0, 0.0, [0, 0], [], [])]),
     "col_ge_K": cif(2, 6, [blk(4, 0.25, 0.0, [0, 1, 2], [2, 7], [1, 2])], [blk(8, 1.0, 0.0, [0, 0, 0], [], [])]),
+    # plus value rounds to an infinite fp32 alone, but the float64 plane sum is finite
+    "cross_plane_inf_cancel": cif(1, 6, [blk(8, 3.0e38, 0.0, [0, 2], [1, 4], [255, 1])],
+                                  [blk(8, 3.0e38, 0.0, [0, 1], [1], [254])]),
+    "plus_inf": cif(1, 6, [blk(8, 3.0e38, 0.0, [0, 1], [2], [255])], [blk(8, 1.0, 0.0, [0, 0], [], [])]),
+    "minus_inf": cif(1, 6, [blk(8, 1.0, 0.0, [0, 0], [], [])], [blk(8, 3.0e38, 0.0, [0, 1], [2], [255])]),
+    # rows wider than a decode work item (column segments) and many (block, row) pairs
+    "wide_rows": _random_cif(3, 2500, 3, 2, 0.2, 11),
+    "many_pairs": _random_cif(70, 7, 4, 3, 0.5, 12),
+    "wide_rows_bad": _random_cif(3, 2500, 3, 2, 0.2, 13, break_at=1900),
 }
 
 
