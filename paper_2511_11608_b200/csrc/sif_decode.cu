@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
     const uint32_t span = nr * W;  // buffer elements (rows are contiguous when nsegr == 1)
     for (uint32_t k = lane; k < 2 * bmw; k += 32) bm[k] = 0;
     __syncwarp();
-    bool nf0 = false;  // a plus-plane value rounded to a non-finite fp32 (re-checked at the store)
+    uint32_t nf0 = 0;  // a plus-plane value rounded to a non-finite fp32 (re-checked at the store)
     const uint32_t np = nb * nr;       // (block, row) pairs, block-major
     for (uint32_t g0 = 0; g0 < np; g0 += 32) {
       const uint32_t g1 = min(np, g0 + 32u);
@@ -279,6 +279,7 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
       const uint32_t M = __shfl_sync(0xFFFFFFFFu, inc, 31);
       const uint32_t exc = inc - cnt;
       if (pi < g1) pb[w][lane].x -= exc;
+      uint32_t lastcol = 0, lastjl = 0xFFFFFFFFu;
       for (uint32_t m0 = 0; m0 < M; m0 += 32) {
         const uint32_t m = m0 + lane;
         // owner of entry m: the last pair (with entries) starting at or before m in this
@@ -297,10 +298,20 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
         const uint32_t e = B.x + m;
         const uint32_t rij = C.y & 0x7FFFFFFFu;
         const bool minus = (C.y >> 31) != 0;
-        const uint32_t col = m < M ? ld_field(in, cbj + (uint64_t)e * cb, cb) : 0u;
+        // col and code fields are fetched together (one memory round trip per window)
+        const uint64_t qbj = (uint64_t)A.z | ((uint64_t)A.w << 32);
+        uint32_t col = 0, code = 0;
+        if (m < M) {
+          col = ld_field(in, cbj + (uint64_t)e * cb, cb);
+          code = ld_field(in, qbj + (uint64_t)e * B.y, B.y);
+        }
         // the previous entry e-1 of the same pair sits in the previous lane of this window
-        const uint32_t colp = __shfl_up_sync(0xFFFFFFFFu, col, 1);
-        const uint32_t jlp = __shfl_up_sync(0xFFFFFFFFu, jl, 1);
+        // (lane 0: the last lane of the previous window)
+        uint32_t colp = __shfl_up_sync(0xFFFFFFFFu, col, 1);
+        uint32_t jlp = __shfl_up_sync(0xFFFFFFFFu, jl, 1);
+        if (lane == 0) { colp = lastcol; jlp = lastjl; }
+        lastcol = __shfl_sync(0xFFFFFFFFu, col, 31);
+        lastjl = __shfl_sync(0xFFFFFFFFu, jl, 31);
         bool wr = false;
         uint32_t pos = 0;
         double v = 0.0;
@@ -309,7 +320,7 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
           else {
             // strictly increasing within the row (codec.py:244-247)
             if (e > C.x) {
-              const uint32_t prev = (lane > 0 && jlp == jl) ? colp : ld_field(in, cbj + (uint64_t)(e - 1) * cb, cb);
+              const uint32_t prev = jlp == jl ? colp : ld_field(in, cbj + (uint64_t)(e - 1) * cb, cb);
               if (prev >= col) fl |= FLAG_CORRUPT;
             }
             if (col >= c0 && col < c1) {
@@ -317,13 +328,11 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
               pos = rij * W + (col - c0);
               const uint32_t old = atomicOr(bm + (minus ? bmw : 0u) + (pos >> 5), 1u << (pos & 31));
               if (old & (1u << (pos & 31))) fl |= FLAG_CORRUPT;  // codec.py:248-250 (overlap)
-              const uint64_t qbj = (uint64_t)A.z | ((uint64_t)A.w << 32);
-              const uint32_t code = ld_field(in, qbj + (uint64_t)e * B.y, B.y);
               v = __dadd_rn(__dmul_rn((double)code, (double)__uint_as_float(B.z)), (double)__uint_as_float(B.w));
               if (!minus) {
                 const float f = __double2float_rn(v);  // f32(0 + v)
                 buf[pos] = f;
-                nf0 |= (__float_as_uint(f) & 0x7F800000u) == 0x7F800000u;
+                nf0 |= (__float_as_uint(f) & 0x7F800000u) == 0x7F800000u ? 1u : 0u;
               }
             }
           }
@@ -346,7 +355,7 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
       }
     }
     // store (nr full rows, or one row segment) and re-zero the buffer
-    const bool chk = __any_sync(0xFFFFFFFFu, nf0);
+    const bool chk = __any_sync(0xFFFFFFFFu, nf0 != 0);
     float* dst = out + (uint64_t)r0 * K + c0;
     uint32_t bad = 0;
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
