@@ -153,6 +153,15 @@ const char* sif_profile_kernel_name(int k);
 int sif_gen_synthetic(void* d_x, uint32_t rows, uint32_t cols, uint32_t dtype, uint32_t kind,
                       uint64_t sid, void* stream);
 
+/* ---- fixture tensors and .tns validation ----
+ * sif_fixture_tensor: random_tensor(rows, cols, seed, dist) values (tensor.py:90-111,
+ * rng.py:30-52) for n = rows*cols fp32 elements; dist 0 = "uniform" (bit-identical),
+ * 1 = "gaussian" (CUDA log/sin/cos; see sif_synth.cu).
+ * sif_count_nonfinite: number of NaN/Inf elements of x into *d_count (device u64), the
+ * finiteness check of load_tensor / DenseTensor (tensor.py:35-36, :84-85). */
+int sif_fixture_tensor(float* d_x, uint64_t n, uint64_t seed, int dist, void* stream);
+int sif_count_nonfinite(const float* d_x, uint64_t n, unsigned long long* d_count, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

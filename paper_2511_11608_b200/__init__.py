@@ -36,6 +36,9 @@ from .codec import (
     synthetic,
 )
 from . import shard
+from .stats import payload_upper_bound, stats
+from .tensor import load_tensor, random_tensor, save_tensor
+from .timemodel import DeviceTimeModel
 from .errors import (
     CapacityError,
     ConfigError,

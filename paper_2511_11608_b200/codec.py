@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import ConfigError, NonFiniteError, ShapeError, raise_for
+from .errors import _BY_STATUS, ConfigError, NonFiniteError, ShapeError, SlicerError, raise_for, reason_message
 
 Q_MAX = 16
 MODE_ABQ = "abq"
@@ -368,7 +368,15 @@ class BatchDecoder:
         st = self.status.cpu().numpy()
         bad = np.flatnonzero(st != 0)
         if bad.size:
-            raise_for(int(st[bad[0]]), f"stream {int(bad[0])} of the batch")
+            i = int(bad[0])
+            t = self.table(i)
+            msg = reason_message(int(t[1, 7]), int(t[1, 8]), struct.pack("<I", int(t[1, 9])), int(t[0, 1]),
+                                 int(t[0, 2]))
+            if msg is None:
+                raise_for(int(st[i]), f"stream {i} of the batch")
+            if self.B > 1:
+                msg += f" (stream {i} of the batch)"
+            raise _BY_STATUS.get(int(st[i]), SlicerError)(msg)
         return self
 
     def table(self, i: int) -> np.ndarray:

@@ -20,6 +20,13 @@ namespace sif {
 constexpr int DNT = 256;
 constexpr int TROW_U32 = 16;  // table row: 16 x u32 = 64 bytes
 constexpr uint32_t FLAG_CORRUPT = 1u, FLAG_NONFINITE = 2u;
+// Failure reasons (table row 1, words 4..8) so the host can raise the reference's message
+// (codec.py:320-385, :235-251, tensor.py:27-36); see errors.py REASONS.
+enum : uint32_t {
+  R_NONE = 0, R_SHORT = 1, R_MAGIC = 2, R_CRC = 3, R_VERSION = 4, R_MODE = 5, R_QVEC = 6, R_BLKHDR = 7,
+  R_QRANGE = 8, R_BLKPAY = 9, R_TRAIL = 10, R_CAPACITY = 11, R_SHAPE_MISMATCH = 12, R_CORRUPT = 16,
+  R_SHAPE = 32, R_NONFINITE = 33
+};
 
 struct DecArgs {
   const sif_dec_desc* descs;
@@ -50,8 +57,9 @@ __global__ void sif_parse_kernel(DecArgs a) {
   const uint64_t len = d.in_len;
   const uint64_t max_rows = a.table_stride / TROW_U32 - 2;
   uint32_t pre = 0, walk = 0, N = 0, K = 0, mp = 0, mm = 0, mode = 0, qb = 0, nb = 0, crc = 0;
-  if (len < (uint64_t)(kHeaderBytes + kCrcBytes)) pre = SIF_ERR_STREAM_FORMAT;  // codec.py:321
-  else if (in[0] != 'S' || in[1] != 'I' || in[2] != 'F' || in[3] != '1') pre = SIF_ERR_STREAM_FORMAT;
+  uint32_t pre_r = R_NONE, walk_r = R_NONE, walk_x = 0;
+  if (len < (uint64_t)(kHeaderBytes + kCrcBytes)) { pre = SIF_ERR_STREAM_FORMAT; pre_r = R_SHORT; }  // codec.py:321
+  else if (in[0] != 'S' || in[1] != 'I' || in[2] != 'F' || in[3] != '1') { pre = SIF_ERR_STREAM_FORMAT; pre_r = R_MAGIC; }
   if (!pre) {
     crc = rd_u32(in, len - 4);
     const uint32_t ver = (uint32_t)in[4] | ((uint32_t)in[5] << 8);
@@ -61,26 +69,26 @@ __global__ void sif_parse_kernel(DecArgs a) {
     mode = in[27];
     mp = (uint32_t)in[28] | ((uint32_t)in[29] << 8);
     mm = (uint32_t)in[30] | ((uint32_t)in[31] << 8);
-    if (ver != 1) walk = SIF_ERR_STREAM_FORMAT;  // codec.py:331-332
-    else if (mode > 1) walk = SIF_ERR_STREAM_FORMAT;  // codec.py:333-334
+    if (ver != 1) { walk = SIF_ERR_STREAM_FORMAT; walk_r = R_VERSION; walk_x = ver; }  // codec.py:331-332
+    else if (mode > 1) { walk = SIF_ERR_STREAM_FORMAT; walk_r = R_MODE; walk_x = mode; }  // codec.py:333-334
     else {
       uint64_t pos = kHeaderBytes;
       if (mode == 1) {
-        if (len < pos + mp + mm) walk = SIF_ERR_STREAM_FORMAT;  // codec.py:340-341
+        if (len < pos + mp + mm) { walk = SIF_ERR_STREAM_FORMAT; walk_r = R_QVEC; }  // codec.py:340-341
         pos += mp + mm;
       }
       const uint32_t cb = col_bits(K);
       const uint64_t nblk = (uint64_t)mp + mm;
       for (uint64_t b = 0; b < nblk && !walk; ++b) {
-        if (len < pos + kBlockMetaBytes + 4ull * ((uint64_t)N + 1)) { walk = SIF_ERR_STREAM_FORMAT; break; }
+        if (len < pos + kBlockMetaBytes + 4ull * ((uint64_t)N + 1)) { walk = SIF_ERR_STREAM_FORMAT; walk_r = R_BLKHDR; break; }
         const uint32_t q = in[pos];
-        if (q < 1 || q > (uint32_t)kQMax) { walk = SIF_ERR_CORRUPT_STREAM; break; }  // codec.py:351-352
+        if (q < 1 || q > (uint32_t)kQMax) { walk = SIF_ERR_CORRUPT_STREAM; walk_r = R_QRANGE; walk_x = q; break; }  // :351-352
         const uint32_t o = rd_u32(in, pos + 1), vmin = rd_u32(in, pos + 5), nnz = rd_u32(in, pos + 9);
         const uint64_t rp = pos + kBlockMetaBytes;
         pos = rp + 4ull * ((uint64_t)N + 1);
         const uint64_t cbytes = ((uint64_t)nnz * cb + 7) / 8, qbytes = ((uint64_t)nnz * q + 7) / 8;
-        if (len - kCrcBytes < pos + cbytes + qbytes) { walk = SIF_ERR_STREAM_FORMAT; break; }  // :358
-        if (b >= max_rows) { walk = SIF_ERR_CAPACITY; break; }
+        if (len - kCrcBytes < pos + cbytes + qbytes) { walk = SIF_ERR_STREAM_FORMAT; walk_r = R_BLKPAY; break; }  // :358
+        if (b >= max_rows) { walk = SIF_ERR_CAPACITY; walk_r = R_CAPACITY; break; }
         uint32_t* row = tab + (2 + b) * TROW_U32;
         row[0] = q; row[1] = nnz; row[2] = o; row[3] = vmin;
         row[4] = (uint32_t)rp; row[5] = (uint32_t)(rp >> 32);
@@ -88,7 +96,7 @@ __global__ void sif_parse_kernel(DecArgs a) {
         row[8] = (uint32_t)(pos + cbytes); row[9] = (uint32_t)((pos + cbytes) >> 32);
         pos += cbytes + qbytes;
       }
-      if (!walk && pos != len - kCrcBytes) walk = SIF_ERR_STREAM_FORMAT;  // codec.py:384-385
+      if (!walk && pos != len - kCrcBytes) { walk = SIF_ERR_STREAM_FORMAT; walk_r = R_TRAIL; }  // codec.py:384-385
       nb = (uint32_t)nblk;
     }
   }
@@ -97,6 +105,10 @@ __global__ void sif_parse_kernel(DecArgs a) {
   tab[TROW_U32 + 1] = crc;
   tab[TROW_U32 + 2] = (uint32_t)len;
   tab[TROW_U32 + 3] = (uint32_t)(len >> 32);
+  tab[TROW_U32 + 4] = pre_r;
+  tab[TROW_U32 + 5] = walk_r;
+  tab[TROW_U32 + 6] = walk_x;
+  tab[TROW_U32 + 9] = len >= 4 ? rd_u32(in, 0) : 0u;  // magic bytes for the error message
 }
 
 // ------------------------------------------------------------------------------- CRC
@@ -159,6 +171,24 @@ __device__ __noinline__ double plus_value(const uint32_t* tab, const uint8_t* in
 }
 
 // ------------------------------------------------------------------------------- scatter
+// Corrupt-stream reasons are ranked like the reference's validation order (codec.py:235-251:
+// blocks in plane order, inside a block the five checks in order); the IF keeps the first
+// one (atomicMax of its complement in acc[3]) so the error message names the same check.
+enum : uint32_t { CK_ROWPTR = 0, CK_ROWPTR_NNZ = 1, CK_COL_RANGE = 2, CK_COL_ORDER = 3, CK_OVERLAP = 4 };
+__device__ __forceinline__ uint32_t corrupt_key(uint32_t b, uint32_t check) { return b * 8u + check; }
+
+__device__ __forceinline__ void flush_flags(const DecArgs& a, int cur, uint32_t fl, uint32_t ck) {
+  fl = __reduce_or_sync(0xFFFFFFFFu, fl);
+  ck = __reduce_min_sync(0xFFFFFFFFu, ck);
+  if ((threadIdx.x & 31) == 0) {
+    if (ck != 0xFFFFFFFFu) {
+      fl |= FLAG_CORRUPT;
+      atomicMax(a.acc + 4ull * cur + 3, 0xFFFFFFFFu - ck);
+    }
+    if (fl) atomicOr(a.acc + 4ull * cur + 1, fl);
+  }
+}
+
 // Work item = (stream, row group, column segment): R = max(1, segw / K) consecutive rows of
 // at most segw columns; a warp owns a contiguous range of items.  Lanes hold one (block,
 // row) pair each (pairs block-major, plus blocks first, in groups of 32): block metadata
@@ -193,13 +223,12 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
   const uint8_t* in = nullptr;
   float* out = nullptr;
   uint32_t fl = 0;
+  uint32_t ck = 0xFFFFFFFFu;  // first failing (block, check) of this warp's part of the IF
   for (uint64_t it = i0; it < i1; ++it) {
     if (cur < 0 || it >= ib1) {
-      if (cur >= 0) {
-        fl = __reduce_or_sync(0xFFFFFFFFu, fl);
-        if (lane == 0 && fl) atomicOr(a.acc + 4ull * cur + 1, fl);
-      }
+      if (cur >= 0) flush_flags(a, cur, fl, ck);
       fl = 0;
+      ck = 0xFFFFFFFFu;
       int lo = cur < 0 ? 0 : cur, hi = a.n - 1;
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -248,9 +277,8 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
         const uint64_t qbit = 8ull * ((uint64_t)m2v.x | ((uint64_t)m2v.y << 32));
         const uint32_t p0 = ld_u32_le(in, rpo + 4ull * r), p1 = ld_u32_le(in, rpo + 4ull * (r + 1));
         if (sg == 0) {
-          if (p1 < p0) fl |= FLAG_CORRUPT;  // codec.py:238-241
-          if (r == 0 && p0 != 0) fl |= FLAG_CORRUPT;
-          if (r + 1 == N && p1 != nnz) fl |= FLAG_CORRUPT;
+          if (r == 0 && p0 != 0) ck = min(ck, corrupt_key(b, CK_ROWPTR));  // codec.py:238-239
+          if (p1 < p0 || (r + 1 == N && p1 != nnz)) ck = min(ck, corrupt_key(b, CK_ROWPTR_NNZ));  // :240-241
         }
         uint32_t lo = min(p0, nnz), hi = max(lo, min(p1, nnz));
         const uint32_t rs0 = lo;
@@ -273,7 +301,7 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
         // pair parameters in shared memory (entry base stored as lo - exclusive prefix)
         pa[w][lane] = make_uint4((uint32_t)cbit, (uint32_t)(cbit >> 32), (uint32_t)qbit, (uint32_t)(qbit >> 32));
         pb[w][lane] = make_uint4(lo, q, m0v.z, m0v.w);
-        pc[w][lane] = make_uint2(rs0, ri | (b >= mp ? 0x80000000u : 0u));
+        pc[w][lane] = make_uint2(rs0, ri | (b << 10) | (b >= mp ? 0x80000000u : 0u));
       }
       const uint32_t inc = warp_incl_scan_u32(cnt);
       const uint32_t M = __shfl_sync(0xFFFFFFFFu, inc, 31);
@@ -296,7 +324,7 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
         const uint2 C = pc[w][jl];
         const uint64_t cbj = (uint64_t)A.x | ((uint64_t)A.y << 32);
         const uint32_t e = B.x + m;
-        const uint32_t rij = C.y & 0x7FFFFFFFu;
+        const uint32_t rij = C.y & 0x3FFu, bj = (C.y >> 10) & 0x1FFFFu;
         const bool minus = (C.y >> 31) != 0;
         // col and code fields are fetched together (one memory round trip per window)
         const uint64_t qbj = (uint64_t)A.z | ((uint64_t)A.w << 32);
@@ -316,18 +344,18 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
         uint32_t pos = 0;
         double v = 0.0;
         if (m < M) {
-          if (col >= K) fl |= FLAG_CORRUPT;  // codec.py:242-243
+          if (col >= K) ck = min(ck, corrupt_key(bj, CK_COL_RANGE));  // codec.py:242-243
           else {
             // strictly increasing within the row (codec.py:244-247)
             if (e > C.x) {
               const uint32_t prev = jlp == jl ? colp : ld_field(in, cbj + (uint64_t)(e - 1) * cb, cb);
-              if (prev >= col) fl |= FLAG_CORRUPT;
+              if (prev >= col) ck = min(ck, corrupt_key(bj, CK_COL_ORDER));
             }
             if (col >= c0 && col < c1) {
               wr = true;
               pos = rij * W + (col - c0);
               const uint32_t old = atomicOr(bm + (minus ? bmw : 0u) + (pos >> 5), 1u << (pos & 31));
-              if (old & (1u << (pos & 31))) fl |= FLAG_CORRUPT;  // codec.py:248-250 (overlap)
+              if (old & (1u << (pos & 31))) ck = min(ck, corrupt_key(bj, CK_OVERLAP));  // codec.py:248-250
               v = __dadd_rn(__dmul_rn((double)code, (double)__uint_as_float(B.z)), (double)__uint_as_float(B.w));
               if (!minus) {
                 const float f = __double2float_rn(v);  // f32(0 + v)
@@ -379,10 +407,7 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
     if (bad) fl |= FLAG_NONFINITE;
     __syncwarp();
   }
-  if (cur >= 0) {
-    fl = __reduce_or_sync(0xFFFFFFFFu, fl);
-    if (lane == 0 && fl) atomicOr(a.acc + 4ull * cur + 1, fl);
-  }
+  if (cur >= 0) flush_flags(a, cur, fl, ck);
 }
 
 // ------------------------------------------------------------------------------- finalize
@@ -395,20 +420,23 @@ __global__ void sif_dfinal_kernel(DecArgs a) {
   const sif_dec_desc d = a.descs[i];
   uint32_t* acc = a.acc + 4ull * i;
   const uint32_t walk = tab[0], N = tab[1], K = tab[2], pre = tab[TROW_U32 + 0];
-  const uint32_t crc_raw = acc[0], flags = acc[1];
+  const uint32_t crc_raw = acc[0], flags = acc[1], ckey = 0xFFFFFFFFu - acc[3];
   const bool shape_ok = a.parse_only || (N == d.rows && K == d.cols);
   int st = SIF_OK;
-  if (pre) st = (int)pre;
-  else if (crc_finish(crc_raw, d.in_len - 8) != tab[TROW_U32 + 1]) st = SIF_ERR_STREAM_FORMAT;  // :325-327
-  else if (walk) st = (int)walk;
-  else if (!shape_ok) st = SIF_ERR_CAPACITY;
+  uint32_t r = R_NONE, x = 0;
+  if (pre) { st = (int)pre; r = tab[TROW_U32 + 4]; }
+  else if (crc_finish(crc_raw, d.in_len - 8) != tab[TROW_U32 + 1]) { st = SIF_ERR_STREAM_FORMAT; r = R_CRC; }  // :325-327
+  else if (walk) { st = (int)walk; r = tab[TROW_U32 + 5]; x = tab[TROW_U32 + 6]; }
+  else if (!shape_ok) { st = SIF_ERR_CAPACITY; r = R_SHAPE_MISMATCH; }
   else if (!a.parse_only) {
-    if (flags & FLAG_CORRUPT) st = SIF_ERR_CORRUPT_STREAM;
-    else if (N < 1 || K < 1) st = SIF_ERR_SHAPE;
-    else if (flags & FLAG_NONFINITE) st = SIF_ERR_NONFINITE;
+    if (flags & FLAG_CORRUPT) { st = SIF_ERR_CORRUPT_STREAM; r = R_CORRUPT + (ckey & 7u); x = ckey >> 3; }
+    else if (N < 1 || K < 1) { st = SIF_ERR_SHAPE; r = R_SHAPE; }
+    else if (flags & FLAG_NONFINITE) { st = SIF_ERR_NONFINITE; r = R_NONFINITE; }
   }
   a.status[i] = st;
-  acc[0] = 0; acc[1] = 0; acc[2] = 0;
+  reinterpret_cast<uint32_t*>(a.table + (uint64_t)i * a.table_stride)[TROW_U32 + 7] = r;
+  reinterpret_cast<uint32_t*>(a.table + (uint64_t)i * a.table_stride)[TROW_U32 + 8] = x;
+  acc[0] = 0; acc[1] = 0; acc[2] = 0; acc[3] = 0;
 }
 
 }  // namespace sif

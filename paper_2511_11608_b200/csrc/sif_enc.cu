@@ -1464,15 +1464,28 @@ __global__ void __launch_bounds__(CNT) enc_members(EArgs a) {
     const uint64_t slot = min((uint64_t)CH, f.T - (uint64_t)(c - f.ch0) * CH);  // member slot capacity
     const bool one = (uint64_t)B * n <= slot;
     uint32_t i = 0;
+    // the first 64 candidates of the next unit are loaded while the current unit is processed
+    uint2 nx[2];
+    {
+      const uint32_t uo = __shfl_sync(0xFFFFFFFFu, my_uo, 0), un = __shfl_sync(0xFFFFFFFFu, my_un, 0);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) nx[h] = 32 * h + lane < un ? __ldg(gl + uo + 32 * h + lane) : make_uint2(0, 0);
+    }
     for (int u = 0; u < UNITS; ++u) {
       const uint32_t uo = __shfl_sync(0xFFFFFFFFu, my_uo, u), un = __shfl_sync(0xFFFFFFFFu, my_un, u);
+      uint2 cu[2] = {nx[0], nx[1]};
+      if (u + 1 < UNITS) {
+        const uint32_t uo1 = __shfl_sync(0xFFFFFFFFu, my_uo, u + 1), un1 = __shfl_sync(0xFFFFFFFFu, my_un, u + 1);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) nx[h] = 32 * h + lane < un1 ? __ldg(gl + uo1 + 32 * h + lane) : make_uint2(0, 0);
+      }
       for (uint32_t j0 = 0; j0 < un; j0 += 64) {
         // two windows in flight: both loads issued before either is used
         uint2 ev[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const uint32_t j = j0 + 32 * h + lane;
-          ev[h] = j < un ? __ldg(gl + uo + j) : make_uint2(0, 0);
+          ev[h] = j0 == 0 ? cu[h] : (j < un ? __ldg(gl + uo + j) : make_uint2(0, 0));
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {

@@ -617,4 +617,22 @@ int sif_gen_synthetic(void* x, uint32_t rows, uint32_t cols, uint32_t dtype, uin
   return check_cuda(cudaGetLastError());
 }
 
+int sif_fixture_tensor(float* x, uint64_t n, uint64_t seed, int dist, void* stream) {
+  if ((!x && n) || (dist != 0 && dist != 1)) return SIF_ERR_INVALID_ARG;
+  if (n == 0) return SIF_OK;
+  const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+  sif::sif_fixture_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(x, n, seed, (uint32_t)dist);
+  return check_cuda(cudaGetLastError());
+}
+
+int sif_count_nonfinite(const float* x, uint64_t n, unsigned long long* d_count, void* stream) {
+  if ((!x && n) || !d_count || (reinterpret_cast<uintptr_t>(x) & 15)) return SIF_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (check_cuda(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s))) return SIF_ERR_CUDA;
+  if (n == 0) return SIF_OK;
+  const unsigned grid = (unsigned)std::min<uint64_t>((n / 4 + 255) / 256 + 1, 148ull * 8);
+  sif::sif_nonfinite_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const uint32_t*>(x), n, d_count);
+  return check_cuda(cudaGetLastError());
+}
+
 }  // extern "C"

@@ -51,6 +51,14 @@ def ref_error_kind(fn, *a):
         return type(e).__name__
 
 
+def ref_error_msg(fn, *a):
+    try:
+        fn(*a)
+        return None
+    except slicer.SlicerError as e:
+        return str(e)
+
+
 def make_inputs(gen: np.random.Generator, kind: str, rows: int, cols: int, seed: int) -> np.ndarray:
     t = rows * cols
     if kind == "uniform":
@@ -255,7 +263,9 @@ def main():
             j = len(corrupt)
             arrays[f"bad{j}"] = np.frombuffer(bad, dtype=np.uint8)
             corrupt.append(dict(case=ci, tag=tag, rows=c["rows"], cols=c["cols"], error=kind,
-                                deser_error=ref_error_kind(slicer.deserialize, bad)))
+                                deser_error=ref_error_kind(slicer.deserialize, bad),
+                                msg=ref_error_msg(lambda d: slicer.decode(slicer.deserialize(d)), bad),
+                                deser_msg=ref_error_msg(slicer.deserialize, bad)))
 
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
     with open(os.path.join(HERE, "cases.json"), "w") as f:

@@ -114,6 +114,7 @@ def main():
             arrays[f"{name}_err"] = np.frombuffer(b"", np.uint8)
         except SlicerError as e:
             arrays[f"{name}_err"] = np.frombuffer(type(e).__name__.encode(), np.uint8)
+            arrays[f"{name}_msg"] = np.frombuffer(str(e).encode(), np.uint8)
         names.append(name)
         print(name, len(data), hashlib.sha256(data).hexdigest()[:16],
               arrays[f"{name}_err"].tobytes().decode() or "ok")
