@@ -195,6 +195,13 @@ def _enc_descs(xs, outs, caps, seeds, dtypes):
     return arr
 
 
+def _raise_enc(status: int, i: int, n: int) -> None:
+    """Encoder status -> the reference's exception and message (atkf.py:50-51)."""
+    if status == 2:
+        raise NonFiniteError("input tensor contains NaN or Inf" + (f" (IF {i} of the batch)" if n > 1 else ""))
+    raise_for(status, f"IF {i} of the batch")
+
+
 class BatchEncoder:
     """Plan + uploaded descriptors for a fixed batch of IF buffers (reusable across steps).
 
@@ -236,7 +243,7 @@ class BatchEncoder:
         st = self.status.cpu().numpy()
         bad = np.flatnonzero(st != 0)
         if bad.size:
-            raise_for(int(st[bad[0]]), f"IF {int(bad[0])} of the batch")
+            _raise_enc(int(st[bad[0]]), int(bad[0]), self.B)
         return self
 
     def payloads(self) -> list:
