@@ -82,7 +82,8 @@ struct IfSt {
   uint32_t crc_acc, seg_done;
   uint32_t bcount[MAXB];  // block member totals (K4 atomics)
   // multi-kernel select state (enc_select<1|2>, enc_gather<1|2>)
-  uint32_t sel_phase;     // 0 done, 1 needs the tau-bin gather, 2 needs the cut-bin gather
+  uint32_t sel_phase;     // 0 done, 1 needs the tau-bin gather, 2 needs the cut-bin gather,
+                          // 4 resolved by enc_select_tiny
   int32_t dtau;
   uint64_t rt, cnt_nz;
   uint32_t nA, pend_n, nreg, sel_lo;
@@ -812,6 +813,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   const IfInfo f = a.info[ifi];
   IfSt& st = a.st[ifi];
   const uint64_t kk = f.kk, seed = f.seed;
+  if (PH == 0 && st.sel_phase == 4) return;  // resolved by enc_select_tiny
   if (PH > 0) {
     if (st.sel_phase != (uint32_t)PH) return;
     if (PH == 2) {
@@ -1265,6 +1267,157 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   }
 }
 
+
+// ---------------------------------------------------------------------------------------
+// K3t: one warp per single-chunk IF (T <= CH, e.g. a decode-step token) on the common path
+// (lambda = 0, k > 0, bracket hit, no NaN/Inf, candidates fit TCAP).  The candidates are
+// held in shared memory and every select of enc_select is a warp radix select (8-bit
+// digits, MSB first) on a composite key, with syncwarp only:
+//   tau      k-th largest |x| key; ties: the r-th smallest splitmix64 hash (atkf.py:37-41,
+//            :71-84), exactly the order select_exact uses (key desc, hash asc);
+//   MS cuts  element of rank j*base among the kept elements of a sign plane by
+//            (value desc, flat index asc) (msplit.py:54-80): composite (key << 12) | (4095 - x).
+// IfSt is written exactly as enc_select writes it; enc_select<0> skips these IFs
+// (sel_phase = 4).  Other IFs are left to enc_select.
+constexpr int TCAP = 1024;  // candidates per IF held by one warp
+constexpr int TNT = 128;    // threads per CTA (4 IFs)
+
+// r-th largest (1-based) composite comp(i) over i < n with pred(i), nbits significant bits.
+template <class Pred, class Comp>
+__device__ __forceinline__ uint64_t warp_select(uint32_t* hist, uint32_t n, uint64_t r, int nbits, Pred pred,
+                                                Comp comp) {
+  const int lane = threadIdx.x & 31;
+  uint64_t prefix = 0;
+  int shift = nbits;
+  while (shift > 0) {
+    const int wd = shift < 8 ? shift : 8;
+    shift -= wd;
+    const int top = shift + wd;
+    const uint64_t hmask = top >= 64 ? 0ull : (~0ull << top);
+    for (int k = lane; k < 256; k += 32) hist[k] = 0;
+    __syncwarp();
+    for (uint32_t i = lane; i < n; i += 32) {
+      if (!pred(i)) continue;
+      const uint64_t c = comp(i);
+      if ((c & hmask) == prefix) atomicAdd(&hist[(uint32_t)(c >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    // lane l owns bins 255-8l .. 248-8l (descending)
+    uint32_t v[8], sum = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { v[j] = hist[255 - 8 * lane - j]; sum += v[j]; }
+    const uint32_t inc = warp_incl_scan_u32(sum), exc = inc - sum;
+    const bool mine = (uint64_t)exc < r && r <= (uint64_t)inc;
+    uint32_t dg = 0, rr = 0;
+    if (mine) {
+      uint32_t acc = exc;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (dg == 0 && rr == 0 && (uint64_t)acc + v[j] >= r) { dg = 255u - 8u * lane - j; rr = (uint32_t)(r - acc); }
+        acc += v[j];
+      }
+    }
+    const uint32_t src = __ffs(__ballot_sync(0xFFFFFFFFu, mine)) - 1;
+    dg = __shfl_sync(0xFFFFFFFFu, dg, src);
+    r = __shfl_sync(0xFFFFFFFFu, rr, src);
+    prefix |= (uint64_t)dg << shift;
+    __syncwarp();
+  }
+  return prefix;
+}
+
+__global__ void __launch_bounds__(TNT) enc_select_tiny(EArgs a) {
+  __shared__ uint2 cand[TNT / 32][TCAP];
+  __shared__ uint32_t hst[TNT / 32][256];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int ifi = blockIdx.x * (TNT / 32) + w;
+  if (ifi >= a.n) return;
+  const IfInfo& f = a.info[ifi];
+  IfSt& st = a.st[ifi];
+  const uint64_t kk = f.kk;
+  const uint32_t n = st.ncand;
+  if (a.atkf_only || f.hslot >= 0 || f.T > (uint64_t)CH || a.lam != 0.0 || kk == 0 || st.err ||
+      st.maxkey >= kNonFiniteKey || st.lo < 1 || st.cnt_lo < kk || n > (uint32_t)TCAP || n < kk)
+    return;  // enc_select handles it
+  uint2* c = cand[w];
+  uint32_t* h = hst[w];
+  const uint2* L = le(a, f);
+  for (uint32_t i = lane; i < n; i += 32) c[i] = __ldcg(L + i);
+  __syncwarp();
+  auto all = [](uint32_t) { return true; };
+  // ---- tau: kk-th largest key (candidates are all nonzero: lo >= 1)
+  const uint32_t tau_key = (uint32_t)warp_select(h, n, kk, 31, all, [&](uint32_t i) -> uint64_t {
+    return c[i].x & 0x7FFFFFFFu;
+  });
+  uint32_t gt = 0, eq = 0;
+  for (uint32_t i = lane; i < n; i += 32) {
+    const uint32_t k = c[i].x & 0x7FFFFFFFu;
+    gt += k > tau_key;
+    eq += k == tau_key;
+  }
+  gt = __reduce_add_sync(0xFFFFFFFFu, gt);
+  eq = __reduce_add_sync(0xFFFFFFFFu, eq);
+  const uint64_t r_eq = kk - gt;
+  const bool tie_all = r_eq == eq;
+  const uint64_t seed = f.seed;
+  uint64_t h_star = 0;
+  if (!tie_all) {  // r_eq-th smallest hash among the ties = r_eq-th largest of ~hash
+    h_star = ~warp_select(h, n, r_eq, 64, [&](uint32_t i) { return (c[i].x & 0x7FFFFFFFu) == tau_key; },
+                          [&](uint32_t i) -> uint64_t { return ~splitmix(seed, c[i].y); });
+  }
+  // ---- kept flags (bit 31 of the index word) and kept counts per sign
+  uint32_t k0 = 0, k1 = 0;
+  for (uint32_t i = lane; i < n; i += 32) {
+    const uint2 e = c[i];
+    const uint32_t k = e.x & 0x7FFFFFFFu;
+    const bool kp = k > tau_key || (k == tau_key && (tie_all || splitmix(seed, e.y) <= h_star));
+    if (kp) { if (e.x >> 31) ++k1; else ++k0; }
+    c[i].y = e.y | (kp ? 0x80000000u : 0u);
+  }
+  __syncwarp();
+  uint64_t nnz[2];
+  nnz[0] = __reduce_add_sync(0xFFFFFFFFu, k0);
+  nnz[1] = __reduce_add_sync(0xFFFFFFFFu, k1);
+  // ---- MS cuts (msplit.py:68-80)
+  const int mcfg[2] = {a.m_plus, a.m_minus};
+  uint64_t meff[2], base[2];
+  for (int sg = 0; sg < 2; ++sg) {
+    const uint64_t m = (uint64_t)mcfg[sg];
+    meff[sg] = nnz[sg] < m ? nnz[sg] : m;
+    if (meff[sg] < 1) meff[sg] = 1;
+    base[sg] = nnz[sg] / meff[sg];
+  }
+  const int B = (int)(meff[0] + meff[1]);
+  const int ncut0 = (int)meff[0] - 1;
+  const int ncut = B - 2;
+  for (int ci = 0; ci < ncut; ++ci) {
+    const uint32_t sg = ci < ncut0 ? 0u : 1u;
+    const int j = (sg == 0 ? ci : ci - ncut0) + 1;
+    const uint64_t cc = warp_select(
+        h, n, (uint64_t)j * base[sg] + 1, 31 + 12,
+        [&](uint32_t i) { return (c[i].x >> 31) == sg && (c[i].y >> 31) != 0u; },
+        [&](uint32_t i) -> uint64_t {
+          return ((uint64_t)(c[i].x & 0x7FFFFFFFu) << 12) | (uint64_t)(4095u - (c[i].y & 0xFFFu));
+        });
+    if (lane == 0) { st.cut_key[ci] = (uint32_t)(cc >> 12); st.cut_idx[ci] = 4095u - (uint32_t)(cc & 0xFFFu); }
+  }
+  if (lane == 0) {
+    const double tau = (double)__uint_as_float(tau_key);
+    st.flags = tie_all ? F_TIE_ALL : 0u;
+    st.tau_key = tau_key;
+    st.ck_star = tau_key;
+    st.h_star = h_star;
+    st.tau = tau;
+    st.tau_p = __dmul_rn(__dadd_rn(1.0, a.lam), tau);
+    st.tau_m = -__dmul_rn(__dsub_rn(1.0, a.lam), tau);
+    st.nnz[0] = nnz[0]; st.nnz[1] = nnz[1];
+    st.base[0] = base[0]; st.base[1] = base[1];
+    st.meff0 = (uint32_t)meff[0];
+    st.B = (uint32_t)B; st.ncut0 = (uint32_t)ncut0; st.ncut = (uint32_t)ncut;
+    st.ncand = n;
+    st.sel_phase = 4;  // resolved here; enc_select<0> skips the IF
+  }
+}
 
 // ---------------------------------------------------------------------------------------
 // Per-IF kept test and block id, evaluated by the chunk kernels from IfSt.

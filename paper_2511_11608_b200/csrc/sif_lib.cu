@@ -235,6 +235,7 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
   if (st) return st;
   memset(p, 0, sizeof(*p));
   uint64_t kmax = 0, nch = 0, nhist = 0, lists = 0, nseg = 0;
+  bool tiny = false;  // some IF may take the warp-per-IF select (enc_select_tiny)
   for (int i = 0; i < n; ++i) {
     if (d[i].rows < 1 || d[i].cols < 1) return SIF_ERR_SHAPE;  // tensor.py:27-28
     const uint64_t T = (uint64_t)d[i].rows * d[i].cols;
@@ -247,6 +248,7 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
     const uint64_t ch = (T + sif::CH - 1) / sif::CH;
     nch += ch;
     if (ch > 1) ++nhist;
+    if (ch == 1 && !atkf && c->lam == 0.0 && sif::keep_count(c->s, T) > 0) tiny = true;
     lists += up(16 * T, 256);
     nseg += crc_segments(d[i].out_cap);
     if (crc_segments(d[i].out_cap) > (uint64_t)sif::CRC_PIECES_MAX) return SIF_ERR_INVALID_ARG;
@@ -263,7 +265,8 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
   p->cap_smem = (int32_t)nhist;
   p->max_blocks = maxb;
   p->tiles = (int32_t)nch;
-  p->flags = atkf | (kmax * 2 > (uint64_t)kBigNcand ? 2 : 0);  // bit 0: ATKF-only, bit 1: multi-kernel select
+  // bit 0: ATKF-only, bit 1: multi-kernel select, bit 2: warp-per-IF select for small IFs
+  p->flags = atkf | (kmax * 2 > (uint64_t)kBigNcand ? 2 : 0) | (tiny ? 4 : 0);
   p->ws_desc_off = w.info;
   p->ws_aux_off = w.fixedq;
   p->ws_spill_off = w.lists;
@@ -405,6 +408,7 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   { ProfScope ps(KP_STREAM, s); sif::enc_stream<<<std::min<unsigned>(nch, g_stream), sif::CNT, kSmemStream, s>>>(a); }
   {
     ProfScope ps(KP_SELECT, s);
+    if (p->flags & 4) sif::enc_select_tiny<<<(n + sif::TNT / 32 - 1) / (sif::TNT / 32), sif::TNT, 0, s>>>(a);
     sif::enc_select<0><<<n, sif::SNT, kSmemSelect, s>>>(a);
     if (a.big_ncand) {  // some IF is large enough for the multi-kernel select
       sif::enc_gather<1><<<std::min<unsigned>(wgrid, g_gather), sif::CNT, 0, s>>>(a);

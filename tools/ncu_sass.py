@@ -7,7 +7,13 @@ out = subprocess.run(["ncu", "-i", rep, "-k", "regex:" + kre, "--page", "source"
                      capture_output=True, text=True).stdout
 lines = out.splitlines()
 rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
-h = rows[0]; ix = {k: i for i, k in enumerate(h)}; data = rows[1:]
+h = rows[0]; ix = {k: i for i, k in enumerate(h)}
+data = []
+for r in rows[1:]:
+    if r and r[0] == "Kernel Name":
+        break  # first matching launch only
+    if len(r) >= len(h) - 1:
+        data.append(r)
 ie, ss = ix["Instructions Executed"], ix["Warp Stall Sampling (All Samples)"]
 tot = sum(int(r[ie] or 0) for r in data); tots = sum(int(r[ss] or 0) for r in data)
 print(f"total exec {tot}  samples {tots}  instrs {len(data)}")
