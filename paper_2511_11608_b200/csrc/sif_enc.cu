@@ -1270,39 +1270,40 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
 
 // ---------------------------------------------------------------------------------------
 // K3t: one warp per single-chunk IF (T <= CH, e.g. a decode-step token) on the common path
-// (lambda = 0, k > 0, bracket hit, no NaN/Inf, candidates fit TCAP).  The candidates are
-// held in shared memory and every select of enc_select is a warp radix select (8-bit
-// digits, MSB first) on a composite key, with syncwarp only:
-//   tau      k-th largest |x| key; ties: the r-th smallest splitmix64 hash (atkf.py:37-41,
-//            :71-84), exactly the order select_exact uses (key desc, hash asc);
-//   MS cuts  element of rank j*base among the kept elements of a sign plane by
-//            (value desc, flat index asc) (msplit.py:54-80): composite (key << 12) | (4095 - x).
+// (lambda = 0, k > 0, bracket hit, no NaN/Inf, candidates fit TCAP).  The warp sorts its
+// candidates once in shared memory by the composite (|x| key desc, sign, flat index asc)
+// (bitonic, syncwarp only) and reads everything enc_select computes off the sorted order:
+//   tau      key at position k-1; ties (equal keys, contiguous) keep the r smallest
+//            splitmix64 hashes (atkf.py:37-41, :71-84);
+//   MS cuts  inside a sign plane the sorted order is (value desc, flat index asc)
+//            (msplit.py:54-80), so the cut of rank j*base is found by one counting pass.
 // IfSt is written exactly as enc_select writes it; enc_select<0> skips these IFs
 // (sel_phase = 4).  Other IFs are left to enc_select.
 constexpr int TCAP = 1024;  // candidates per IF held by one warp
 constexpr int TNT = 128;    // threads per CTA (4 IFs)
 
-// r-th largest (1-based) composite comp(i) over i < n with pred(i), nbits significant bits.
-template <class Pred, class Comp>
-__device__ __forceinline__ uint64_t warp_select(uint32_t* hist, uint32_t n, uint64_t r, int nbits, Pred pred,
-                                                Comp comp) {
+// r-th largest (1-based) 64-bit value(i) over i in [i0, i1), 8-bit radix digits, one
+// shared-memory histogram per warp with match_any-aggregated increments.
+template <class Val>
+__device__ __forceinline__ uint64_t warp_select_range(uint32_t* hist, uint32_t i0, uint32_t i1, uint64_t r,
+                                                      Val val) {
   const int lane = threadIdx.x & 31;
   uint64_t prefix = 0;
-  int shift = nbits;
-  while (shift > 0) {
-    const int wd = shift < 8 ? shift : 8;
-    shift -= wd;
-    const int top = shift + wd;
-    const uint64_t hmask = top >= 64 ? 0ull : (~0ull << top);
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    const uint64_t hmask = shift >= 56 ? 0ull : (~0ull << (shift + 8));
     for (int k = lane; k < 256; k += 32) hist[k] = 0;
     __syncwarp();
-    for (uint32_t i = lane; i < n; i += 32) {
-      if (!pred(i)) continue;
-      const uint64_t c = comp(i);
-      if ((c & hmask) == prefix) atomicAdd(&hist[(uint32_t)(c >> shift) & 255u], 1u);
+    for (uint32_t b = i0; b < i1; b += 32) {
+      const uint32_t i = b + lane;
+      uint32_t d = 0xFFFFFFFFu;
+      if (i < i1) {
+        const uint64_t v = val(i);
+        if ((v & hmask) == prefix) d = (uint32_t)(v >> shift) & 255u;
+      }
+      const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
+      if (d != 0xFFFFFFFFu && lane == __ffs(peers) - 1) hist[d] += __popc(peers);
+      __syncwarp();
     }
-    __syncwarp();
-    // lane l owns bins 255-8l .. 248-8l (descending)
     uint32_t v[8], sum = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) { v[j] = hist[255 - 8 * lane - j]; sum += v[j]; }
@@ -1311,9 +1312,10 @@ __device__ __forceinline__ uint64_t warp_select(uint32_t* hist, uint32_t n, uint
     uint32_t dg = 0, rr = 0;
     if (mine) {
       uint32_t acc = exc;
+      bool got = false;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        if (dg == 0 && rr == 0 && (uint64_t)acc + v[j] >= r) { dg = 255u - 8u * lane - j; rr = (uint32_t)(r - acc); }
+        if (!got && (uint64_t)acc + v[j] >= r) { dg = 255u - 8u * lane - j; rr = (uint32_t)(r - acc); got = true; }
         acc += v[j];
       }
     }
@@ -1327,7 +1329,7 @@ __device__ __forceinline__ uint64_t warp_select(uint32_t* hist, uint32_t n, uint
 }
 
 __global__ void __launch_bounds__(TNT) enc_select_tiny(EArgs a) {
-  __shared__ uint2 cand[TNT / 32][TCAP];
+  __shared__ uint64_t srt[TNT / 32][TCAP];
   __shared__ uint32_t hst[TNT / 32][256];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int ifi = blockIdx.x * (TNT / 32) + w;
@@ -1339,46 +1341,58 @@ __global__ void __launch_bounds__(TNT) enc_select_tiny(EArgs a) {
   if (a.atkf_only || f.hslot >= 0 || f.T > (uint64_t)CH || a.lam != 0.0 || kk == 0 || st.err ||
       st.maxkey >= kNonFiniteKey || st.lo < 1 || st.cnt_lo < kk || n > (uint32_t)TCAP || n < kk)
     return;  // enc_select handles it
-  uint2* c = cand[w];
+  uint64_t* c = srt[w];
   uint32_t* h = hst[w];
   const uint2* L = le(a, f);
-  for (uint32_t i = lane; i < n; i += 32) c[i] = __ldcg(L + i);
+  uint32_t P = 32;
+  while (P < n) P <<= 1;
+  // composite: key (31 bits) | plus-sign flag | ~flat index; padding 0 sorts last
+  for (uint32_t i = lane; i < P; i += 32) {
+    uint64_t v = 0;
+    if (i < n) {
+      const uint2 e = __ldcg(L + i);
+      v = ((uint64_t)(e.x & 0x7FFFFFFFu) << 33) | ((uint64_t)((e.x >> 31) ^ 1u) << 32) | (uint64_t)(~e.y);
+    }
+    c[i] = v;
+  }
   __syncwarp();
-  auto all = [](uint32_t) { return true; };
-  // ---- tau: kk-th largest key (candidates are all nonzero: lo >= 1)
-  const uint32_t tau_key = (uint32_t)warp_select(h, n, kk, 31, all, [&](uint32_t i) -> uint64_t {
-    return c[i].x & 0x7FFFFFFFu;
-  });
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t q = lane; q < P / 2; q += 32) {
+        const uint32_t i = ((q & ~(j - 1)) << 1) | (q & (j - 1)), ix = i | j;
+        const uint64_t x = c[i], y = c[ix];
+        const bool desc = (i & k) == 0;
+        if (desc ? (x < y) : (x > y)) { c[i] = y; c[ix] = x; }
+      }
+      __syncwarp();
+    }
+  }
+  auto key_at = [&](uint32_t p) -> uint32_t { return (uint32_t)(c[p] >> 33); };
+  // ---- tau and its ties [G, G+E) in the sorted order
+  const uint32_t tau_key = key_at((uint32_t)kk - 1);
   uint32_t gt = 0, eq = 0;
   for (uint32_t i = lane; i < n; i += 32) {
-    const uint32_t k = c[i].x & 0x7FFFFFFFu;
+    const uint32_t k = key_at(i);
     gt += k > tau_key;
     eq += k == tau_key;
   }
-  gt = __reduce_add_sync(0xFFFFFFFFu, gt);
-  eq = __reduce_add_sync(0xFFFFFFFFu, eq);
-  const uint64_t r_eq = kk - gt;
-  const bool tie_all = r_eq == eq;
+  const uint32_t G = __reduce_add_sync(0xFFFFFFFFu, gt), E = __reduce_add_sync(0xFFFFFFFFu, eq);
+  const uint64_t r_eq = kk - G;
+  const bool tie_all = r_eq == E;
   const uint64_t seed = f.seed;
   uint64_t h_star = 0;
-  if (!tie_all) {  // r_eq-th smallest hash among the ties = r_eq-th largest of ~hash
-    h_star = ~warp_select(h, n, r_eq, 64, [&](uint32_t i) { return (c[i].x & 0x7FFFFFFFu) == tau_key; },
-                          [&](uint32_t i) -> uint64_t { return ~splitmix(seed, c[i].y); });
-  }
-  // ---- kept flags (bit 31 of the index word) and kept counts per sign
+  if (!tie_all)  // the r_eq-th smallest hash among the ties = the r_eq-th largest ~hash
+    h_star = ~warp_select_range(h, G, G + E, r_eq,
+                                [&](uint32_t i) -> uint64_t { return ~splitmix(seed, ~(uint32_t)c[i]); });
+  // ---- kept counts per sign and MS cuts: rank of each kept element inside its plane
   uint32_t k0 = 0, k1 = 0;
   for (uint32_t i = lane; i < n; i += 32) {
-    const uint2 e = c[i];
-    const uint32_t k = e.x & 0x7FFFFFFFu;
-    const bool kp = k > tau_key || (k == tau_key && (tie_all || splitmix(seed, e.y) <= h_star));
-    if (kp) { if (e.x >> 31) ++k1; else ++k0; }
-    c[i].y = e.y | (kp ? 0x80000000u : 0u);
+    const bool kp = i < G || (i < G + E && (tie_all || splitmix(seed, ~(uint32_t)c[i]) <= h_star));
+    if (kp) { if ((c[i] >> 32) & 1u) ++k0; else ++k1; }
   }
-  __syncwarp();
   uint64_t nnz[2];
   nnz[0] = __reduce_add_sync(0xFFFFFFFFu, k0);
   nnz[1] = __reduce_add_sync(0xFFFFFFFFu, k1);
-  // ---- MS cuts (msplit.py:68-80)
   const int mcfg[2] = {a.m_plus, a.m_minus};
   uint64_t meff[2], base[2];
   for (int sg = 0; sg < 2; ++sg) {
@@ -1390,16 +1404,34 @@ __global__ void __launch_bounds__(TNT) enc_select_tiny(EArgs a) {
   const int B = (int)(meff[0] + meff[1]);
   const int ncut0 = (int)meff[0] - 1;
   const int ncut = B - 2;
-  for (int ci = 0; ci < ncut; ++ci) {
-    const uint32_t sg = ci < ncut0 ? 0u : 1u;
-    const int j = (sg == 0 ? ci : ci - ncut0) + 1;
-    const uint64_t cc = warp_select(
-        h, n, (uint64_t)j * base[sg] + 1, 31 + 12,
-        [&](uint32_t i) { return (c[i].x >> 31) == sg && (c[i].y >> 31) != 0u; },
-        [&](uint32_t i) -> uint64_t {
-          return ((uint64_t)(c[i].x & 0x7FFFFFFFu) << 12) | (uint64_t)(4095u - (c[i].y & 0xFFFu));
-        });
-    if (lane == 0) { st.cut_key[ci] = (uint32_t)(cc >> 12); st.cut_idx[ci] = 4095u - (uint32_t)(cc & 0xFFFu); }
+  if (ncut > 0) {
+    uint32_t run0 = 0, run1 = 0;  // kept elements of each plane before this window
+    const uint32_t le_mask = 0xFFFFFFFFu >> (31 - lane);
+    for (uint32_t b0 = 0; b0 < G + E; b0 += 32) {
+      const uint32_t i = b0 + lane;
+      bool kp = false;
+      uint32_t sg = 0;
+      if (i < n) {
+        kp = i < G || (i < G + E && (tie_all || splitmix(seed, ~(uint32_t)c[i]) <= h_star));
+        sg = ((c[i] >> 32) & 1u) ? 0u : 1u;
+      }
+      const uint32_t m0 = __ballot_sync(0xFFFFFFFFu, kp && sg == 0), m1 = __ballot_sync(0xFFFFFFFFu, kp && sg == 1);
+      if (kp) {
+        const uint64_t rank = (uint64_t)(sg == 0 ? run0 + __popc(m0 & le_mask) : run1 + __popc(m1 & le_mask));
+        const uint64_t bs = base[sg];
+        // rank j*base + 1 (1-based) starts block j, j = 1 .. meff-1
+        if (bs > 0 && (rank - 1) % bs == 0) {
+          const uint64_t j = (rank - 1) / bs;
+          if (j >= 1 && j < meff[sg]) {
+            const int ci = (sg == 0 ? 0 : ncut0) + (int)j - 1;
+            st.cut_key[ci] = (uint32_t)(c[i] >> 33);
+            st.cut_idx[ci] = ~(uint32_t)c[i];
+          }
+        }
+      }
+      run0 += __popc(m0);
+      run1 += __popc(m1);
+    }
   }
   if (lane == 0) {
     const double tau = (double)__uint_as_float(tau_key);
