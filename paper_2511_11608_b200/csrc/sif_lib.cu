@@ -22,10 +22,11 @@ int check_cuda(cudaError_t e) { return e == cudaSuccess ? SIF_OK : SIF_ERR_CUDA;
 
 // ---- optional per-kernel timing (diagnostics; sif_profile_enable)
 enum { KP_PREP, KP_STREAM, KP_SELECT, KP_MEMBERS, KP_ABQ1, KP_ABQ2, KP_LAYOUT, KP_PACK, KP_CRC, KP_PARSE, KP_DCRC,
-       KP_SCATTER, KP_DFINAL, KP_N };
-const char* kKpNames[KP_N] = {"enc_prep", "enc_stream", "enc_select", "enc_members", "enc_abq<1>", "enc_abq<0>",
+       KP_SCATTER, KP_DFINAL, KP_SELECT_TINY, KP_GATHER1, KP_SELECT1, KP_GATHER2, KP_SELECT2, KP_N };
+const char* kKpNames[KP_N] = {"enc_prep", "enc_stream", "enc_select<0>", "enc_members", "enc_abq<1>", "enc_abq<0>",
                               "enc_layout", "enc_pack", "enc_crc", "sif_parse_kernel", "sif_dcrc_kernel",
-                              "sif_scatter_kernel", "sif_dfinal_kernel"};
+                              "sif_scatter_kernel", "sif_dfinal_kernel", "enc_select_tiny", "enc_gather<1>",
+                              "enc_select<1>", "enc_gather<2>", "enc_select<2>"};
 struct ProfRec { int k; cudaEvent_t a, b; };
 bool g_prof = false;
 std::vector<ProfRec> g_recs;
@@ -406,17 +407,17 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   const unsigned wgrid = std::max(1u, (nch + sif::CNT / 32 - 1) / (sif::CNT / 32));  // >= 1 chunk per warp
   { ProfScope ps(KP_PREP, s); sif::enc_prep<<<n, 512, 0, s>>>(a); }
   { ProfScope ps(KP_STREAM, s); sif::enc_stream<<<std::min<unsigned>(nch, g_stream), sif::CNT, kSmemStream, s>>>(a); }
-  {
-    ProfScope ps(KP_SELECT, s);
-    if (p->flags & 4) sif::enc_select_tiny<<<(n + sif::TNT / 32 - 1) / (sif::TNT / 32), sif::TNT, 0, s>>>(a);
-    sif::enc_select<0><<<n, sif::SNT, kSmemSelect, s>>>(a);
-    if (a.big_ncand) {  // some IF is large enough for the multi-kernel select
-      sif::enc_gather<1><<<std::min<unsigned>(wgrid, g_gather), sif::CNT, 0, s>>>(a);
-      sif::enc_select<1><<<n, sif::SNT, kSmemSelect, s>>>(a);
-      if (!atkf) {
-        sif::enc_gather<2><<<std::min<unsigned>(wgrid, g_gather), sif::CNT, 0, s>>>(a);
-        sif::enc_select<2><<<n, sif::SNT, kSmemSelect, s>>>(a);
-      }
+  if (p->flags & 4) {
+    ProfScope ps(KP_SELECT_TINY, s);
+    sif::enc_select_tiny<<<(n + sif::TNT / 32 - 1) / (sif::TNT / 32), sif::TNT, 0, s>>>(a);
+  }
+  { ProfScope ps(KP_SELECT, s); sif::enc_select<0><<<n, sif::SNT, kSmemSelect, s>>>(a); }
+  if (a.big_ncand) {  // some IF is large enough for the multi-kernel select
+    { ProfScope ps(KP_GATHER1, s); sif::enc_gather<1><<<std::min<unsigned>(wgrid, g_gather), sif::CNT, 0, s>>>(a); }
+    { ProfScope ps(KP_SELECT1, s); sif::enc_select<1><<<n, sif::SNT, kSmemSelect, s>>>(a); }
+    if (!atkf) {
+      { ProfScope ps(KP_GATHER2, s); sif::enc_gather<2><<<std::min<unsigned>(wgrid, g_gather), sif::CNT, 0, s>>>(a); }
+      { ProfScope ps(KP_SELECT2, s); sif::enc_select<2><<<n, sif::SNT, kSmemSelect, s>>>(a); }
     }
   }
   if (!atkf) {

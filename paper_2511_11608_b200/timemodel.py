@@ -6,7 +6,7 @@ schema, same nearest-grid-point lookups) that feeds the planner's encode-time es
 `calibrate` fills the tables with measured per-IF times of this implementation's kernels
 (per-kernel CUDA events, sif_profile_enable), mapped onto the reference's stages:
 
-    t_atkf(s, lambda)  enc_prep + enc_stream + enc_select        (ATKF: tau, ties, MS cuts)
+    t_atkf(s, lambda)  enc_prep + enc_stream + enc_select*/enc_gather*  (ATKF: tau, ties, MS cuts)
     t_ms(M+, M-)       enc_members + enc_layout + enc_pack + enc_crc   (MS blocks, CSR, .sif)
     t_abq(q)           (enc_abq<1> + enc_abq<0>) / (M+ + M-)     (per block, as the planner charges)
 
@@ -20,7 +20,8 @@ from dataclasses import dataclass
 
 from .errors import ConfigError
 
-ATKF_KERNELS = ("enc_prep", "enc_stream", "enc_select")
+ATKF_KERNELS = ("enc_prep", "enc_stream", "enc_select_tiny", "enc_select<0>", "enc_gather<1>", "enc_select<1>",
+                "enc_gather<2>", "enc_select<2>")
 MS_KERNELS = ("enc_members", "enc_layout", "enc_pack", "enc_crc")
 ABQ_KERNELS = ("enc_abq<1>", "enc_abq<0>")
 

@@ -9,9 +9,11 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/${TAG}_smoke
 for c in c2 c3 c4; do timeout 600 python bench.py --config $c --steps 20 --warmup 5 > $O/${TAG}_bench_$c.json 2> $O/${TAG}_bench_$c.err; done
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > $O/${TAG}_bench_ref_c2.json 2> $O/${TAG}_bench_ref_c2.err
 KRE='regex:enc_|sif_(parse|dcrc|scatter|dfinal)'
-for c in c2 c3 c4; do
-  timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KRE" -c 26 --csv --log-file $O/${TAG}_launches_$c.csv python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k "$KRE" -s 13 -c 13 -o $O/${TAG}_full_$c python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+# kernels per encode+decode step: c2 13, c3 14 (+enc_select_tiny), c4 17 (+2 gathers, +2 select phases)
+for ck in c2:13 c3:14 c4:17; do
+  c=${ck%%:*}; K=${ck##*:}
+  timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KRE" -c $((2 * K)) --csv --log-file $O/${TAG}_launches_$c.csv python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k "$KRE" -s $K -c $K -o $O/${TAG}_full_$c python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 done
 
 # summarise on the box (reports are too large to bring back together), keep the c2 report
