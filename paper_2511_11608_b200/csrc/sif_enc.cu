@@ -167,9 +167,9 @@ struct List {
   }
 };
 
-// Visit every list element (order-free) as f(bits, idx, true).  Global parts are read 4
-// entries per thread per step with independent 8-byte loads.
-template <int NT, class F>
+// Visit every list element (order-free) as f(bits, idx, true).  Global parts are read U
+// entries per thread per step with independent 8-byte loads (U loads in flight).
+template <int NT, int U = 4, class F>
 __device__ __forceinline__ void list_foreach(const List& L, uint32_t n, F f) {
   const uint32_t ns = n < L.cap ? n : L.cap;
   for (uint32_t i = threadIdx.x; i < ns; i += NT) {
@@ -178,15 +178,15 @@ __device__ __forceinline__ void list_foreach(const List& L, uint32_t n, F f) {
   }
   if (n > L.cap) {
     const uint32_t m = n - L.cap;
-    for (uint32_t i0 = 0; i0 < m; i0 += 4 * NT) {
-      uint2 e[4];
+    for (uint32_t i0 = 0; i0 < m; i0 += U * NT) {
+      uint2 e[U];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < U; ++k) {
         const uint32_t i = i0 + threadIdx.x + k * NT;
         e[k] = i < m ? __ldcg(L.g + i) : make_uint2(0, 0);
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < U; ++k)
         if (i0 + threadIdx.x + k * NT < m) f(e[k].x, e[k].y, true);
     }
   }
@@ -248,11 +248,11 @@ __device__ void find_digit(SelSh& sh, const uint32_t* H, int nb, uint64_t r) {
 // flat indices are).  As soon as the bin holding rank r has <= GCAP elements they are
 // gathered and ranked directly.  Used for huge single-value tie sets.
 struct GatE;
-template <int NT, class KeyFn>
+template <int NT, int U = 4, class KeyFn>
 __device__ uint64_t radix_select64(SelSh& sh, uint32_t* hist, const List& L, uint32_t n, uint64_t r, KeyFn fn,
                                    int nbits = 64);
 
-template <int NT, class KeyFn>
+template <int NT, int U, class KeyFn>
 __device__ uint64_t radix_select64(SelSh& sh, uint32_t* hist, const List& L, uint32_t n, uint64_t r, KeyFn fn,
                                    int nbits) {
   GatE* gl = reinterpret_cast<GatE*>(hist + 2 * HB);
@@ -262,7 +262,7 @@ __device__ uint64_t radix_select64(SelSh& sh, uint32_t* hist, const List& L, uin
     const int shf = hi - wdt, nb = 1 << wdt;
     for (int i = threadIdx.x; i < nb; i += NT) hist[i] = 0;
     __syncthreads();
-    list_foreach<NT>(L, n, [&](uint32_t b, uint32_t x, bool v) {
+    list_foreach<NT, U>(L, n, [&](uint32_t b, uint32_t x, bool v) {
       uint64_t k = 0;
       if (v && fn(b, x, k) && (k & mask) == prefix) atomicAdd(&hist[(int)((k >> shf) & (uint64_t)(nb - 1))], 1u);
     });
@@ -278,7 +278,7 @@ __device__ uint64_t radix_select64(SelSh& sh, uint32_t* hist, const List& L, uin
       // small bin: gather its keys and take the r-th largest directly
       if (threadIdx.x == 0) sh.gcount = 0;
       __syncthreads();
-      list_foreach<NT>(L, n, [&](uint32_t b, uint32_t x, bool v) {
+      list_foreach<NT, U>(L, n, [&](uint32_t b, uint32_t x, bool v) {
         uint64_t k = 0;
         if (v && fn(b, x, k) && (k & mask) == prefix) gl[atomicAdd(&sh.gcount, 1u)].sec = k;
       });
@@ -312,7 +312,7 @@ struct SelRes {
 // the bin holding rank r; the bin's elements are gathered and ranked exactly.  A bin that
 // is one key value with more than GCAP members resolves the secondary order by a radix
 // select on the secondary key.  scratch: 2*HB u32 + GCAP GatE.
-template <int NT, class Pred, class KeyF, class SecF>
+template <int NT, int U = 4, class Pred, class KeyF, class SecF>
 __device__ SelRes select_exact(SelSh& sh, uint32_t* scratch, const List& L, uint32_t n, Pred pred, KeyF keyf,
                                SecF secf, uint64_t klo, uint64_t khi, uint64_t r, int sec_bits = 64) {
   constexpr int NW = NT / 32;
@@ -327,7 +327,7 @@ __device__ SelRes select_exact(SelSh& sh, uint32_t* scratch, const List& L, uint
     const int nb = (int)(((span - 1) >> shf) + 1);
     for (int i = tid; i < nb; i += NT) hist[i] = 0;
     __syncthreads();
-    list_foreach<NT>(L, n, [&](uint32_t b, uint32_t x, bool v) {
+    list_foreach<NT, U>(L, n, [&](uint32_t b, uint32_t x, bool v) {
       if (v && pred(b, x)) {
         const uint64_t k = keyf(b);
         if (k >= klo && k < khi) atomicAdd(&hist[(int)((k - klo) >> shf)], 1u);
@@ -357,7 +357,7 @@ __device__ SelRes select_exact(SelSh& sh, uint32_t* scratch, const List& L, uint
       const uint32_t kk = (uint32_t)klo;
       // smallest secondary keys first: select the r-th largest of (2^sec_bits - 1 - sec)
       const uint64_t smax = sec_bits >= 64 ? ~0ull : ((1ull << sec_bits) - 1ull);
-      const uint64_t top = radix_select64<NT>(sh, hist, L, n, r, [&](uint32_t b, uint32_t x, uint64_t& k) {
+      const uint64_t top = radix_select64<NT, U>(sh, hist, L, n, r, [&](uint32_t b, uint32_t x, uint64_t& k) {
         if (!pred(b, x) || keyf(b) != kk) return false;
         k = smax - secf(b, x);
         return true;
@@ -368,7 +368,7 @@ __device__ SelRes select_exact(SelSh& sh, uint32_t* scratch, const List& L, uint
   }
   if (tid == 0) sh.gcount = 0;
   __syncthreads();
-  list_foreach<NT>(L, n, [&](uint32_t b, uint32_t x, bool v) {
+  list_foreach<NT, U>(L, n, [&](uint32_t b, uint32_t x, bool v) {
     bool in = v && pred(b, x);
     const uint64_t k = in ? keyf(b) : 0;
     in = in && k >= klo && k < khi;
@@ -802,6 +802,7 @@ struct K3Sh {
 template <int PH>
 __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   constexpr int NT = SNT;
+  constexpr int LU = PH > 0 ? 16 : 4;  // loads in flight per thread in list passes (big IFs: deep)
   extern __shared__ __align__(16) uint8_t dsm_raw[];
   uint32_t* dsm = reinterpret_cast<uint32_t*>(dsm_raw);
   __shared__ K3Sh k3;
@@ -825,7 +826,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
         const uint32_t g = st.pend_reg[p];
         const List Bp{nullptr, gat + st.reg_off[g], 0};
         const uint32_t dc = st.pend_d[p];
-        const SelRes r = select_exact<NT>(
+        const SelRes r = select_exact<NT, LU>(
             sh, scratch, Bp, st.reg_cnt[g], [](uint32_t, uint32_t) { return true; }, key31,
             [](uint32_t, uint32_t x) -> uint64_t { return x; }, (uint64_t)dc << DSH, (uint64_t)(dc + 1) << DSH,
             st.pend_r[p], 31);
@@ -909,7 +910,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   if (!hist_ok) {
     for (int k = tid; k < 2 * ND; k += NT) hist[k] = 0;
     __syncthreads();
-    list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t, bool v) {
+    list_foreach<NT, LU>(L, ncand, [&](uint32_t b, uint32_t, bool v) {
       if (v) atomicAdd(&hist[((b >> 31) ? ND : 0) + ((b & 0x7FFFFFFFu) >> DSH)], 1u);
     });
   }
@@ -921,7 +922,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   else if (lo == 0) {
     cnt_nz = (uint64_t)ncand - hist[0] - hist[ND];  // digit 0 holds zeros and tiny values
     uint32_t tiny = 0;
-    list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t, bool v) {
+    list_foreach<NT, LU>(L, ncand, [&](uint32_t b, uint32_t, bool v) {
       const uint32_t key = b & 0x7FFFFFFFu;
       tiny += (v && key != 0 && (key >> DSH) == 0) ? 1u : 0u;
     });
@@ -950,12 +951,12 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   if (kk > 0 && !only_nonzero) {
     if (zero_mode && cnt_nz < kk) {
       // tau == 0 (ATKF-only mode): every nonzero is kept; choose kk - nnz zeros by hash
-      const SelRes s = select_exact<NT>(sh, scratch, L, ncand, all_pred, key31, hash_of, 0, 1, kk - cnt_nz);
+      const SelRes s = select_exact<NT, LU>(sh, scratch, L, ncand, all_pred, key31, hash_of, 0, 1, kk - cnt_nz);
       h_star = s.sec;
       tie_all = s.all_ties;
     } else if (!fast) {
       const uint64_t klo = lo_neg < lo ? lo_neg : lo;
-      const SelRes s = select_exact<NT>(sh, scratch, L, ncand, all_pred, key31, hash_of, klo,
+      const SelRes s = select_exact<NT, LU>(sh, scratch, L, ncand, all_pred, key31, hash_of, klo,
                                         (uint64_t)st.maxkey + 1, kk);
       tau_key = s.key;
       ck_star = s.key;
@@ -1002,13 +1003,13 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
         rt = kk - sh.fd_above;
         if (tid == 0) k3.nA = 0;
         __syncthreads();
-        list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t x, bool v) {
+        list_foreach<NT, LU>(L, ncand, [&](uint32_t b, uint32_t x, bool v) {
           if (v && ((b & 0x7FFFFFFFu) >> DSH) == (uint32_t)dtau) A.set(atomicAdd(&k3.nA, 1u), b, x);
         });
         __syncthreads();
         nA = k3.nA;
       }
-      const SelRes s = select_exact<NT>(sh, scratch, A, nA, all_pred, key31, hash_of, (uint64_t)dtau << DSH,
+      const SelRes s = select_exact<NT, LU>(sh, scratch, A, nA, all_pred, key31, hash_of, (uint64_t)dtau << DSH,
                                         (uint64_t)(dtau + 1) << DSH, rt);
       tau_key = s.key;
       ck_star = s.key;
@@ -1025,7 +1026,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
       const double v = (double)__uint_as_float(b);
       return ((v > tau_p || v < tau_m) ? (1ull << 31) : 0ull) | (uint64_t)(b & 0x7FFFFFFFu);
     };
-    const SelRes s = select_exact<NT>(sh, scratch, L, ncand, all_pred, ckey, hash_of, 0, 1ull << 32, kk);
+    const SelRes s = select_exact<NT, LU>(sh, scratch, L, ncand, all_pred, ckey, hash_of, 0, 1ull << 32, kk);
     ck_star = s.key;
     h_star = s.sec;
     tie_all = s.all_ties;
@@ -1082,7 +1083,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
     __syncthreads();
     if (dtau >= 0) {
       uint32_t c0 = 0, c1 = 0;
-      list_foreach<NT>(A, nA, [&](uint32_t b, uint32_t x, bool v) {
+      list_foreach<NT, LU>(A, nA, [&](uint32_t b, uint32_t x, bool v) {
         if (v && kept_of(b, x)) { if (b >> 31) ++c1; else ++c0; }
       });
       c0 = __reduce_add_sync(0xFFFFFFFFu, c0);
@@ -1113,7 +1114,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
     if (keep_none) { nnz[0] = 0; nnz[1] = 0; }
   } else {
     uint32_t c0 = 0, c1 = 0;
-    list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t x, bool v) {
+    list_foreach<NT, LU>(L, ncand, [&](uint32_t b, uint32_t x, bool v) {
       if (v && (b & 0x7FFFFFFFu) != 0 && kept_of(b, x)) { if (b >> 31) ++c1; else ++c0; }
     });
     c0 = __reduce_add_sync(0xFFFFFFFFu, c0);
@@ -1151,7 +1152,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
       const uint32_t dc = sh.fd_digit;
       const uint64_t rc = r1 - sh.fd_above;
       if ((int)dc == dtau) {
-        const SelRes r = select_exact<NT>(
+        const SelRes r = select_exact<NT, LU>(
             sh, scratch, A, nA, [&](uint32_t b, uint32_t x) { return (b >> 31) == s && kept_of(b, x); }, key31,
             [](uint32_t, uint32_t x) -> uint64_t { return x; }, (uint64_t)dc << DSH, (uint64_t)(dc + 1) << DSH, rc,
             31);
@@ -1210,7 +1211,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
       }
       __syncthreads();
       uint2* gat = me(a, f);
-      list_foreach<NT>(L, ncand, [&](uint32_t b, uint32_t x, bool v) {
+      list_foreach<NT, LU>(L, ncand, [&](uint32_t b, uint32_t x, bool v) {
         const uint32_t d = ((b >> 31) ? ND : 0) + ((b & 0x7FFFFFFFu) >> DSH);
         if (v && ((pm[d >> 5] >> (d & 31)) & 1u)) {
           const uint32_t g = pslot[d];
@@ -1223,7 +1224,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
         const uint32_t g = k3.pend_reg[p];
         const List Bp{nullptr, gat + k3.reg_off[g], 0};
         const uint32_t dc = k3.pend_d[p];
-        const SelRes r = select_exact<NT>(
+        const SelRes r = select_exact<NT, LU>(
             sh, scratch, Bp, k3.reg_cnt[g], [](uint32_t, uint32_t) { return true; }, key31,
             [](uint32_t, uint32_t x) -> uint64_t { return x; }, (uint64_t)dc << DSH, (uint64_t)(dc + 1) << DSH,
             k3.pend_r[p], 31);
@@ -1236,7 +1237,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
       const uint32_t s = ci < ncut0 ? 0u : 1u;
       const int j = (s == 0 ? ci : ci - ncut0) + 1;
       const uint64_t rank0 = (uint64_t)j * base[s];
-      const SelRes r = select_exact<NT>(
+      const SelRes r = select_exact<NT, LU>(
           sh, scratch, L, ncand,
           [&](uint32_t b, uint32_t x) { return (b >> 31) == s && (b & 0x7FFFFFFFu) != 0 && kept_of(b, x); }, key31,
           [](uint32_t, uint32_t x) -> uint64_t { return x; }, 1, 1ull << 31, rank0 + 1, 31);
