@@ -35,6 +35,12 @@ CONFIGS = {
     # configs[3]: Llama prefill IF 2048 x 4096 bf16, batch 32
     "c4": dict(kind=1, rows=2048, cols=4096, batch=32, dtype="bf16",
                workload="C4: Llama-class prefill IF 2048x4096 bf16, batch 32"),
+    # configs[4]: 8192 independent client streams (mixed vision/LLM shapes) sharded over the
+    # GPUs of the job (strong scaling: the 8192 are split, not replicated)
+    "c5": dict(mixed=8192, dtype="mixed bf16/fp32",
+               workload="C5: 8192 independent client IF streams, mixed shapes by sid mod 8 (0-3 decode token "
+                        "1x4096 bf16, 4-6 ResNet IF 1024x196 fp32, 7 prefill chunk 256x4096 bf16), sharded over "
+                        "the job's GPUs by longest-processing-time on bytes"),
 }
 CODEC = dict(s=0.9, lam=0.0, m_plus=3, m_minus=3, q_bit=8, delta=0.01)
 
@@ -133,15 +139,13 @@ def _cpu_worker(args):
     return dt, len(blob), int(y.size)
 
 
-def cpu_measure(conf, n_if: int, steps: int, warmup: int, cores: int):
+def cpu_measure_jobs(jobs, raw_per_step: int, steps: int, warmup: int, cores: int):
     """Times the oracle (CPU restatement of the reference) on host cores: each step
-    encodes+decodes a bounded sample of `n_if` IFs of the workload shape in a process pool."""
+    encodes+decodes the IFs of `jobs` (kind, rows, cols, sid, codec) in a process pool."""
     import multiprocessing as mp
 
-    b_in = 4 if conf["dtype"] == "fp32" else 2
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
-        jobs = [(conf["kind"], conf["rows"], conf["cols"], 100000 + i, CODEC) for i in range(n_if)]
         for _ in range(warmup):
             pool.map(_cpu_worker, jobs[: max(1, cores)])
         t0 = time.perf_counter()
@@ -150,19 +154,49 @@ def cpu_measure(conf, n_if: int, steps: int, warmup: int, cores: int):
             res = pool.map(_cpu_worker, jobs)
             plen = sum(r[1] for r in res)
         wall = time.perf_counter() - t0
-    raw = steps * n_if * conf["rows"] * conf["cols"] * b_in
+    raw = steps * raw_per_step
     return dict(value=raw / wall / 1e9, seconds=wall, payload_bytes=plen, raw_bytes=raw)
+
+
+def cpu_measure(conf, n_if: int, steps: int, warmup: int, cores: int):
+    """The oracle on a bounded sample of `n_if` IFs of the workload shape."""
+    if conf.get("mixed"):
+        return cpu_measure_mixed(conf, n_if, steps, warmup, cores)
+    b_in = 4 if conf["dtype"] == "fp32" else 2
+    jobs = [(conf["kind"], conf["rows"], conf["cols"], 100000 + i, CODEC) for i in range(n_if)]
+    return cpu_measure_jobs(jobs, n_if * conf["rows"] * conf["cols"] * b_in, steps, warmup, cores)
+
+
+def _mixed_sample(n_if: int):
+    """Deterministic subsample of the C5 mix keeping its 4:3:1 proportions (every k-th sid)."""
+    from paper_2511_11608_b200.shard import mixed_workload
+
+    mix = mixed_workload(8192)
+    groups = max(1, n_if // 8)
+    gstride = max(1, 1024 // groups)  # 1024 groups of 8 sids in the mix
+    sids = [(g * gstride) * 8 + k for g in range(groups) for k in range(8)]
+    return [(sid,) + tuple(mix[sid]) for sid in sids]
+
+
+def cpu_measure_mixed(conf, n_if: int, steps: int, warmup: int, cores: int):
+    sample = _mixed_sample(n_if)
+    jobs = [(kind, r, c, sid, CODEC) for sid, kind, r, c, _b in sample]
+    raw = sum(r * c * b for _sid, _k, r, c, b in sample)
+    return cpu_measure_jobs(jobs, raw, steps, warmup, cores)
 
 
 def run_reference(args, conf, rank):
     if rank != 0:
         return
     cores = len(os.sched_getaffinity(0))
-    per_if = {"c2": 0.15, "c3": 0.004, "c4": 8.0}[args.config]
-    n_if = max(cores, int(min(conf["batch"], max(cores, 2.0 * cores / per_if))))
-    n_if = min(n_if, conf["batch"])
+    per_if = {"c2": 0.15, "c3": 0.004, "c4": 8.0, "c5": 0.03}[args.config]
+    batch = conf.get("batch", conf.get("mixed"))
+    n_if = max(cores, int(min(batch, max(cores, 2.0 * cores / per_if))))
+    n_if = min(n_if, batch)
+    if conf.get("mixed"):
+        n_if = max(8, n_if // 8 * 8)
     r = cpu_measure(conf, n_if, args.steps, args.warmup, cores)
-    sample = f"{n_if} IFs of the workload shape per step (of {conf['batch']}), {cores} processes, oracle/ NumPy port"
+    sample = f"{n_if} IFs of the workload shape per step (of {batch}), {cores} processes, oracle/ NumPy port"
     line = dict(metric=METRIC, value=round(r["value"], 6), unit="GB/s", n_gpus=args.gpus, steps=args.steps,
                 warmup=args.warmup, ms_per_step=r["seconds"] * 1e3 / max(1, args.steps), higher_is_better=True,
                 scaling="weak", vs_baseline=None, dtype=conf["dtype"], data="synthetic",
@@ -170,7 +204,11 @@ def run_reference(args, conf, rank):
                 impl="reference",
                 cpu_baseline=dict(value=round(r["value"], 6), unit="GB/s", cores=cores, kind="port", sample=sample),
                 e2e=dict(value=round(r["value"], 6), unit="GB/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0),
-                bits_per_element=8.0 * r["payload_bytes"] / (n_if * conf["rows"] * conf["cols"]))
+                bits_per_element=8.0 * r["payload_bytes"] / (
+                    sum(rr * cc for _s, _k, rr, cc, _b in _mixed_sample(n_if)) if conf.get("mixed")
+                    else n_if * conf["rows"] * conf["cols"]))
+    if conf.get("mixed"):
+        line["scaling"] = "strong"
     print(json.dumps(line), flush=True)
 
 
@@ -390,6 +428,166 @@ def run_ours(args, conf, rank, world, local_rank):
         pg.destroy_process_group()
 
 
+def run_ours_mixed(args, conf, rank, world, local_rank):
+    """C5: this rank's share of the 8192 mixed streams (LPT by bytes), one ListEncoder launch
+    sequence per step, pipelined over `depth` slots like the homogeneous configs."""
+    import torch
+
+    import paper_2511_11608_b200 as sif
+    from paper_2511_11608_b200.shard import mixed_workload, shard_streams
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    mix = mixed_workload(conf["mixed"])
+    mine = shard_streams([(r, c, b) for _k, r, c, b in mix], world, rank)
+    xs, seeds = [], []
+    for sid in mine:
+        kind, r, c, b = mix[sid]
+        t = torch.empty((r, c), dtype=torch.float32 if b == 4 else torch.bfloat16, device=dev)
+        sif.synthetic(kind, r, c, sid, out=t)
+        xs.append(t)
+        seeds.append(sid)
+    cfg = sif.CodecConfig(**CODEC)
+    raw_bytes = sum(mix[sid][1] * mix[sid][2] * mix[sid][3] for sid in mine)
+    job_raw = sum(r * c * b for _k, r, c, b in mix)
+    elems = sum(mix[sid][1] * mix[sid][2] for sid in mine)
+    dense_out = 4 * elems
+    pipe = sif.BatchPipeline(xs, cfg, seeds, depth=args.depth, graphs=args.graph)
+    slot0 = pipe.slots[0]
+    payload_total = int(slot0["enc"].out_len.cpu().numpy().sum())
+    alg_enc, alg_dec = raw_bytes + payload_total, payload_total + dense_out
+    stream = torch.cuda.current_stream()
+    pipe.begin()
+    for _ in range(args.warmup):
+        pipe.step()
+    pipe.end()
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        pipe.begin()
+        for _ in range(args.steps):
+            pipe.step()
+        pipe.end()
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    st_ms = t_start.elapsed_time(t_end) / args.steps
+    pipe.check()
+    assert torch.equal(pipe.ys(0), pipe.ys(len(pipe.slots) - 1)), "slots disagree"
+    enc, dec = slot0["enc"], slot0["dec"]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        enc.run()
+        ev[i][1].record(stream)
+        dec.run()
+        ev[i][2].record(stream)
+    torch.cuda.synchronize()
+    enc_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps
+    dec_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps
+    if pg:
+        t = torch.tensor([st_ms, enc_ms, dec_ms], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        st_ms, enc_ms, dec_ms = [float(v) for v in t.cpu().numpy()]
+    kprof = _kernel_profile(sif, lambda: (enc.run(), dec.run()), args.steps)
+    # e2e: pinned host streams -> H2D -> encode -> decode -> D2H (ListRoundTrip)
+    rt = sif.ListRoundTrip([x.cpu() for x in xs], cfg, seeds, parts=4)
+    for _ in range(2):
+        rt.run()
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    e2e_steps = max(2, min(args.steps, 10))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        rt.run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    rt.check()
+    for k in (0, len(xs) // 2, len(xs) - 1):
+        assert torch.equal(rt.y(k), dec.outs[k].cpu()), "e2e decode differs"
+    if pg:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    cpu = None
+    if rank == 0 and args.cpu_baseline:
+        cores = len(os.sched_getaffinity(0))
+        n_if = max(8, min(2048, int(2.0 * cores / 0.03)) // 8 * 8)
+        r = cpu_measure_mixed(conf, n_if, 2, 1, cores)
+        cpu = dict(value=round(r["value"], 6), unit="GB/s", cores=cores, kind="port",
+                   sample=f"{n_if} streams of the mix (every k-th group of 8 sids) x 2 steps, {cores} processes, "
+                          f"oracle/ NumPy port ({r['seconds']:.1f} s)")
+    if rank == 0:
+        hbm, peak_kind = _peaks()
+        step_gbs = (alg_enc + alg_dec) / (st_ms * 1e-3) / 1e9
+        kernels = {}
+        prof_ms = sum(v["ms_total"] for v in kprof.values()) or 1.0
+        for name, v in kprof.items():
+            per = v["ms_total"] / v["launches"]
+            alg = _alg_bytes(name, raw_bytes, payload_total, dense_out)
+            kernels[name] = dict(us_per_launch=round(per * 1e3, 2), launches_per_step=v["launches"] // args.steps,
+                                 share=round(v["ms_total"] / prof_ms, 4), alg_bytes_per_launch=alg,
+                                 alg_gbs=round(alg / (per * 1e-3) / 1e9, 1) if alg else 0.0)
+        cand = [k for k, v in kernels.items() if v["alg_bytes_per_launch"]]
+        dom = max(cand, key=lambda k: kernels[k]["us_per_launch"]) if cand else None
+        roof = None
+        if dom:
+            kd = kernels[dom]
+            roof = dict(bound="hbm", kernel=dom, achieved=kd["alg_gbs"], peak=hbm, unit="GB/s",
+                        frac=round(kd["alg_gbs"] / hbm, 4), traffic=(_ncu_traffic("c5") or {}).get(dom),
+                        peak_source=peak_kind, algorithmic_bytes_per_launch=kd["alg_bytes_per_launch"],
+                        us_per_launch=kd["us_per_launch"], share_of_step=kd["share"],
+                        note="per-launch duration from CUDA events around each library kernel")
+        counts = {}
+        for sid in mine:
+            counts[mix[sid][1:3]] = counts.get(mix[sid][1:3], 0) + 1
+        line = dict(
+            metric=METRIC, value=round(job_raw / (st_ms * 1e-3) / 1e9, 3), unit="GB/s", n_gpus=world,
+            steps=args.steps, warmup=args.warmup, ms_per_step=round(st_ms, 5), higher_is_better=True,
+            scaling="strong", vs_baseline=None, dtype=conf["dtype"],
+            data="synthetic (integer-exact device generator, SURVEY.md §8(d))",
+            config=dict(workload=conf["workload"], codec=CODEC, streams_total=conf["mixed"],
+                        streams_rank0=len(mine), shapes_rank0={f"{r}x{c}": n for (r, c), n in counts.items()},
+                        parallelism=f"dp{world} (streams sharded by LPT on bytes, no collectives)",
+                        launch=("CUDA graph per step" if args.graph else "direct launches") +
+                               f", {args.depth} pipeline slot(s) on separate streams",
+                        l2="per-step inputs %.0f MB/GPU exceed the 126 MB L2; no flush" % (raw_bytes / 1e6)),
+            roofline=roof,
+            roofline_step=dict(achieved=round(step_gbs, 2), frac=round(step_gbs / hbm, 4), unit="GB/s",
+                               algorithmic_bytes_per_step=alg_enc + alg_dec, encode_ms=round(enc_ms, 5),
+                               decode_ms=round(dec_ms, 5)),
+            kernels=kernels,
+            bits_per_element=round(8.0 * payload_total / elems, 6),
+            raw_gbs_per_gpu=round(raw_bytes / (st_ms * 1e-3) / 1e9, 3),
+            e2e=dict(value=round(job_raw / (e2e_ms * 1e-3) / 1e9, 3), unit="GB/s", h2d_bytes_per_step=rt.h2d_bytes,
+                     d2h_bytes_per_step=rt.d2h_bytes, ms_per_step=round(e2e_ms, 4),
+                     api="ListRoundTrip: pinned host streams -> H2D -> encode -> .sif (device) -> decode -> D2H, "
+                         "4 groups pipelined over 3 streams"),
+            gpu_launches=sum(v["launches"] for v in kprof.values()),
+            clocks=clk.summary(),
+            cpu_baseline=cpu,
+        )
+        print(json.dumps(line), flush=True)
+    if pg:
+        pg.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -410,6 +608,9 @@ def main():
     conf = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, conf, rank)
+        return
+    if conf.get("mixed"):
+        run_ours_mixed(args, conf, rank, world, local_rank)
         return
     run_ours(args, conf, rank, world, local_rank)
 

@@ -15,6 +15,7 @@ from .codec import (
     BatchEncoder,
     BatchPipeline,
     ListEncoder,
+    ListRoundTrip,
     CodecConfig,
     HostRoundTrip,
     Payload,

@@ -531,16 +531,29 @@ class BatchPipeline:
     `xs` is the device input batch read by every step (refill it between steps in a real
     server); `ys(slot)` is the decoded output of a slot."""
 
-    def __init__(self, xs: torch.Tensor, cfg: CodecConfig, seeds, depth: int = 2, graphs: bool = True):
+    def __init__(self, xs, cfg: CodecConfig, seeds, depth: int = 2, graphs: bool = True):
+        """xs: a (B, rows, cols) CUDA tensor, or a list of 2-D CUDA tensors of mixed shapes and
+        dtypes (ListEncoder; decoded outputs then live in one flat fp32 buffer per slot)."""
         self.xs = xs
-        self.B, self.rows, self.cols = xs.shape
+        mixed = isinstance(xs, (list, tuple))
+        if mixed:
+            self.B, self.rows, self.cols = len(xs), 0, 0
+        else:
+            self.B, self.rows, self.cols = xs.shape
         seeds = list(seeds)
         self.slots = []
         for _ in range(max(1, depth)):
-            enc = BatchEncoder(xs, cfg, seeds)
-            enc.run().check()
-            lens = enc.out_len.cpu().numpy()
-            dec = BatchDecoder([enc.out.data_ptr() + i * enc.cap for i in range(self.B)], lens, self.rows, self.cols)
+            if mixed:
+                enc = ListEncoder(list(xs), cfg, seeds)
+                enc.run().check()
+                lens = enc.out_len.cpu().numpy()
+                dec = BatchDecoder([enc.out.data_ptr() + o for o in enc.offs], lens, shapes=enc.shapes)
+            else:
+                enc = BatchEncoder(xs, cfg, seeds)
+                enc.run().check()
+                lens = enc.out_len.cpu().numpy()
+                dec = BatchDecoder([enc.out.data_ptr() + i * enc.cap for i in range(self.B)], lens, self.rows,
+                                   self.cols)
             dec.run().check()
             st = torch.cuda.Stream()
             fn = (lambda e=enc, d=dec: (e.run(), d.run()))
@@ -676,6 +689,110 @@ class HostRoundTrip:
     @property
     def d2h_bytes(self) -> int:
         return int(self.y_host.numel() * 4)
+
+
+class ListRoundTrip:
+    """HostRoundTrip for a list of IFs of mixed shapes and dtypes (e.g. one GPU's shard of
+    the mixed vision/LLM streams).  The host inputs sit back to back in one pinned byte
+    buffer (16-byte aligned starts), the decoded fp32 outputs in one pinned float buffer;
+    contiguous groups of streams are pipelined like HostRoundTrip's sub-batches (upload of
+    group i+1 and download of group i-1 overlap the kernels of group i)."""
+
+    def __init__(self, x_host_list: list, cfg: CodecConfig, seeds, parts: int = 4):
+        seeds = list(seeds)
+        self.n = len(x_host_list)
+        self.shapes = [tuple(int(v) for v in t.shape) for t in x_host_list]
+        self.dtypes = [t.dtype for t in x_host_list]
+        nb = [t.numel() * t.element_size() for t in x_host_list]
+        self.in_off, acc = [], 0
+        for b in nb:
+            self.in_off.append(acc)
+            acc += (b + 15) // 16 * 16
+        self.x_host = torch.empty(max(16, acc), dtype=torch.uint8).pin_memory()
+        for t, o, b in zip(x_host_list, self.in_off, nb):
+            self.x_host[o:o + b].copy_(t.contiguous().reshape(-1).view(torch.uint8))
+        ne = [r * c for r, c in self.shapes]
+        self.out_off, acc = [], 0
+        for e in ne:
+            self.out_off.append(acc)
+            acc += (e + 3) // 4 * 4
+        self.y_host = torch.empty(max(4, acc), dtype=torch.float32).pin_memory()
+        self._nb, self._ne = nb, ne
+        parts = max(1, min(parts, self.n))
+        bounds = [self.n * i // parts for i in range(parts + 1)]
+        dev = torch.device("cuda")
+        self.parts = []
+        for i in range(parts):
+            i0, i1 = bounds[i], bounds[i + 1]
+            h0, h1 = self.in_off[i0], (self.in_off[i1] if i1 < self.n else self.x_host.numel())
+            dbuf = torch.empty(max(16, h1 - h0), dtype=torch.uint8, device=dev)
+            xs = [dbuf[self.in_off[k] - h0: self.in_off[k] - h0 + nb[k]].view(self.dtypes[k]).view(self.shapes[k])
+                  for k in range(i0, i1)]
+            enc = ListEncoder(xs, cfg, seeds[i0:i1])
+            o0, o1 = self.out_off[i0], (self.out_off[i1] if i1 < self.n else self.y_host.numel())
+            self.parts.append(dict(i0=i0, i1=i1, h0=h0, h1=h1, o0=o0, o1=o1, dbuf=dbuf, enc=enc, dec=None))
+        self.s_in, self.s_run, self.s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        self._lens_known = False
+
+    def _decoders(self):
+        for p in self.parts:
+            enc = p["enc"]
+            lens = enc.out_len.cpu().numpy()
+            p["dec"] = BatchDecoder([enc.out.data_ptr() + o for o in enc.offs], lens, shapes=enc.shapes)
+        self._lens_known = True
+
+    def run(self):
+        if not self._lens_known:
+            for p in self.parts:
+                p["dbuf"][: p["h1"] - p["h0"]].copy_(self.x_host[p["h0"]:p["h1"]])
+                p["enc"].run()
+            torch.cuda.synchronize()
+            self._decoders()
+        cur = torch.cuda.current_stream()
+        for st in (self.s_in, self.s_run, self.s_out):
+            st.wait_stream(cur)
+        ev_in, ev_run = [], []
+        for p in self.parts:
+            with torch.cuda.stream(self.s_in):
+                p["dbuf"][: p["h1"] - p["h0"]].copy_(self.x_host[p["h0"]:p["h1"]], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(self.s_in)
+                ev_in.append(e)
+        for p, e in zip(self.parts, ev_in):
+            with torch.cuda.stream(self.s_run):
+                self.s_run.wait_event(e)
+                p["enc"].run()
+                p["dec"].run()
+                e2 = torch.cuda.Event()
+                e2.record(self.s_run)
+                ev_run.append(e2)
+        for p, e in zip(self.parts, ev_run):
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(e)
+                n = p["o1"] - p["o0"]
+                self.y_host[p["o0"]:p["o1"]].copy_(p["dec"].out[:n], non_blocking=True)
+        for st in (self.s_in, self.s_run, self.s_out):
+            cur.wait_stream(st)
+        return self
+
+    def check(self):
+        for p in self.parts:
+            p["enc"].check()
+            p["dec"].check()
+        return self
+
+    def y(self, k: int) -> torch.Tensor:
+        """Decoded stream k (pinned host view), after run() and a synchronize."""
+        r, c = self.shapes[k]
+        return self.y_host[self.out_off[k]: self.out_off[k] + r * c].view(r, c)
+
+    @property
+    def h2d_bytes(self) -> int:
+        return int(sum(self._nb))
+
+    @property
+    def d2h_bytes(self) -> int:
+        return int(4 * sum(self._ne))
 
 
 # ---------------------------------------------------------------------------- graphs

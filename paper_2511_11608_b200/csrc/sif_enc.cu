@@ -117,6 +117,7 @@ struct EArgs {
   const uint32_t* seg_base;  // [n+1] prefix of CRC segments per IF
   uint64_t* prof;            // optional phase timestamps of enc_select (16 per IF, debug)
   uint32_t big_ncand;        // IFs with more candidates use the multi-kernel select (0: never)
+  uint32_t* big_list;        // [n] IFs on the multi-kernel select path, [n] = their count
 };
 
 __device__ __forceinline__ void prof_mark(const EArgs& a, int ifi, int k) {
@@ -671,6 +672,7 @@ __global__ void __launch_bounds__(512) enc_prep(EArgs a) {
     const uint32_t k2 = __float_as_uint(__double2float_rd(t));
     lo_neg = k2 > 1 ? k2 : 1u;
   }
+  if (i == 0 && tid == 0) a.big_list[a.n] = 0;
   if (tid == 0) {
     st.lo = lo; st.lo_neg = lo_neg; st.ncand = 0; st.maxkey = 0; st.cnt_lo = 0; st.err = E_NONE; st.flags = 0;
     st.P = 0; st.crc_acc = 0; st.seg_done = 0; st.sel_phase = 0;
@@ -978,6 +980,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
           st.ncand = ncand;
           st.cnt_nz = cnt_nz;
           st.sel_phase = 1;
+          a.big_list[atomicAdd(&a.big_list[a.n], 1u)] = (uint32_t)ifi;  // the gathers visit these IFs only
         }
         return;
       }
@@ -1516,27 +1519,64 @@ __device__ __forceinline__ void warp_range(const EArgs& a, uint32_t& c0, uint32_
 // warp-aggregated (one atomic per region per window).
 template <int G>
 __global__ void __launch_bounds__(CNT) enc_gather(EArgs a) {
+  constexpr uint32_t LCAP = 2048;  // listed IFs whose chunk prefix fits shared memory
+  __shared__ uint32_t lpre[LCAP + 1];
+  __shared__ uint32_t scan_s[33];
   const int lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
-  uint32_t c0, c1;
-  warp_range(a, c0, c1);
-  uint32_t cur = 0xFFFFFFFFu, dtau = 0, nreg = 0, rkey = 0xFFFFFFFFu, roff = 0;
-  for (uint32_t c = c0; c < c1; ++c) {
-    const uint32_t ifi = a.ch_if[c];
-    IfSt& st = a.st[ifi];
-    if (st.sel_phase != (uint32_t)G) continue;
-    const IfInfo& f = a.info[ifi];
-    if (ifi != cur) {
-      cur = ifi;
-      if (G == 1) dtau = (uint32_t)st.dtau;
-      else {
-        nreg = st.nreg;
-        rkey = lane < (int)nreg ? st.reg_key[lane] : 0xFFFFFFFFu;
-        roff = lane < (int)nreg ? st.reg_off[lane] : 0u;
-      }
-    }
-    const uint2* gl = le(a, f);
-    uint2* gat = me(a, f);
+  const uint32_t GW = gridDim.x * (CNT / 32), gw = blockIdx.x * (CNT / 32) + (threadIdx.x >> 5);
+  const uint32_t nbig = min(a.big_list[a.n], LCAP);
+  // only the IFs on the multi-kernel path (big_list): their chunks, concatenated, are split
+  // into one contiguous range per warp (balanced whatever the mix of IF sizes)
+  if (threadIdx.x == 0) lpre[0] = 0;
+  for (uint32_t b0 = 0; b0 < nbig; b0 += CNT) {
+    const uint32_t li = b0 + threadIdx.x;
+    const uint32_t v = li < nbig ? a.info[a.big_list[li]].nch : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan_u32(v, scan_s, &tot);
+    if (li < nbig) lpre[li + 1] = lpre[b0] + ex + v;
+    __syncthreads();
+  }
+  // every IF listed (e.g. a batch of prefill IFs): plain contiguous ranges over all chunks;
+  // otherwise contiguous ranges over the concatenated chunks of the listed IFs
+  const bool all = a.big_list[a.n] >= (uint32_t)a.n;
+  const uint32_t V = all ? (uint32_t)a.nch : lpre[nbig];
+  const uint32_t v0 = (uint32_t)((uint64_t)V * gw / GW), v1 = (uint32_t)((uint64_t)V * (gw + 1) / GW);
+  uint32_t li = 0;
+  if (!all) {
+    uint32_t lo = 0, hi = nbig;  // last li with lpre[li] <= v0
+    while (lo + 1 < hi) { const uint32_t mid = (lo + hi) >> 1; if (lpre[mid] <= v0) lo = mid; else hi = mid; }
+    li = lo;
+  }
+  uint32_t dtau = 0, nreg = 0, rkey = 0xFFFFFFFFu, roff = 0;
+  for (uint32_t v = v0; v < v1 && (all || li < nbig); ++li) {
+   uint32_t ifi, vb, vend, cbeg, cend;
+   if (all) {
+     ifi = a.ch_if[v];
+     vb = v;
+     vend = min(v1, a.info[ifi].ch0 + a.info[ifi].nch);
+     cbeg = vb;
+     cend = vend;
+   } else {
+     ifi = a.big_list[li];
+     vb = v;
+     vend = min(v1, lpre[li + 1]);
+     cbeg = a.info[ifi].ch0 + (vb - lpre[li]);
+     cend = a.info[ifi].ch0 + (vend - lpre[li]);
+   }
+   v = vend;
+   IfSt& st = a.st[ifi];
+   if (st.sel_phase != (uint32_t)G) continue;
+   const IfInfo& f = a.info[ifi];
+   if (G == 1) dtau = (uint32_t)st.dtau;
+   else {
+     nreg = st.nreg;
+     rkey = lane < (int)nreg ? st.reg_key[lane] : 0xFFFFFFFFu;
+     roff = lane < (int)nreg ? st.reg_off[lane] : 0u;
+   }
+   const uint2* gl = le(a, f);
+   uint2* gat = me(a, f);
+   for (uint32_t c = cbeg; c < cend; ++c) {
     const uint32_t my_uo = lane < UNITS ? a.u_off[(uint64_t)c * UNITS + lane] : 0u;
     const uint32_t my_un = lane < UNITS ? a.u_cnt[(uint64_t)c * UNITS + lane] : 0u;
     for (int u = 0; u < UNITS; ++u) {
@@ -1582,6 +1622,7 @@ __global__ void __launch_bounds__(CNT) enc_gather(EArgs a) {
         }
       }
     }
+  }
   }
 }
 

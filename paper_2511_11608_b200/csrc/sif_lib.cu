@@ -93,7 +93,8 @@ inline int num_sms() {
 
 // Workspace sections of an encode plan (all offsets 256-byte aligned).
 struct EncWs {
-  uint64_t info, st, ch_if, ch_e0, u_off, u_cnt, bcnt, bpre, brs, blast, bprev, hist, fixedq, keptoff, segbase, lists;
+  uint64_t info, st, ch_if, ch_e0, u_off, u_cnt, bcnt, bpre, brs, blast, bprev, hist, fixedq, keptoff, segbase, biglist,
+      lists;
 };
 
 EncWs enc_ws(uint64_t n, uint64_t nch, uint64_t maxb, uint64_t nhist, uint64_t nq) {
@@ -115,6 +116,7 @@ EncWs enc_ws(uint64_t n, uint64_t nch, uint64_t maxb, uint64_t nhist, uint64_t n
   w.fixedq = take(nq);
   w.keptoff = take(8 * n);
   w.segbase = take(4 * (n + 1));
+  w.biglist = take(4 * (n + 1));
   w.lists = off;
   return w;
 }
@@ -364,6 +366,7 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   a.ch_blast = reinterpret_cast<int32_t*>(wb + w.blast);
   a.ch_bprev = reinterpret_cast<int32_t*>(wb + w.bprev);
   a.hist = reinterpret_cast<uint32_t*>(wb + w.hist);
+  a.big_list = reinterpret_cast<uint32_t*>(wb + w.biglist);
   a.ws = wb;
   a.s = c->s; a.lam = c->lam; a.delta = c->delta;
   a.m_plus = c->m_plus; a.m_minus = c->m_minus; a.q_bit = c->q_bit; a.mode = c->mode;
