@@ -804,7 +804,7 @@ struct K3Sh {
 template <int PH>
 __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   constexpr int NT = SNT;
-  constexpr int LU = PH > 0 ? 16 : 4;  // loads in flight per thread in list passes (big IFs: deep)
+  constexpr int LU = PH > 0 ? 16 : 8;  // loads in flight per thread in list passes (big IFs: deep)
   extern __shared__ __align__(16) uint8_t dsm_raw[];
   uint32_t* dsm = reinterpret_cast<uint32_t*>(dsm_raw);
   __shared__ K3Sh k3;
