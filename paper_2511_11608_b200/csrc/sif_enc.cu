@@ -820,11 +820,12 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   if (PH > 0) {
     if (st.sel_phase != (uint32_t)PH) return;
     if (PH == 2) {
-      // cut bins gathered into their regions of the gather area: exact selects
+      // cut bins gathered into their regions of the gather area: exact selects, one CTA
+      // per pending cut (blockIdx.y); sel_phase stays 2 until the next run's enc_prep
       auto key31 = [](uint32_t b) -> uint64_t { return b & 0x7FFFFFFFu; };
       const uint32_t np = st.pend_n;
       uint2* gat = me(a, f);
-      for (uint32_t p = 0; p < np; ++p) {
+      for (uint32_t p = blockIdx.y; p < np; p += gridDim.y) {
         const uint32_t g = st.pend_reg[p];
         const List Bp{nullptr, gat + st.reg_off[g], 0};
         const uint32_t dc = st.pend_d[p];
@@ -835,7 +836,6 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
         if (tid == 0) { st.cut_key[st.pend_ci[p]] = r.key; st.cut_idx[st.pend_ci[p]] = (uint32_t)r.sec; }
         __syncthreads();
       }
-      if (tid == 0) st.sel_phase = 0;
       return;
     }
   }

@@ -420,7 +420,11 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
     { ProfScope ps(KP_SELECT1, s); sif::enc_select<1><<<n, sif::SNT, kSmemSelect, s>>>(a); }
     if (!atkf) {
       { ProfScope ps(KP_GATHER2, s); sif::enc_gather<2><<<std::min<unsigned>(wgrid, g_gather), sif::CNT, 0, s>>>(a); }
-      { ProfScope ps(KP_SELECT2, s); sif::enc_select<2><<<n, sif::SNT, kSmemSelect, s>>>(a); }
+      {
+        ProfScope ps(KP_SELECT2, s);
+        const dim3 g2(n, (unsigned)std::max(1, std::min(maxb - 2, 8)));  // one CTA per pending cut
+        sif::enc_select<2><<<g2, sif::SNT, kSmemSelect, s>>>(a);
+      }
     }
   }
   if (!atkf) {
