@@ -22,3 +22,15 @@ def golden():
         meta = json.load(f)
     arrays = dict(np.load(os.path.join(GOLDEN_DIR, "golden.npz")))
     return meta, arrays
+
+
+@pytest.fixture(scope="module")
+def sif():
+    """The package on a CUDA device; a GPU test run without one fails loudly (no fallback)."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test without a CUDA device")
+    import paper_2511_11608_b200 as m
+
+    return m

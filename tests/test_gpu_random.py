@@ -1,0 +1,68 @@
+"""Randomized parity sweep (GPU vs the pinned oracle): 400 seeded random IFs and codec
+configurations, biased to the shapes and value distributions that select different device
+paths -- single-chunk IFs (warp-per-IF select), multi-chunk IFs (CTA select), heavy ties
+(bf16 grids, repeated values), ReLU zeros, one-signed planes, lambda > 0, fixed-Q, extreme
+s / q_bit / delta.  Every payload must equal the oracle's bytes and every decode its bits."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _values(rng, kind, t):
+    if kind == 0:
+        return rng.standard_normal(t).astype(np.float32)
+    if kind == 1:  # bf16 grid: many exact ties
+        v = (rng.standard_normal(t) * 4).astype(np.float32)
+        return (v.view(np.uint32) & 0xFFFF0000).view(np.float32)
+    if kind == 2:  # few distinct values
+        return rng.choice(np.array([-3, -1, -0.5, 0, 0.25, 1, 2, 7], np.float32), size=t)
+    if kind == 3:  # ReLU-like
+        return np.maximum(rng.standard_normal(t).astype(np.float32) - 0.5, 0).astype(np.float32)
+    if kind == 4:  # one sign, integer valued
+        return -rng.integers(1, 50, size=t).astype(np.float32)
+    return np.full(t, np.float32(rng.choice([0.0, 1.5, -2.0])), np.float32)  # constant
+
+
+def _case(rng):
+    if rng.random() < 0.7:
+        rows, cols = int(rng.integers(1, 33)), int(rng.integers(1, 129))
+    else:
+        rows, cols = int(rng.integers(8, 80)), int(rng.integers(64, 400))
+    kind = int(rng.choice(6, p=[0.3, 0.25, 0.15, 0.15, 0.1, 0.05]))
+    x = _values(rng, kind, rows * cols).reshape(rows, cols)
+    s = float(rng.choice([0.0, 1.0, rng.random(), rng.random(), rng.uniform(0.8, 0.99)]))
+    lam = 0.0 if rng.random() < 0.7 else float(rng.uniform(0, 0.9))
+    mp, mm = int(rng.integers(1, 5)), int(rng.integers(1, 5))
+    qb = int(rng.choice([1, 2, 4, 8, 8, 8, 12, 16]))
+    delta = float(rng.choice([0.0, 0.01, 0.01, 0.1, 1.0]))
+    fixed = ()
+    if rng.random() < 0.15:
+        fixed = tuple(int(v) for v in rng.integers(1, 17, size=mp + mm))
+    return x, kind, dict(s=s, lam=lam, m_plus=mp, m_minus=mm, q_bit=qb, delta=delta,
+                         mode="fixed_q" if fixed else "abq", fixed_q=fixed), int(rng.integers(0, 1 << 62))
+
+
+def test_random_sweep_matches_oracle(sif):
+    from oracle import sif_oracle as O
+
+    rng = np.random.default_rng(20261017)
+    fails = []
+    for i in range(400):
+        x, kind, kw, seed = _case(rng)
+        ref = O.encode_bytes(x, O.Cfg(**kw), seed)
+        xt = torch.from_numpy(x).cuda()
+        if kind == 1 and rng.random() < 0.5:
+            xt = xt.to(torch.bfloat16)  # exact: the values are on the bf16 grid
+        p = sif.encode(xt, sif.CodecConfig(**kw), seed=seed)
+        got = sif.serialize(p)
+        if got != ref:
+            fails.append(f"case {i}: shape {x.shape} kind {kind} cfg {kw} seed {seed}: payload differs "
+                         f"({len(got)} vs {len(ref)} bytes)")
+            continue
+        y = sif.decode(p).cpu().numpy()
+        if not np.array_equal(y.view(np.uint32), O.decode_bytes(ref).view(np.uint32)):
+            fails.append(f"case {i}: decode differs")
+    assert not fails, "\n".join(fails[:10]) + f"\n({len(fails)} failures)"
