@@ -602,16 +602,33 @@ __global__ void __launch_bounds__(512) enc_prep(EArgs a) {
     uint32_t* keys = sh8k;
     uint32_t* h = sh8k + 8192;
     const uint32_t n = (uint32_t)T;
+    uint32_t kor = 0, kand = 0xFFFFFFFFu;
     for (uint32_t e = tid; e < n; e += NT) {
       const uint32_t b = f.dtype == SIF_DTYPE_F32 ? __ldg(reinterpret_cast<const uint32_t*>(f.x) + e)
                                                   : (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(f.x) + e) << 16;
       keys[e] = b & 0x7FFFFFFFu;
+      kor |= b & 0x7FFFFFFFu;
+      kand &= b & 0x7FFFFFFFu;
     }
+    // bits equal in every key (e.g. the low 16 bits of bf16 data) need no histogram level
+    kor = __reduce_or_sync(0xFFFFFFFFu, kor);
+    kand = __reduce_and_sync(0xFFFFFFFFu, kand);
+    if ((tid & 31) == 0) { sh.red[tid >> 5] = kor; sh.red[16 + (tid >> 5)] = kand; }
+    __syncthreads();
+    uint32_t vary = 0, cand = 0xFFFFFFFFu;
+    for (int w = 0; w < NT / 32; ++w) { vary |= sh.red[w]; cand &= sh.red[16 + w]; }
+    vary ^= cand;  // bits that differ between some keys
     uint64_t r = kk;
     uint32_t prefix = 0, mask = 0;
     const int shifts[3] = {20, 9, 0}, widths[3] = {11, 11, 9};
     for (int lev = 0; lev < 3; ++lev) {
       const int shf = shifts[lev], nb = 1 << widths[lev];
+      const uint32_t lmask = (uint32_t)(nb - 1) << shf;
+      if ((vary & lmask) == 0) {  // one bin holds every remaining key: its digit is the common bits
+        prefix |= cand & lmask;
+        mask |= lmask;
+        continue;
+      }
       for (int k = tid; k < nb; k += NT) h[k] = 0;
       __syncthreads();
       for (uint32_t e = tid; e < n; e += NT) {
@@ -621,7 +638,7 @@ __global__ void __launch_bounds__(512) enc_prep(EArgs a) {
       __syncthreads();
       find_digit<NT>(sh, h, nb, r);
       prefix |= sh.fd_digit << shf;
-      mask |= (uint32_t)(nb - 1) << shf;
+      mask |= lmask;
       r -= sh.fd_above;
       __syncthreads();
     }
