@@ -504,10 +504,12 @@ static DecWs dec_ws(uint64_t n, uint64_t maxrows) {
 }
 
 // Elements per decode work item (a group of whole rows, or a segment of one long row).
+// Batches of narrow IFs (every K <= 1280) take 1280-element row groups (fewer work items,
+// still 4 CTAs per SM); wider rows are cut into 1024-column segments.
 static uint32_t dec_segw(const sif_dec_desc* d, int n) {
-  (void)d;
-  (void)n;
-  return 1024;
+  for (int i = 0; i < n; ++i)
+    if (d[i].cols > 1280) return 1024;
+  return 1280;
 }
 
 int sif_dec_plan(const sif_dec_desc* d, int n, sif_plan* p) {
