@@ -26,18 +26,18 @@ METRIC = "IF encode+decode GB/s per GPU (and 8-GPU aggregate) vs HBM roofline; b
 
 CONFIGS = {
     # BASELINE.json configs[1]: ResNet-50 IF batch 256 (headline, N=1 workload)
-    "c2": dict(kind=0, rows=1024, cols=196, batch=256, dtype="fp32",
+    "c2": dict(kind=0, rows=1024, cols=196, batch=256, dtype="fp32", depth=4,
                workload="C2: ResNet-50 split-point IF 1x1024x14x14 fp32 (rows=1024 channels, cols=196), "
                         "batch 256 clients per GPU, synthetic ReLU-sparse"),
     # configs[2]: Llama decode-step hidden states, 1 token x 4096, 1024 clients
-    "c3": dict(kind=1, rows=1, cols=4096, batch=1024, dtype="bf16",
+    "c3": dict(kind=1, rows=1, cols=4096, batch=1024, dtype="bf16", depth=8,
                workload="C3: Llama-class decode-step hidden state 1x4096 bf16, 1024 concurrent clients"),
     # configs[3]: Llama prefill IF 2048 x 4096 bf16, batch 32
-    "c4": dict(kind=1, rows=2048, cols=4096, batch=32, dtype="bf16",
+    "c4": dict(kind=1, rows=2048, cols=4096, batch=32, dtype="bf16", depth=4,
                workload="C4: Llama-class prefill IF 2048x4096 bf16, batch 32"),
     # configs[4]: 8192 independent client streams (mixed vision/LLM shapes) sharded over the
     # GPUs of the job (strong scaling: the 8192 are split, not replicated)
-    "c5": dict(mixed=8192, dtype="mixed bf16/fp32",
+    "c5": dict(mixed=8192, dtype="mixed bf16/fp32", depth=2,
                workload="C5: 8192 independent client IF streams, mixed shapes by sid mod 8 (0-3 decode token "
                         "1x4096 bf16, 4-6 ResNet IF 1024x196 fp32, 7 prefill chunk 256x4096 bf16), sharded over "
                         "the job's GPUs by longest-processing-time on bytes"),
@@ -598,14 +598,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch the kernels directly instead of replaying CUDA graphs")
-    ap.add_argument("--depth", type=int, default=3,
-                    help="pipeline slots: consecutive steps overlap on this many streams (1 = sequential)")
+    ap.add_argument("--depth", type=int, default=None,
+                    help="pipeline slots: consecutive steps overlap on this many streams (1 = sequential); "
+                         "default per config (c2 4, c3 8, c4 4, c5 2: measured, tools/sweep_depth*.sh)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     conf = CONFIGS[args.config]
+    if args.depth is None:
+        args.depth = conf.get("depth", 3)
     if args.impl == "reference":
         run_reference(args, conf, rank)
         return

@@ -582,10 +582,12 @@ __device__ __forceinline__ void unit_span(const EArgs& a, const IfInfo& f, uint3
 // ---------------------------------------------------------------------------------------
 // K1: per-IF setup: accumulators and the sampled bracket lo (speculation only: a missed
 // bracket is detected in K3 and the IF re-streamed).
-__global__ void __launch_bounds__(512) enc_prep(EArgs a) {
-  constexpr int NT = 512;
-  constexpr int EXACT_T = 8192;  // IFs up to this size get the exact tau key as lo
-  __shared__ uint32_t sh8k[8192 + 2048];
+// SMALL: a batch whose IFs all fit one chunk (<= 4096 elements): narrow CTAs and only the
+// exact-tau path, so many IFs share an SM.
+template <int NT, bool SMALL>
+__global__ void __launch_bounds__(NT) enc_prep(EArgs a) {
+  constexpr int EXACT_T = SMALL ? CH : 8192;  // IFs up to this size get the exact tau key as lo
+  __shared__ uint32_t sh8k[(SMALL ? CH : 8192) + 2048];
   __shared__ SelSh sh;
   const int i = blockIdx.x, tid = threadIdx.x;
   const IfInfo f = a.info[i];
@@ -600,7 +602,7 @@ __global__ void __launch_bounds__(512) enc_prep(EArgs a) {
   if (T <= EXACT_T && kk > 0) {
     // exact: the kk-th largest |x| key by a 3-level radix select in shared memory
     uint32_t* keys = sh8k;
-    uint32_t* h = sh8k + 8192;
+    uint32_t* h = sh8k + (SMALL ? CH : 8192);
     const uint32_t n = (uint32_t)T;
     uint32_t kor = 0, kand = 0xFFFFFFFFu;
     for (uint32_t e = tid; e < n; e += NT) {
@@ -643,7 +645,7 @@ __global__ void __launch_bounds__(512) enc_prep(EArgs a) {
       __syncthreads();
     }
     lo = prefix > 0 ? prefix : 1u;  // tau == 0: every nonzero is a candidate
-  } else if (T > 32768 && kk > 0 && 2 * kk <= T) {
+  } else if (!SMALL && T > 32768 && kk > 0 && 2 * kk <= T) {
     constexpr int NSECT = 512, SB = 8192, PERT = NSECT / NT;
     for (int k = tid; k < SB; k += NT) sh8k[k] = 0;
     uint32_t sv[PERT][8];

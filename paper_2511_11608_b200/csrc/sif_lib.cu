@@ -239,6 +239,7 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
   memset(p, 0, sizeof(*p));
   uint64_t kmax = 0, nch = 0, nhist = 0, lists = 0, nseg = 0;
   bool tiny = false;  // some IF may take the warp-per-IF select (enc_select_tiny)
+  bool all_small = n > 0;  // every IF fits one chunk: narrow enc_prep
   for (int i = 0; i < n; ++i) {
     if (d[i].rows < 1 || d[i].cols < 1) return SIF_ERR_SHAPE;  // tensor.py:27-28
     const uint64_t T = (uint64_t)d[i].rows * d[i].cols;
@@ -252,6 +253,7 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
     nch += ch;
     if (ch > 1) ++nhist;
     if (ch == 1 && !atkf && c->lam == 0.0 && sif::keep_count(c->s, T) > 0) tiny = true;
+    if (ch > 1) all_small = false;
     lists += up(16 * T, 256);
     nseg += crc_segments(d[i].out_cap);
     if (crc_segments(d[i].out_cap) > (uint64_t)sif::CRC_PIECES_MAX) return SIF_ERR_INVALID_ARG;
@@ -268,8 +270,9 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
   p->cap_smem = (int32_t)nhist;
   p->max_blocks = maxb;
   p->tiles = (int32_t)nch;
-  // bit 0: ATKF-only, bit 1: multi-kernel select, bit 2: warp-per-IF select for small IFs
-  p->flags = atkf | (kmax * 2 > (uint64_t)kBigNcand ? 2 : 0) | (tiny ? 4 : 0);
+  // bit 0: ATKF-only, bit 1: multi-kernel select, bit 2: warp-per-IF select for small IFs,
+  // bit 3: every IF fits one chunk (narrow enc_prep)
+  p->flags = atkf | (kmax * 2 > (uint64_t)kBigNcand ? 2 : 0) | (tiny ? 4 : 0) | (all_small ? 8 : 0);
   p->ws_desc_off = w.info;
   p->ws_aux_off = w.fixedq;
   p->ws_spill_off = w.lists;
@@ -408,7 +411,11 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   const unsigned nch = (unsigned)p->tiles;
   const unsigned n = (unsigned)p->n;
   const unsigned wgrid = std::max(1u, (nch + sif::CNT / 32 - 1) / (sif::CNT / 32));  // >= 1 chunk per warp
-  { ProfScope ps(KP_PREP, s); sif::enc_prep<<<n, 512, 0, s>>>(a); }
+  {
+    ProfScope ps(KP_PREP, s);
+    if (p->flags & 8) sif::enc_prep<128, true><<<n, 128, 0, s>>>(a);  // every IF fits one chunk
+    else sif::enc_prep<512, false><<<n, 512, 0, s>>>(a);
+  }
   { ProfScope ps(KP_STREAM, s); sif::enc_stream<<<std::min<unsigned>(nch, g_stream), sif::CNT, kSmemStream, s>>>(a); }
   if (p->flags & 4) {
     ProfScope ps(KP_SELECT_TINY, s);
