@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
         // pair parameters in shared memory (entry base stored as lo - exclusive prefix)
         pa[w][lane] = make_uint4((uint32_t)cbit, (uint32_t)(cbit >> 32), (uint32_t)qbit, (uint32_t)(qbit >> 32));
         pb[w][lane] = make_uint4(lo, q, m0v.z, m0v.w);
-        pc[w][lane] = make_uint2(rs0, ri | (b << 10) | (b >= mp ? 0x80000000u : 0u));
+        pc[w][lane] = make_uint2(rs0, ri | (b << 11) | (b >= mp ? 0x80000000u : 0u));  // ri < segw <= 2047
       }
       const uint32_t inc = warp_incl_scan_u32(cnt);
       const uint32_t M = __shfl_sync(0xFFFFFFFFu, inc, 31);
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
         const uint2 C = pc[w][jl];
         const uint64_t cbj = (uint64_t)A.x | ((uint64_t)A.y << 32);
         const uint32_t e = B.x + m;
-        const uint32_t rij = C.y & 0x3FFu, bj = (C.y >> 10) & 0x1FFFFu;
+        const uint32_t rij = C.y & 0x7FFu, bj = (C.y >> 11) & 0xFFFFFu;
         const bool minus = (C.y >> 31) != 0;
         // col and code fields are fetched together (one memory round trip per window)
         const uint64_t qbj = (uint64_t)A.z | ((uint64_t)A.w << 32);

@@ -66,3 +66,29 @@ def test_random_sweep_matches_oracle(sif):
         if not np.array_equal(y.view(np.uint32), O.decode_bytes(ref).view(np.uint32)):
             fails.append(f"case {i}: decode differs")
     assert not fails, "\n".join(fails[:10]) + f"\n({len(fails)} failures)"
+
+
+def test_path_boundaries_match_oracle(sif):
+    """Shapes and keep counts at the switch points of the device paths: one chunk (4096
+    elements) vs two, the warp-select capacity (1024 candidates), decode row groups of 1280
+    vs 1024-column segments, single rows and single columns."""
+    from oracle import sif_oracle as O
+
+    rng = np.random.default_rng(7)
+    cases = [((1, 4096), 0.75), ((1, 4096), 0.76), ((1, 4096), 0.5), ((1, 4097), 0.9), ((2, 2048), 0.9),
+             ((1, 1280), 0.5), ((1, 1281), 0.5), ((3, 1279), 0.2), ((2, 1280), 0.0), ((4096, 1), 0.9),
+             ((64, 64), 0.75), ((1, 1), 0.0), ((1, 1), 1.0), ((1, 2), 0.5)]
+    fails = []
+    for (r, c), s in cases:
+        for kind in (0, 1):
+            x = _values(rng, kind, r * c).reshape(r, c)
+            kw = dict(s=s, m_plus=3, m_minus=2, q_bit=8, delta=0.01)
+            ref = O.encode_bytes(x, O.Cfg(**kw), 11)
+            p = sif.encode(torch.from_numpy(x).cuda(), sif.CodecConfig(**kw), seed=11)
+            if sif.serialize(p) != ref:
+                fails.append(f"{(r, c)} s={s} kind={kind}: payload differs")
+                continue
+            y = sif.decode(p).cpu().numpy()
+            if not np.array_equal(y.view(np.uint32), O.decode_bytes(ref).view(np.uint32)):
+                fails.append(f"{(r, c)} s={s} kind={kind}: decode differs")
+    assert not fails, "\n".join(fails)
