@@ -77,7 +77,8 @@ def test_path_boundaries_match_oracle(sif):
     rng = np.random.default_rng(7)
     cases = [((1, 4096), 0.75), ((1, 4096), 0.76), ((1, 4096), 0.5), ((1, 4097), 0.9), ((2, 2048), 0.9),
              ((1, 1280), 0.5), ((1, 1281), 0.5), ((3, 1279), 0.2), ((2, 1280), 0.0), ((4096, 1), 0.9),
-             ((64, 64), 0.75), ((1, 1), 0.0), ((1, 1), 1.0), ((1, 2), 0.5)]
+             ((64, 64), 0.75), ((1, 1), 0.0), ((1, 1), 1.0), ((1, 2), 0.5), ((1300, 1), 0.7),
+             ((2561, 2), 0.9), ((3000, 3), 0.95), ((427, 3), 0.5), ((5, 1281), 0.9)]
     fails = []
     for (r, c), s in cases:
         for kind in (0, 1):
