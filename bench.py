@@ -380,9 +380,11 @@ def run_ours(args, conf, rank, world, local_rank):
             kernels[name] = dict(us_per_launch=round(per * 1e3, 2), launches_per_step=v["launches"] // args.steps,
                                  share=round(v["ms_total"] / prof_ms, 4), alg_bytes_per_launch=alg,
                                  alg_gbs=round(alg / (per * 1e-3) / 1e9, 1) if alg else 0.0)
-        # dominant kernel: the longest one that carries compulsory (algorithmic) traffic
+        # dominant kernel: the one that moves the most compulsory (algorithmic) bytes (ties:
+        # the longer one) -- the decode scatter writing the dense IF in every config
         cand = [k for k, v in kernels.items() if v["alg_bytes_per_launch"]]
-        dom = max(cand, key=lambda k: kernels[k]["us_per_launch"]) if cand else None
+        dom = max(cand, key=lambda k: (kernels[k]["alg_bytes_per_launch"], kernels[k]["us_per_launch"])) \
+            if cand else None
         traffic = (_ncu_traffic(args.config) or {}).get(dom) if dom else None
         roof = None
         if dom:
@@ -545,7 +547,8 @@ def run_ours_mixed(args, conf, rank, world, local_rank):
                                  share=round(v["ms_total"] / prof_ms, 4), alg_bytes_per_launch=alg,
                                  alg_gbs=round(alg / (per * 1e-3) / 1e9, 1) if alg else 0.0)
         cand = [k for k, v in kernels.items() if v["alg_bytes_per_launch"]]
-        dom = max(cand, key=lambda k: kernels[k]["us_per_launch"]) if cand else None
+        dom = max(cand, key=lambda k: (kernels[k]["alg_bytes_per_launch"], kernels[k]["us_per_launch"])) \
+            if cand else None
         roof = None
         if dom:
             kd = kernels[dom]
