@@ -199,7 +199,7 @@ __device__ __forceinline__ void flush_flags(const DecArgs& a, int cur, uint32_t 
 // an element held by both planes is summed in float64 (plus value recovered from its
 // block).  Within a window plus entries are written before minus entries.  The buffer is
 // stored with 16-byte streaming stores and re-zeroed in the same pass.
-__global__ void __launch_bounds__(DNT, 4) sif_scatter_kernel(DecArgs a) {
+__global__ void __launch_bounds__(DNT, 3) sif_scatter_kernel(DecArgs a) {
   extern __shared__ __align__(16) uint8_t dsm_raw[];
   __shared__ uint4 pa[DNT / 32][32], pb[DNT / 32][32];
   __shared__ uint2 pc[DNT / 32][32];
