@@ -1654,7 +1654,7 @@ struct K4W {
   uint32_t cnt[MAXB], mn[MAXB], mx[MAXB], xl[MAXB], pos[MAXB];
 };
 
-__global__ void __launch_bounds__(CNT) enc_members(EArgs a) {
+__global__ void __launch_bounds__(CNT, 5) enc_members(EArgs a) {
   __shared__ KeptCtx kcs[CNT / 32];
   __shared__ K4W wst[CNT / 32];
   __shared__ int8_t sblk[CNT / 32][CH];
