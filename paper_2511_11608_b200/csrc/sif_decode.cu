@@ -115,7 +115,7 @@ __global__ void sif_parse_kernel(DecArgs a) {
 // One warp per 2 KiB CRC-32 piece of a stream (pieces aligned to the end of [4, len-4)):
 // raw piece CRC shifted over the pieces after it (kPieceShift) and XOR-combined into the
 // stream's accumulator (GF(2) linearity).
-__global__ void __launch_bounds__(DNT) sif_dcrc_kernel(DecArgs a) {
+__global__ void __launch_bounds__(DNT, 8) sif_dcrc_kernel(DecArgs a) {
   __shared__ uint32_t t4[1024];
   __shared__ uint32_t stage[DNT / 32][544];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

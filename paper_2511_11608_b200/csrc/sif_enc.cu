@@ -2198,7 +2198,7 @@ __global__ void __launch_bounds__(CNT, 4) enc_pack(EArgs a) {
 // the pieces after it with one multiply (kPieceShift) and XORs it into the IF's
 // accumulator (GF(2) linearity).  Piece slots are sized from the capacity; the warp that
 // completes an IF's last slot writes the CRC, the length and the status.
-__global__ void __launch_bounds__(CNT) enc_crc(EArgs a) {
+__global__ void __launch_bounds__(CNT, 6) enc_crc(EArgs a) {
   __shared__ uint32_t t4[1024];
   __shared__ uint32_t stage[CNT / 32][544];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
