@@ -1831,9 +1831,10 @@ __global__ void __launch_bounds__(CNT, 4) enc_abq(EArgs a) {
   warp_range(a, c0, c1);
   uint32_t cur = 0xFFFFFFFFu;
   int B = 0;
+  bool skipif = false;  // pass B: no block of the current IF needs the lower levels
   auto flush = [&]() {
     __syncwarp();
-    if (cur != 0xFFFFFFFFu) {
+    if (cur != 0xFFFFFFFFu && !skipif) {
       IfSt& st = a.st[cur];
       for (int k = lane; k < B * 16; k += 32)
         if (acc_s[k]) atomicAdd((unsigned long long*)&st.S[k], (unsigned long long)acc_s[k]);
@@ -1848,12 +1849,21 @@ __global__ void __launch_bounds__(CNT, 4) enc_abq(EArgs a) {
     if (ifi != cur) {
       flush();
       B = (int)st.B;
+      cur = ifi;
+      skipif = false;
+      if (!FIRST) {  // pass B: nothing to do unless some block stays within delta at q_bit-1
+        bool act = false;
+        if (lane < B && st.bmin[lane] < st.bmax[lane])
+          act = !(__ddiv_rn((double)st.S[lane * 16 + qb - 1], (double)st.bcount[lane]) > a.delta);
+        skipif = !__any_sync(0xFFFFFFFFu, act);
+        if (skipif) continue;
+      }
       for (int k = lane; k < B * 16; k += 32) acc_s[k] = 0;
       for (int k = lane; k < B * 16; k += 32) {
         const int b = k >> 4, q = (k & 15) + 1;
         const uint32_t m0 = st.bmin[b], m1 = st.bmax[b];
         const double vmin = (double)__uint_as_float(m0), vmax = (double)__uint_as_float(m1);
-        if (q <= qb) {
+        if (q <= qb && (!FIRST || q >= qb - 1)) {  // pass A needs the scales of q_bit and q_bit-1 only
           const double o = __ddiv_rn(__dsub_rn(vmax, vmin), (double)((1u << q) - 1u));
           par[b].o[q] = o;
           par[b].inv[q] = __drcp_rn(o);
@@ -1869,9 +1879,9 @@ __global__ void __launch_bounds__(CNT, 4) enc_abq(EArgs a) {
           par[b].act = act ? 1u : 0u;
         }
       }
-      cur = ifi;
       __syncwarp();
     }
+    if (skipif) continue;
     const uint32_t bcnt = lane < B ? a.ch_bcnt[(uint64_t)c * maxb + lane] : 0u;
     const uint32_t brs = lane < B ? a.ch_brs[(uint64_t)c * maxb + lane] : 0u;
     const uint2* gm = me(a, f) + (uint64_t)(c - f.ch0) * CH;
