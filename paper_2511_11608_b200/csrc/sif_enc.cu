@@ -1654,15 +1654,13 @@ struct K4W {
   uint32_t cnt[MAXB], mn[MAXB], mx[MAXB], xl[MAXB], pos[MAXB];
 };
 
-__global__ void __launch_bounds__(CNT, 5) enc_members(EArgs a) {
+__global__ void __launch_bounds__(CNT, 6) enc_members(EArgs a) {
   __shared__ KeptCtx kcs[CNT / 32];
   __shared__ K4W wst[CNT / 32];
-  __shared__ int8_t sblk[CNT / 32][CH];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t lt = (1u << lane) - 1u;
   KeptCtx& kc = kcs[w];
   K4W& ws = wst[w];
-  int8_t* bk = sblk[w];
   uint32_t c0, c1;
   warp_range(a, c0, c1);
   uint32_t cur = 0xFFFFFFFFu;
@@ -1740,7 +1738,6 @@ __global__ void __launch_bounds__(CNT, 5) enc_members(EArgs a) {
           int blk = -1;
           if (j < un) {
             if (kc.kept(e.x, e.y)) blk = kc.block_of(e.x, e.y);
-            if (!one) bk[i + j] = (int8_t)blk;
           }
           const uint32_t peers = __match_any_sync(0xFFFFFFFFu, blk);
           const bool last = blk >= 0 && lane == 31 - __clz(peers);
@@ -1782,10 +1779,10 @@ __global__ void __launch_bounds__(CNT, 5) enc_members(EArgs a) {
         uint2 ev[2];
         int bv[2];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < 2; ++h) {  // block ids recomputed (the two-pass case is rare)
           const uint32_t j = j0 + 32 * h + lane;
-          bv[h] = j < un ? (int)bk[i + j] : -1;
-          ev[h] = bv[h] >= 0 ? __ldg(gl + uo + j) : make_uint2(0, 0);
+          ev[h] = j < un ? __ldg(gl + uo + j) : make_uint2(0, 0);
+          bv[h] = (j < un && kc.kept(ev[h].x, ev[h].y)) ? kc.block_of(ev[h].x, ev[h].y) : -1;
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
