@@ -2192,8 +2192,12 @@ __global__ void __launch_bounds__(CNT, 4) enc_pack(EArgs a) {
         if (valid)
           for (int32_t r = rp + 1; r <= (int32_t)row; ++r) st_u32_le(out, p.rp + 4ull * (uint32_t)r, p0 + j);
         rprev = __shfl_sync(0xFFFFFFFFu, (int32_t)row, (int)nv - 1);
-        pack_window(out32, pbuf[w][0], col, valid, cb, Rc, Ec, j0, nv, cyc);
-        pack_window(out32, pbuf[w][1], code, valid, p.q, Rq, Eq, j0, nv, cyq);
+        // 8-bit fields are whole bytes of the MSB-first stream (bitstream.py:12-20): plain
+        // byte stores, no word assembly (sections start on byte boundaries)
+        if (cb == 8) { if (valid) out[(Rc >> 3) + j] = (uint8_t)col; }
+        else pack_window(out32, pbuf[w][0], col, valid, cb, Rc, Ec, j0, nv, cyc);
+        if (p.q == 8) { if (valid) out[(Rq >> 3) + j] = (uint8_t)code; }
+        else pack_window(out32, pbuf[w][1], code, valid, p.q, Rq, Eq, j0, nv, cyq);
       }
     }
   }
