@@ -93,3 +93,31 @@ def test_path_boundaries_match_oracle(sif):
             if not np.array_equal(y.view(np.uint32), O.decode_bytes(ref).view(np.uint32)):
                 fails.append(f"{(r, c)} s={s} kind={kind}: decode differs")
     assert not fails, "\n".join(fails)
+
+
+def test_multi_kernel_select_path_matches_oracle(sif):
+    """IFs with more than 128K candidates take the multi-kernel select (enc_gather<1/2>,
+    enc_select<1/2>, one CTA per pending cut).  One C4-shaped prefill IF (2048x4096 bf16) and
+    one fp32 IF with heavy ties, batched together, must match the oracle byte for byte; the
+    ATKF-only entry point (atkf_filter) must keep the oracle's indices on the same IF."""
+    from oracle import sif_oracle as O
+    from oracle.synth import KIND_LLM, synth
+
+    x1 = synth(KIND_LLM, 2048, 4096, 5)  # bf16 values widened to fp32
+    rng = np.random.default_rng(3)
+    x2 = rng.choice(np.array([-4, -2, -1, 1, 2, 3, 5], np.float32), size=(768, 2048)).astype(np.float32)
+    cfgs = [dict(s=0.9, m_plus=3, m_minus=3, q_bit=8, delta=0.01),
+            dict(s=0.8, lam=0.0, m_plus=4, m_minus=2, q_bit=6, delta=0.2)]
+    for kw in cfgs:
+        refs = [O.encode_bytes(x, O.Cfg(**kw), sd) for x, sd in ((x1, 5), (x2, 6))]
+        xs = [torch.from_numpy(x1).cuda().to(torch.bfloat16), torch.from_numpy(x2).cuda()]
+        ps = sif.encode_list(xs, sif.CodecConfig(**kw), [5, 6])
+        for p, ref, name in zip(ps, refs, ("prefill", "ties")):
+            assert p.to_bytes() == ref, f"{name} {kw}: payload differs"
+        ys = sif.decode_list(ps)
+        for y, ref in zip(ys, refs):
+            assert np.array_equal(y.cpu().numpy().view(np.uint32), O.decode_bytes(ref).view(np.uint32))
+    a = sif.atkf_filter(torch.from_numpy(x1).cuda().to(torch.bfloat16), 0.9, 0.0, 5)
+    ra = O.atkf(x1.reshape(-1), 0.9, 0.0, 5)
+    assert np.array_equal(a.kept_indices.cpu().numpy(), ra.kept)
+    assert a.tau == ra.tau
