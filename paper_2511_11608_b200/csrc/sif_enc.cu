@@ -118,6 +118,7 @@ struct EArgs {
   uint64_t* prof;            // optional phase timestamps of enc_select (16 per IF, debug)
   uint32_t big_ncand;        // IFs with more candidates use the multi-kernel select (0: never)
   uint32_t* big_list;        // [n] IFs on the multi-kernel select path, [n] = their count
+  uint32_t inject;           // test-only fault injection (SIF_TEST_INJECT): bit 0 = sampled bracket misses
 };
 
 __device__ __forceinline__ void prof_mark(const EArgs& a, int ifi, int k) {
@@ -684,6 +685,7 @@ __global__ void __launch_bounds__(NT) enc_prep(EArgs a) {
     find_digit<NT>(sh, sh8k, SB, (uint64_t)rlo);
     lo = sh.fd_found ? (sh.fd_digit << 18) : 1u;
     if (lo == 0) lo = 1;
+    if (a.inject & 1u) lo = 0x7F000000u;  // fault injection (tests): the bracket misses, K3 re-streams
   }
   uint32_t lo_neg = lo;
   if (a.lam > 0.0 && lo > 1) {

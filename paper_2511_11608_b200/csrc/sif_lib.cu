@@ -370,6 +370,7 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   a.ch_bprev = reinterpret_cast<int32_t*>(wb + w.bprev);
   a.hist = reinterpret_cast<uint32_t*>(wb + w.hist);
   a.big_list = reinterpret_cast<uint32_t*>(wb + w.biglist);
+  a.inject = getenv("SIF_TEST_INJECT") ? (uint32_t)atoi(getenv("SIF_TEST_INJECT")) : 0u;  // tests only
   a.ws = wb;
   a.s = c->s; a.lam = c->lam; a.delta = c->delta;
   a.m_plus = c->m_plus; a.m_minus = c->m_minus; a.q_bit = c->q_bit; a.mode = c->mode;

@@ -122,3 +122,35 @@ def test_multi_kernel_select_path_matches_oracle(sif):
     ra = O.atkf(x1.reshape(-1), 0.9, 0.0, 5)
     assert np.array_equal(a.kept_indices.cpu().numpy(), ra.kept)
     assert a.tau == ra.tau
+
+
+def test_bracket_miss_restream_matches_oracle():
+    """The sampled tau bracket of enc_prep is speculative; when it misses (fewer than k
+    elements above it) enc_select re-streams the IF with every nonzero as a candidate.  The
+    miss is forced here (SIF_TEST_INJECT=1, read per launch by the library) on multi-chunk
+    IFs, including one that then exceeds the multi-kernel threshold; payloads must still
+    equal the oracle's.  Runs in a subprocess so the injection cannot leak."""
+    import subprocess
+    import sys
+
+    code = r"""
+import numpy as np, torch, sys
+sys.path.insert(0, '.')
+import paper_2511_11608_b200 as sif
+from oracle import sif_oracle as O
+rng = np.random.default_rng(11)
+xs = [rng.standard_normal((300, 200)).astype(np.float32),
+      np.maximum(rng.standard_normal((1024, 196)).astype(np.float32) - 0.3, 0).astype(np.float32),
+      rng.choice(np.array([-3, -1, 1, 2, 4], np.float32), size=(600, 1024)).astype(np.float32)]
+kw = dict(s=0.9, m_plus=3, m_minus=2, q_bit=8, delta=0.01)
+ps = sif.encode_list([torch.from_numpy(x).cuda() for x in xs], sif.CodecConfig(**kw), [1, 2, 3])
+for p, x, sd in zip(ps, xs, (1, 2, 3)):
+    assert p.to_bytes() == O.encode_bytes(x, O.Cfg(**kw), sd), sd
+print("ok")
+"""
+    import os
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SIF_TEST_INJECT="1")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-4000:]
