@@ -108,7 +108,8 @@ def test_multi_kernel_select_path_matches_oracle(sif):
     x2 = rng.choice(np.array([-4, -2, -1, 1, 2, 3, 5], np.float32), size=(768, 2048)).astype(np.float32)
     cfgs = [dict(s=0.9, m_plus=3, m_minus=3, q_bit=8, delta=0.01),
             dict(s=0.8, lam=0.0, m_plus=4, m_minus=2, q_bit=6, delta=0.2),
-            dict(s=0.9, lam=0.3, m_plus=2, m_minus=3, q_bit=8, delta=0.05)]  # lambda > 0: generic select
+            dict(s=0.9, lam=0.3, m_plus=2, m_minus=3, q_bit=8, delta=0.05),  # lambda > 0: generic select
+            dict(s=0.85, m_plus=3, m_minus=3, q_bit=8, mode="fixed_q", fixed_q=(9, 6, 4, 8, 5, 3))]
     for kw in cfgs:
         refs = [O.encode_bytes(x, O.Cfg(**kw), sd) for x, sd in ((x1, 5), (x2, 6))]
         xs = [torch.from_numpy(x1).cuda().to(torch.bfloat16), torch.from_numpy(x2).cuda()]
