@@ -330,8 +330,14 @@ __global__ void __launch_bounds__(DNT, 3) sif_scatter_kernel(DecArgs a) {
         const uint64_t qbj = (uint64_t)A.z | ((uint64_t)A.w << 32);
         uint32_t col = 0, code = 0;
         if (m < M) {
-          col = ld_field(in, cbj + (uint64_t)e * cb, cb);
-          code = ld_field(in, qbj + (uint64_t)e * B.y, B.y);
+          // IFs with 8-bit cols (K <= 256): byte fields are single byte loads
+          if (cb == 8) {
+            col = (uint32_t)__ldg(in + (cbj >> 3) + e);
+            code = B.y == 8 ? (uint32_t)__ldg(in + (qbj >> 3) + e) : ld_field(in, qbj + (uint64_t)e * B.y, B.y);
+          } else {
+            col = ld_field(in, cbj + (uint64_t)e * cb, cb);
+            code = ld_field(in, qbj + (uint64_t)e * B.y, B.y);
+          }
         }
         // the previous entry e-1 of the same pair sits in the previous lane of this window
         // (lane 0: the last lane of the previous window)
