@@ -462,7 +462,7 @@ __device__ __forceinline__ void load_unit(const void* xp, uint32_t dtype, uint32
     const uint32_t* x = reinterpret_cast<const uint32_t*>(xp) + e0 + b;
     if (b + 16 <= n) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) raw.r[j] = __ldg(reinterpret_cast<const uint4*>(x) + j);
+      for (int j = 0; j < 4; ++j) raw.r[j] = __ldcs(reinterpret_cast<const uint4*>(x) + j);  // read once: evict-first
     } else {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -478,7 +478,7 @@ __device__ __forceinline__ void load_unit(const void* xp, uint32_t dtype, uint32
     raw.r[3] = make_uint4(0, 0, 0, 0);
     if (b + 16 <= n) {
 #pragma unroll
-      for (int j = 0; j < 2; ++j) raw.r[j] = __ldg(reinterpret_cast<const uint4*>(x) + j);
+      for (int j = 0; j < 2; ++j) raw.r[j] = __ldcs(reinterpret_cast<const uint4*>(x) + j);  // read once: evict-first
     } else {
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
