@@ -1715,7 +1715,7 @@ __global__ void __launch_bounds__(CNT, 6) enc_members(EArgs a) {
     {
       const uint32_t uo = __shfl_sync(0xFFFFFFFFu, my_uo, 0), un = __shfl_sync(0xFFFFFFFFu, my_un, 0);
 #pragma unroll
-      for (int h = 0; h < 2; ++h) nx[h] = 32 * h + lane < un ? __ldg(gl + uo + 32 * h + lane) : make_uint2(0, 0);
+      for (int h = 0; h < 2; ++h) nx[h] = 32 * h + lane < un ? __ldcs(gl + uo + 32 * h + lane) : make_uint2(0, 0);
     }
     for (int u = 0; u < UNITS; ++u) {
       const uint32_t uo = __shfl_sync(0xFFFFFFFFu, my_uo, u), un = __shfl_sync(0xFFFFFFFFu, my_un, u);
@@ -1723,7 +1723,7 @@ __global__ void __launch_bounds__(CNT, 6) enc_members(EArgs a) {
       if (u + 1 < UNITS) {
         const uint32_t uo1 = __shfl_sync(0xFFFFFFFFu, my_uo, u + 1), un1 = __shfl_sync(0xFFFFFFFFu, my_un, u + 1);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) nx[h] = 32 * h + lane < un1 ? __ldg(gl + uo1 + 32 * h + lane) : make_uint2(0, 0);
+        for (int h = 0; h < 2; ++h) nx[h] = 32 * h + lane < un1 ? __ldcs(gl + uo1 + 32 * h + lane) : make_uint2(0, 0);
       }
       for (uint32_t j0 = 0; j0 < un; j0 += 64) {
         // two windows in flight: both loads issued before either is used
@@ -1731,7 +1731,7 @@ __global__ void __launch_bounds__(CNT, 6) enc_members(EArgs a) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const uint32_t j = j0 + 32 * h + lane;
-          ev[h] = j0 == 0 ? cu[h] : (j < un ? __ldg(gl + uo + j) : make_uint2(0, 0));
+          ev[h] = j0 == 0 ? cu[h] : (j < un ? __ldcs(gl + uo + j) : make_uint2(0, 0));
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -2177,13 +2177,13 @@ __global__ void __launch_bounds__(CNT, 4) enc_pack(EArgs a) {
       const uint32_t Rc = (uint32_t)p.bc + p0 * cb, Rq = (uint32_t)p.bq + p0 * p.q;
       const uint32_t Ec = Rc + n * cb, Eq = Rq + n * p.q;
       Carry cyc{0xFFFFFFFFu, 0u}, cyq{0xFFFFFFFFu, 0u};
-      uint2 enext = lane < n ? __ldg(gm + rs + lane) : make_uint2(0, 0);
+      uint2 enext = lane < n ? __ldcs(gm + rs + lane) : make_uint2(0, 0);
       for (uint32_t j0 = 0; j0 < n; j0 += 32) {
         const uint32_t j = j0 + lane;
         const uint32_t nv = min(32u, n - j0);
         const bool valid = j < n;
         const uint2 e = enext;  // prefetched; the next window's entry is requested now
-        if (j0 + 32 < n) enext = j + 32 < n ? __ldg(gm + rs + j + 32) : make_uint2(0, 0);
+        if (j0 + 32 < n) enext = j + 32 < n ? __ldcs(gm + rs + j + 32) : make_uint2(0, 0);
         const uint32_t key = e.x & 0x7FFFFFFFu;
         const uint32_t x = e.y;
         const uint32_t code = (valid && !p.degen) ? quant_code(key, p.vmin, p.o64, p.inv, lv_) : 0u;
