@@ -1895,15 +1895,15 @@ __global__ void __launch_bounds__(CNT, 4) enc_abq(EArgs a) {
         const int q = qb - 1;
         const double oq = par[b].o[q], iq = par[b].inv[q];
         uint32_t acc = 0;
-        for (uint32_t i0 = 0; i0 < nb; i0 += 64) {
-          uint32_t kv[2];
+        for (uint32_t i0 = 0; i0 < nb; i0 += 128) {
+          uint32_t kv[4];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < 4; ++h) {
             const uint32_t i = i0 + 32 * h + lane;
             kv[h] = i < nb ? __ldg(&gm[rs + i].x) & 0x7FFFFFFFu : 0xFFFFFFFFu;
           }
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < 4; ++h) {
             if (kv[h] != 0xFFFFFFFFu) {
               const uint32_t r = quant_code(kv[h], vmin, oref, iref, lref) >> 1;
               const uint32_t cq = quant_code(kv[h], vmin, oq, iq, (1u << q) - 1u);
