@@ -71,13 +71,19 @@ typedef struct sif_enc_desc {
 } sif_enc_desc;
 
 /* One .sif stream to decode into a dense fp32 rows x cols tensor.  `in` is 4-byte
- * aligned device memory holding in_len bytes; rows/cols must match the stream header. */
+ * aligned device memory; rows/cols must match the stream header.
+ * in_len_dev == NULL: the stream is in_len bytes long.
+ * in_len_dev != NULL: in_len is the capacity of `in` and the stream length is read ON THE
+ * DEVICE from *in_len_dev when the decode runs -- point it at the encoder's d_out_len[i]
+ * so a plan (or a captured CUDA graph) of encode -> decode stays valid when the inputs,
+ * and therefore the payload lengths, change from one run to the next. */
 typedef struct sif_dec_desc {
   const uint8_t* in;
   uint64_t in_len;
   float* out;
   uint32_t rows;
   uint32_t cols;
+  const uint64_t* in_len_dev;
 } sif_dec_desc;
 
 /* Launch plan for a batch (host-only computation, POD). */
@@ -133,11 +139,12 @@ int sif_dec_run(const sif_plan* plan, int parse_only, void* d_ws, int32_t* d_sta
 int sif_decode_batched(const sif_dec_desc* descs, int n, int parse_only, void* d_ws,
                        size_t ws_bytes, int32_t* d_status, void* stream);
 
-/* Block table written by decode/parse (one row per block, plus blocks first):
- * {q, nnz, rowptr_off, cols_off, codes_off, o_bits, vmin_bits, reserved} as uint32,
- * for IF i at d_ws + plan.ws_aux_off + i * sif_dec_table_stride(plan) bytes; the first
- * row holds {status, rows, cols, m_plus, m_minus, mode, q_bit, nblocks}. */
-uint64_t sif_dec_table_stride(const sif_plan* plan);
+/* Block table written by decode/parse: 64-byte rows of uint32.  Row 0 holds {status,
+ * rows, cols, m_plus, m_minus, mode, q_bit, nblocks}; row 1 {framing status, crc, len lo,
+ * len hi, reasons...}; then one row per block (plus blocks first) {q, nnz, o_bits,
+ * vmin_bits, rowptr_off (u64), cols_off (u64), codes_off (u64)}.  Stream i's table starts
+ * sif_dec_table_offset(plan, descs, i) bytes into d_ws (descs as passed to sif_dec_plan). */
+uint64_t sif_dec_table_offset(const sif_plan* plan, const sif_dec_desc* descs, int i);
 
 /* ---- per-kernel timing (diagnostics) ----
  * While enabled, every kernel launched by sif_enc_run / sif_dec_run is bracketed by CUDA

@@ -17,6 +17,9 @@ from .codec import (
     ListEncoder,
     ListRoundTrip,
     CodecConfig,
+    CompressedIF,
+    EncodedBlock,
+    QuantSpec,
     HostRoundTrip,
     Payload,
     atkf_filter,
@@ -26,6 +29,7 @@ from .codec import (
     decode,
     decode_batch,
     decode_list,
+    decoder_for,
     deserialize,
     encode,
     encode_batch,

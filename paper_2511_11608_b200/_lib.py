@@ -25,7 +25,7 @@ class EncDesc(ctypes.Structure):
 
 class DecDesc(ctypes.Structure):
     _fields_ = [("inp", c_void_p), ("in_len", c_uint64), ("out", c_void_p), ("rows", c_uint32),
-                ("cols", c_uint32)]
+                ("cols", c_uint32), ("in_len_dev", c_void_p)]
 
 
 class Plan(ctypes.Structure):
@@ -35,7 +35,7 @@ class Plan(ctypes.Structure):
                 ("ws_spill_off", c_uint64)]
 
 
-assert ctypes.sizeof(EncDesc) == 48 and ctypes.sizeof(DecDesc) == 32 and ctypes.sizeof(Plan) == 64
+assert ctypes.sizeof(EncDesc) == 48 and ctypes.sizeof(DecDesc) == 40 and ctypes.sizeof(Plan) == 64
 
 EXPORTS = {
     "sif_version": (c_int, []),
@@ -55,7 +55,7 @@ EXPORTS = {
     "sif_dec_upload": (c_int, [POINTER(Plan), POINTER(DecDesc), c_void_p, c_void_p]),
     "sif_dec_run": (c_int, [POINTER(Plan), c_int, c_void_p, c_void_p, c_void_p]),
     "sif_decode_batched": (c_int, [POINTER(DecDesc), c_int, c_int, c_void_p, c_size_t, c_void_p, c_void_p]),
-    "sif_dec_table_stride": (c_uint64, [POINTER(Plan)]),
+    "sif_dec_table_offset": (c_uint64, [POINTER(Plan), POINTER(DecDesc), c_int]),
     "sif_gen_synthetic": (c_int, [c_void_p, c_uint32, c_uint32, c_uint32, c_uint32, c_uint64, c_void_p]),
     "sif_profile_enable": (c_int, [c_int]),
     "sif_profile_read": (c_int, [POINTER(c_double), POINTER(c_int32), c_int]),

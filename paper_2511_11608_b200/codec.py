@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import struct
+import zlib
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -179,6 +180,260 @@ class Payload:
         return self.nbytes == other.nbytes and bool(torch.equal(self.tensor(), other.tensor()))
 
 
+# ---------------------------------------------------------------------------- CompressedIF
+@dataclass(frozen=True)
+class QuantSpec:
+    """quant.py:24-36 (q bits, step o, v_min, v_max, degenerate)."""
+
+    q: int
+    o: float
+    v_min: float
+    v_max: float
+    degenerate: bool = False
+
+
+def _canonical_vmax(q: int, o: float, v_min: float, degenerate: bool) -> float:
+    """canonicalize_spec (quant.py:76-85): v_max recoverable from the wire fields."""
+    if degenerate:
+        return float(v_min)
+    with np.errstate(over="ignore"):  # a corrupt-but-framed stream may overflow to inf, as in the reference
+        return float(np.float32(np.float64(np.float32(v_min)) + np.float64(np.float32(o)) * ((1 << q) - 1)))
+
+
+def _unpack_fields(buf: np.ndarray, byte_off: int, n: int, w: int) -> np.ndarray:
+    """n MSB-first w-bit fields starting at byte_off (bitstream.py:36-62 BitReader order)."""
+    if n == 0:
+        return np.zeros(0, dtype=np.uint32)
+    bits = np.arange(n, dtype=np.int64) * w
+    byte = byte_off + (bits >> 3)
+    sh = (bits & 7).astype(np.uint64)
+    b = np.concatenate([buf, np.zeros(8, dtype=np.uint8)])
+    word = np.zeros(n, dtype=np.uint64)
+    for j in range(8):
+        word = (word << np.uint64(8)) | b[byte + j].astype(np.uint64)
+    return ((word >> (np.uint64(64 - w) - sh)) & np.uint64((1 << w) - 1)).astype(np.uint32)
+
+
+def _pack_fields(vals, w: int) -> bytes:
+    """MSB-first w-bit fields, zero-padded to a byte (bitstream.py:6-30 BitWriter)."""
+    v = np.asarray(vals, dtype=np.int64).reshape(-1)
+    if v.size == 0:
+        return b""
+    if v.min() < 0 or v.max() >= (1 << w):
+        bad = int(v[(v < 0) | (v >= (1 << w))][0])
+        raise ValueError(f"value {bad} does not fit in {w} bits")
+    bits = ((v[:, None].astype(np.uint64) >> np.arange(w - 1, -1, -1, dtype=np.uint64)) & np.uint64(1))
+    return np.packbits(bits.astype(np.uint8).reshape(-1)).tobytes()
+
+
+class EncodedBlock:
+    """codec.py:108-140: one sign-plane block (spec + CSR scatter of codes).
+
+    Blocks of a GPU-produced stream keep their arrays (row_ptr, cols, codes) packed in
+    the stream and unpack them on first access; blocks built by hand hold the arrays
+    given.  Equality follows codec.py:129-140 (v_max is not compared)."""
+
+    __slots__ = ("__dict__", "_src")
+    _ARRAYS = ("row_ptr", "cols", "codes")
+
+    def __init__(self, q, o, v_min, v_max, degenerate, row_ptr=None, cols=None, codes=None):
+        d = self.__dict__
+        d["q"], d["o"], d["v_min"], d["v_max"], d["degenerate"] = q, o, v_min, v_max, degenerate
+        object.__setattr__(self, "_src", None)
+        if row_ptr is not None or cols is not None or codes is not None:
+            d["row_ptr"], d["cols"], d["codes"] = row_ptr, cols, codes
+
+    @classmethod
+    def _lazy(cls, q, o, v_min, v_max, degenerate, src):
+        b = cls(q, o, v_min, v_max, degenerate)
+        object.__setattr__(b, "_src", src)  # (host bytes, rows, rowptr_off, cols_off, codes_off, nnz, cb)
+        return b
+
+    def __getattr__(self, name):
+        src = object.__getattribute__(self, "_src")
+        if name in EncodedBlock._ARRAYS and src is not None:
+            host, rows, rp, co, qo, nnz, cb = src
+            d = self.__dict__
+            d["row_ptr"] = np.frombuffer(host, dtype="<u4", count=rows + 1, offset=rp).astype(np.uint32)
+            d["cols"] = _unpack_fields(host, co, nnz, cb)
+            d["codes"] = _unpack_fields(host, qo, nnz, self.q)
+            return d[name]
+        raise AttributeError(name)
+
+    def __setattr__(self, name, value):
+        raise AttributeError(f"cannot assign to field {name!r}")  # frozen (dataclass frozen=True)
+
+    @property
+    def nnz(self) -> int:
+        src = object.__getattribute__(self, "_src")
+        if src is not None and "codes" not in self.__dict__:
+            return int(src[5])
+        return int(np.asarray(self.codes).size)
+
+    @property
+    def spec(self) -> QuantSpec:
+        return QuantSpec(self.q, self.o, self.v_min, self.v_max, self.degenerate)
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, EncodedBlock):
+            return NotImplemented
+        return (self.q == other.q and np.float32(self.o) == np.float32(other.o)
+                and np.float32(self.v_min) == np.float32(other.v_min) and self.degenerate == other.degenerate
+                and np.array_equal(self.row_ptr, other.row_ptr) and np.array_equal(self.cols, other.cols)
+                and np.array_equal(self.codes, other.codes))
+
+    __hash__ = None
+
+    def __repr__(self):
+        return (f"EncodedBlock(q={self.q!r}, o={self.o!r}, v_min={self.v_min!r}, v_max={self.v_max!r}, "
+                f"degenerate={self.degenerate!r})")
+
+
+class CompressedIF:
+    """codec.py:143-172: the compressed IF with the reference's fields and properties.
+
+    `encode` / `deserialize` return one backed by its `.sif` stream in DEVICE memory
+    (`.payload`): `decode` and `serialize` use those bytes directly.  One built from
+    fields (e.g. `type(c)(**{**c.__dict__, "blocks_plus": ...})`, as the reference's
+    tests do) is serialized from its fields (codec.py:283-317) when decoded, so decode
+    validates exactly what the object holds."""
+
+    __slots__ = ("__dict__", "_sif", "__weakref__")
+    _FIELDS = ("rows", "cols", "s", "lam", "q_bit", "delta", "mode", "m_plus", "m_minus", "q_vector",
+               "blocks_plus", "blocks_minus")
+
+    def __init__(self, rows, cols, s, lam, q_bit, delta, mode, m_plus, m_minus, q_vector, blocks_plus,
+                 blocks_minus):
+        d = self.__dict__
+        for k, v in zip(self._FIELDS, (rows, cols, s, lam, q_bit, delta, mode, m_plus, m_minus, q_vector,
+                                       blocks_plus, blocks_minus)):
+            d[k] = v
+        object.__setattr__(self, "_sif", None)
+
+    def __setattr__(self, name, value):
+        raise AttributeError(f"cannot assign to field {name!r}")  # frozen
+
+    def __eq__(self, other):
+        if not isinstance(other, CompressedIF):
+            return NotImplemented
+        return tuple(getattr(self, k) for k in self._FIELDS) == tuple(getattr(other, k) for k in self._FIELDS)
+
+    __hash__ = None
+
+    def __repr__(self):
+        return ("CompressedIF(" + ", ".join(f"{k}={getattr(self, k)!r}" for k in self._FIELDS[:10]) +
+                f", blocks_plus=<{len(self.blocks_plus)}>, blocks_minus=<{len(self.blocks_minus)}>)")
+
+    @property
+    def shape(self) -> tuple:
+        return (self.rows, self.cols)
+
+    @property
+    def all_blocks(self) -> tuple:
+        return self.blocks_plus + self.blocks_minus
+
+    @property
+    def total_nnz(self) -> int:
+        return sum(b.nnz for b in self.all_blocks)
+
+    @property
+    def payload_bits(self) -> int:
+        return payload_bits_exact(self)
+
+    # ---- device stream
+    @property
+    def payload(self) -> "Payload":
+        """The `.sif` stream in device memory (serialized from the fields if built by hand)."""
+        sif = object.__getattribute__(self, "_sif")
+        if sif is None:
+            data = _serialize_fields(self)
+            buf, n = _device_bytes(data)
+            sif = (Payload(buf, n, self.rows, self.cols), np.frombuffer(data, dtype=np.uint8))
+            object.__setattr__(self, "_sif", sif)
+        return sif[0]
+
+    @property
+    def nbytes(self) -> int:
+        return self.payload.nbytes
+
+    @property
+    def buf(self) -> torch.Tensor:
+        return self.payload.buf
+
+    def tensor(self) -> torch.Tensor:
+        return self.payload.tensor()
+
+    def to_bytes(self) -> bytes:
+        sif = object.__getattribute__(self, "_sif")
+        if sif is not None and sif[1] is not None:
+            return sif[1].tobytes()
+        return self.payload.to_bytes()
+
+    __bytes__ = to_bytes
+
+    def blocks(self) -> list:
+        """Per-block metadata dicts {q, nnz, o, v_min, plane} (CLI / stats reports)."""
+        return [dict(q=b.q, nnz=b.nnz, o=b.o, v_min=b.v_min, plane="plus" if i < len(self.blocks_plus) else "minus")
+                for i, b in enumerate(self.all_blocks)]
+
+    @classmethod
+    def _from_stream(cls, p: "Payload", host: np.ndarray | None = None) -> "CompressedIF":
+        """View of a well-formed `.sif` stream (already checked on the device): header and
+        block fields parsed like codec.py:328-399, arrays unpacked lazily."""
+        if host is None:
+            host = p.buf[: p.nbytes].cpu().numpy()
+        hb = host.tobytes() if host.size < 4096 else None
+        ver, rows, cols, s, lam, qb, dl, mode_code, mp, mm = struct.unpack_from("<HIIffBfBHH", hb or host[:32].tobytes(),
+                                                                               4)
+        mode = MODE_FIXED if mode_code == 1 else MODE_ABQ
+        pos = HEADER_BYTES
+        qv = ()
+        if mode == MODE_FIXED:
+            qv = tuple(int(v) for v in host[pos: pos + mp + mm])
+            pos += mp + mm
+        cb = col_bits(cols)
+        blocks = []
+        for _ in range(mp + mm):
+            q, o, v_min, nnz = struct.unpack_from("<BffI", host[pos: pos + 13].tobytes(), 0)
+            rp = pos + BLOCK_FIXED_BYTES
+            co = rp + 4 * (rows + 1)
+            cbytes = (nnz * cb + 7) // 8
+            qo = co + cbytes
+            pos = qo + (nnz * q + 7) // 8
+            src = (host, rows, rp, co, qo, nnz, cb)
+            degenerate = False
+            if o == 1.0:  # codec.py:365: needs the codes
+                codes = _unpack_fields(host, qo, nnz, q)
+                degenerate = nnz == 0 or int(codes.max()) == 0
+            blocks.append(EncodedBlock._lazy(int(q), float(o), float(v_min),
+                                             _canonical_vmax(int(q), float(o), float(v_min), degenerate),
+                                             bool(degenerate), src))
+        c = cls(rows=int(rows), cols=int(cols), s=float(s), lam=float(lam), q_bit=int(qb), delta=float(dl), mode=mode,
+                m_plus=int(mp), m_minus=int(mm), q_vector=qv, blocks_plus=tuple(blocks[:mp]),
+                blocks_minus=tuple(blocks[mp:]))
+        object.__setattr__(c, "_sif", (p, host))
+        return c
+
+
+def _serialize_fields(c: CompressedIF) -> bytes:
+    """serialize (codec.py:283-317) of a CompressedIF built from fields (host packing of a
+    host object; streams produced by the GPU encoder never come through here)."""
+    body = bytearray(struct.pack("<HIIffBfBHH", 1, c.rows, c.cols, np.float32(c.s), np.float32(c.lam), c.q_bit,
+                                 np.float32(c.delta), _MODE_CODES[c.mode], c.m_plus, c.m_minus))
+    if c.mode == MODE_FIXED:
+        if len(c.q_vector) != c.m_plus + c.m_minus:
+            raise ConfigError("q_vector length does not match block counts")
+        body += bytes(int(q) for q in c.q_vector)
+    cb = col_bits(c.cols)
+    for b in c.all_blocks:
+        body += struct.pack("<BffI", b.q, np.float32(b.o), np.float32(b.v_min), b.nnz)
+        body += np.asarray(b.row_ptr).astype("<u4").tobytes()
+        body += _pack_fields(b.cols, cb)
+        body += _pack_fields(b.codes, b.q)
+    crc = zlib.crc32(bytes(body)) & 0xFFFFFFFF
+    return b"SIF1" + bytes(body) + struct.pack("<I", crc)
+
+
 # ---------------------------------------------------------------------------- encode
 def _enc_descs(xs, outs, caps, seeds, dtypes):
     n = len(xs)
@@ -300,15 +555,17 @@ def encode_list(xs: list, cfg: CodecConfig, seeds) -> list:
     return enc.payloads()
 
 
-def encode(x, cfg: CodecConfig, seed: int = 0) -> Payload:
-    """serialize(encode(x, cfg, seed)) of the reference, computed on the GPU."""
+def encode(x, cfg: CodecConfig, seed: int = 0) -> CompressedIF:
+    """encode(x, cfg, seed) of the reference (codec.py:186-232), computed on the GPU: the
+    result's `.sif` stream (== serialize(encode(...)) of the reference) stays in device
+    memory; its CompressedIF fields are read from one copy of the stream."""
     if not isinstance(cfg, CodecConfig):
         raise ConfigError("cfg must be a CodecConfig")
     seed = _check_seed(seed)
     xt, dt = _as_if(x)
     enc = BatchEncoder(xt.unsqueeze(0), cfg, [seed])
     enc.run().check()
-    return enc.payloads()[0]
+    return CompressedIF._from_stream(enc.payloads()[0])
 
 
 def encode_batch(xs: torch.Tensor, cfg: CodecConfig, seeds) -> list:
@@ -317,22 +574,46 @@ def encode_batch(xs: torch.Tensor, cfg: CodecConfig, seeds) -> list:
     return enc.payloads()
 
 
-def serialize(p: Payload) -> bytes:
+def decoder_for(enc, out: torch.Tensor | None = None) -> "BatchDecoder":
+    """A decoder of everything `enc` (BatchEncoder / ListEncoder) writes, planned from the
+    buffer capacities: each run() reads the payload lengths from `enc.out_len` on the
+    device, so enc.run(); dec.run() stays valid (and graph-capturable) for any input data."""
+    lp = [enc.out_len.data_ptr() + 8 * i for i in range(enc.B)]
+    if isinstance(enc, ListEncoder):
+        return BatchDecoder([enc.out.data_ptr() + o for o in enc.offs], enc.caps, shapes=enc.shapes, len_ptrs=lp)
+    return BatchDecoder([enc.out.data_ptr() + i * enc.cap for i in range(enc.B)], [enc.cap] * enc.B, enc.rows,
+                        enc.cols, out=out, len_ptrs=lp)
+
+
+def serialize(p) -> bytes:
+    """codec.py:283-317: the `.sif` bytes of a CompressedIF (or a Payload)."""
     return p.to_bytes()
 
 
-def payload_bits_exact(p: Payload) -> int:
-    return 8 * p.nbytes
+def payload_bits_exact(p) -> int:
+    """codec.py:269-280, from the format arithmetic (equals 8 * len(serialize(p)))."""
+    if isinstance(p, Payload):
+        return 8 * p.nbytes
+    cb = col_bits(p.cols)
+    total = HEADER_BYTES + (len(p.q_vector) if p.mode == MODE_FIXED else 0)
+    for b in p.all_blocks:
+        total += BLOCK_FIXED_BYTES + 4 * (p.rows + 1) + (b.nnz * cb + 7) // 8 + (b.nnz * b.q + 7) // 8
+    return 8 * (total + CRC_BYTES)
 
 
 # ---------------------------------------------------------------------------- decode
 class BatchDecoder:
     """Plan + descriptors for decoding B streams into a (B, rows, cols) fp32 tensor, or, with
     `shapes` (one (rows, cols) per stream), into per-stream tensors `self.outs` (views of one
-    flat buffer)."""
+    flat buffer).
+
+    `lens` are the stream lengths -- or, with `len_ptrs` (device addresses of uint64
+    lengths, e.g. an encoder's `out_len` entries), the capacities of the buffers: the real
+    lengths are then read on the device by every run(), so one plan (or CUDA graph) decodes
+    whatever the encoder last produced."""
 
     def __init__(self, bufs, lens, rows: int = 0, cols: int = 0, out: torch.Tensor | None = None,
-                 parse_only: bool = False, shapes=None):
+                 parse_only: bool = False, shapes=None, len_ptrs=None):
         self.B = len(lens)
         dev = torch.device("cuda")
         if shapes is None:
@@ -359,6 +640,7 @@ class BatchDecoder:
             arr[i].out = self.out.data_ptr() + offs[i] * 4
             arr[i].rows = shapes[i][0]
             arr[i].cols = shapes[i][1]
+            arr[i].in_len_dev = int(len_ptrs[i]) if len_ptrs is not None else None
         self._descs = arr
         self.plan = _lib.Plan()
         raise_for(_L().sif_dec_plan(arr, self.B, ctypes.byref(self.plan)), "sif_dec_plan")
@@ -387,12 +669,15 @@ class BatchDecoder:
         return self
 
     def table(self, i: int) -> np.ndarray:
-        stride = int(_L().sif_dec_table_stride(ctypes.byref(self.plan)))
-        base = self.plan.ws_aux_off + i * stride
-        return self.ws[base: base + stride].cpu().numpy().view(np.uint32).reshape(-1, 16)
+        base = int(_L().sif_dec_table_offset(ctypes.byref(self.plan), self._descs, i))
+        end = (int(_L().sif_dec_table_offset(ctypes.byref(self.plan), self._descs, i + 1)) if i + 1 < self.B
+               else self.plan.ws_aux_off + 64 * self.plan.ws_spill_off)
+        return self.ws[base: end].cpu().numpy().view(np.uint32).reshape(-1, 16)
 
 
 def _device_bytes(data) -> tuple[torch.Tensor, int]:
+    if isinstance(data, CompressedIF):
+        data = data.payload
     if isinstance(data, Payload):
         return data.buf, data.nbytes
     if isinstance(data, torch.Tensor):
@@ -417,9 +702,9 @@ def _header_shape(buf: torch.Tensor, n: int) -> tuple[int, int]:
     return struct.unpack_from("<II", h, 6)
 
 
-def deserialize(data) -> Payload:
-    """codec.py:320-399 checks (length, magic, CRC, version, mode, framing, q range) on
-    the device; raises StreamFormatError / CorruptStreamError like the reference."""
+def _check_stream(data) -> Payload:
+    """codec.py:320-385 checks (length, magic, CRC, version, mode, framing, q range) on the
+    device; raises StreamFormatError / CorruptStreamError like the reference."""
     buf, n = _device_bytes(data)
     rows, cols = _header_shape(buf, n)
     dec = BatchDecoder([buf.data_ptr()], [n], rows, cols, out=torch.empty((1, 0, 0), device="cuda"),
@@ -428,12 +713,25 @@ def deserialize(data) -> Payload:
     return Payload(buf, n, rows, cols)
 
 
+def deserialize(data) -> CompressedIF:
+    """codec.py:320-399: the stream is checked on the device, then viewed as a CompressedIF
+    (fields from the header and block headers, arrays unpacked on access)."""
+    host = None
+    if isinstance(data, (bytes, bytearray, memoryview)):
+        host = np.frombuffer(bytes(data), dtype=np.uint8)
+    return CompressedIF._from_stream(_check_stream(data), host)
+
+
 def decode(p) -> torch.Tensor:
-    """decode(deserialize(bytes)) of the reference: fp32 (rows, cols) CUDA tensor."""
-    if not isinstance(p, Payload):
-        buf, n = _device_bytes(p)
-        rows, cols = _header_shape(buf, n)
-        p = Payload(buf, n, rows, cols)
+    """decode(c) (codec.py:254-266) of a CompressedIF, or decode(deserialize(data)) of
+    `.sif` bytes / a Payload: fp32 (rows, cols) CUDA tensor, bit-identical to the
+    reference's DenseTensor values."""
+    if isinstance(p, CompressedIF):
+        p = p.payload
+    elif not isinstance(p, Payload):
+        # the framing and CRC checks run first (codec.py:320-385): a damaged shape field
+        # raises StreamFormatError instead of sizing the output from it
+        p = _check_stream(p)
     dec = BatchDecoder([p.buf.data_ptr()], [p.nbytes], p.rows, p.cols)
     dec.run().check()
     return dec.out[0]
@@ -529,39 +827,37 @@ class BatchPipeline:
     `step()`s rotate over the slots, so the decode of batch i overlaps the encode of batch
     i+1 (the kernels are latency-bound and leave SM resources free for each other).
     `xs` is the device input batch read by every step (refill it between steps in a real
-    server); `ys(slot)` is the decoded output of a slot."""
+    server: the decoders read each payload's length on the device, so nothing is planned
+    from one step's data); `ys(slot)` is the decoded output of a slot."""
 
-    def __init__(self, xs, cfg: CodecConfig, seeds, depth: int = 2, graphs: bool = True):
+    def __init__(self, xs, cfg: CodecConfig, seeds, depth: int = 2, graphs: bool = True, slot_inputs=None):
         """xs: a (B, rows, cols) CUDA tensor, or a list of 2-D CUDA tensors of mixed shapes and
-        dtypes (ListEncoder; decoded outputs then live in one flat fp32 buffer per slot)."""
+        dtypes (ListEncoder; decoded outputs then live in one flat fp32 buffer per slot).
+        slot_inputs: optional list of (xs_j, seeds_j), one per slot (depth = its length):
+        every slot then reads its own input batch (distinct buffers, e.g. the requests of
+        consecutive steps) instead of all slots sharing `xs`."""
         self.xs = xs
         mixed = isinstance(xs, (list, tuple))
         if mixed:
             self.B, self.rows, self.cols = len(xs), 0, 0
         else:
             self.B, self.rows, self.cols = xs.shape
-        seeds = list(seeds)
+        if slot_inputs is None:
+            slot_inputs = [(xs, list(seeds))] * max(1, depth)
         self.slots = []
-        for _ in range(max(1, depth)):
+        for xj, sj in slot_inputs:
             if mixed:
-                enc = ListEncoder(list(xs), cfg, seeds)
-                enc.run().check()
-                lens = enc.out_len.cpu().numpy()
-                dec = BatchDecoder([enc.out.data_ptr() + o for o in enc.offs], lens, shapes=enc.shapes)
+                enc = ListEncoder(list(xj), cfg, list(sj))
             else:
-                enc = BatchEncoder(xs, cfg, seeds)
-                enc.run().check()
-                lens = enc.out_len.cpu().numpy()
-                dec = BatchDecoder([enc.out.data_ptr() + i * enc.cap for i in range(self.B)], lens, self.rows,
-                                   self.cols)
-            dec.run().check()
+                enc = BatchEncoder(xj, cfg, list(sj))
+            dec = decoder_for(enc)
             st = torch.cuda.Stream()
             fn = (lambda e=enc, d=dec: (e.run(), d.run()))
             g = None
             if graphs:
                 with torch.cuda.stream(st):
                     g = capture_graph(fn)
-            self.slots.append(dict(enc=enc, dec=dec, stream=st, graph=g, fn=fn))
+            self.slots.append(dict(enc=enc, dec=dec, stream=st, graph=g, fn=fn, xs=xj, seeds=list(sj)))
         self.i = 0
         torch.cuda.synchronize()
 
@@ -625,27 +921,11 @@ class HostRoundTrip:
             xs = torch.empty((b1 - b0, self.rows, self.cols), dtype=x_host.dtype, device=dev)
             enc = BatchEncoder(xs, cfg, seeds[b0:b1])
             ys = torch.empty((b1 - b0, self.rows, self.cols), dtype=torch.float32, device=dev)
-            self.parts.append(dict(b0=b0, b1=b1, xs=xs, enc=enc, ys=ys, dec=None))
+            self.parts.append(dict(b0=b0, b1=b1, xs=xs, enc=enc, ys=ys, dec=decoder_for(enc, out=ys)))
         self.s_in, self.s_run, self.s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-        self._lens_known = False
-
-    def _decoders(self):
-        # payload lengths are data dependent: plan the decoders once, after a first encode
-        for p in self.parts:
-            lens = p["enc"].out_len.cpu().numpy()
-            cap = p["enc"].cap
-            p["dec"] = BatchDecoder([p["enc"].out.data_ptr() + i * cap for i in range(len(lens))], lens, self.rows,
-                                    self.cols, out=p["ys"])
-        self._lens_known = True
 
     def run(self):
         """One pipelined pass over the whole batch (stream-ordered; synchronize to read)."""
-        if not self._lens_known:
-            for p in self.parts:
-                p["xs"].copy_(self.x_host[p["b0"]:p["b1"]])
-                p["enc"].run()
-            torch.cuda.synchronize()
-            self._decoders()
         cur = torch.cuda.current_stream()
         for st in (self.s_in, self.s_run, self.s_out):
             st.wait_stream(cur)
@@ -730,24 +1010,11 @@ class ListRoundTrip:
                   for k in range(i0, i1)]
             enc = ListEncoder(xs, cfg, seeds[i0:i1])
             o0, o1 = self.out_off[i0], (self.out_off[i1] if i1 < self.n else self.y_host.numel())
-            self.parts.append(dict(i0=i0, i1=i1, h0=h0, h1=h1, o0=o0, o1=o1, dbuf=dbuf, enc=enc, dec=None))
+            self.parts.append(dict(i0=i0, i1=i1, h0=h0, h1=h1, o0=o0, o1=o1, dbuf=dbuf, enc=enc,
+                                   dec=decoder_for(enc)))
         self.s_in, self.s_run, self.s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-        self._lens_known = False
-
-    def _decoders(self):
-        for p in self.parts:
-            enc = p["enc"]
-            lens = enc.out_len.cpu().numpy()
-            p["dec"] = BatchDecoder([enc.out.data_ptr() + o for o in enc.offs], lens, shapes=enc.shapes)
-        self._lens_known = True
 
     def run(self):
-        if not self._lens_known:
-            for p in self.parts:
-                p["dbuf"][: p["h1"] - p["h0"]].copy_(self.x_host[p["h0"]:p["h1"]])
-                p["enc"].run()
-            torch.cuda.synchronize()
-            self._decoders()
         cur = torch.cuda.current_stream()
         for st in (self.s_in, self.s_run, self.s_out):
             st.wait_stream(cur)

@@ -24,15 +24,15 @@ constexpr uint32_t FLAG_CORRUPT = 1u, FLAG_NONFINITE = 2u;
 // (codec.py:320-385, :235-251, tensor.py:27-36); see errors.py REASONS.
 enum : uint32_t {
   R_NONE = 0, R_SHORT = 1, R_MAGIC = 2, R_CRC = 3, R_VERSION = 4, R_MODE = 5, R_QVEC = 6, R_BLKHDR = 7,
-  R_QRANGE = 8, R_BLKPAY = 9, R_TRAIL = 10, R_CAPACITY = 11, R_SHAPE_MISMATCH = 12, R_CORRUPT = 16,
+  R_QRANGE = 8, R_BLKPAY = 9, R_TRAIL = 10, R_CAPACITY = 11, R_SHAPE_MISMATCH = 12, R_LEN_OVER = 13, R_CORRUPT = 16,
   R_SHAPE = 32, R_NONFINITE = 33
 };
 
 struct DecArgs {
   const sif_dec_desc* descs;
   int n;
-  uint32_t* table;        // per IF: (2 + maxb) rows of TROW_U32
-  uint64_t table_stride;  // in u32
+  uint32_t* table;        // per IF: (2 + max blocks of that stream) rows of TROW_U32
+  const uint64_t* tab_off;  // [n+1] start of each stream's table rows (u32 units)
   uint32_t* acc;          // per IF: {crc, flags, count, pad}
   int parse_only;
   int32_t* status;
@@ -43,6 +43,12 @@ struct DecArgs {
 
 constexpr uint64_t SEGD = CRC_PIECE;  // CRC bytes per warp piece
 
+__device__ __forceinline__ uint32_t* dtab(const DecArgs& a, int i) { return a.table + a.tab_off[i]; }
+// Stream length as resolved by the parse kernel (table row 1, words 2..3).
+__device__ __forceinline__ uint64_t dlen(const uint32_t* tab) {
+  return (uint64_t)tab[TROW_U32 + 2] | ((uint64_t)tab[TROW_U32 + 3] << 32);
+}
+
 // ------------------------------------------------------------------------------- parse
 __device__ __forceinline__ uint32_t rd_u32(const uint8_t* p, uint64_t o) {
   return (uint32_t)p[o] | ((uint32_t)p[o + 1] << 8) | ((uint32_t)p[o + 2] << 16) | ((uint32_t)p[o + 3] << 24);
@@ -52,13 +58,22 @@ __global__ void sif_parse_kernel(DecArgs a) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
   const sif_dec_desc d = a.descs[i];
-  uint32_t* tab = a.table + (uint64_t)i * a.table_stride;
+  uint32_t* tab = dtab(a, i);
   const uint8_t* in = d.in;
-  const uint64_t len = d.in_len;
-  const uint64_t max_rows = a.table_stride / TROW_U32 - 2;
+  // the stream length comes from the descriptor, or -- for payloads still being produced on
+  // the device (a pipelined encode -> decode) -- from the encoder's out_len, read here
+  uint64_t len = d.in_len;
+  bool over = false;
+  if (d.in_len_dev) {
+    const uint64_t l = *d.in_len_dev;
+    over = l > d.in_len;
+    len = over ? 0 : l;
+  }
+  const uint64_t max_rows = (a.tab_off[i + 1] - a.tab_off[i]) / TROW_U32 - 2;
   uint32_t pre = 0, walk = 0, N = 0, K = 0, mp = 0, mm = 0, mode = 0, qb = 0, nb = 0, crc = 0;
   uint32_t pre_r = R_NONE, walk_r = R_NONE, walk_x = 0;
-  if (len < (uint64_t)(kHeaderBytes + kCrcBytes)) { pre = SIF_ERR_STREAM_FORMAT; pre_r = R_SHORT; }  // codec.py:321
+  if (over) { pre = SIF_ERR_CAPACITY; pre_r = R_LEN_OVER; }  // longer than the buffer it lives in
+  else if (len < (uint64_t)(kHeaderBytes + kCrcBytes)) { pre = SIF_ERR_STREAM_FORMAT; pre_r = R_SHORT; }  // codec.py:321
   else if (in[0] != 'S' || in[1] != 'I' || in[2] != 'F' || in[3] != '1') { pre = SIF_ERR_STREAM_FORMAT; pre_r = R_MAGIC; }
   if (!pre) {
     crc = rd_u32(in, len - 4);
@@ -131,10 +146,11 @@ __global__ void __launch_bounds__(DNT, 8) sif_dcrc_kernel(DecArgs a) {
     }
     const int ifi = lo;
     const uint32_t piece = (uint32_t)(gp - a.seg_base[lo]);
-    const uint32_t* tab = a.table + (uint64_t)ifi * a.table_stride;
+    const uint32_t* tab = dtab(a, ifi);
     if (tab[TROW_U32 + 0]) continue;  // length / magic failure: no CRC
     const sif_dec_desc d = a.descs[ifi];
-    const uint64_t b0 = 4, b1 = d.in_len - 4;
+    // pieces are planned from the buffer capacity; those past the real length exit here
+    const uint64_t b0 = 4, b1 = dlen(tab) - 4;
     const uint64_t e1 = (uint64_t)piece * SEGD < b1 - b0 ? b1 - (uint64_t)piece * SEGD : b0;
     const uint64_t e0 = e1 - b0 > SEGD ? e1 - SEGD : b0;
     if (e0 >= e1) continue;
@@ -238,7 +254,7 @@ __global__ void __launch_bounds__(DNT, 3) sif_scatter_kernel(DecArgs a) {
       ib0 = a.item_base[cur];
       ib1 = a.item_base[cur + 1];
       const sif_dec_desc d = a.descs[cur];
-      tab = a.table + (uint64_t)cur * a.table_stride;
+      tab = dtab(a, cur);
       const uint32_t walk = tab[0], pre = tab[TROW_U32 + 0];
       N = tab[1]; K = tab[2]; mp = tab[3]; nb = tab[7];
       ok = !pre && !walk && N == d.rows && K == d.cols && !a.parse_only;
@@ -422,7 +438,7 @@ __global__ void __launch_bounds__(DNT, 3) sif_scatter_kernel(DecArgs a) {
 __global__ void sif_dfinal_kernel(DecArgs a) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
-  const uint32_t* tab = a.table + (uint64_t)i * a.table_stride;
+  uint32_t* tab = dtab(a, i);
   const sif_dec_desc d = a.descs[i];
   uint32_t* acc = a.acc + 4ull * i;
   const uint32_t walk = tab[0], N = tab[1], K = tab[2], pre = tab[TROW_U32 + 0];
@@ -431,7 +447,7 @@ __global__ void sif_dfinal_kernel(DecArgs a) {
   int st = SIF_OK;
   uint32_t r = R_NONE, x = 0;
   if (pre) { st = (int)pre; r = tab[TROW_U32 + 4]; }
-  else if (crc_finish(crc_raw, d.in_len - 8) != tab[TROW_U32 + 1]) { st = SIF_ERR_STREAM_FORMAT; r = R_CRC; }  // :325-327
+  else if (crc_finish(crc_raw, dlen(tab) - 8) != tab[TROW_U32 + 1]) { st = SIF_ERR_STREAM_FORMAT; r = R_CRC; }  // :325-327
   else if (walk) { st = (int)walk; r = tab[TROW_U32 + 5]; x = tab[TROW_U32 + 6]; }
   else if (!shape_ok) { st = SIF_ERR_CAPACITY; r = R_SHAPE_MISMATCH; }
   else if (!a.parse_only) {
@@ -440,8 +456,8 @@ __global__ void sif_dfinal_kernel(DecArgs a) {
     else if (flags & FLAG_NONFINITE) { st = SIF_ERR_NONFINITE; r = R_NONFINITE; }
   }
   a.status[i] = st;
-  reinterpret_cast<uint32_t*>(a.table + (uint64_t)i * a.table_stride)[TROW_U32 + 7] = r;
-  reinterpret_cast<uint32_t*>(a.table + (uint64_t)i * a.table_stride)[TROW_U32 + 8] = x;
+  tab[TROW_U32 + 7] = r;
+  tab[TROW_U32 + 8] = x;
   acc[0] = 0; acc[1] = 0; acc[2] = 0; acc[3] = 0;
 }
 

@@ -354,18 +354,17 @@ __device__ SelRes select_exact(SelSh& sh, uint32_t* scratch, const List& L, uint
     res.n_eq = cnt;
     res.r_eq = r;
     res.all_ties = r == cnt;
-    res.sec = 0;
-    if (!res.all_ties) {
-      const uint32_t kk = (uint32_t)klo;
-      // smallest secondary keys first: select the r-th largest of (2^sec_bits - 1 - sec)
-      const uint64_t smax = sec_bits >= 64 ? ~0ull : ((1ull << sec_bits) - 1ull);
-      const uint64_t top = radix_select64<NT, U>(sh, hist, L, n, r, [&](uint32_t b, uint32_t x, uint64_t& k) {
-        if (!pred(b, x) || keyf(b) != kk) return false;
-        k = smax - secf(b, x);
-        return true;
-      }, sec_bits);
-      res.sec = smax - top;
-    }
+    // the secondary key of the r-th tie is needed even when r == cnt (every tie selected):
+    // MS cuts (msplit.py:64) place the block boundary at that element's flat index
+    const uint32_t kk = (uint32_t)klo;
+    // smallest secondary keys first: select the r-th largest of (2^sec_bits - 1 - sec)
+    const uint64_t smax = sec_bits >= 64 ? ~0ull : ((1ull << sec_bits) - 1ull);
+    const uint64_t top = radix_select64<NT, U>(sh, hist, L, n, r, [&](uint32_t b, uint32_t x, uint64_t& k) {
+      if (!pred(b, x) || keyf(b) != kk) return false;
+      k = smax - secf(b, x);
+      return true;
+    }, sec_bits);
+    res.sec = smax - top;
     return res;
   }
   if (tid == 0) sh.gcount = 0;

@@ -6,6 +6,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <vector>
 
 #include "sif.h"
@@ -28,21 +30,23 @@ const char* kKpNames[KP_N] = {"enc_prep", "enc_stream", "enc_select<0>", "enc_me
                               "sif_scatter_kernel", "sif_dfinal_kernel", "enc_select_tiny", "enc_gather<1>",
                               "enc_select<1>", "enc_gather<2>", "enc_select<2>"};
 struct ProfRec { int k; cudaEvent_t a, b; };
-bool g_prof = false;
+std::atomic<bool> g_prof{false};
+std::mutex g_prof_mu;  // guards g_recs (launches may come from several host threads)
 std::vector<ProfRec> g_recs;
 struct ProfScope {
   int k;
   cudaStream_t s;
   cudaEvent_t a = nullptr, b = nullptr;
   ProfScope(int kk, cudaStream_t ss) : k(kk), s(ss) {
-    if (!g_prof) return;
+    if (!g_prof.load(std::memory_order_relaxed)) return;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a, s);
   }
   ~ProfScope() {
-    if (!g_prof || !a) return;
+    if (!a) return;
     cudaEventRecord(b, s);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
     g_recs.push_back({k, a, b});
   }
 };
@@ -69,26 +73,83 @@ uint32_t h_x8n(uint64_t nbytes) {  // x^(8 n) mod P, reflected
   }
   return p;
 }
-int crc_tables_init() {
-  static int done = 0;
-  if (done) return SIF_OK;
+
+// Fraction of the resident CTA slots a persistent kernel takes (SIF_GRID_FRAC, default 1):
+// below 1 leaves room for kernels of other in-flight batches on other streams.
+double grid_frac() {
+  static const double f = [] {
+    const char* e = getenv("SIF_GRID_FRAC");
+    const double v = e && *e ? atof(e) : 1.0;
+    return (v > 0.0 && v <= 1.0) ? v : 1.0;
+  }();
+  return f;
+}
+
+template <class K>
+int resident_grid(K kfn, int threads, int smem, uint64_t work, int sms) {
+  int per = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, threads, smem) != cudaSuccess || per < 1) per = 1;
+  const uint64_t slots = std::max<uint64_t>(1, (uint64_t)(per * sms * grid_frac()));
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>(work, slots));
+}
+
+constexpr uint32_t kBigNcand = 131072;  // candidates above which an IF uses the multi-kernel select
+constexpr int kSmemStream = (2 * sif::CH + 2 * sif::ND) * 4;
+constexpr int kSmemSelect = (2 * sif::ND + 2 * sif::HB + sif::GCAP * 4 + 2 * sif::GSM) * 4;
+inline int smem_abq(int maxb) { return (sif::CNT / 32) * maxb * (int)(sizeof(sif::AbqPar) + 16 * 8); }
+inline int smem_pack(int maxb) { return (sif::CNT / 32) * maxb * (int)sizeof(sif::PackPar); }
+inline uint32_t crc_segments(uint64_t cap) { return (uint32_t)std::max<uint64_t>(1, (cap + sif::CRC_PIECE - 1) / sif::CRC_PIECE); }
+constexpr int kSmemScatterMax = (sif::DNT / 32) * (1280 * 4 + 2 * ((1280 + 31) / 32) * 4);
+
+// Per-device state: everything that depends on the device a call runs on (the CRC piece
+// shift table in that device's __constant__/__device__ memory, kernel attributes, SM
+// count, resident grid sizes).  Initialised once per device on first use; a process may
+// drive several GPUs (one host thread per GPU, or one thread switching devices).
+struct DevState {
+  std::once_flag once;
+  int status = SIF_OK;
+  int sms = 148;
+  int g_stream = 1, g_members = 1, g_gather = 1, g_crc = 1, g_dcrc = 1, g_scatter = 1;
+  std::mutex mu;  // guards the per-maxb grid cache
+  int g_abq[sif::MAXB + 1] = {0};
+  int g_pack[sif::MAXB + 1] = {0};
+};
+constexpr int kMaxDevices = 64;
+DevState g_dev[kMaxDevices];
+
+int dev_init(DevState& ds, int dev) {
+  if (cudaDeviceGetAttribute(&ds.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || ds.sms <= 0) ds.sms = 148;
   std::vector<uint32_t> t(sif::CRC_PIECES_MAX);
   const uint32_t step = h_x8n(sif::CRC_PIECE);
   t[0] = 1u << 31;
   for (int j = 1; j < sif::CRC_PIECES_MAX; ++j) t[j] = h_crc_mult(step, t[j - 1]);
   if (cudaMemcpyToSymbol(sif::kPieceShift, t.data(), 4ull * sif::CRC_PIECES_MAX) != cudaSuccess) return SIF_ERR_CUDA;
-  done = 1;
+  if (check_cuda(cudaFuncSetAttribute(sif::enc_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemStream)) ||
+      check_cuda(cudaFuncSetAttribute(sif::enc_select<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
+      check_cuda(cudaFuncSetAttribute(sif::enc_select<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
+      check_cuda(cudaFuncSetAttribute(sif::enc_select<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
+      check_cuda(cudaFuncSetAttribute(sif::enc_abq<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_abq(sif::MAXB))) ||
+      check_cuda(cudaFuncSetAttribute(sif::enc_abq<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_abq(sif::MAXB))) ||
+      check_cuda(cudaFuncSetAttribute(sif::enc_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pack(sif::MAXB))) ||
+      check_cuda(cudaFuncSetAttribute(sif::sif_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kSmemScatterMax)))
+    return SIF_ERR_CUDA;
+  const uint64_t big = 1ull << 30;
+  ds.g_gather = resident_grid(sif::enc_gather<1>, sif::CNT, 0, big, ds.sms);
+  ds.g_crc = resident_grid(sif::enc_crc, sif::CNT, 0, big, ds.sms);
+  ds.g_stream = resident_grid(sif::enc_stream, sif::CNT, kSmemStream, big, ds.sms);
+  ds.g_members = resident_grid(sif::enc_members, sif::CNT, 0, big, ds.sms);
+  ds.g_dcrc = resident_grid(sif::sif_dcrc_kernel, sif::DNT, 0, big, ds.sms);
   return SIF_OK;
 }
 
-inline int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
-  }
-  return sms;
+// State of the calling thread's current device (initialised on first use), or nullptr.
+DevState* dev_state() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
+  DevState& ds = g_dev[dev];
+  std::call_once(ds.once, [&] { ds.status = dev_init(ds, dev); });
+  return ds.status == SIF_OK ? &ds : nullptr;
 }
 
 // Workspace sections of an encode plan (all offsets 256-byte aligned).
@@ -121,34 +182,6 @@ EncWs enc_ws(uint64_t n, uint64_t nch, uint64_t maxb, uint64_t nhist, uint64_t n
   return w;
 }
 
-// Chunk-kernel grid: persistent CTAs, as many as can be resident.
-// Fraction of the resident CTA slots a persistent kernel takes (SIF_GRID_FRAC, default 1):
-// below 1 leaves room for kernels of other in-flight batches on other streams.
-double grid_frac() {
-  static double f = -1.0;
-  if (f < 0.0) {
-    const char* e = getenv("SIF_GRID_FRAC");
-    f = e && *e ? atof(e) : 1.0;
-    if (!(f > 0.0 && f <= 1.0)) f = 1.0;
-  }
-  return f;
-}
-
-template <class K>
-int resident_grid(K kfn, int threads, int smem, uint64_t work) {
-  int per = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, threads, smem) != cudaSuccess || per < 1) per = 1;
-  const uint64_t slots = std::max<uint64_t>(1, (uint64_t)(per * num_sms() * grid_frac()));
-  return (int)std::max<uint64_t>(1, std::min<uint64_t>(work, slots));
-}
-
-constexpr uint32_t kBigNcand = 131072;  // candidates above which an IF uses the multi-kernel select
-constexpr int kSmemStream = (2 * sif::CH + 2 * sif::ND) * 4;
-constexpr int kSmemSelect = (2 * sif::ND + 2 * sif::HB + sif::GCAP * 4 + 2 * sif::GSM) * 4;
-inline int smem_abq(int maxb) { return (sif::CNT / 32) * maxb * (int)(sizeof(sif::AbqPar) + 16 * 8); }
-inline int smem_pack(int maxb) { return (sif::CNT / 32) * maxb * (int)sizeof(sif::PackPar); }
-inline uint32_t crc_segments(uint64_t cap) { return (uint32_t)std::max<uint64_t>(1, (cap + sif::CRC_PIECE - 1) / sif::CRC_PIECE); }
-
 }  // namespace
 
 extern "C" {
@@ -156,7 +189,7 @@ extern "C" {
 int sif_version(void) { return 1; }
 
 int sif_profile_enable(int on) {
-  g_prof = on != 0;
+  g_prof.store(on != 0);
   return SIF_OK;
 }
 
@@ -164,6 +197,7 @@ int sif_profile_read(double* ms, int32_t* count, int maxk) {
   if (!ms || !count || maxk < 0) return SIF_ERR_INVALID_ARG;
   for (int k = 0; k < maxk; ++k) { ms[k] = 0.0; count[k] = 0; }
   int st = SIF_OK;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
   for (const ProfRec& r : g_recs) {
     float t = 0.f;
     if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) st = SIF_ERR_CUDA;
@@ -286,7 +320,7 @@ int sif_enc_plan(const sif_enc_desc* d, int n, const sif_codec_cfg* c, sif_plan*
 
 int sif_enc_upload(const sif_plan* p, const sif_enc_desc* d, const sif_codec_cfg* c, void* ws, void* stream) {
   if (!p || !ws || !c || (p->n > 0 && !d)) return SIF_ERR_INVALID_ARG;
-  if (crc_tables_init()) return SIF_ERR_CUDA;
+  if (!dev_state()) return SIF_ERR_CUDA;
   cudaStream_t s = (cudaStream_t)stream;
   uint8_t* wb = (uint8_t*)ws;
   const int n = p->n;
@@ -384,31 +418,20 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   // alone); enabled when the batch holds an IF whose keep count exceeds half the cut-off
   a.big_ncand = (p->flags & 2) ? kBigNcand : 0u;
   a.prof = reinterpret_cast<uint64_t*>(getenv("SIF_PROF_PTR") ? strtoull(getenv("SIF_PROF_PTR"), nullptr, 0) : 0ull);
-  static bool attrs = false;
-  if (!attrs) {
-    if (check_cuda(cudaFuncSetAttribute(sif::enc_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemStream)) ||
-        check_cuda(cudaFuncSetAttribute(sif::enc_select<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
-        check_cuda(cudaFuncSetAttribute(sif::enc_select<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
-        check_cuda(cudaFuncSetAttribute(sif::enc_select<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
-        check_cuda(cudaFuncSetAttribute(sif::enc_abq<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_abq(sif::MAXB))) ||
-        check_cuda(cudaFuncSetAttribute(sif::enc_abq<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_abq(sif::MAXB))) ||
-        check_cuda(cudaFuncSetAttribute(sif::enc_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pack(sif::MAXB))))
-      return SIF_ERR_CUDA;
-    attrs = true;
-  }
+  DevState* ds = dev_state();
+  if (!ds) return SIF_ERR_CUDA;
   const int maxb = p->max_blocks;
-  static int g_stream = 0, g_members = 0, g_abq = 0, g_pack = 0, g_maxb = -1, g_crc = 0, g_gather = 0;
-  if (!g_stream) {
-    g_gather = resident_grid(sif::enc_gather<1>, sif::CNT, 0, 1ull << 30);
-    g_crc = (int)std::max<uint64_t>(1, (uint64_t)resident_grid(sif::enc_crc, sif::CNT, 0, 1ull << 30));
-    g_stream = resident_grid(sif::enc_stream, sif::CNT, kSmemStream, 1ull << 30);
-    g_members = resident_grid(sif::enc_members, sif::CNT, 0, 1ull << 30);
+  int g_abq, g_pack;
+  {
+    std::lock_guard<std::mutex> lk(ds->mu);
+    if (!ds->g_abq[maxb]) {
+      ds->g_abq[maxb] = resident_grid(sif::enc_abq<1>, sif::CNT, smem_abq(maxb), 1ull << 30, ds->sms);
+      ds->g_pack[maxb] = resident_grid(sif::enc_pack, sif::CNT, smem_pack(maxb), 1ull << 30, ds->sms);
+    }
+    g_abq = ds->g_abq[maxb];
+    g_pack = ds->g_pack[maxb];
   }
-  if (g_maxb != maxb) {
-    g_abq = resident_grid(sif::enc_abq<1>, sif::CNT, smem_abq(maxb), 1ull << 30);
-    g_pack = resident_grid(sif::enc_pack, sif::CNT, smem_pack(maxb), 1ull << 30);
-    g_maxb = maxb;
-  }
+  const int g_stream = ds->g_stream, g_members = ds->g_members, g_gather = ds->g_gather, g_crc = ds->g_crc;
   const unsigned nch = (unsigned)p->tiles;
   const unsigned n = (unsigned)p->n;
   const unsigned wgrid = std::max(1u, (nch + sif::CNT / 32 - 1) / (sif::CNT / 32));  // >= 1 chunk per warp
@@ -494,16 +517,26 @@ static uint32_t dec_segments(uint64_t len) {
   return (uint32_t)std::max<uint64_t>(1, (body + sif::SEGD - 1) / sif::SEGD);
 }
 
+// Table rows of one stream: 2 header rows + one per block.  A block takes at least
+// 13 + 4 (rows + 1) bytes (codec.py:303-315), so a stream of in_len bytes (or capacity)
+// holds at most (in_len - 36) / that many blocks; at most 2 * 65535 (u16 M+ / M-).
+static uint64_t dec_table_rows(const sif_dec_desc& d) {
+  const uint64_t per = 13ull + 4ull * ((uint64_t)d.rows + 1);
+  const uint64_t body = d.in_len > 36 ? d.in_len - 36 : 0;
+  return 2 + std::min<uint64_t>(body / per + 1, 2ull * 65535);
+}
+
 struct DecWs {
-  uint64_t desc, table, acc, segbase, itembase, total;
+  uint64_t desc, table, taboff, acc, segbase, itembase, total;
 };
 
-static DecWs dec_ws(uint64_t n, uint64_t maxrows) {
+static DecWs dec_ws(uint64_t n, uint64_t table_rows) {
   DecWs w;
   uint64_t off = 0;
   auto take = [&](uint64_t bytes) { const uint64_t o = off; off += up(std::max<uint64_t>(bytes, 1), 256); return o; };
   w.desc = take(sizeof(sif_dec_desc) * n);
-  w.table = take((2 + maxrows) * 64ull * n);
+  w.table = take(table_rows * 64ull);
+  w.taboff = take(8ull * (n + 1));
   w.acc = take(16ull * n);
   w.segbase = take(4ull * (n + 1));
   w.itembase = take(8ull * (n + 1));
@@ -523,11 +556,11 @@ static uint32_t dec_segw(const sif_dec_desc* d, int n) {
 int sif_dec_plan(const sif_dec_desc* d, int n, sif_plan* p) {
   if (!p || (n > 0 && !d) || n < 0) return SIF_ERR_INVALID_ARG;
   memset(p, 0, sizeof(*p));
-  uint64_t maxrows = 0, nseg = 0;
+  uint64_t rows = 0, nseg = 0;
   for (int i = 0; i < n; ++i) {
     if (!d[i].in || (reinterpret_cast<uintptr_t>(d[i].in) & 3)) return SIF_ERR_INVALID_ARG;
-    const uint64_t blk = d[i].in_len > 32 ? (d[i].in_len - 32) / 17 + 1 : 1;
-    maxrows = std::max(maxrows, blk);
+    if (d[i].in_len_dev && (reinterpret_cast<uintptr_t>(d[i].in_len_dev) & 7)) return SIF_ERR_INVALID_ARG;
+    rows += dec_table_rows(d[i]);
     nseg += dec_segments(d[i].in_len);
     if (dec_segments(d[i].in_len) > (uint32_t)sif::CRC_PIECES_MAX) return SIF_ERR_INVALID_ARG;
   }
@@ -537,39 +570,47 @@ int sif_dec_plan(const sif_dec_desc* d, int n, sif_plan* p) {
   p->threads = sif::DNT;
   p->tiles = (int32_t)segw;    // decode plans: columns per work item
   p->cluster = (int32_t)nseg;  // decode plans: CRC segment CTAs
-  p->max_blocks = (int32_t)std::min<uint64_t>(maxrows, 1u << 30);
+  p->max_blocks = 0;
   p->smem_bytes = (sif::DNT / 32) * (int)(segw * 4 + 2 * ((segw + 31) / 32) * 4);
-  const DecWs w = dec_ws(std::max(n, 1), maxrows);
+  const DecWs w = dec_ws(std::max(n, 1), rows);
   p->ws_desc_off = w.desc;
   p->ws_aux_off = w.table;
-  p->ws_spill_off = w.acc;
+  p->ws_spill_off = rows;  // decode plans: total table rows
   p->ws_bytes = w.total;
   return SIF_OK;
 }
 
-uint64_t sif_dec_table_stride(const sif_plan* p) { return p ? (2ull + (uint64_t)p->max_blocks) * 64ull : 0; }
+uint64_t sif_dec_table_offset(const sif_plan* p, const sif_dec_desc* d, int i) {
+  if (!p || !d || i < 0 || i >= p->n) return 0;
+  uint64_t rows = 0;
+  for (int k = 0; k < i; ++k) rows += dec_table_rows(d[k]);
+  return p->ws_aux_off + 64ull * rows;
+}
 
 int sif_dec_upload(const sif_plan* p, const sif_dec_desc* d, void* ws, void* stream) {
   if (!p || !ws) return SIF_ERR_INVALID_ARG;
-  if (crc_tables_init()) return SIF_ERR_CUDA;
+  if (!dev_state()) return SIF_ERR_CUDA;
   cudaStream_t s = (cudaStream_t)stream;
   uint8_t* wb = (uint8_t*)ws;
   if (p->n == 0) return SIF_OK;
-  const DecWs w = dec_ws(p->n, p->max_blocks);
+  const DecWs w = dec_ws(p->n, p->ws_spill_off);
   if (check_cuda(cudaMemcpyAsync(wb + w.desc, d, sizeof(sif_dec_desc) * p->n, cudaMemcpyHostToDevice, s)))
     return SIF_ERR_CUDA;
   const uint32_t segw = (uint32_t)p->tiles;
   std::vector<uint32_t> seg((size_t)p->n + 1, 0);
-  std::vector<uint64_t> items((size_t)p->n + 1, 0);
+  std::vector<uint64_t> items((size_t)p->n + 1, 0), toff((size_t)p->n + 1, 0);
   for (int i = 0; i < p->n; ++i) {
     seg[i + 1] = seg[i] + dec_segments(d[i].in_len);
     const uint32_t R = d[i].cols <= segw && d[i].cols ? segw / d[i].cols : 1u;  // rows per item
     items[i + 1] = items[i] + (uint64_t)((d[i].rows + R - 1) / R) * ((d[i].cols + segw - 1) / segw);
+    toff[i + 1] = toff[i] + dec_table_rows(d[i]) * sif::TROW_U32;
   }
   if (check_cuda(cudaMemsetAsync(wb + w.acc, 0, 16ull * p->n, s))) return SIF_ERR_CUDA;
   if (check_cuda(cudaMemcpyAsync(wb + w.segbase, seg.data(), 4ull * (p->n + 1), cudaMemcpyHostToDevice, s)))
     return SIF_ERR_CUDA;
   if (check_cuda(cudaMemcpyAsync(wb + w.itembase, items.data(), 8ull * (p->n + 1), cudaMemcpyHostToDevice, s)))
+    return SIF_ERR_CUDA;
+  if (check_cuda(cudaMemcpyAsync(wb + w.taboff, toff.data(), 8ull * (p->n + 1), cudaMemcpyHostToDevice, s)))
     return SIF_ERR_CUDA;
   return check_cuda(cudaStreamSynchronize(s));
 }
@@ -577,15 +618,17 @@ int sif_dec_upload(const sif_plan* p, const sif_dec_desc* d, void* ws, void* str
 int sif_dec_run(const sif_plan* p, int parse_only, void* ws, int32_t* status, void* stream) {
   if (!p || !ws || !status) return SIF_ERR_INVALID_ARG;
   if (p->n == 0) return SIF_OK;
+  DevState* ds = dev_state();
+  if (!ds) return SIF_ERR_CUDA;
   cudaStream_t s = (cudaStream_t)stream;
   uint8_t* wb = (uint8_t*)ws;
-  const DecWs w = dec_ws(p->n, p->max_blocks);
+  const DecWs w = dec_ws(p->n, p->ws_spill_off);
   sif::DecArgs a;
   memset(&a, 0, sizeof(a));
   a.descs = reinterpret_cast<const sif_dec_desc*>(wb + w.desc);
   a.n = p->n;
   a.table = reinterpret_cast<uint32_t*>(wb + w.table);
-  a.table_stride = (2ull + (uint64_t)p->max_blocks) * sif::TROW_U32;
+  a.tab_off = reinterpret_cast<const uint64_t*>(wb + w.taboff);
   a.acc = reinterpret_cast<uint32_t*>(wb + w.acc);
   a.parse_only = parse_only;
   a.status = status;
@@ -594,26 +637,18 @@ int sif_dec_run(const sif_plan* p, int parse_only, void* ws, int32_t* status, vo
   a.segw = p->tiles;
   { ProfScope ps(KP_PARSE, s); sif::sif_parse_kernel<<<(p->n + 127) / 128, 128, 0, s>>>(a); }
   {
-    static int g_dcrc = 0;
-    if (!g_dcrc) g_dcrc = resident_grid(sif::sif_dcrc_kernel, sif::DNT, 0, 1ull << 30);
-    const unsigned warps = (unsigned)p->cluster, grid = std::min<unsigned>((warps + sif::DNT / 32 - 1) / (sif::DNT / 32), g_dcrc);
+    const unsigned warps = (unsigned)p->cluster;
+    const unsigned grid = std::min<unsigned>((warps + sif::DNT / 32 - 1) / (sif::DNT / 32), ds->g_dcrc);
     ProfScope ps(KP_DCRC, s);
     sif::sif_dcrc_kernel<<<std::max(1u, grid), sif::DNT, 0, s>>>(a);
   }
   if (!parse_only) {
-    static int attr_bytes = 0;
-    if (p->smem_bytes > attr_bytes) {
-      if (check_cuda(cudaFuncSetAttribute(sif::sif_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          std::max(p->smem_bytes, 1))))
-        return SIF_ERR_CUDA;
-      attr_bytes = p->smem_bytes;
-    }
     int per = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sif::sif_scatter_kernel, sif::DNT, p->smem_bytes) != cudaSuccess ||
         per < 1)
       per = 1;
     ProfScope ps(KP_SCATTER, s);
-    sif::sif_scatter_kernel<<<(unsigned)(per * num_sms()), sif::DNT, p->smem_bytes, s>>>(a);
+    sif::sif_scatter_kernel<<<(unsigned)(per * ds->sms), sif::DNT, p->smem_bytes, s>>>(a);
   }
   { ProfScope ps(KP_DFINAL, s); sif::sif_dfinal_kernel<<<(p->n + 127) / 128, 128, 0, s>>>(a); }
   return check_cuda(cudaGetLastError());

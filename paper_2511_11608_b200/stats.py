@@ -23,6 +23,7 @@ from .codec import (
     MODE_ABQ,
     MODE_FIXED,
     CodecConfig,
+    CompressedIF,
     Payload,
     col_bits,
     deserialize,
@@ -70,7 +71,7 @@ def header_fields(p: Payload) -> dict:
 
 def stats(p) -> dict:
     """The `slicer stats --json` dictionary (cli.py:199-236) of a payload or `.sif` bytes."""
-    if not isinstance(p, Payload):
+    if not isinstance(p, (Payload, CompressedIF)):
         p = deserialize(p)
     h = header_fields(p)
     blocks = p.blocks()

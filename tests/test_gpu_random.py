@@ -155,3 +155,36 @@ print("ok")
     env = dict(os.environ, SIF_TEST_INJECT="1")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-4000:]
+
+
+def _tie_cut_if(a_big, rows, cols, seed):
+    """A plus plane whose MS cut (rank base, M+ = 2) is the LAST element of a tie group
+    larger than the exact-ranking capacity (1024): A distinct values above 1, 1500 copies
+    of 1.0, A + 1498 distinct values below 1; everything else 0 and s chosen so exactly
+    these are kept."""
+    rng = np.random.default_rng(seed)
+    big = (1.0 + (np.arange(a_big) + 1) * 2.0 ** -12).astype(np.float32)
+    ties = np.ones(1500, np.float32)
+    small = (0.1 + np.arange(a_big + 1498) * (0.8 / (a_big + 1498))).astype(np.float32)
+    vals = np.concatenate([big, ties, small])
+    x = np.zeros(rows * cols, np.float32)
+    x[rng.permutation(rows * cols)[: vals.size]] = vals
+    k = vals.size
+    s = 1.0 - (k + 0.5) / (rows * cols)  # floor((1 - s) T + 1e-9) == k
+    return x.reshape(rows, cols), s
+
+
+def test_ms_cut_at_last_element_of_large_tie_group(sif):
+    """Regression (found by the C5 workload parity, stream 6055): an MS cut that lands on
+    the last member of a tie group with more than 1024 members must still place the block
+    boundary at that member's flat index (msplit.py:64) -- single-CTA select and the
+    multi-kernel select of large IFs, lambda = 0 and lambda > 0."""
+    from oracle import sif_oracle as O
+
+    for a_big, rows, cols in ((1000, 300, 200), (32000, 2048, 64)):
+        x, s = _tie_cut_if(a_big, rows, cols, a_big)
+        for lam in (0.0, 0.05):
+            kw = dict(s=s, lam=lam, m_plus=2, m_minus=1, q_bit=8, delta=0.01)
+            ref = O.encode_bytes(x, O.Cfg(**kw), 3)
+            p = sif.encode(torch.from_numpy(x).cuda(), sif.CodecConfig(**kw), seed=3)
+            assert p.to_bytes() == ref, (a_big, lam)
