@@ -100,6 +100,8 @@ typedef struct sif_plan {
   uint64_t ws_desc_off; /* offsets of the sections inside the workspace     */
   uint64_t ws_aux_off;
   uint64_t ws_spill_off;
+  int32_t n_fused;      /* encode: IFs finished by the per-IF back end          */
+  int32_t reserved;     /* encode: IFs on the token path (one CTA each)         */
 } sif_plan;
 
 /* ---- scalars (host) ---- */
@@ -119,6 +121,12 @@ int sif_enc_upload(const sif_plan* plan, const sif_enc_desc* descs, const sif_co
                    void* d_ws, void* stream);
 int sif_enc_run(const sif_plan* plan, const sif_codec_cfg* cfg, void* d_ws, uint64_t* d_out_len,
                 int32_t* d_status, void* stream);
+/* Size classes: multi-chunk IFs of tmin..tmax elements (default: none) finish their encode
+ * in the per-IF back end (one CTA per IF after the stream pass), all others in the chunk
+ * pipeline; both produce the same bytes.  Process-wide, read by sif_enc_plan (a plan keeps
+ * the routing it was made with). */
+int sif_set_fused_range(uint64_t tmin, uint64_t tmax);
+int sif_get_fused_range(uint64_t* tmin, uint64_t* tmax);
 /* plan + upload + run in one call. */
 int sif_encode_batched(const sif_enc_desc* descs, int n, const sif_codec_cfg* cfg, void* d_ws,
                        size_t ws_bytes, uint64_t* d_out_len, int32_t* d_status, void* stream);

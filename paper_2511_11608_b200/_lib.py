@@ -32,10 +32,10 @@ class Plan(ctypes.Structure):
     _fields_ = [("n", c_int32), ("cluster", c_int32), ("threads", c_int32), ("smem_bytes", c_int32),
                 ("cap_smem", c_int32), ("max_blocks", c_int32), ("tiles", c_int32), ("flags", c_int32),
                 ("ws_bytes", c_uint64), ("ws_desc_off", c_uint64), ("ws_aux_off", c_uint64),
-                ("ws_spill_off", c_uint64)]
+                ("ws_spill_off", c_uint64), ("n_fused", c_int32), ("reserved", c_int32)]
 
 
-assert ctypes.sizeof(EncDesc) == 48 and ctypes.sizeof(DecDesc) == 40 and ctypes.sizeof(Plan) == 64
+assert ctypes.sizeof(EncDesc) == 48 and ctypes.sizeof(DecDesc) == 40 and ctypes.sizeof(Plan) == 72
 
 EXPORTS = {
     "sif_version": (c_int, []),
@@ -44,6 +44,8 @@ EXPORTS = {
     "sif_validate_cfg": (c_int, [POINTER(CodecCfgC)]),
     "sif_max_payload_bytes": (c_uint64, [c_uint32, c_uint32, POINTER(CodecCfgC)]),
     "sif_status_string": (ctypes.c_char_p, [c_int]),
+    "sif_set_fused_range": (c_int, [c_uint64, c_uint64]),
+    "sif_get_fused_range": (c_int, [POINTER(c_uint64), POINTER(c_uint64)]),
     "sif_enc_plan": (c_int, [POINTER(EncDesc), c_int, POINTER(CodecCfgC), POINTER(Plan)]),
     "sif_enc_upload": (c_int, [POINTER(Plan), POINTER(EncDesc), POINTER(CodecCfgC), c_void_p, c_void_p]),
     "sif_enc_run": (c_int, [POINTER(Plan), POINTER(CodecCfgC), c_void_p, c_void_p, c_void_p, c_void_p]),

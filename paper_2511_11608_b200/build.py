@@ -10,7 +10,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libsif.so")
-SOURCES = ["sif_lib.cu", "sif_enc.cu", "sif_decode.cu", "sif_synth.cu", "sif_common.cuh",
+SOURCES = ["sif_lib.cu", "sif_enc.cu", "sif_post.cu", "sif_token.cu", "sif_decode.cu", "sif_synth.cu", "sif_common.cuh",
            "sif_crc_tables.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "1835"]

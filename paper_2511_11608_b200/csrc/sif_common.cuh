@@ -216,12 +216,15 @@ __device__ uint32_t crc_cta_staged(const uint8_t* base, uint64_t b0, uint64_t b1
                                    uint32_t* stage, uint32_t part = 0, uint32_t nparts = 1) {
   constexpr int NW = NT / 32;
   constexpr int LOGNT = NT >= 1024 ? 10 : NT >= 512 ? 9 : NT >= 256 ? 8 : NT >= 128 ? 7 : NT >= 64 ? 6 : 5;
+  static_assert(NT <= 1024, "crc_cta_staged: at most 1024 threads");
   constexpr int64_t L = 64, SPAN = L * NT, WORDS = SPAN / 4;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint64_t n = b1 > b0 ? b1 - b0 : 0;
   const int64_t rounds = (int64_t)((n + SPAN - 1) / SPAN);
   const uint32_t* gw = reinterpret_cast<const uint32_t*>(base);
-  const uint32_t myshift = kCrcShift64[NT - 1 - tid];
+  // x^(8*64*(NT-1-tid)): the table covers 512 chunks; x^(8*64*512) = x^(2^18) = kX2n[18]
+  const uint32_t myshift = (NT - 1 - tid) < 512 ? kCrcShift64[NT - 1 - tid]
+                                                : crc_mult(kCrcShift64[NT - 1 - tid - 512], kX2n[18]);
   const int lognp = nparts >= 8 ? 3 : nparts >= 4 ? 2 : nparts >= 2 ? 1 : 0;
   uint32_t total = 0;
   int64_t qtop = rounds - 1;

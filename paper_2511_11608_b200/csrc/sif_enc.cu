@@ -50,6 +50,11 @@ enum : uint32_t {
   F_KEEP_NONE = 1u, F_ONLY_NONZERO = 2u, F_ZERO_MODE = 4u, F_USE_CLS = 8u, F_TIE_ALL = 16u
 };
 enum : uint32_t { E_NONE = 0u, E_NONFINITE = 1u, E_CAPACITY = 2u };
+// PATH_PIPE: every stage is a chunk / per-IF kernel of this file.  PATH_POST: prep and
+// stream as PATH_PIPE, then one CTA per IF runs select .. CRC with the candidate list in
+// shared memory (enc_post, sif_post.cu).
+// PATH_TOKEN: the whole encode of a token-sized IF in one CTA (enc_token, sif_token.cu).
+enum : uint32_t { PATH_PIPE = 0u, PATH_POST = 1u, PATH_TOKEN = 2u };
 
 // Static per-IF description, built on the host (sif_enc_upload).
 struct IfInfo {
@@ -59,9 +64,10 @@ struct IfInfo {
   uint32_t N, K, cb, dtype;
   uint32_t ch0, nch;
   int32_t hslot;
-  uint32_t pad;
+  uint32_t path;      // PATH_PIPE / PATH_POST
   uint64_t list_off;  // workspace byte offset of the candidate list: uint2[T]
   uint64_t gat_off;   // gather spill / member slots: uint2[T]
+  uint64_t sp_off;    // PATH_POST: the candidates beyond enc_post's shared-memory part, uint2[T]
 };
 
 // Dynamic per-IF state (device).
@@ -115,7 +121,7 @@ struct EArgs {
   const uint64_t* kept_off;
   double* tau3;
   const uint32_t* seg_base;  // [n+1] prefix of CRC segments per IF
-  uint64_t* prof;            // optional phase timestamps of enc_select (16 per IF, debug)
+  uint64_t* prof;            // optional phase timestamps (32 per IF: enc_select 0-8, enc_post 16-23; debug)
   uint32_t big_ncand;        // IFs with more candidates use the multi-kernel select (0: never)
   uint32_t* big_list;        // [n] IFs on the multi-kernel select path, [n] = their count
   uint32_t inject;           // test-only fault injection (SIF_TEST_INJECT): bit 0 = sampled bracket misses
@@ -125,7 +131,7 @@ __device__ __forceinline__ void prof_mark(const EArgs& a, int ifi, int k) {
   if (a.prof && threadIdx.x == 0) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.prof[(uint64_t)ifi * 16 + k] = t;
+    a.prof[(uint64_t)ifi * 32 + k] = t;
   }
 }
 
@@ -167,6 +173,7 @@ struct List {
     if (i < cap) s[i] = make_uint2(b, x);
     else __stcg(g + (i - cap), make_uint2(b, x));
   }
+  __device__ __forceinline__ uint2 get(uint32_t i) const { return i < cap ? s[i] : __ldcg(g + (i - cap)); }
 };
 
 // Visit every list element (order-free) as f(bits, idx, true).  Global parts are read U
@@ -584,19 +591,14 @@ __device__ __forceinline__ void unit_span(const EArgs& a, const IfInfo& f, uint3
 // bracket is detected in K3 and the IF re-streamed).
 // SMALL: a batch whose IFs all fit one chunk (<= 4096 elements): narrow CTAs and only the
 // exact-tau path, so many IFs share an SM.
+// Candidate bracket lo for IF f (K1): the exact tau key for IFs of <= EXACT_T elements (3
+// radix levels in shared memory), otherwise a sampled lower bound (4096 elements, 13-bit
+// key histogram, 3-sigma margin); 1 when no bracket applies.  sh8k: >= EXACT_T + 2048 u32
+// of shared memory (8192 + 2048 covers both).
 template <int NT, bool SMALL>
-__global__ void __launch_bounds__(NT) enc_prep(EArgs a) {
+__device__ __forceinline__ uint32_t bracket_lo(const EArgs& a, const IfInfo& f, uint32_t* sh8k, SelSh& sh) {
   constexpr int EXACT_T = SMALL ? CH : 8192;  // IFs up to this size get the exact tau key as lo
-  __shared__ uint32_t sh8k[(SMALL ? CH : 8192) + 2048];
-  __shared__ SelSh sh;
-  const int i = blockIdx.x, tid = threadIdx.x;
-  const IfInfo f = a.info[i];
-  IfSt& st = a.st[i];
-  for (int b = tid; b < a.maxb; b += NT) { st.bmin[b] = 0x7FFFFFFFu; st.bmax[b] = 0u; }
-  for (int k = tid; k < a.maxb * 16; k += NT) st.S[k] = 0ull;
-  for (int b = tid; b < a.maxb; b += NT) st.bcount[b] = 0u;
-  // (the IF's digit histogram is zeroed by enc_select after it has read it, and by
-  //  sif_enc_upload before the first run)
+  const int tid = threadIdx.x;
   const uint64_t T = f.T, kk = f.kk;
   uint32_t lo = 1;
   if (T <= EXACT_T && kk > 0) {
@@ -686,13 +688,30 @@ __global__ void __launch_bounds__(NT) enc_prep(EArgs a) {
     if (lo == 0) lo = 1;
     if (a.inject & 1u) lo = 0x7F000000u;  // fault injection (tests): the bracket misses, K3 re-streams
   }
+  return lo;
+}
+
+template <int NT, bool SMALL>
+__global__ void __launch_bounds__(NT) enc_prep(EArgs a) {
+  __shared__ uint32_t sh8k[(SMALL ? CH : 8192) + 2048];
+  __shared__ SelSh sh;
+  const int i = blockIdx.x, tid = threadIdx.x;
+  const IfInfo f = a.info[i];
+  IfSt& st = a.st[i];
+  if (i == 0 && tid == 0) a.big_list[a.n] = 0;
+  if (f.path == PATH_TOKEN) return;  // encoded by enc_token
+  for (int b = tid; b < a.maxb; b += NT) { st.bmin[b] = 0x7FFFFFFFu; st.bmax[b] = 0u; }
+  for (int k = tid; k < a.maxb * 16; k += NT) st.S[k] = 0ull;
+  for (int b = tid; b < a.maxb; b += NT) st.bcount[b] = 0u;
+  // (the IF's digit histogram is zeroed by enc_select after it has read it, and by
+  //  sif_enc_upload before the first run)
+  uint32_t lo = bracket_lo<NT, SMALL>(a, f, sh8k, sh);
   uint32_t lo_neg = lo;
   if (a.lam > 0.0 && lo > 1) {
     const double t = __dmul_rn(__dsub_rn(1.0, a.lam), (double)__uint_as_float(lo));
     const uint32_t k2 = __float_as_uint(__double2float_rd(t));
     lo_neg = k2 > 1 ? k2 : 1u;
   }
-  if (i == 0 && tid == 0) a.big_list[a.n] = 0;
   if (tid == 0) {
     st.lo = lo; st.lo_neg = lo_neg; st.ncand = 0; st.maxkey = 0; st.cnt_lo = 0; st.err = E_NONE; st.flags = 0;
     st.P = 0; st.crc_acc = 0; st.seg_done = 0; st.sel_phase = 0;
@@ -821,18 +840,19 @@ struct K3Sh {
 // then gathered by all SMs (enc_gather<1>), PH 1 selects tau inside it, counts the kept
 // elements, finds every MS cut's digit and resolves the cuts inside tau's bin; the other
 // cut bins are gathered by all SMs (enc_gather<2>) and PH 2 resolves those cuts.
-template <int PH>
-__global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
-  constexpr int NT = SNT;
+// The body of K3 for IF `ifi`, run by every thread of a CTA of NT threads.  dsm: dynamic
+// shared memory of kSmemSelect bytes (hist | scratch | gbuf).  FUSED: called by the fused
+// per-IF encoder (enc_fused), whose stream phase already left the IF's digit histogram in
+// `hist` and resolved any bracket miss; no multi-kernel split.
+template <int PH, int NT, bool FUSED>
+__device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_t* dsm, K3Sh& k3,
+                                          const List* Lin = nullptr) {
   constexpr int LU = PH > 0 ? 16 : 8;  // loads in flight per thread in list passes (big IFs: deep)
-  extern __shared__ __align__(16) uint8_t dsm_raw[];
-  uint32_t* dsm = reinterpret_cast<uint32_t*>(dsm_raw);
-  __shared__ K3Sh k3;
   SelSh& sh = k3.s;
   uint32_t* hist = dsm;                         // 2*ND
   uint32_t* scratch = dsm + 2 * ND;             // 2*HB + GCAP*4
   uint32_t* gbuf = scratch + 2 * HB + GCAP * 4; // 2*GSM (also the re-stream stage)
-  const int ifi = blockIdx.x, tid = threadIdx.x;
+  const int tid = threadIdx.x;
   const IfInfo f = a.info[ifi];
   IfSt& st = a.st[ifi];
   const uint64_t kk = f.kk, seed = f.seed;
@@ -875,7 +895,9 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   uint32_t ncand = st.ncand;
   bool hist_ok = false;
   prof_mark(a, ifi, 0);
-  if (PH == 0 && kk > 0 && st.cnt_lo < kk && lo > floor_lo) {
+  if (FUSED) {
+    hist_ok = true;
+  } else if (PH == 0 && kk > 0 && st.cnt_lo < kk && lo > floor_lo) {
     // bracket missed (or tau == 0): re-stream keeping every nonzero (every element in
     // ATKF-only mode); this CTA writes the list in chunk order and the histogram in SMEM
     lo = floor_lo;
@@ -928,7 +950,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
     for (int k = tid; k < 2 * ND / 4; k += NT) h4[k] = __ldcg(gh + k);
     hist_ok = true;
   }
-  const List L{nullptr, le(a, f), 0};
+  const List L = (FUSED && Lin) ? *Lin : List{nullptr, le(a, f), 0};
   if (!hist_ok) {
     for (int k = tid; k < 2 * ND; k += NT) hist[k] = 0;
     __syncthreads();
@@ -986,7 +1008,7 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
       tie_all = s.all_ties;
     } else {
       prof_mark(a, ifi, 2);
-      if (PH == 0 && a.big_ncand && ncand > a.big_ncand) {
+      if (!FUSED && PH == 0 && a.big_ncand && ncand > a.big_ncand) {
         // digit of tau over both signs; its bin is gathered by enc_gather<1> (all SMs)
         uint32_t* comb = scratch;
         for (int k = tid; k < ND; k += NT) comb[k] = hist[k] + hist[ND + k];
@@ -1291,6 +1313,14 @@ __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   }
 }
 
+template <int PH>
+__global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
+  extern __shared__ __align__(16) uint8_t dsm_raw[];
+  __shared__ K3Sh k3;
+  if (a.info[blockIdx.x].path != PATH_PIPE) return;  // selected by enc_post
+  select_if<PH, SNT, false>(a, (int)blockIdx.x, reinterpret_cast<uint32_t*>(dsm_raw), k3);
+}
+
 
 // ---------------------------------------------------------------------------------------
 // K3t: one warp per single-chunk IF (T <= CH, e.g. a decode-step token) on the common path
@@ -1361,6 +1391,7 @@ __global__ void __launch_bounds__(TNT) enc_select_tiny(EArgs a) {
   const IfInfo& f = a.info[ifi];
   IfSt& st = a.st[ifi];
   const uint64_t kk = f.kk;
+  if (f.path != PATH_PIPE) return;
   const uint32_t n = st.ncand;
   if (a.atkf_only || f.hslot >= 0 || f.T > (uint64_t)CH || a.lam != 0.0 || kk == 0 || st.err ||
       st.maxkey >= kNonFiniteKey || st.lo < 1 || st.cnt_lo < kk || n > (uint32_t)TCAP || n < kk)
@@ -1672,7 +1703,7 @@ __global__ void __launch_bounds__(CNT, 6) enc_members(EArgs a) {
     const uint32_t ifi = a.ch_if[c];
     const IfInfo& f = a.info[ifi];
     IfSt& st = a.st[ifi];
-    if (st.err) continue;
+    if (st.err || f.path != PATH_PIPE) continue;
     if (ifi != cur) {
       __syncwarp();
       if (lane == 0) {
@@ -1843,7 +1874,7 @@ __global__ void __launch_bounds__(CNT, 4) enc_abq(EArgs a) {
     const uint32_t ifi = a.ch_if[c];
     const IfInfo& f = a.info[ifi];
     IfSt& st = a.st[ifi];
-    if (st.err) continue;
+    if (st.err || f.path != PATH_PIPE) continue;
     if (ifi != cur) {
       flush();
       B = (int)st.B;
@@ -1954,7 +1985,7 @@ __global__ void __launch_bounds__(256) enc_layout(EArgs a) {
   const int ifi = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const IfInfo f = a.info[ifi];
   IfSt& st = a.st[ifi];
-  if (st.err) return;
+  if (f.path != PATH_PIPE || st.err) return;
   const int B = (int)st.B;
   const uint32_t ch0 = f.ch0, nch = f.nch;
   // chunk prefixes of block b (warp b % 8): member offsets and the last row before the chunk
@@ -2137,7 +2168,7 @@ __global__ void __launch_bounds__(CNT, 4) enc_pack(EArgs a) {
     const uint32_t ifi = a.ch_if[c];
     const IfInfo& f = a.info[ifi];
     IfSt& st = a.st[ifi];
-    if (st.err) continue;
+    if (st.err || f.path != PATH_PIPE) continue;
     if (ifi != cur) {
       __syncwarp();
       B = (int)st.B;

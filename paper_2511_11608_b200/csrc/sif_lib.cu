@@ -12,7 +12,7 @@
 
 #include "sif.h"
 #include "sif_decode.cu"
-#include "sif_enc.cu"
+#include "sif_token.cu"
 #include "sif_synth.cu"
 
 namespace {
@@ -24,11 +24,11 @@ int check_cuda(cudaError_t e) { return e == cudaSuccess ? SIF_OK : SIF_ERR_CUDA;
 
 // ---- optional per-kernel timing (diagnostics; sif_profile_enable)
 enum { KP_PREP, KP_STREAM, KP_SELECT, KP_MEMBERS, KP_ABQ1, KP_ABQ2, KP_LAYOUT, KP_PACK, KP_CRC, KP_PARSE, KP_DCRC,
-       KP_SCATTER, KP_DFINAL, KP_SELECT_TINY, KP_GATHER1, KP_SELECT1, KP_GATHER2, KP_SELECT2, KP_N };
+       KP_SCATTER, KP_DFINAL, KP_SELECT_TINY, KP_GATHER1, KP_SELECT1, KP_GATHER2, KP_SELECT2, KP_FUSED, KP_TOKEN, KP_N };
 const char* kKpNames[KP_N] = {"enc_prep", "enc_stream", "enc_select<0>", "enc_members", "enc_abq<1>", "enc_abq<0>",
                               "enc_layout", "enc_pack", "enc_crc", "sif_parse_kernel", "sif_dcrc_kernel",
                               "sif_scatter_kernel", "sif_dfinal_kernel", "enc_select_tiny", "enc_gather<1>",
-                              "enc_select<1>", "enc_gather<2>", "enc_select<2>"};
+                              "enc_select<1>", "enc_gather<2>", "enc_select<2>", "enc_post", "enc_token"};
 struct ProfRec { int k; cudaEvent_t a, b; };
 std::atomic<bool> g_prof{false};
 std::mutex g_prof_mu;  // guards g_recs (launches may come from several host threads)
@@ -110,6 +110,8 @@ struct DevState {
   int status = SIF_OK;
   int sms = 148;
   int g_stream = 1, g_members = 1, g_gather = 1, g_crc = 1, g_dcrc = 1, g_scatter = 1;
+  int post_smem = 0;       // enc_post: dynamic shared memory (all that is left next to its static part)
+  uint32_t post_lcap = 0;  // enc_post: candidates held in shared memory
   std::mutex mu;  // guards the per-maxb grid cache
   int g_abq[sif::MAXB + 1] = {0};
   int g_pack[sif::MAXB + 1] = {0};
@@ -128,12 +130,24 @@ int dev_init(DevState& ds, int dev) {
       check_cuda(cudaFuncSetAttribute(sif::enc_select<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
       check_cuda(cudaFuncSetAttribute(sif::enc_select<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
       check_cuda(cudaFuncSetAttribute(sif::enc_select<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
+
       check_cuda(cudaFuncSetAttribute(sif::enc_abq<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_abq(sif::MAXB))) ||
       check_cuda(cudaFuncSetAttribute(sif::enc_abq<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_abq(sif::MAXB))) ||
       check_cuda(cudaFuncSetAttribute(sif::enc_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pack(sif::MAXB))) ||
       check_cuda(cudaFuncSetAttribute(sif::sif_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kSmemScatterMax)))
     return SIF_ERR_CUDA;
+  {
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, sif::enc_post) != cudaSuccess) return SIF_ERR_CUDA;
+    int optin = 0;
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return SIF_ERR_CUDA;
+    ds.post_smem = optin - (int)fa.sharedSizeBytes;
+    if (ds.post_smem < sif::kSmemSelectBytes + 8 * 1024) return SIF_ERR_CUDA;
+    ds.post_lcap = (uint32_t)((ds.post_smem - sif::kSmemSelectBytes) / 8);
+    if (check_cuda(cudaFuncSetAttribute(sif::enc_post, cudaFuncAttributeMaxDynamicSharedMemorySize, ds.post_smem)))
+      return SIF_ERR_CUDA;
+  }
   const uint64_t big = 1ull << 30;
   ds.g_gather = resident_grid(sif::enc_gather<1>, sif::CNT, 0, big, ds.sms);
   ds.g_crc = resident_grid(sif::enc_crc, sif::CNT, 0, big, ds.sms);
@@ -155,7 +169,7 @@ DevState* dev_state() {
 // Workspace sections of an encode plan (all offsets 256-byte aligned).
 struct EncWs {
   uint64_t info, st, ch_if, ch_e0, u_off, u_cnt, bcnt, bpre, brs, blast, bprev, hist, fixedq, keptoff, segbase, biglist,
-      lists;
+      fused, tokens, lists;
 };
 
 EncWs enc_ws(uint64_t n, uint64_t nch, uint64_t maxb, uint64_t nhist, uint64_t nq) {
@@ -178,6 +192,8 @@ EncWs enc_ws(uint64_t n, uint64_t nch, uint64_t maxb, uint64_t nhist, uint64_t n
   w.keptoff = take(8 * n);
   w.segbase = take(4 * (n + 1));
   w.biglist = take(4 * (n + 1));
+  w.fused = take(4 * (n + 1));
+  w.tokens = take(4 * (n + 1));
   w.lists = off;
   return w;
 }
@@ -266,6 +282,41 @@ uint64_t sif_max_payload_bytes(uint32_t rows, uint32_t cols, const sif_codec_cfg
 }
 
 // ------------------------------------------------------------------ encode
+// IFs of [tmin, tmax] elements (env SIF_FUSED_MIN / SIF_FUSED_MAX, or sif_set_fused_range;
+// default: none) take the per-IF back end after the stream pass (one CTA per IF from the
+// candidate list to the .sif stream, sif_post.cu); the others the chunk kernels.  Only
+// multi-chunk IFs qualify.  Read when a plan is made.  Measured on C2 (256 x 1024x196): the
+// per-IF back end is correct but slower than the chunk kernels in the pipelined steady
+// state (one 1024-thread CTA per SM holds ~210 KB of shared memory, so other slots' kernels
+// cannot co-reside, and the passes execute more instructions), hence off by default.
+static std::atomic<uint64_t> g_fmin{0}, g_fmax{0};
+static std::once_flag g_frange_once;
+static void fused_range(uint64_t& tmin, uint64_t& tmax) {
+  std::call_once(g_frange_once, [] {
+    const char* e0 = getenv("SIF_FUSED_MIN");
+    const char* e1 = getenv("SIF_FUSED_MAX");
+    g_fmin = e0 && *e0 ? strtoull(e0, nullptr, 0) : 1ull;
+    g_fmax = e1 && *e1 ? strtoull(e1, nullptr, 0) : 0ull;
+  });
+  tmin = g_fmin.load();
+  tmax = g_fmax.load();
+}
+static bool is_fused(uint64_t T, int atkf) {
+  uint64_t tmin, tmax;
+  fused_range(tmin, tmax);
+  return !atkf && T > (uint64_t)sif::CH && T < (1ull << 25) && T >= tmin && T <= tmax;
+}
+
+// Token path: IFs of <= 4096 elements with lambda = 0, k >= 1 and at most 8 blocks are
+// encoded start to finish by enc_token (one CTA each); SIF_TOKEN=0 turns it off.
+static bool is_token(uint64_t T, int atkf, const sif_codec_cfg* c) {
+  static const bool on = [] { const char* e = getenv("SIF_TOKEN"); return !(e && *e == '0'); }();
+  if (!on || atkf || T > (uint64_t)sif::KT || c->lam != 0.0) return false;
+  const uint64_t k = sif::keep_count(c->s, T);
+  if (k < 1) return false;
+  return std::min<uint64_t>(c->m_plus, k) + std::min<uint64_t>(c->m_minus, k) <= (uint64_t)sif::KB;
+}
+
 static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, int atkf, sif_plan* p) {
   if (!d || !p || n < 0) return SIF_ERR_INVALID_ARG;
   int st = sif_validate_cfg(c);
@@ -274,6 +325,7 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
   uint64_t kmax = 0, nch = 0, nhist = 0, lists = 0, nseg = 0;
   bool tiny = false;  // some IF may take the warp-per-IF select (enc_select_tiny)
   bool all_small = n > 0;  // every IF fits one chunk: narrow enc_prep
+  int nfused = 0, ntoken = 0;
   for (int i = 0; i < n; ++i) {
     if (d[i].rows < 1 || d[i].cols < 1) return SIF_ERR_SHAPE;  // tensor.py:27-28
     const uint64_t T = (uint64_t)d[i].rows * d[i].cols;
@@ -281,19 +333,31 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
     if (d[i].dtype != SIF_DTYPE_F32 && d[i].dtype != SIF_DTYPE_BF16) return SIF_ERR_INVALID_ARG;
     if (!d[i].x || (reinterpret_cast<uintptr_t>(d[i].x) & 15)) return SIF_ERR_INVALID_ARG;
     if (!atkf && (!d[i].out || (reinterpret_cast<uintptr_t>(d[i].out) & 15))) return SIF_ERR_INVALID_ARG;
-    kmax = std::max(kmax, sif::keep_count(c->s, T));
     if (sif_max_payload_bytes(d[i].rows, d[i].cols, c) >= (1ull << 29)) return SIF_ERR_INVALID_ARG;  // u32 bit offsets
+    if (crc_segments(d[i].out_cap) > (uint64_t)sif::CRC_PIECES_MAX) return SIF_ERR_INVALID_ARG;
+    if (is_token(T, atkf, c)) {  // enc_token does it all
+      ++ntoken;
+      lists += up(16 * T, 256);
+      continue;
+    }
     const uint64_t ch = (T + sif::CH - 1) / sif::CH;
     nch += ch;
     if (ch > 1) ++nhist;
-    if (ch == 1 && !atkf && c->lam == 0.0 && sif::keep_count(c->s, T) > 0) tiny = true;
     if (ch > 1) all_small = false;
+    if (is_fused(T, atkf)) {  // stream pass as the pipeline, then enc_post
+      ++nfused;
+      lists += up(24 * T, 256);
+      continue;
+    }
     lists += up(16 * T, 256);
+    kmax = std::max(kmax, sif::keep_count(c->s, T));
+    if (ch == 1 && !atkf && c->lam == 0.0 && sif::keep_count(c->s, T) > 0) tiny = true;
     nseg += crc_segments(d[i].out_cap);
-    if (crc_segments(d[i].out_cap) > (uint64_t)sif::CRC_PIECES_MAX) return SIF_ERR_INVALID_ARG;
   }
   if (nch >= (1ull << 31) || nseg >= (1ull << 31)) return SIF_ERR_INVALID_ARG;
-  const uint64_t kk = std::max<uint64_t>(1, kmax);
+  uint64_t kall = kmax;  // the block bound covers the fused IFs too
+  for (int i = 0; i < n; ++i) kall = std::max(kall, sif::keep_count(c->s, (uint64_t)d[i].rows * d[i].cols));
+  const uint64_t kk = std::max<uint64_t>(1, kall);
   const int maxb = (int)(std::min<uint64_t>(c->m_plus, kk) + std::min<uint64_t>(c->m_minus, kk));
   if (maxb > sif::MAXB) return SIF_ERR_CONFIG;  // more blocks than the encoder supports
   const EncWs w = enc_ws(n, nch, maxb, nhist, (uint64_t)c->m_plus + c->m_minus);
@@ -311,6 +375,23 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
   p->ws_aux_off = w.fixedq;
   p->ws_spill_off = w.lists;
   p->ws_bytes = w.lists + lists;
+  p->n_fused = nfused;
+  p->reserved = ntoken;  // encode plans: IFs on the token path
+  if (ntoken == n) p->flags &= ~8;  // no pipeline IF: nothing to narrow
+  return SIF_OK;
+}
+
+int sif_set_fused_range(uint64_t tmin, uint64_t tmax) {
+  uint64_t a, b;
+  fused_range(a, b);  // env defaults first, then the override
+  g_fmin = tmin;
+  g_fmax = tmax;
+  return SIF_OK;
+}
+
+int sif_get_fused_range(uint64_t* tmin, uint64_t* tmax) {
+  if (!tmin || !tmax) return SIF_ERR_INVALID_ARG;
+  fused_range(*tmin, *tmax);
   return SIF_OK;
 }
 
@@ -328,6 +409,7 @@ int sif_enc_upload(const sif_plan* p, const sif_enc_desc* d, const sif_codec_cfg
   std::vector<sif::IfInfo> info((size_t)std::max(n, 1));
   std::vector<uint32_t> ch_if((size_t)std::max(p->tiles, 1)), ch_e0((size_t)std::max(p->tiles, 1));
   std::vector<uint32_t> seg((size_t)n + 1, 0);
+  std::vector<uint32_t> fused, tokens;
   uint64_t ch = 0, lists = w.lists;
   int32_t hs = 0;
   for (int i = 0; i < n; ++i) {
@@ -344,14 +426,33 @@ int sif_enc_upload(const sif_plan* p, const sif_enc_desc* d, const sif_codec_cfg
     f.K = d[i].cols;
     f.cb = sif::col_bits(d[i].cols);
     f.dtype = d[i].dtype;
-    const uint64_t nc = (f.T + sif::CH - 1) / sif::CH;
+    const uint64_t nc = is_token(f.T, p->flags & 1, c) ? 0 : (f.T + sif::CH - 1) / sif::CH;
     f.ch0 = (uint32_t)ch;
     f.nch = (uint32_t)nc;
     f.hslot = nc > 1 ? hs++ : -1;
     f.list_off = lists;
     f.gat_off = lists + 8 * f.T;
-    lists += up(16 * f.T, 256);
-    seg[i + 1] = seg[i] + crc_segments(f.cap);
+    f.path = sif::PATH_PIPE;
+    if (is_token(f.T, p->flags & 1, c)) {
+      f.path = sif::PATH_TOKEN;
+      f.ch0 = 0;
+      f.nch = 0;
+      f.hslot = -1;
+      lists += up(16 * f.T, 256);
+      seg[i + 1] = seg[i];
+      tokens.push_back((uint32_t)i);
+      continue;
+    }
+    if (is_fused(f.T, p->flags & 1)) {  // no CRC pieces: enc_post finishes the stream
+      f.path = sif::PATH_POST;
+      f.sp_off = lists + 16 * f.T;
+      lists += up(24 * f.T, 256);
+      seg[i + 1] = seg[i];
+      fused.push_back((uint32_t)i);
+    } else {
+      lists += up(16 * f.T, 256);
+      seg[i + 1] = seg[i] + crc_segments(f.cap);
+    }
     for (uint64_t k = 0; k < nc; ++k) {
       ch_if[ch + k] = (uint32_t)i;
       ch_e0[ch + k] = (uint32_t)(k * sif::CH);
@@ -366,6 +467,12 @@ int sif_enc_upload(const sif_plan* p, const sif_enc_desc* d, const sif_codec_cfg
     if (check_cuda(cudaMemcpyAsync(wb + w.ch_e0, ch_e0.data(), 4ull * ch, cudaMemcpyHostToDevice, s)))
       return SIF_ERR_CUDA;
     if (check_cuda(cudaMemcpyAsync(wb + w.segbase, seg.data(), 4ull * (n + 1), cudaMemcpyHostToDevice, s)))
+      return SIF_ERR_CUDA;
+    if (!fused.empty() &&
+        check_cuda(cudaMemcpyAsync(wb + w.fused, fused.data(), 4ull * fused.size(), cudaMemcpyHostToDevice, s)))
+      return SIF_ERR_CUDA;
+    if (!tokens.empty() &&
+        check_cuda(cudaMemcpyAsync(wb + w.tokens, tokens.data(), 4ull * tokens.size(), cudaMemcpyHostToDevice, s)))
       return SIF_ERR_CUDA;
   }
   if (c->mode == SIF_MODE_FIXED &&
@@ -435,12 +542,23 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   const unsigned nch = (unsigned)p->tiles;
   const unsigned n = (unsigned)p->n;
   const unsigned wgrid = std::max(1u, (nch + sif::CNT / 32 - 1) / (sif::CNT / 32));  // >= 1 chunk per warp
+  if (p->reserved > 0) {
+    ProfScope ps(KP_TOKEN, s);
+    sif::enc_token<<<(unsigned)p->reserved, sif::KNT, 0, s>>>(a, reinterpret_cast<const uint32_t*>(wb + w.tokens));
+  }
+  if (p->reserved == p->n) return check_cuda(cudaGetLastError());
   {
     ProfScope ps(KP_PREP, s);
     if (p->flags & 8) sif::enc_prep<128, true><<<n, 128, 0, s>>>(a);  // every IF fits one chunk
     else sif::enc_prep<512, false><<<n, 512, 0, s>>>(a);
   }
   { ProfScope ps(KP_STREAM, s); sif::enc_stream<<<std::min<unsigned>(nch, g_stream), sif::CNT, kSmemStream, s>>>(a); }
+  if (p->n_fused > 0) {
+    ProfScope ps(KP_FUSED, s);
+    sif::enc_post<<<(unsigned)p->n_fused, sif::PNT, ds->post_smem, s>>>(a, reinterpret_cast<const uint32_t*>(wb + w.fused),
+                                                                        ds->post_lcap);
+  }
+  if (p->n_fused == p->n) return check_cuda(cudaGetLastError());
   if (p->flags & 4) {
     ProfScope ps(KP_SELECT_TINY, s);
     sif::enc_select_tiny<<<(n + sif::TNT / 32 - 1) / (sif::TNT / 32), sif::TNT, 0, s>>>(a);

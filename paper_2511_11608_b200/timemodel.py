@@ -145,7 +145,26 @@ def calibrate(rows: int = 1024, cols: int = 196, batch: int = 64, kind: int = 0,
               q_grid=(4, 8, 16), delta: float = 0.01, reps: int = 5) -> DeviceTimeModel:
     """Measure the three stage tables on the current GPU for IFs of shape rows x cols
     (device synthetic generator `kind`).  Each grid axis varies alone
-    around the base point (s=0.9, lambda=0, M=3/3, q_bit=8)."""
+    around the base point (s=0.9, lambda=0, M=3/3, q_bit=8).  The stages are timed on the
+    chunk pipeline, whose kernels map one-to-one onto the planner's stages (the fused
+    per-IF kernel is switched off for the calibration and restored afterwards)."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+
+    L = _lib.load()
+    tmin, tmax = ctypes.c_uint64(), ctypes.c_uint64()
+    L.sif_get_fused_range(ctypes.byref(tmin), ctypes.byref(tmax))
+    L.sif_set_fused_range(1, 0)
+    try:
+        return _calibrate(rows, cols, batch, kind, dtype, s_grid, lam_grid, m_grid, q_grid, delta, reps)
+    finally:
+        L.sif_set_fused_range(tmin.value, tmax.value)
+
+
+def _calibrate(rows, cols, batch, kind, dtype, s_grid, lam_grid, m_grid, q_grid, delta, reps):
     import torch
 
     from .codec import CodecConfig, synthetic

@@ -188,3 +188,33 @@ def test_ms_cut_at_last_element_of_large_tie_group(sif):
             ref = O.encode_bytes(x, O.Cfg(**kw), 3)
             p = sif.encode(torch.from_numpy(x).cuda(), sif.CodecConfig(**kw), seed=3)
             assert p.to_bytes() == ref, (a_big, lam)
+
+
+def test_per_if_back_end_matches_oracle(sif):
+    """The opt-in per-IF encoder back end (sif_set_fused_range; enc_post) on C2-shaped IFs,
+    a bracket-miss IF (fault injection off: heavy ties force many candidates), lambda > 0,
+    fixed-Q and delta large enough to descend: byte-identical to the oracle."""
+    import ctypes
+
+    from oracle import sif_oracle as O
+    from oracle.synth import synth
+
+    L = sif._lib.load()
+    lo, hi = ctypes.c_uint64(), ctypes.c_uint64()
+    L.sif_get_fused_range(ctypes.byref(lo), ctypes.byref(hi))
+    L.sif_set_fused_range(4097, 1 << 20)
+    try:
+        rng = np.random.default_rng(17)
+        xs = [synth(0, 1024, 196, 3), synth(1, 64, 4096, 4),
+              rng.choice(np.array([-3, -1, 1, 2, 4], np.float32), size=(300, 200)).astype(np.float32),
+              rng.standard_normal((100, 97)).astype(np.float32)]
+        cfgs = [dict(s=0.9, m_plus=3, m_minus=3, q_bit=8, delta=0.01),
+                dict(s=0.8, lam=0.2, m_plus=2, m_minus=3, q_bit=8, delta=0.05),
+                dict(s=0.7, m_plus=4, m_minus=4, q_bit=6, delta=0.5),
+                dict(s=0.85, m_plus=3, m_minus=3, q_bit=8, mode="fixed_q", fixed_q=(9, 6, 4, 8, 5, 3))]
+        for kw in cfgs:
+            ps = sif.encode_list([torch.from_numpy(x).cuda() for x in xs], sif.CodecConfig(**kw), [5, 6, 7, 8])
+            for p, x, sd in zip(ps, xs, (5, 6, 7, 8)):
+                assert p.to_bytes() == O.encode_bytes(x, O.Cfg(**kw), sd), (kw, x.shape)
+    finally:
+        L.sif_set_fused_range(lo.value, hi.value)
