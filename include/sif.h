@@ -44,6 +44,10 @@ enum sif_status {
 enum { SIF_DTYPE_F32 = 0, SIF_DTYPE_BF16 = 1 };
 enum { SIF_MODE_ABQ = 0, SIF_MODE_FIXED = 1 };
 
+/* Effective blocks (min(M+, k) + min(M-, k), msplit.py:34-38) per IF the encoder supports;
+ * sif_enc_plan returns SIF_ERR_CONFIG above it (the reference has no limit). */
+#define SIF_MAX_BLOCKS 64
+
 /* CodecConfig (codec.py:61-92).  fixed_q is a HOST pointer with m_plus+m_minus entries
  * (plus-plane entries first), read only during sif_enc_upload / sif_encode_batched. */
 typedef struct sif_codec_cfg {
@@ -146,6 +150,11 @@ int sif_dec_upload(const sif_plan* plan, const sif_dec_desc* descs, void* d_ws, 
 int sif_dec_run(const sif_plan* plan, int parse_only, void* d_ws, int32_t* d_status, void* stream);
 int sif_decode_batched(const sif_dec_desc* descs, int n, int parse_only, void* d_ws,
                        size_t ws_bytes, int32_t* d_status, void* stream);
+/* Size class: streams of at most max_elems dense elements (default and maximum 4096; 0 =
+ * none) are decoded by one CTA each in a single launch (the stream staged in shared
+ * memory), the others by the four-kernel path; both give the same output, status and
+ * block table.  Process-wide, read by sif_dec_plan (a plan keeps its routing). */
+int sif_set_small_decode(uint64_t max_elems);
 
 /* Block table written by decode/parse: 64-byte rows of uint32.  Row 0 holds {status,
  * rows, cols, m_plus, m_minus, mode, q_bit, nblocks}; row 1 {framing status, crc, len lo,

@@ -450,6 +450,22 @@ def _enc_descs(xs, outs, caps, seeds, dtypes):
     return arr
 
 
+MAX_BLOCKS = 64  # effective blocks (M+ + M-) per IF the device encoder supports (SIF_MAX_BLOCKS)
+
+
+def _check_block_count(cfg, sizes) -> None:
+    """The encoder holds per-block state for at most MAX_BLOCKS effective blocks per IF
+    (msplit.py:34-38: m_eff = max(1, min(M, nnz)) per plane); the reference has no such
+    limit, so a larger configuration is refused up front with a ConfigError that says so."""
+    if not sizes:
+        return
+    k = max(1, max(int(_L().sif_keep_count(float(cfg.s), int(t))) for t in sizes))
+    b = min(cfg.m_plus, k) + min(cfg.m_minus, k)
+    if b > MAX_BLOCKS:
+        raise ConfigError(f"m_plus + m_minus gives {b} effective blocks per IF; this device encoder supports at most "
+                          f"{MAX_BLOCKS} (the reference has no limit)")
+
+
 def _raise_enc(status: int, i: int, n: int) -> None:
     """Encoder status -> the reference's exception and message (atkf.py:50-51)."""
     if status == 2:
@@ -482,6 +498,7 @@ class BatchEncoder:
         self._descs = _enc_descs(xs_list, outs, [self.cap] * self.B, self.seeds, [self.dtype] * self.B)
         self._cfg_c, self._keep = cfg._c()
         self.plan = _lib.Plan()
+        _check_block_count(cfg, [self.rows * self.cols])
         raise_for(_L().sif_enc_plan(self._descs, self.B, ctypes.byref(self._cfg_c), ctypes.byref(self.plan)),
                   "sif_enc_plan")
         self.ws = torch.empty(max(1, self.plan.ws_bytes), dtype=torch.uint8, device=dev)
@@ -533,6 +550,7 @@ class ListEncoder:
         self._descs = _enc_descs(self.xs, outs, self.caps, self.seeds, [d for _, d in ts])
         self._cfg_c, self._keep = cfg._c()
         self.plan = _lib.Plan()
+        _check_block_count(cfg, [r * c for r, c in self.shapes])
         raise_for(_L().sif_enc_plan(self._descs, self.B, ctypes.byref(self._cfg_c), ctypes.byref(self.plan)),
                   "sif_enc_plan")
         self.ws = torch.empty(max(1, self.plan.ws_bytes), dtype=torch.uint8, device=dev)
@@ -859,6 +877,7 @@ class BatchPipeline:
                     g = capture_graph(fn)
             self.slots.append(dict(enc=enc, dec=dec, stream=st, graph=g, fn=fn, xs=xj, seeds=list(sj)))
         self.i = 0
+        self.ran = [False] * len(self.slots)  # statuses of a slot that never stepped are the warm-up's
         torch.cuda.synchronize()
 
     def begin(self):
@@ -869,6 +888,7 @@ class BatchPipeline:
 
     def step(self):
         sl = self.slots[self.i % len(self.slots)]
+        self.ran[self.i % len(self.slots)] = True
         self.i += 1
         with torch.cuda.stream(sl["stream"]):
             if sl["graph"] is not None:
@@ -884,9 +904,12 @@ class BatchPipeline:
             cur.wait_stream(sl["stream"])
 
     def check(self):
-        for sl in self.slots:
-            sl["enc"].check()
-            sl["dec"].check()
+        """Raise the reference's exception for the first failing IF of any slot that has
+        stepped (a slot's statuses are those of its last step)."""
+        for sl, ran in zip(self.slots, self.ran):
+            if ran:
+                sl["enc"].check()
+                sl["dec"].check()
         return self
 
     def ys(self, slot: int = 0) -> torch.Tensor:

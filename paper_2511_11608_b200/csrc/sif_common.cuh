@@ -211,7 +211,9 @@ __device__ uint32_t crc_cta_raw(const uint8_t* base, uint64_t b0, uint64_t b1, c
 // stage: >= 16*NT u32 of shared memory; red: >= NT/32 + 1 u32.
 // part/nparts: this CTA handles rounds q = part, part + nparts, ... (counted from b1) and
 // returns its partial already shifted to b1; partials of all parts XOR to the raw CRC.
-template <int NT>
+// GENERIC: base is any 4-byte aligned address (e.g. a shared-memory copy of the bytes),
+// read with plain loads; otherwise global memory read through L2 (ld.global.cg).
+template <int NT, bool GENERIC = false>
 __device__ uint32_t crc_cta_staged(const uint8_t* base, uint64_t b0, uint64_t b1, const uint32_t* t4, uint32_t* red,
                                    uint32_t* stage, uint32_t part = 0, uint32_t nparts = 1) {
   constexpr int NW = NT / 32;
@@ -240,8 +242,13 @@ __device__ uint32_t crc_cta_staged(const uint8_t* base, uint64_t b0, uint64_t b1
       const int64_t j = tid + (int64_t)k * NT;
       const int64_t a = rs + 4 * j;
       const int64_t w0 = fl + j;
-      lov[k] = (a + 4 > (int64_t)b0 && w0 >= 0 && 4 * w0 + 4 > (int64_t)b0) ? __ldcg(gw + w0) : 0u;
-      hiv[k] = (a + 4 > (int64_t)b0 && sh8 && 4 * (w0 + 1) < (int64_t)b1) ? __ldcg(gw + w0 + 1) : 0u;
+      if (GENERIC) {
+        lov[k] = (a + 4 > (int64_t)b0 && w0 >= 0 && 4 * w0 + 4 > (int64_t)b0) ? gw[w0] : 0u;
+        hiv[k] = (a + 4 > (int64_t)b0 && sh8 && 4 * (w0 + 1) < (int64_t)b1) ? gw[w0 + 1] : 0u;
+      } else {
+        lov[k] = (a + 4 > (int64_t)b0 && w0 >= 0 && 4 * w0 + 4 > (int64_t)b0) ? __ldcg(gw + w0) : 0u;
+        hiv[k] = (a + 4 > (int64_t)b0 && sh8 && 4 * (w0 + 1) < (int64_t)b1) ? __ldcg(gw + w0 + 1) : 0u;
+      }
     }
 #pragma unroll
     for (int k = 0; k < WORDS / NT; ++k) {

@@ -39,6 +39,8 @@ struct DecArgs {
   const uint32_t* seg_base;    // [n+1] prefix of CRC segments per stream
   const uint64_t* item_base;   // [n+1] prefix of (row, column segment) work items per stream
   int segw;                    // columns per work item (<= 1024, multiple of 4)
+  const uint32_t* small;       // [n] 1: stream decoded by sif_dec_small (one CTA per stream)
+  const uint32_t* small_list;  // the small streams, in batch order
 };
 
 constexpr uint64_t SEGD = CRC_PIECE;  // CRC bytes per warp piece
@@ -54,21 +56,24 @@ __device__ __forceinline__ uint32_t rd_u32(const uint8_t* p, uint64_t o) {
   return (uint32_t)p[o] | ((uint32_t)p[o + 1] << 8) | ((uint32_t)p[o + 2] << 16) | ((uint32_t)p[o + 3] << 24);
 }
 
-__global__ void sif_parse_kernel(DecArgs a) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.n) return;
-  const sif_dec_desc d = a.descs[i];
+// The stream length comes from the descriptor, or -- for payloads still being produced on
+// the device (a pipelined encode -> decode) -- from the encoder's out_len, read here.
+// over: the device length exceeds the buffer the stream lives in.
+__device__ __forceinline__ uint64_t stream_len(const sif_dec_desc& d, bool& over) {
+  over = false;
+  if (!d.in_len_dev) return d.in_len;
+  const uint64_t l = *d.in_len_dev;
+  over = l > d.in_len;
+  return over ? 0 : l;
+}
+
+// Walk one stream's framing exactly in the order of deserialize (codec.py:320-385) and
+// write its block table.  `in` is the stream (device memory, or a shared-memory copy of
+// its first len bytes).
+// mirror (optional, shared memory): the first mirror_rows table rows are written there too.
+__device__ void parse_stream(const DecArgs& a, int i, const uint8_t* in, uint64_t len, bool over,
+                             uint32_t* mirror = nullptr, uint32_t mirror_rows = 0) {
   uint32_t* tab = dtab(a, i);
-  const uint8_t* in = d.in;
-  // the stream length comes from the descriptor, or -- for payloads still being produced on
-  // the device (a pipelined encode -> decode) -- from the encoder's out_len, read here
-  uint64_t len = d.in_len;
-  bool over = false;
-  if (d.in_len_dev) {
-    const uint64_t l = *d.in_len_dev;
-    over = l > d.in_len;
-    len = over ? 0 : l;
-  }
   const uint64_t max_rows = (a.tab_off[i + 1] - a.tab_off[i]) / TROW_U32 - 2;
   uint32_t pre = 0, walk = 0, N = 0, K = 0, mp = 0, mm = 0, mode = 0, qb = 0, nb = 0, crc = 0;
   uint32_t pre_r = R_NONE, walk_r = R_NONE, walk_x = 0;
@@ -104,26 +109,37 @@ __global__ void sif_parse_kernel(DecArgs a) {
         const uint64_t cbytes = ((uint64_t)nnz * cb + 7) / 8, qbytes = ((uint64_t)nnz * q + 7) / 8;
         if (len - kCrcBytes < pos + cbytes + qbytes) { walk = SIF_ERR_STREAM_FORMAT; walk_r = R_BLKPAY; break; }  // :358
         if (b >= max_rows) { walk = SIF_ERR_CAPACITY; walk_r = R_CAPACITY; break; }
+        const uint32_t rv[10] = {q, nnz, o, vmin, (uint32_t)rp, (uint32_t)(rp >> 32), (uint32_t)pos,
+                                 (uint32_t)(pos >> 32), (uint32_t)(pos + cbytes), (uint32_t)((pos + cbytes) >> 32)};
         uint32_t* row = tab + (2 + b) * TROW_U32;
-        row[0] = q; row[1] = nnz; row[2] = o; row[3] = vmin;
-        row[4] = (uint32_t)rp; row[5] = (uint32_t)(rp >> 32);
-        row[6] = (uint32_t)pos; row[7] = (uint32_t)(pos >> 32);
-        row[8] = (uint32_t)(pos + cbytes); row[9] = (uint32_t)((pos + cbytes) >> 32);
+        for (int k = 0; k < 10; ++k) row[k] = rv[k];
+        if (2 + b < mirror_rows)
+          for (int k = 0; k < 10; ++k) mirror[(2 + b) * TROW_U32 + k] = rv[k];
         pos += cbytes + qbytes;
       }
       if (!walk && pos != len - kCrcBytes) { walk = SIF_ERR_STREAM_FORMAT; walk_r = R_TRAIL; }  // codec.py:384-385
       nb = (uint32_t)nblk;
     }
   }
-  tab[0] = walk; tab[1] = N; tab[2] = K; tab[3] = mp; tab[4] = mm; tab[5] = mode; tab[6] = qb; tab[7] = nb;
-  tab[TROW_U32 + 0] = pre;
-  tab[TROW_U32 + 1] = crc;
-  tab[TROW_U32 + 2] = (uint32_t)len;
-  tab[TROW_U32 + 3] = (uint32_t)(len >> 32);
-  tab[TROW_U32 + 4] = pre_r;
-  tab[TROW_U32 + 5] = walk_r;
-  tab[TROW_U32 + 6] = walk_x;
-  tab[TROW_U32 + 9] = len >= 4 ? rd_u32(in, 0) : 0u;  // magic bytes for the error message
+  const uint32_t h0[8] = {walk, N, K, mp, mm, mode, qb, nb};
+  const uint32_t h1[10] = {pre, crc, (uint32_t)len, (uint32_t)(len >> 32), pre_r, walk_r, walk_x, 0u, 0u,
+                           len >= 4 ? rd_u32(in, 0) : 0u};  // [9]: magic bytes for the error message
+  for (int k = 0; k < 8; ++k) tab[k] = h0[k];
+  for (int k = 0; k < 10; ++k)
+    if (k != 7 && k != 8) tab[TROW_U32 + k] = h1[k];  // 7, 8: reason, set by the final pass
+  if (mirror_rows >= 2) {
+    for (int k = 0; k < 8; ++k) mirror[k] = h0[k];
+    for (int k = 0; k < 10; ++k) mirror[TROW_U32 + k] = h1[k];
+  }
+}
+
+__global__ void sif_parse_kernel(DecArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n || (a.small && a.small[i])) return;  // small streams: sif_dec_small
+  const sif_dec_desc d = a.descs[i];
+  bool over;
+  const uint64_t len = stream_len(d, over);
+  parse_stream(a, i, d.in, len, over);
 }
 
 // ------------------------------------------------------------------------------- CRC
@@ -432,12 +448,173 @@ __global__ void __launch_bounds__(DNT, 3) sif_scatter_kernel(DecArgs a) {
   if (cur >= 0) flush_flags(a, cur, fl, ck);
 }
 
+// ------------------------------------------------------------------------------- small streams
+// sif_dec_small: one CTA per stream whose dense output fits in shared memory (rows * cols
+// <= SMALL_T; a decode-step token 1 x 4096, or any small IF) -- the whole decode of the
+// stream in one launch for the batch.  The stream (up to SMALL_CAP bytes) is copied into
+// shared memory once; the framing walk (parse_stream), CRC, row_ptr / cols validation
+// (codec.py:235-251), unpack, float64 dequantize (quant.py:67-73) and the fp32 dense
+// buffer (codec.py:257-266) all work from shared memory, and the output is written with
+// one coalesced pass.  Same block table, reason codes and error precedence as the
+// four-kernel path (sif_dfinal_kernel).
+constexpr int DSN = 128;             // threads per small-stream CTA
+constexpr uint32_t SMALL_T = 4096;   // max dense elements of a small stream
+constexpr uint32_t SMALL_CAP = 4096; // stream bytes staged in shared memory
+constexpr uint32_t SMALL_ROWS = 34;  // table rows mirrored in shared memory (2 + 32 blocks)
+
+// Generic-address versions of ld_u32_le / ld_field (the shared-memory copy or the stream
+// itself; base 4-byte aligned).
+__device__ __forceinline__ uint32_t gen_u32_le(const uint8_t* base, uint64_t off) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(base);
+  const uint64_t wi = off >> 2;
+  const uint32_t sh = 8u * (uint32_t)(off & 3u);
+  const uint32_t lo = w[wi];
+  return sh ? __funnelshift_r(lo, w[wi + 1], sh) : lo;
+}
+__device__ __forceinline__ uint32_t gen_field(const uint8_t* base, uint64_t bit, uint32_t wd) {
+  const uint32_t* p = reinterpret_cast<const uint32_t*>(base);
+  const uint64_t wi = bit >> 5;
+  const uint32_t sh = (uint32_t)(bit & 31u);
+  uint64_t hi = (uint64_t)bswap32(p[wi]) << 32;
+  if (sh + wd > 32u) hi |= bswap32(p[wi + 1]);
+  return (uint32_t)((hi << sh) >> (64u - wd));
+}
+
+struct SmallSh {
+  float buf[SMALL_T];                 // the dense output (first: the CRC staging area)
+  uint32_t bm[2][SMALL_T / 32];       // elements written by the plus / minus plane
+  uint32_t t4[1024];                  // CRC slice tables
+  uint32_t cp[SMALL_CAP / 4 + 4];     // the stream, zero padded
+  uint32_t tab[SMALL_ROWS * TROW_U32]; // the first table rows (header + blocks)
+  uint32_t red[DSN / 32 + 1];
+  uint32_t ck, fl;
+};
+
+__global__ void __launch_bounds__(DSN, 7) sif_dec_small(DecArgs a) {
+  __shared__ __align__(16) SmallSh sh;
+  static_assert(DSN * 16 <= SMALL_T, "CRC staging must fit the dense buffer");
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int i = (int)a.small_list[blockIdx.x];
+  const sif_dec_desc d = a.descs[i];
+  bool over;
+  const uint64_t len = stream_len(d, over);
+  const bool staged = len <= SMALL_CAP;
+  if (staged) {
+    const uint32_t* gw = reinterpret_cast<const uint32_t*>(d.in);
+    const uint32_t nfull = (uint32_t)(len / 4), nw = (uint32_t)((len + 3) / 4);
+    for (uint32_t k = tid; k < nw + 4; k += DSN) {
+      uint32_t v = 0;
+      if (k < nfull) v = __ldg(gw + k);
+      else if (k < nw)  // the partial last word: byte loads (nothing past the stream is read)
+        for (uint32_t b = 0; 4 * k + b < len; ++b) v |= (uint32_t)__ldg(d.in + 4 * k + b) << (8 * b);
+      sh.cp[k] = v;
+    }
+  }
+  for (int k = tid; k < 1024; k += DSN) sh.t4[k] = (&kCrcTab4[0][0])[k];
+  if (tid == 0) { sh.ck = 0xFFFFFFFFu; sh.fl = 0; }
+  __syncthreads();
+  const uint8_t* src = staged ? reinterpret_cast<const uint8_t*>(sh.cp) : d.in;
+  if (tid == 0) parse_stream(a, i, src, len, over, sh.tab, SMALL_ROWS);
+  __syncthreads();  // the table rows written by thread 0 are visible to the CTA
+  uint32_t* gtab = dtab(a, i);
+  const uint32_t pre = sh.tab[TROW_U32 + 0];
+  uint32_t crc_raw = 0;
+  if (!pre) {
+    uint32_t* cst = reinterpret_cast<uint32_t*>(sh.buf);
+    crc_raw = staged ? crc_cta_staged<DSN, true>(src, 4, len - 4, sh.t4, sh.red, cst)
+                     : crc_cta_staged<DSN>(d.in, 4, len - 4, sh.t4, sh.red, cst);
+  }
+  const bool crc_ok = !pre && crc_finish(crc_raw, len - 8) == sh.tab[TROW_U32 + 1];
+  const uint32_t walk = sh.tab[0], N = sh.tab[1], K = sh.tab[2], mp = sh.tab[3], nb = sh.tab[7];
+  // block rows: shared-memory mirror when they all fit, else the global table
+  const uint32_t* tab = nb + 2 <= SMALL_ROWS ? sh.tab : gtab;
+  const bool shape_ok = a.parse_only || (N == d.rows && K == d.cols);
+  const bool ok = crc_ok && !walk && !a.parse_only && N == d.rows && K == d.cols;
+  uint32_t ck = 0xFFFFFFFFu, fl = 0;
+  if (ok) {
+    const uint32_t T = N * K, cb = col_bits(K);
+    for (uint32_t k = tid; k < T; k += DSN) sh.buf[k] = 0.f;
+    for (uint32_t k = tid; k < 2 * SMALL_T / 32; k += DSN) (&sh.bm[0][0])[k] = 0u;
+    __syncthreads();
+    for (uint32_t b = 0; b < nb; ++b) {
+      const uint32_t* row = tab + (2ull + b) * TROW_U32;
+      const uint32_t q = row[0], nnz = row[1];
+      const double o = (double)__uint_as_float(row[2]), vmin = (double)__uint_as_float(row[3]);
+      const uint64_t rpo = (uint64_t)row[4] | ((uint64_t)row[5] << 32);
+      const uint64_t cbit = 8ull * ((uint64_t)row[6] | ((uint64_t)row[7] << 32));
+      const uint64_t qbit = 8ull * ((uint64_t)row[8] | ((uint64_t)row[9] << 32));
+      const uint32_t minus = b >= mp ? 1u : 0u;
+      for (uint32_t r = tid; r < N; r += DSN) {  // codec.py:238-241
+        const uint32_t p0 = gen_u32_le(src, rpo + 4ull * r), p1 = gen_u32_le(src, rpo + 4ull * (r + 1));
+        if (r == 0 && p0 != 0) ck = min(ck, corrupt_key(b, CK_ROWPTR));
+        if (p1 < p0 || (r + 1 == N && p1 != nnz)) ck = min(ck, corrupt_key(b, CK_ROWPTR_NNZ));
+      }
+      for (uint32_t m = tid; m < nnz; m += DSN) {
+        // the entry's row: the last r < N with row_ptr[r] <= m
+        uint32_t lo = 0, hi = N - 1;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi + 1) >> 1;
+          if (gen_u32_le(src, rpo + 4ull * mid) <= m) lo = mid; else hi = mid - 1;
+        }
+        const uint32_t r = lo;
+        const uint32_t col = gen_field(src, cbit + (uint64_t)m * cb, cb);
+        if (col >= K) { ck = min(ck, corrupt_key(b, CK_COL_RANGE)); continue; }  // codec.py:242-243
+        if (m > gen_u32_le(src, rpo + 4ull * r) && gen_field(src, cbit + (uint64_t)(m - 1) * cb, cb) >= col)
+          ck = min(ck, corrupt_key(b, CK_COL_ORDER));  // codec.py:244-247
+        const uint32_t pos = r * K + col, bit = 1u << (pos & 31u);
+        if (atomicOr(&sh.bm[minus][pos >> 5], bit) & bit) ck = min(ck, corrupt_key(b, CK_OVERLAP));  // :248-250
+        const uint32_t code = gen_field(src, qbit + (uint64_t)m * q, q);
+        const double v = __dadd_rn(__dmul_rn((double)code, o), vmin);
+        float f;
+        if (!minus) f = __double2float_rn(v);  // f32(0 + v)
+        else if (sh.bm[0][pos >> 5] & bit)  // both planes: summed in float64 (codec.py:257-266)
+          f = __double2float_rn(__dsub_rn(plus_value(gtab, d.in, mp, r, col, cb), v));
+        else f = __double2float_rn(-v);  // f32(0 - v)
+        sh.buf[pos] = f;
+      }
+      __syncthreads();  // blocks in order: an overlap is charged to the later block
+    }
+    for (uint32_t k = tid; k < T; k += DSN)
+      if ((__float_as_uint(sh.buf[k]) & 0x7F800000u) == 0x7F800000u) fl = FLAG_NONFINITE;
+    float* dst = d.out;
+    if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && (T & 3u) == 0) {
+      for (uint32_t k = 4 * tid; k < T; k += 4 * DSN)
+        __stcs(reinterpret_cast<float4*>(dst + k), *reinterpret_cast<const float4*>(sh.buf + k));
+    } else {
+      for (uint32_t k = tid; k < T; k += DSN) __stcs(dst + k, sh.buf[k]);
+    }
+  }
+  ck = __reduce_min_sync(0xFFFFFFFFu, ck);
+  fl = __reduce_or_sync(0xFFFFFFFFu, fl);
+  if (lane == 0) {
+    if (ck != 0xFFFFFFFFu) atomicMin(&sh.ck, ck);
+    if (fl) atomicOr(&sh.fl, fl);
+  }
+  __syncthreads();
+  if (tid == 0) {  // the reference's error precedence (as sif_dfinal_kernel)
+    int st = SIF_OK;
+    uint32_t r = R_NONE, x = 0;
+    if (pre) { st = (int)pre; r = sh.tab[TROW_U32 + 4]; }
+    else if (!crc_ok) { st = SIF_ERR_STREAM_FORMAT; r = R_CRC; }  // codec.py:325-327
+    else if (walk) { st = (int)walk; r = sh.tab[TROW_U32 + 5]; x = sh.tab[TROW_U32 + 6]; }
+    else if (!shape_ok) { st = SIF_ERR_CAPACITY; r = R_SHAPE_MISMATCH; }
+    else if (!a.parse_only) {
+      if (sh.ck != 0xFFFFFFFFu) { st = SIF_ERR_CORRUPT_STREAM; r = R_CORRUPT + (sh.ck & 7u); x = sh.ck >> 3; }
+      else if (N < 1 || K < 1) { st = SIF_ERR_SHAPE; r = R_SHAPE; }
+      else if (sh.fl & FLAG_NONFINITE) { st = SIF_ERR_NONFINITE; r = R_NONFINITE; }
+    }
+    a.status[i] = st;
+    gtab[TROW_U32 + 7] = r;
+    gtab[TROW_U32 + 8] = x;
+  }
+}
+
 // ------------------------------------------------------------------------------- finalize
 // One thread per stream: the reference's error precedence (codec.py:320-385, :235-252,
 // tensor.py:27-36) from framing, CRC and validation flags; resets the accumulators.
 __global__ void sif_dfinal_kernel(DecArgs a) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.n) return;
+  if (i >= a.n || (a.small && a.small[i])) return;
   uint32_t* tab = dtab(a, i);
   const sif_dec_desc d = a.descs[i];
   uint32_t* acc = a.acc + 4ull * i;

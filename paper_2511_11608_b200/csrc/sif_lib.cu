@@ -24,11 +24,12 @@ int check_cuda(cudaError_t e) { return e == cudaSuccess ? SIF_OK : SIF_ERR_CUDA;
 
 // ---- optional per-kernel timing (diagnostics; sif_profile_enable)
 enum { KP_PREP, KP_STREAM, KP_SELECT, KP_MEMBERS, KP_ABQ1, KP_ABQ2, KP_LAYOUT, KP_PACK, KP_CRC, KP_PARSE, KP_DCRC,
-       KP_SCATTER, KP_DFINAL, KP_SELECT_TINY, KP_GATHER1, KP_SELECT1, KP_GATHER2, KP_SELECT2, KP_FUSED, KP_TOKEN, KP_N };
+       KP_SCATTER, KP_DFINAL, KP_SELECT_TINY, KP_GATHER1, KP_SELECT1, KP_GATHER2, KP_SELECT2, KP_FUSED, KP_TOKEN, KP_DSMALL, KP_N };
 const char* kKpNames[KP_N] = {"enc_prep", "enc_stream", "enc_select<0>", "enc_members", "enc_abq<1>", "enc_abq<0>",
                               "enc_layout", "enc_pack", "enc_crc", "sif_parse_kernel", "sif_dcrc_kernel",
                               "sif_scatter_kernel", "sif_dfinal_kernel", "enc_select_tiny", "enc_gather<1>",
-                              "enc_select<1>", "enc_gather<2>", "enc_select<2>", "enc_post", "enc_token"};
+                              "enc_select<1>", "enc_gather<2>", "enc_select<2>", "enc_post", "enc_token",
+                              "sif_dec_small"};
 struct ProfRec { int k; cudaEvent_t a, b; };
 std::atomic<bool> g_prof{false};
 std::mutex g_prof_mu;  // guards g_recs (launches may come from several host threads)
@@ -94,7 +95,7 @@ int resident_grid(K kfn, int threads, int smem, uint64_t work, int sms) {
 }
 
 constexpr uint32_t kBigNcand = 131072;  // candidates above which an IF uses the multi-kernel select
-constexpr int kSmemStream = (2 * sif::CH + 2 * sif::ND) * 4;
+constexpr int kSmemStream = sif::RING_BYTES + 2 * sif::ND * 4 + (sif::CNT / 32) * sif::UE * 2;
 constexpr int kSmemSelect = (2 * sif::ND + 2 * sif::HB + sif::GCAP * 4 + 2 * sif::GSM) * 4;
 inline int smem_abq(int maxb) { return (sif::CNT / 32) * maxb * (int)(sizeof(sif::AbqPar) + 16 * 8); }
 inline int smem_pack(int maxb) { return (sif::CNT / 32) * maxb * (int)sizeof(sif::PackPar); }
@@ -324,6 +325,7 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
   memset(p, 0, sizeof(*p));
   uint64_t kmax = 0, nch = 0, nhist = 0, lists = 0, nseg = 0;
   bool tiny = false;  // some IF may take the warp-per-IF select (enc_select_tiny)
+  bool any_f32 = false;  // some streamed IF is fp32 (16 KB stream ring slots)
   bool all_small = n > 0;  // every IF fits one chunk: narrow enc_prep
   int nfused = 0, ntoken = 0;
   for (int i = 0; i < n; ++i) {
@@ -342,6 +344,7 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
     }
     const uint64_t ch = (T + sif::CH - 1) / sif::CH;
     nch += ch;
+    if (d[i].dtype == SIF_DTYPE_F32) any_f32 = true;
     if (ch > 1) ++nhist;
     if (ch > 1) all_small = false;
     if (is_fused(T, atkf)) {  // stream pass as the pipeline, then enc_post
@@ -359,6 +362,7 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
   for (int i = 0; i < n; ++i) kall = std::max(kall, sif::keep_count(c->s, (uint64_t)d[i].rows * d[i].cols));
   const uint64_t kk = std::max<uint64_t>(1, kall);
   const int maxb = (int)(std::min<uint64_t>(c->m_plus, kk) + std::min<uint64_t>(c->m_minus, kk));
+  static_assert(sif::MAXB == SIF_MAX_BLOCKS, "sif.h SIF_MAX_BLOCKS");
   if (maxb > sif::MAXB) return SIF_ERR_CONFIG;  // more blocks than the encoder supports
   const EncWs w = enc_ws(n, nch, maxb, nhist, (uint64_t)c->m_plus + c->m_minus);
   p->n = n;
@@ -369,8 +373,8 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
   p->max_blocks = maxb;
   p->tiles = (int32_t)nch;
   // bit 0: ATKF-only, bit 1: multi-kernel select, bit 2: warp-per-IF select for small IFs,
-  // bit 3: every IF fits one chunk (narrow enc_prep)
-  p->flags = atkf | (kmax * 2 > (uint64_t)kBigNcand ? 2 : 0) | (tiny ? 4 : 0) | (all_small ? 8 : 0);
+  // bit 3: every IF fits one chunk (narrow enc_prep), bit 4: some streamed IF is fp32
+  p->flags = atkf | (kmax * 2 > (uint64_t)kBigNcand ? 2 : 0) | (tiny ? 4 : 0) | (all_small ? 8 : 0) | (any_f32 ? 16 : 0);
   p->ws_desc_off = w.info;
   p->ws_aux_off = w.fixedq;
   p->ws_spill_off = w.lists;
@@ -524,6 +528,7 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   // multi-kernel select for IFs with many candidates (one CTA per IF would scan them
   // alone); enabled when the batch holds an IF whose keep count exceeds half the cut-off
   a.big_ncand = (p->flags & 2) ? kBigNcand : 0u;
+  a.stream_slot = (p->flags & 16) ? sif::CH * 4 : sif::CH * 2;
   a.prof = reinterpret_cast<uint64_t*>(getenv("SIF_PROF_PTR") ? strtoull(getenv("SIF_PROF_PTR"), nullptr, 0) : 0ull);
   DevState* ds = dev_state();
   if (!ds) return SIF_ERR_CUDA;
@@ -645,8 +650,20 @@ static uint64_t dec_table_rows(const sif_dec_desc& d) {
 }
 
 struct DecWs {
-  uint64_t desc, table, taboff, acc, segbase, itembase, total;
+  uint64_t desc, table, taboff, acc, segbase, itembase, small, slist, total;
 };
+
+// Streams decoded by sif_dec_small (one CTA each): the dense output fits in shared memory.
+static std::atomic<uint64_t> g_small_max{sif::SMALL_T};
+static bool dec_is_small(const sif_dec_desc& d) {
+  return d.rows >= 1 && d.cols >= 1 && (uint64_t)d.rows * d.cols <= g_small_max.load(std::memory_order_relaxed);
+}
+
+int sif_set_small_decode(uint64_t max_elems) {
+  if (max_elems > sif::SMALL_T) return SIF_ERR_INVALID_ARG;
+  g_small_max.store(max_elems);
+  return SIF_OK;
+}
 
 static DecWs dec_ws(uint64_t n, uint64_t table_rows) {
   DecWs w;
@@ -658,6 +675,8 @@ static DecWs dec_ws(uint64_t n, uint64_t table_rows) {
   w.acc = take(16ull * n);
   w.segbase = take(4ull * (n + 1));
   w.itembase = take(8ull * (n + 1));
+  w.small = take(4ull * n);
+  w.slist = take(4ull * n);
   w.total = off;
   return w;
 }
@@ -675,10 +694,12 @@ int sif_dec_plan(const sif_dec_desc* d, int n, sif_plan* p) {
   if (!p || (n > 0 && !d) || n < 0) return SIF_ERR_INVALID_ARG;
   memset(p, 0, sizeof(*p));
   uint64_t rows = 0, nseg = 0;
+  int nsmall = 0;
   for (int i = 0; i < n; ++i) {
     if (!d[i].in || (reinterpret_cast<uintptr_t>(d[i].in) & 3)) return SIF_ERR_INVALID_ARG;
     if (d[i].in_len_dev && (reinterpret_cast<uintptr_t>(d[i].in_len_dev) & 7)) return SIF_ERR_INVALID_ARG;
     rows += dec_table_rows(d[i]);
+    if (dec_is_small(d[i])) { ++nsmall; continue; }
     nseg += dec_segments(d[i].in_len);
     if (dec_segments(d[i].in_len) > (uint32_t)sif::CRC_PIECES_MAX) return SIF_ERR_INVALID_ARG;
   }
@@ -695,6 +716,7 @@ int sif_dec_plan(const sif_dec_desc* d, int n, sif_plan* p) {
   p->ws_aux_off = w.table;
   p->ws_spill_off = rows;  // decode plans: total table rows
   p->ws_bytes = w.total;
+  p->n_fused = nsmall;     // decode plans: streams on the small-stream kernel
   return SIF_OK;
 }
 
@@ -717,12 +739,25 @@ int sif_dec_upload(const sif_plan* p, const sif_dec_desc* d, void* ws, void* str
   const uint32_t segw = (uint32_t)p->tiles;
   std::vector<uint32_t> seg((size_t)p->n + 1, 0);
   std::vector<uint64_t> items((size_t)p->n + 1, 0), toff((size_t)p->n + 1, 0);
+  std::vector<uint32_t> small((size_t)p->n, 0), slist;
   for (int i = 0; i < p->n; ++i) {
+    toff[i + 1] = toff[i] + dec_table_rows(d[i]) * sif::TROW_U32;
+    if (dec_is_small(d[i])) {  // no CRC pieces / work items on the four-kernel path
+      small[i] = 1;
+      slist.push_back((uint32_t)i);
+      seg[i + 1] = seg[i];
+      items[i + 1] = items[i];
+      continue;
+    }
     seg[i + 1] = seg[i] + dec_segments(d[i].in_len);
     const uint32_t R = d[i].cols <= segw && d[i].cols ? segw / d[i].cols : 1u;  // rows per item
     items[i + 1] = items[i] + (uint64_t)((d[i].rows + R - 1) / R) * ((d[i].cols + segw - 1) / segw);
-    toff[i + 1] = toff[i] + dec_table_rows(d[i]) * sif::TROW_U32;
   }
+  if (check_cuda(cudaMemcpyAsync(wb + w.small, small.data(), 4ull * p->n, cudaMemcpyHostToDevice, s)))
+    return SIF_ERR_CUDA;
+  if (!slist.empty() &&
+      check_cuda(cudaMemcpyAsync(wb + w.slist, slist.data(), 4ull * slist.size(), cudaMemcpyHostToDevice, s)))
+    return SIF_ERR_CUDA;
   if (check_cuda(cudaMemsetAsync(wb + w.acc, 0, 16ull * p->n, s))) return SIF_ERR_CUDA;
   if (check_cuda(cudaMemcpyAsync(wb + w.segbase, seg.data(), 4ull * (p->n + 1), cudaMemcpyHostToDevice, s)))
     return SIF_ERR_CUDA;
@@ -753,6 +788,13 @@ int sif_dec_run(const sif_plan* p, int parse_only, void* ws, int32_t* status, vo
   a.seg_base = reinterpret_cast<const uint32_t*>(wb + w.segbase);
   a.item_base = reinterpret_cast<const uint64_t*>(wb + w.itembase);
   a.segw = p->tiles;
+  a.small = reinterpret_cast<const uint32_t*>(wb + w.small);
+  a.small_list = reinterpret_cast<const uint32_t*>(wb + w.slist);
+  if (p->n_fused > 0) {
+    ProfScope ps(KP_DSMALL, s);
+    sif::sif_dec_small<<<(unsigned)p->n_fused, sif::DSN, 0, s>>>(a);
+  }
+  if (p->n_fused == p->n) return check_cuda(cudaGetLastError());
   { ProfScope ps(KP_PARSE, s); sif::sif_parse_kernel<<<(p->n + 127) / 128, 128, 0, s>>>(a); }
   {
     const unsigned warps = (unsigned)p->cluster;

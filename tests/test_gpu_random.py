@@ -218,3 +218,26 @@ def test_per_if_back_end_matches_oracle(sif):
                 assert p.to_bytes() == O.encode_bytes(x, O.Cfg(**kw), sd), (kw, x.shape)
     finally:
         L.sif_set_fused_range(lo.value, hi.value)
+
+
+def test_stream_ring_tails_match_oracle(sif):
+    """IFs whose size is not a whole number of 16-byte vectors (fp32 T % 4 != 0, bf16 T % 8
+    != 0) and whose last chunk is a few elements long: the stream kernel's bulk-copy ring
+    copies the tail with plain loads (nothing past the IF is read).  fp32 and bf16 inputs,
+    lambda = 0 and lambda > 0."""
+    from oracle import sif_oracle as O
+
+    rng = np.random.default_rng(21)
+    shapes = [(1, 4097), (3, 2731), (2, 4099), (5, 1639), (7, 1171), (1, 8195), (13, 631), (4099, 3)]
+    fails = []
+    for (r, c) in shapes:
+        for dt in (torch.float32, torch.bfloat16):
+            for lam in (0.0, 0.2):
+                x = torch.from_numpy(_values(rng, 1, r * c).reshape(r, c)).to(dt)
+                xf = x.float().numpy()
+                kw = dict(s=0.8, lam=lam, m_plus=3, m_minus=3, q_bit=8, delta=0.01)
+                ref = O.encode_bytes(xf, O.Cfg(**kw), 5)
+                p = sif.encode(x.cuda(), sif.CodecConfig(**kw), seed=5)
+                if sif.serialize(p) != ref:
+                    fails.append(f"{(r, c)} {dt} lam={lam}: payload differs")
+    assert not fails, "\n".join(fails)
