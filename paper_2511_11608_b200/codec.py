@@ -450,13 +450,14 @@ def _enc_descs(xs, outs, caps, seeds, dtypes):
     return arr
 
 
-MAX_BLOCKS = 64  # effective blocks (M+ + M-) per IF the device encoder supports (SIF_MAX_BLOCKS)
+MAX_BLOCKS = 32  # effective blocks (M+ + M-) per IF the device encoder supports (SIF_MAX_BLOCKS)
 
 
 def _check_block_count(cfg, sizes) -> None:
     """The encoder holds per-block state for at most MAX_BLOCKS effective blocks per IF
-    (msplit.py:34-38: m_eff = max(1, min(M, nnz)) per plane); the reference has no such
-    limit, so a larger configuration is refused up front with a ConfigError that says so."""
+    (msplit.py:34-38: m_eff = max(1, min(M, nnz)) per plane), planned from the bound
+    min(M+, k) + min(M-, k); the reference has no such limit, so a configuration above it is
+    refused up front with a ConfigError that says so (as sif_enc_plan does)."""
     if not sizes:
         return
     k = max(1, max(int(_L().sif_keep_count(float(cfg.s), int(t))) for t in sizes))

@@ -261,13 +261,15 @@ __device__ uint32_t crc_cta_staged(const uint8_t* base, uint64_t b0, uint64_t b1
     }
     __syncthreads();
     uint32_t c = 0;
-    const uint32_t* w = stage + tid * (L / 4);
+    if (rs + L * (tid + 1) > (int64_t)b0) {  // a chunk wholly before b0 is zeros: raw CRC 0
+      const uint32_t* w = stage + tid * (L / 4);
 #pragma unroll 4
-    for (int k = 0; k < L / 4; ++k) {
-      const uint32_t x = w[k] ^ c;
-      c = t4[768 + (x & 0xFFu)] ^ t4[512 + ((x >> 8) & 0xFFu)] ^ t4[256 + ((x >> 16) & 0xFFu)] ^ t4[x >> 24];
+      for (int k = 0; k < L / 4; ++k) {
+        const uint32_t x = w[k] ^ c;
+        c = t4[768 + (x & 0xFFu)] ^ t4[512 + ((x >> 8) & 0xFFu)] ^ t4[256 + ((x >> 16) & 0xFFu)] ^ t4[x >> 24];
+      }
+      if (c) c = crc_mult(myshift, c);
     }
-    if (c) c = crc_mult(myshift, c);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c ^= __shfl_xor_sync(0xFFFFFFFFu, c, o);
     if (lane == 0) red[wid] = c;

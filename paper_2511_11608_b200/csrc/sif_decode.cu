@@ -4,10 +4,10 @@
 //   sif_parse_kernel   one thread per stream walks the header/block framing exactly in the
 //                      order of deserialize (codec.py:320-385) and writes a block table.
 //   sif_dcrc_kernel    one CTA per 64 KiB CRC-32 segment of a stream (GF(2)-combined).
-//   sif_scatter_kernel one warp per (row, column segment): row_ptr/cols validation
-//                      (codec.py:235-251), fused unpack + float64 dequantize
-//                      (quant.py:67-73) + scatter into a float64 shared-memory row buffer,
-//                      rounded to fp32 (codec.py:266) and written once with 16-byte stores.
+//   sif_scatter_kernel one warp per work item (a group of rows, or a 4096-column segment):
+//                      row_ptr/cols validation (codec.py:235-251), fused unpack + float64
+//                      dequantize (quant.py:67-73), fp32 values (codec.py:266) stored in
+//                      place into the item's zero-filled output.
 //   sif_dfinal_kernel  folds CRC, framing and validation flags into the reference's error
 //                      precedence and resets the per-stream accumulators.
 
@@ -38,7 +38,7 @@ struct DecArgs {
   int32_t* status;
   const uint32_t* seg_base;    // [n+1] prefix of CRC segments per stream
   const uint64_t* item_base;   // [n+1] prefix of (row, column segment) work items per stream
-  int segw;                    // columns per work item (<= 1024, multiple of 4)
+  int segw;                    // elements per work item (4096)
   const uint32_t* small;       // [n] 1: stream decoded by sif_dec_small (one CTA per stream)
   const uint32_t* small_list;  // the small streams, in batch order
 };
@@ -226,11 +226,13 @@ __device__ __forceinline__ void flush_flags(const DecArgs& a, int cur, uint32_t 
 // row) pair each (pairs block-major, plus blocks first, in groups of 32): block metadata
 // and the row's entry range, staged in shared memory.  The pairs' entries are unpacked 32
 // at a time (cols, codes), validated (codec.py:238-250), dequantized in float64
-// (quant.py:67-73) into a per-warp fp32 buffer: an element held by one plane is
-// f32(0 +/- v), exactly the reference's f64 scatter-add rounded to fp32 (codec.py:257-266);
-// an element held by both planes is summed in float64 (plus value recovered from its
-// block).  Within a window plus entries are written before minus entries.  The buffer is
-// stored with 16-byte streaming stores and re-zeroed in the same pass.
+// (quant.py:67-73) and stored in place: the item's output (contiguous) is zero-filled with
+// 16-byte stores first, then each entry's value is written while those lines are still in
+// L2, so DRAM sees every output line once.  An element held by one plane is f32(0 +/- v),
+// exactly the reference's f64 scatter-add rounded to fp32 (codec.py:257-266); an element
+// held by both planes is summed in float64 (plus value recovered from its block).  Within a
+// window plus entries are written before minus entries.  Shared memory holds only the
+// per-item plane bitmaps (overlap checks), so items are up to 4096 elements.
 __global__ void __launch_bounds__(DNT, 3) sif_scatter_kernel(DecArgs a) {
   extern __shared__ __align__(16) uint8_t dsm_raw[];
   __shared__ uint4 pa[DNT / 32][32], pb[DNT / 32][32];
@@ -239,10 +241,7 @@ __global__ void __launch_bounds__(DNT, 3) sif_scatter_kernel(DecArgs a) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t segw = (uint32_t)a.segw;
   const uint32_t bmw = (segw + 31) / 32;
-  float* buf = reinterpret_cast<float*>(dsm_raw) + (size_t)w * segw;
-  uint32_t* bm = reinterpret_cast<uint32_t*>(reinterpret_cast<float*>(dsm_raw) + (size_t)(DNT / 32) * segw) +
-                 (size_t)w * 2 * bmw;
-  for (uint32_t k = 4 * lane; k < segw; k += 128) *reinterpret_cast<float4*>(buf + k) = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t* bm = reinterpret_cast<uint32_t*>(dsm_raw) + (size_t)w * 2 * bmw;
   const uint64_t GW = (uint64_t)gridDim.x * (DNT / 32);
   const uint64_t gw = (uint64_t)blockIdx.x * (DNT / 32) + w;
   const uint64_t nitems = a.item_base[a.n];
@@ -287,8 +286,17 @@ __global__ void __launch_bounds__(DNT, 3) sif_scatter_kernel(DecArgs a) {
     else { rg = (uint32_t)(li / nsegr); sg = (uint32_t)(li - (uint64_t)rg * nsegr); }
     const uint32_t r0 = rg * R, nr = min(R, N - r0);
     const uint32_t c0 = sg * segw, c1 = min(K, c0 + segw), W = c1 - c0;
-    const uint32_t span = nr * W;  // buffer elements (rows are contiguous when nsegr == 1)
+    const uint32_t span = nr * W;  // item elements (rows are contiguous when nsegr == 1)
     for (uint32_t k = lane; k < 2 * bmw; k += 32) bm[k] = 0;
+    // the item's output is zero-filled first (coalesced), then every entry's value is
+    // stored in place while the lines are still in L2 (row r0 + ri, column col)
+    // (the item is contiguous: whole rows when W == K, else a single row segment)
+    float* dst = out + (uint64_t)r0 * K + c0;
+    if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && (span & 3u) == 0) {
+      for (uint32_t k = 4 * lane; k < span; k += 128) *reinterpret_cast<float4*>(dst + k) = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      for (uint32_t k = lane; k < span; k += 32) dst[k] = 0.f;
+    }
     __syncwarp();
     uint32_t nf0 = 0;  // a plus-plane value rounded to a non-finite fp32 (re-checked at the store)
     const uint32_t np = nb * nr;       // (block, row) pairs, block-major
@@ -333,14 +341,20 @@ __global__ void __launch_bounds__(DNT, 3) sif_scatter_kernel(DecArgs a) {
         // pair parameters in shared memory (entry base stored as lo - exclusive prefix)
         pa[w][lane] = make_uint4((uint32_t)cbit, (uint32_t)(cbit >> 32), (uint32_t)qbit, (uint32_t)(qbit >> 32));
         pb[w][lane] = make_uint4(lo, q, m0v.z, m0v.w);
-        pc[w][lane] = make_uint2(rs0, ri | (b << 11) | (b >= mp ? 0x80000000u : 0u));  // ri < segw <= 2047
+        pc[w][lane] = make_uint2(rs0, ri | (b << 12) | (b >= mp ? 0x80000000u : 0u));  // ri < R <= segw = 4096
       }
       const uint32_t inc = warp_incl_scan_u32(cnt);
       const uint32_t M = __shfl_sync(0xFFFFFFFFu, inc, 31);
       const uint32_t exc = inc - cnt;
       if (pi < g1) pb[w][lane].x -= exc;
       uint32_t lastcol = 0, lastjl = 0xFFFFFFFFu;
-      for (uint32_t m0 = 0; m0 < M; m0 += 32) {
+      // window m0: owner pair of entry m0 + lane, its parameters and its col / code fields.
+      // The fields of window m0 + 32 are fetched while window m0 is processed (two
+      // memory round trips in flight per warp).
+      struct Win {
+        uint32_t jl, e, col, code;  // the rest of the pair's parameters is re-read from smem
+      };
+      auto prep = [&](uint32_t m0, Win& x) {
         const uint32_t m = m0 + lane;
         // owner of entry m: the last pair (with entries) starting at or before m in this
         // window; window position 0 is owned by the pair covering m0
@@ -350,27 +364,32 @@ __global__ void __launch_bounds__(DNT, 3) sif_scatter_kernel(DecArgs a) {
         const uint32_t smask = __reduce_or_sync(0xFFFFFFFFu, starts ? 1u << (st0 - m0) : 0u);
         __syncwarp();
         const uint32_t src = 31u - __clz(smask & (0xFFFFFFFFu >> (31 - lane)));
-        const uint32_t jl = own[w][src];
-        const uint4 A = pa[w][jl];
-        const uint4 B = pb[w][jl];
-        const uint2 C = pc[w][jl];
+        x.jl = own[w][src];
+        const uint4 A = pa[w][x.jl];
+        const uint2 Bxy = *reinterpret_cast<const uint2*>(&pb[w][x.jl]);  // entry base, q
         const uint64_t cbj = (uint64_t)A.x | ((uint64_t)A.y << 32);
-        const uint32_t e = B.x + m;
-        const uint32_t rij = C.y & 0x7FFu, bj = (C.y >> 11) & 0xFFFFFu;
-        const bool minus = (C.y >> 31) != 0;
-        // col and code fields are fetched together (one memory round trip per window)
+        x.e = Bxy.x + m;
         const uint64_t qbj = (uint64_t)A.z | ((uint64_t)A.w << 32);
-        uint32_t col = 0, code = 0;
+        x.col = 0;
+        x.code = 0;
         if (m < M) {
-          // IFs with 8-bit cols (K <= 256): byte fields are single byte loads
-          if (cb == 8) {
-            col = (uint32_t)__ldg(in + (cbj >> 3) + e);
-            code = B.y == 8 ? (uint32_t)__ldg(in + (qbj >> 3) + e) : ld_field(in, qbj + (uint64_t)e * B.y, B.y);
-          } else {
-            col = ld_field(in, cbj + (uint64_t)e * cb, cb);
-            code = ld_field(in, qbj + (uint64_t)e * B.y, B.y);
-          }
+          // byte fields (8-bit cols when K <= 256, 8-bit codes) are single byte loads
+          x.col = cb == 8 ? (uint32_t)__ldg(in + (cbj >> 3) + x.e) : ld_field(in, cbj + (uint64_t)x.e * cb, cb);
+          x.code = Bxy.y == 8 ? (uint32_t)__ldg(in + (qbj >> 3) + x.e) : ld_field(in, qbj + (uint64_t)x.e * Bxy.y, Bxy.y);
         }
+      };
+      Win cw;
+      if (M > 0) prep(0, cw);
+      for (uint32_t m0 = 0; m0 < M; m0 += 32) {
+        const uint32_t m = m0 + lane;
+        Win nw;
+        const bool more = m0 + 32 < M;
+        __syncwarp();  // every lane has read own[] for window m0
+        if (more) prep(m0 + 32, nw);
+        const uint32_t jl = cw.jl, e = cw.e, col = cw.col, code = cw.code;
+        const uint2 C = pc[w][jl];
+        const uint32_t rij = C.y & 0xFFFu, bj = (C.y >> 12) & 0x7FFFFu;
+        const bool minus = (C.y >> 31) != 0;
         // the previous entry e-1 of the same pair sits in the previous lane of this window
         // (lane 0: the last lane of the previous window)
         uint32_t colp = __shfl_up_sync(0xFFFFFFFFu, col, 1);
@@ -386,6 +405,7 @@ __global__ void __launch_bounds__(DNT, 3) sif_scatter_kernel(DecArgs a) {
           else {
             // strictly increasing within the row (codec.py:244-247)
             if (e > C.x) {
+              const uint64_t cbj = (uint64_t)pa[w][jl].x | ((uint64_t)pa[w][jl].y << 32);
               const uint32_t prev = jlp == jl ? colp : ld_field(in, cbj + (uint64_t)(e - 1) * cb, cb);
               if (prev >= col) ck = min(ck, corrupt_key(bj, CK_COL_ORDER));
             }
@@ -394,10 +414,11 @@ __global__ void __launch_bounds__(DNT, 3) sif_scatter_kernel(DecArgs a) {
               pos = rij * W + (col - c0);
               const uint32_t old = atomicOr(bm + (minus ? bmw : 0u) + (pos >> 5), 1u << (pos & 31));
               if (old & (1u << (pos & 31))) ck = min(ck, corrupt_key(bj, CK_OVERLAP));  // codec.py:248-250
-              v = __dadd_rn(__dmul_rn((double)code, (double)__uint_as_float(B.z)), (double)__uint_as_float(B.w));
+              const uint2 ov = *reinterpret_cast<const uint2*>(&pb[w][jl].z);  // o, v_min
+              v = __dadd_rn(__dmul_rn((double)code, (double)__uint_as_float(ov.x)), (double)__uint_as_float(ov.y));
               if (!minus) {
                 const float f = __double2float_rn(v);  // f32(0 + v)
-                buf[pos] = f;
+                dst[pos] = f;
                 nf0 |= (__float_as_uint(f) & 0x7F800000u) == 0x7F800000u ? 1u : 0u;
               }
             }
@@ -414,33 +435,19 @@ __global__ void __launch_bounds__(DNT, 3) sif_scatter_kernel(DecArgs a) {
           } else {
             f = __double2float_rn(-v);  // f32(0 - v)
           }
-          buf[pos] = f;
+          dst[pos] = f;
           if ((__float_as_uint(f) & 0x7F800000u) == 0x7F800000u) fl |= FLAG_NONFINITE;
         }
         __syncwarp();
+        if (more) cw = nw;
       }
     }
-    // store (nr full rows, or one row segment) and re-zero the buffer
-    const bool chk = __any_sync(0xFFFFFFFFu, nf0 != 0);
-    float* dst = out + (uint64_t)r0 * K + c0;
+    // a non-finite plus value may have been summed with a minus entry since: re-check the
+    // item's final values (rare)
     uint32_t bad = 0;
-    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && (span & 3u) == 0) {
-      for (uint32_t k = 4 * lane; k < span; k += 128) {
-        const float4 f = *reinterpret_cast<const float4*>(buf + k);
-        *reinterpret_cast<float4*>(buf + k) = z4;
-        if (chk)
-          bad |= ((__float_as_uint(f.x) & 0x7F800000u) == 0x7F800000u) | ((__float_as_uint(f.y) & 0x7F800000u) == 0x7F800000u) |
-                 ((__float_as_uint(f.z) & 0x7F800000u) == 0x7F800000u) | ((__float_as_uint(f.w) & 0x7F800000u) == 0x7F800000u);
-        __stcs(reinterpret_cast<float4*>(dst + k), f);
-      }
-    } else {
-      for (uint32_t k = lane; k < span; k += 32) {
-        const float f = buf[k];
-        buf[k] = 0.f;
-        if (chk) bad |= (__float_as_uint(f) & 0x7F800000u) == 0x7F800000u;
-        __stcs(dst + k, f);
-      }
+    if (__any_sync(0xFFFFFFFFu, nf0 != 0)) {
+      __syncwarp();
+      for (uint32_t k = lane; k < span; k += 32) bad |= (__float_as_uint(dst[k]) & 0x7F800000u) == 0x7F800000u ? 1u : 0u;
     }
     if (bad) fl |= FLAG_NONFINITE;
     __syncwarp();
@@ -487,7 +494,7 @@ struct SmallSh {
   uint32_t cp[SMALL_CAP / 4 + 4];     // the stream, zero padded
   uint32_t tab[SMALL_ROWS * TROW_U32]; // the first table rows (header + blocks)
   uint32_t red[DSN / 32 + 1];
-  uint32_t ck, fl;
+  uint32_t ck, fl, crcok;
 };
 
 __global__ void __launch_bounds__(DSN, 7) sif_dec_small(DecArgs a) {
@@ -524,13 +531,15 @@ __global__ void __launch_bounds__(DSN, 7) sif_dec_small(DecArgs a) {
     crc_raw = staged ? crc_cta_staged<DSN, true>(src, 4, len - 4, sh.t4, sh.red, cst)
                      : crc_cta_staged<DSN>(d.in, 4, len - 4, sh.t4, sh.red, cst);
   }
-  const bool crc_ok = !pre && crc_finish(crc_raw, len - 8) == sh.tab[TROW_U32 + 1];
+  if (tid == 0) sh.crcok = (!pre && crc_finish(crc_raw, len - 8) == sh.tab[TROW_U32 + 1]) ? 1u : 0u;
+  __syncthreads();
+  const bool crc_ok = sh.crcok != 0;
   const uint32_t walk = sh.tab[0], N = sh.tab[1], K = sh.tab[2], mp = sh.tab[3], nb = sh.tab[7];
   // block rows: shared-memory mirror when they all fit, else the global table
   const uint32_t* tab = nb + 2 <= SMALL_ROWS ? sh.tab : gtab;
   const bool shape_ok = a.parse_only || (N == d.rows && K == d.cols);
   const bool ok = crc_ok && !walk && !a.parse_only && N == d.rows && K == d.cols;
-  uint32_t ck = 0xFFFFFFFFu, fl = 0;
+  uint32_t ck = 0xFFFFFFFFu, fl = 0, nfp = 0;
   if (ok) {
     const uint32_t T = N * K, cb = col_bits(K);
     for (uint32_t k = tid; k < T; k += DSN) sh.buf[k] = 0.f;
@@ -571,11 +580,18 @@ __global__ void __launch_bounds__(DSN, 7) sif_dec_small(DecArgs a) {
           f = __double2float_rn(__dsub_rn(plus_value(gtab, d.in, mp, r, col, cb), v));
         else f = __double2float_rn(-v);  // f32(0 - v)
         sh.buf[pos] = f;
+        // a minus write is final; a non-finite plus value may still be summed with a minus
+        // entry, so it only triggers the full scan below
+        if ((__float_as_uint(f) & 0x7F800000u) == 0x7F800000u) {
+          if (minus) fl = FLAG_NONFINITE;
+          else nfp = 1;
+        }
       }
       __syncthreads();  // blocks in order: an overlap is charged to the later block
     }
-    for (uint32_t k = tid; k < T; k += DSN)
-      if ((__float_as_uint(sh.buf[k]) & 0x7F800000u) == 0x7F800000u) fl = FLAG_NONFINITE;
+    if (__syncthreads_or(nfp))  // non-finite outputs (tensor.py:35-36)
+      for (uint32_t k = tid; k < T; k += DSN)
+        if ((__float_as_uint(sh.buf[k]) & 0x7F800000u) == 0x7F800000u) fl = FLAG_NONFINITE;
     float* dst = d.out;
     if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && (T & 3u) == 0) {
       for (uint32_t k = 4 * tid; k < T; k += 4 * DSN)

@@ -39,7 +39,7 @@ constexpr int UE = CH / UNITS;     // elements per unit
 constexpr int CNT = 256;           // threads of chunk kernels
 constexpr int DSH = 19;            // digit = |x| key >> 19 (12 bits)
 constexpr int ND = 4096;           // digits per sign
-constexpr int MAXB = 64;           // max effective blocks (M+ + M-) per IF
+constexpr int MAXB = 32;           // max effective blocks (M+ + M-) per IF (lane-per-block code)
 constexpr int SNT = 512;           // threads of the per-IF select kernel
 constexpr int HB = 2048;           // radix histogram bins inside select_exact
 constexpr int GCAP = 1024;         // in-SMEM exact ranking capacity
@@ -125,7 +125,6 @@ struct EArgs {
   uint32_t big_ncand;        // IFs with more candidates use the multi-kernel select (0: never)
   uint32_t* big_list;        // [n] IFs on the multi-kernel select path, [n] = their count
   uint32_t inject;           // test-only fault injection (SIF_TEST_INJECT): bit 0 = sampled bracket misses
-  uint32_t stream_slot;      // enc_stream ring slot bytes: 16 KB if the batch holds an fp32 IF, else 8 KB
 };
 
 __device__ __forceinline__ void prof_mark(const EArgs& a, int ifi, int k) {
@@ -755,132 +754,34 @@ __device__ __forceinline__ void flush_if_stream(const EArgs& a, uint32_t ifi, ui
   __syncthreads();
 }
 
-// Bulk-async (TMA engine) helpers: mbarrier ring slots filled by cp.async.bulk.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-// Global -> shared bulk copy (bytes % 16 == 0, both addresses 16-byte aligned) completing
-// on `bar`; the source is read once, so it is marked evict-first in L2.
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile(
-      "{\n"
-      ".reg .b64 pol;\n"
-      "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n"
-      "}\n" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-// K2 ring: RING_BYTES of shared memory cut into slots of one chunk (a.stream_slot bytes:
-// CH fp32 = 16 KB when the batch holds an fp32 IF, else CH bf16 = 8 KB), so 4 or 8 chunks
-// are in flight per CTA.
-constexpr int RING_BYTES = 64 * 1024;
-constexpr int MAX_SLOTS = RING_BYTES / (CH * 2);
-
-// Source of one chunk's bulk copy (computed one iteration ahead of its issue, so the
-// dependent descriptor loads are off the issuing thread's critical path).
-struct ChunkSrc {
-  const uint8_t* src;
-  uint32_t bytes;  // n * bytes per element
-  uint32_t bpe;
-};
-__device__ __forceinline__ ChunkSrc stream_src(const EArgs& a, uint32_t c) {
-  const IfInfo& g = a.info[a.ch_if[c]];
-  const uint64_t e0 = a.ch_e0[c];
-  const uint32_t n = (uint32_t)min((uint64_t)CH, g.T - e0);
-  ChunkSrc d;
-  d.bpe = g.dtype == SIF_DTYPE_F32 ? 4u : 2u;
-  d.bytes = n * d.bpe;
-  d.src = reinterpret_cast<const uint8_t*>(g.x) + e0 * d.bpe;
-  return d;
-}
-
-// Thread 0: start the bulk copy of a chunk into `dst`.  The part past the last whole 16
-// bytes (an IF whose size is not a multiple of 4 fp32 / 8 bf16 elements) is copied with
-// plain loads before the arrive, so nothing past the IF is read.
-__device__ __forceinline__ void stream_issue(const ChunkSrc& d, uint8_t* dst, uint32_t bar) {
-  const uint32_t bulk = d.bytes & ~15u;
-  if (bulk < d.bytes) {
-    if (d.bpe == 4) {
-      for (uint32_t o = bulk; o < d.bytes; o += 4)
-        *reinterpret_cast<uint32_t*>(dst + o) = __ldg(reinterpret_cast<const uint32_t*>(d.src + o));
-    } else {
-      for (uint32_t o = bulk; o < d.bytes; o += 2)
-        *reinterpret_cast<unsigned short*>(dst + o) = __ldg(reinterpret_cast<const unsigned short*>(d.src + o));
-    }
-  }
-  fence_proxy_async();  // the slot's previous contents were read by the generic proxy
-  mbar_arrive_tx(bar, bulk);
-  if (bulk) bulk_g2s(smem_u32(dst), d.src, bulk, bar);
-}
-
-// K2: stream chunks.  Each CTA owns a contiguous range of chunks, staged through a ring of
-// shared-memory slots by bulk-async copies (cp.async.bulk issued by one thread, an mbarrier
-// per slot), so several chunks of HBM reads are in flight while the warps classify; warp w
-// classifies unit w of every chunk from shared memory: lane l owns 16 consecutive
-// elements, read as 16-byte vectors in a rotated order (bank-conflict free); candidates
-// (|x| >= lo, lambda-aware) are compacted in flat order by iterating the set bits, one
-// atomic per unit reserves their list space, and they are copied out coalesced.  Per-IF
-// reductions (max key, count >= lo, SMEM digit histogram) are flushed when the IF changes.
-__global__ void __launch_bounds__(CNT, 2) enc_stream(EArgs a) {
+__global__ void __launch_bounds__(CNT, 3) enc_stream(EArgs a) {
   extern __shared__ __align__(16) uint8_t dsm_raw[];
-  __shared__ __align__(8) uint64_t full[MAX_SLOTS];
+  uint32_t* dsm = reinterpret_cast<uint32_t*>(dsm_raw);
   __shared__ uint32_t sdr[2];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  uint8_t* ring = dsm_raw;
-  uint32_t* hist = reinterpret_cast<uint32_t*>(dsm_raw + RING_BYTES);
-  uint16_t* stage = reinterpret_cast<uint16_t*>(hist + 2 * ND) + w * UE;
-  const uint32_t SLOT = a.stream_slot, NS = RING_BYTES / SLOT;
+  uint2* stage = reinterpret_cast<uint2*>(dsm) + w * UE;
+  uint32_t* hist = dsm + (CNT / 32) * 2 * UE;
   for (int k = tid; k < 2 * ND; k += CNT) hist[k] = 0;
-  if (tid == 0) {
-    sdr[0] = 0xFFFFFFFFu;
-    sdr[1] = 0;
-    for (uint32_t k = 0; k < NS; ++k) mbar_init(smem_u32(&full[k]), 1);
-    mbar_fence_init();
-  }
+  if (tid == 0) { sdr[0] = 0xFFFFFFFFu; sdr[1] = 0; }
   __syncthreads();
   const uint32_t nch = (uint32_t)a.nch;
   const uint32_t c0 = (uint32_t)((uint64_t)nch * blockIdx.x / gridDim.x);
   const uint32_t c1 = (uint32_t)((uint64_t)nch * (blockIdx.x + 1) / gridDim.x);
   if (c0 >= c1) return;
-  ChunkSrc nxt;  // thread 0: the next chunk to issue (c + NS - 1 at iteration c)
-  if (tid == 0) {
-    for (uint32_t k = 0; k + 1 < NS && c0 + k < c1; ++k)
-      stream_issue(stream_src(a, c0 + k), ring + (size_t)k * SLOT, smem_u32(&full[k]));
-    if (c0 + NS - 1 < c1) nxt = stream_src(a, c0 + NS - 1);
-  }
   uint32_t cur = a.ch_if[c0];
   IfInfo f = a.info[cur];
   uint32_t lo = a.st[cur].lo, lo_neg = a.st[cur].lo_neg;
   uint32_t mk = 0, clo = 0, dmin = 0xFFFFFFFFu, dmax = 0;
+  Raw r0, r1;
+  auto prefetch = [&](uint32_t c, Raw& r) {
+    const IfInfo& g = a.info[a.ch_if[c]];
+    uint32_t e0, n;
+    unit_span(a, g, c, (uint32_t)w, e0, n);
+    if (n) load_unit(g.x, g.dtype, e0, n, r);
+  };
+  prefetch(c0, r0);
+  if (c0 + 1 < c1) prefetch(c0 + 1, r1);
   for (uint32_t c = c0; c < c1; ++c) {
-    const uint32_t i = c - c0, slot = i % NS;
-    __syncthreads();  // chunk i-1 is consumed: its slot takes chunk i + NS - 1
-    if (tid == 0 && c + NS - 1 < c1) {
-      const uint32_t ns = (i + NS - 1) % NS;
-      stream_issue(nxt, ring + (size_t)ns * SLOT, smem_u32(&full[ns]));
-      if (c + NS < c1) nxt = stream_src(a, c + NS);
-    }
     const uint32_t ifi = a.ch_if[c];
     if (ifi != cur) {
       flush_if_stream(a, cur, hist, mk, clo, dmin, dmax, sdr);
@@ -889,90 +790,26 @@ __global__ void __launch_bounds__(CNT, 2) enc_stream(EArgs a) {
       lo = a.st[ifi].lo;
       lo_neg = a.st[ifi].lo_neg;
     }
+    Raw r2;
+    if (c + 2 < c1) prefetch(c + 2, r2);
     uint32_t e0, n;
     unit_span(a, f, c, (uint32_t)w, e0, n);
-    mbar_wait(smem_u32(&full[slot]), (i / NS) & 1u);
     const bool asym = lo != lo_neg;
-    const uint32_t b0 = 16u * lane;
-    const uint32_t nl = n >= b0 + 16 ? 16u : (n > b0 ? n - b0 : 0u);
-    const uint32_t vmask = nl == 16 ? 0xFFFFu : ((1u << nl) - 1u);
-    const uint8_t* sl = ring + (size_t)slot * SLOT;
-    const bool f32 = f.dtype == SIF_DTYPE_F32;
-    uint32_t m = 0;
-    if (n) {
-      if (f32) {
-        const uint4* u4 = reinterpret_cast<const uint4*>(sl) + (w * UE + b0) / 4;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t jj = (uint32_t)(j + (lane >> 1)) & 3u;
-          const uint4 q = u4[jj];
-          const uint32_t v[4] = {q.x, q.y, q.z, q.w};
-          uint32_t mj = 0, ml = 0;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint32_t key = v[k] & 0x7FFFFFFFu;
-            mj |= (key >= ((asym && (v[k] >> 31)) ? lo_neg : lo) ? 1u : 0u) << k;
-            if (asym) ml |= (key >= lo ? 1u : 0u) << k;
-          }
-          m |= mj << (4 * jj);
-          if (asym) clo += __popc((ml << (4 * jj)) & vmask);
-        }
-      } else {
-        const uint4* u4 = reinterpret_cast<const uint4*>(sl) + (w * UE + b0) / 8;
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const uint32_t jj = (uint32_t)(j + (lane >> 2)) & 1u;
-          const uint4 q = u4[jj];
-          const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
-          uint32_t mj = 0, ml = 0;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const uint32_t v = (k & 1) ? (wv[k >> 1] & 0xFFFF0000u) : (wv[k >> 1] << 16);
-            const uint32_t key = v & 0x7FFFFFFFu;
-            mj |= (key >= ((asym && (v >> 31)) ? lo_neg : lo) ? 1u : 0u) << k;
-            if (asym) ml |= (key >= lo ? 1u : 0u) << k;
-          }
-          m |= mj << (8 * jj);
-          if (asym) clo += __popc((ml << (8 * jj)) & vmask);
-        }
-      }
-    }
-    m &= vmask;
-    const uint32_t cnt = __popc(m);
-    const uint32_t incl = warp_incl_scan_u32(cnt);
-    uint32_t pos = incl - cnt;
-    while (m) {  // set bits in flat order: unit-local element indices
-      stage[pos++] = b0 + (uint32_t)(__ffs(m) - 1);
-      m &= m - 1u;
-    }
-    const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-    if (!asym && lane == 0) clo += total;
+    uint32_t cnt = 0;
+    if (n) cnt = classify_any(f.dtype, r0, e0, n, lo, lo_neg, asym, stage, clo);
+    if (!asym && lane == 0) clo += cnt;
     uint32_t off = 0;
     if (lane == 0) {
-      off = total ? atomicAdd(&a.st[ifi].ncand, total) : 0u;
+      off = cnt ? atomicAdd(&a.st[ifi].ncand, cnt) : 0u;
       a.u_off[(uint64_t)c * UNITS + w] = off;
-      a.u_cnt[(uint64_t)c * UNITS + w] = total;
+      a.u_cnt[(uint64_t)c * UNITS + w] = cnt;
     }
     off = __shfl_sync(0xFFFFFFFFu, off, 0);
     __syncwarp();
-    uint2* dst = le(a, f) + off;
-    uint32_t* hs = f.hslot >= 0 ? hist : nullptr;
-    const uint32_t* s32 = reinterpret_cast<const uint32_t*>(sl) + w * UE;
-    const unsigned short* s16 = reinterpret_cast<const unsigned short*>(sl) + w * UE;
-    for (uint32_t k = lane; k < total; k += 32) {
-      const uint32_t t = stage[k];
-      const uint32_t bits = f32 ? s32[t] : ((uint32_t)s16[t] << 16);
-      dst[k] = make_uint2(bits, e0 + t);
-      const uint32_t key = bits & 0x7FFFFFFFu;
-      mk = max(mk, key);
-      if (hs) {
-        const uint32_t d = key >> DSH;
-        atomicAdd(&hs[((bits >> 31) ? ND : 0) + d], 1u);
-        dmin = min(dmin, d);
-        dmax = max(dmax, d);
-      }
-    }
+    emit_unit(stage, cnt, le(a, f) + off, f.hslot >= 0 ? hist : nullptr, mk, dmin, dmax);
     __syncwarp();
+    r0 = r1;
+    r1 = r2;
   }
   flush_if_stream(a, cur, hist, mk, clo, dmin, dmax, sdr);
 }

@@ -95,12 +95,12 @@ int resident_grid(K kfn, int threads, int smem, uint64_t work, int sms) {
 }
 
 constexpr uint32_t kBigNcand = 131072;  // candidates above which an IF uses the multi-kernel select
-constexpr int kSmemStream = sif::RING_BYTES + 2 * sif::ND * 4 + (sif::CNT / 32) * sif::UE * 2;
+constexpr int kSmemStream = (2 * sif::CH + 2 * sif::ND) * 4;
 constexpr int kSmemSelect = (2 * sif::ND + 2 * sif::HB + sif::GCAP * 4 + 2 * sif::GSM) * 4;
 inline int smem_abq(int maxb) { return (sif::CNT / 32) * maxb * (int)(sizeof(sif::AbqPar) + 16 * 8); }
 inline int smem_pack(int maxb) { return (sif::CNT / 32) * maxb * (int)sizeof(sif::PackPar); }
 inline uint32_t crc_segments(uint64_t cap) { return (uint32_t)std::max<uint64_t>(1, (cap + sif::CRC_PIECE - 1) / sif::CRC_PIECE); }
-constexpr int kSmemScatterMax = (sif::DNT / 32) * (1280 * 4 + 2 * ((1280 + 31) / 32) * 4);
+constexpr int kSmemScatterMax = (sif::DNT / 32) * 2 * ((4096 + 31) / 32) * 4;
 
 // Per-device state: everything that depends on the device a call runs on (the CRC piece
 // shift table in that device's __constant__/__device__ memory, kernel attributes, SM
@@ -325,7 +325,6 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
   memset(p, 0, sizeof(*p));
   uint64_t kmax = 0, nch = 0, nhist = 0, lists = 0, nseg = 0;
   bool tiny = false;  // some IF may take the warp-per-IF select (enc_select_tiny)
-  bool any_f32 = false;  // some streamed IF is fp32 (16 KB stream ring slots)
   bool all_small = n > 0;  // every IF fits one chunk: narrow enc_prep
   int nfused = 0, ntoken = 0;
   for (int i = 0; i < n; ++i) {
@@ -344,7 +343,6 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
     }
     const uint64_t ch = (T + sif::CH - 1) / sif::CH;
     nch += ch;
-    if (d[i].dtype == SIF_DTYPE_F32) any_f32 = true;
     if (ch > 1) ++nhist;
     if (ch > 1) all_small = false;
     if (is_fused(T, atkf)) {  // stream pass as the pipeline, then enc_post
@@ -373,8 +371,8 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
   p->max_blocks = maxb;
   p->tiles = (int32_t)nch;
   // bit 0: ATKF-only, bit 1: multi-kernel select, bit 2: warp-per-IF select for small IFs,
-  // bit 3: every IF fits one chunk (narrow enc_prep), bit 4: some streamed IF is fp32
-  p->flags = atkf | (kmax * 2 > (uint64_t)kBigNcand ? 2 : 0) | (tiny ? 4 : 0) | (all_small ? 8 : 0) | (any_f32 ? 16 : 0);
+  // bit 3: every IF fits one chunk (narrow enc_prep)
+  p->flags = atkf | (kmax * 2 > (uint64_t)kBigNcand ? 2 : 0) | (tiny ? 4 : 0) | (all_small ? 8 : 0);
   p->ws_desc_off = w.info;
   p->ws_aux_off = w.fixedq;
   p->ws_spill_off = w.lists;
@@ -528,7 +526,6 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   // multi-kernel select for IFs with many candidates (one CTA per IF would scan them
   // alone); enabled when the batch holds an IF whose keep count exceeds half the cut-off
   a.big_ncand = (p->flags & 2) ? kBigNcand : 0u;
-  a.stream_slot = (p->flags & 16) ? sif::CH * 4 : sif::CH * 2;
   a.prof = reinterpret_cast<uint64_t*>(getenv("SIF_PROF_PTR") ? strtoull(getenv("SIF_PROF_PTR"), nullptr, 0) : 0ull);
   DevState* ds = dev_state();
   if (!ds) return SIF_ERR_CUDA;
@@ -681,12 +678,14 @@ static DecWs dec_ws(uint64_t n, uint64_t table_rows) {
   return w;
 }
 
-// Elements per decode work item (a group of whole rows, or a segment of one long row).
-// Batches of narrow IFs (every K <= 1280) take 1280-element row groups (fewer work items,
-// still 4 CTAs per SM); wider rows are cut into 1024-column segments.
+// Elements per decode work item: a group of whole rows, or a segment of one long row.
+// Batches of narrow IFs (every K <= 1280) take 1280-element row groups (small items keep
+// the warps balanced); wider rows take 4096-element items (a 4096-column row is one item,
+// no column-segment searches).  The scatter keeps only two bitmaps per item in shared
+// memory (the output is written in place), so the item size is free.
 static uint32_t dec_segw(const sif_dec_desc* d, int n) {
   for (int i = 0; i < n; ++i)
-    if (d[i].cols > 1280) return 1024;
+    if (d[i].cols > 1280 && !dec_is_small(d[i])) return 4096;
   return 1280;
 }
 
@@ -710,7 +709,7 @@ int sif_dec_plan(const sif_dec_desc* d, int n, sif_plan* p) {
   p->tiles = (int32_t)segw;    // decode plans: columns per work item
   p->cluster = (int32_t)nseg;  // decode plans: CRC segment CTAs
   p->max_blocks = 0;
-  p->smem_bytes = (sif::DNT / 32) * (int)(segw * 4 + 2 * ((segw + 31) / 32) * 4);
+  p->smem_bytes = (sif::DNT / 32) * (int)(2 * ((segw + 31) / 32) * 4);
   const DecWs w = dec_ws(std::max(n, 1), rows);
   p->ws_desc_off = w.desc;
   p->ws_aux_off = w.table;

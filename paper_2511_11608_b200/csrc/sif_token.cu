@@ -366,17 +366,16 @@ __global__ void __launch_bounds__(KNT, 7) enc_token(EArgs a, const uint32_t* tok
   // ---- kept per sign; blocks by plane rank (msplit.py:68-80): in the sorted order a kept
   // element of plane s with rank r belongs to block min(r / base, meff - 1); its first
   // member is the block's cut and holds the block max, its last the block min
-  // (quant.py:50-51).  Warp 0 walks the sorted order.
-  if (w == 0) {
-    uint32_t k0 = 0, k1 = 0;
-    for (uint32_t b0 = 0; b0 < n; b0 += 32) {
-      const uint32_t i = b0 + lane;
-      const bool kp = i < n && kept_sorted(i);
-      const bool plus = i < n && ((srt[i] >> 32) & 1u);
-      k0 += __popc(__ballot_sync(0xFFFFFFFFu, kp && plus));
-      k1 += __popc(__ballot_sync(0xFFFFFFFFu, kp && !plus));
-    }
-    const uint32_t nnz[2] = {k0, k1};
+  // (quant.py:50-51).  Thread t walks the sorted entries [t E, t E + E); its starting plane
+  // ranks come from a block scan of the per-thread kept counts (plus | minus << 16).
+  {
+    const uint32_t E = (n + KNT - 1) / KNT, i0 = tid * E, i1 = min(n, i0 + E);
+    uint32_t kp = 0;
+    for (uint32_t i = i0; i < i1; ++i)
+      if (kept_sorted(i)) kp += ((srt[i] >> 32) & 1u) ? 1u : 0x10000u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan_u32(kp, ts.sh.red, &tot);
+    const uint32_t nnz[2] = {tot & 0xFFFFu, tot >> 16};
     const uint32_t mcfg[2] = {(uint32_t)a.m_plus, (uint32_t)a.m_minus};
     uint32_t meff[2], base[2];
     for (int sg = 0; sg < 2; ++sg) {
@@ -385,30 +384,23 @@ __global__ void __launch_bounds__(KNT, 7) enc_token(EArgs a, const uint32_t* tok
       base[sg] = nnz[sg] / meff[sg];
     }
     const int B = (int)(meff[0] + meff[1]);
-    if (lane < B) { ts.bmin[lane] = 0x7FFFFFFFu; ts.bmax[lane] = 0; ts.ckey[lane] = 0; ts.cidx[lane] = 0; }
-    __syncwarp();
-    uint32_t run0 = 0, run1 = 0;
-    const uint32_t le_mask = 0xFFFFFFFFu >> (31 - lane);
-    for (uint32_t b0 = 0; b0 < n; b0 += 32) {
-      const uint32_t i = b0 + lane;
-      const bool kp = i < n && kept_sorted(i);
-      const uint32_t sg = (i < n && ((srt[i] >> 32) & 1u)) ? 0u : 1u;
-      const uint32_t m0 = __ballot_sync(0xFFFFFFFFu, kp && sg == 0), m1 = __ballot_sync(0xFFFFFFFFu, kp && sg == 1);
-      if (kp) {
-        const uint32_t r = (sg == 0 ? run0 + __popc(m0 & le_mask) : run1 + __popc(m1 & le_mask)) - 1;
-        const uint32_t bs = base[sg], me_ = meff[sg];
-        const uint32_t jl = min(r / bs, me_ - 1);
-        const int b = (sg ? (int)meff[0] : 0) + (int)jl;
-        const uint32_t last = jl + 1 < me_ ? (jl + 1) * bs - 1 : nnz[sg] - 1;
-        if (r == jl * bs) { ts.bmax[b] = key_at(i); ts.ckey[b] = key_at(i); ts.cidx[b] = idx_at(i); }
-        if (r == last) ts.bmin[b] = key_at(i);
-      }
-      run0 += __popc(m0);
-      run1 += __popc(m1);
+    if (tid < B) { ts.bmin[tid] = 0x7FFFFFFFu; ts.bmax[tid] = 0; ts.ckey[tid] = 0; ts.cidx[tid] = 0; }
+    __syncthreads();
+    uint32_t run[2] = {ex & 0xFFFFu, ex >> 16};
+    for (uint32_t i = i0; i < i1; ++i) {
+      if (!kept_sorted(i)) continue;
+      const uint32_t sg = ((srt[i] >> 32) & 1u) ? 0u : 1u;
+      const uint32_t r = run[sg]++;
+      const uint32_t bs = base[sg], me_ = meff[sg];
+      const uint32_t jl = min(r / bs, me_ - 1);
+      const int b = (sg ? (int)meff[0] : 0) + (int)jl;
+      const uint32_t last = jl + 1 < me_ ? (jl + 1) * bs - 1 : nnz[sg] - 1;
+      if (r == jl * bs) { ts.bmax[b] = key_at(i); ts.ckey[b] = key_at(i); ts.cidx[b] = idx_at(i); }
+      if (r == last) ts.bmin[b] = key_at(i);
     }
-    if (lane == 0) {
-      ts.nnz0 = k0;
-      ts.nnz1 = k1;
+    if (tid == 0) {
+      ts.nnz0 = nnz[0];
+      ts.nnz1 = nnz[1];
       ts.B = (uint32_t)B;
       ts.meff0 = meff[0];
       uint32_t acc = 0;
@@ -446,35 +438,36 @@ __global__ void __launch_bounds__(KNT, 7) enc_token(EArgs a, const uint32_t* tok
       }
       return b0 + j;
     };
-    uint64_t lo = 0, hi = 0;
-    for (uint32_t m = cmask; m; m &= m - 1u) {
+    // bc: block + 1 of this thread's candidate number o (0 = not kept), 4 bits each
+    uint64_t lo = 0, hi = 0, bc0 = 0, bc1 = 0;
+    uint32_t o = 0;
+    for (uint32_t m = cmask; m; m &= m - 1u, ++o) {
       const uint32_t e = 32u * tid + (uint32_t)(__ffs(m) - 1);
       const int b = block_of(e, tok_raw(ts, e));
       if (b >= 4) hi += 1ull << (16 * (b - 4));
       else if (b >= 0) lo += 1ull << (16 * b);
+      const uint64_t code = (uint64_t)(b + 1) << (4 * (o & 15u));
+      if (o < 16) bc0 |= code; else bc1 |= code;
     }
     __syncthreads();  // every thread has read the sorted order (memv aliases it)
     uint64_t tot;
     uint64_t plo = block_excl_scan_u64(lo, ts.scan, &tot);
     uint64_t phi = block_excl_scan_u64(hi, ts.scan, &tot);
-    for (uint32_t m = cmask; m; m &= m - 1u) {
-      const uint32_t e = 32u * tid + (uint32_t)(__ffs(m) - 1);
-      const int b = block_of(e, tok_raw(ts, e));
+    o = 0;
+    for (uint32_t m = cmask; m; m &= m - 1u, ++o) {
+      const int b = (int)(((o < 16 ? bc0 : bc1) >> (4 * (o & 15u))) & 15u) - 1;
       if (b < 0) continue;
+      const uint32_t e = 32u * tid + (uint32_t)(__ffs(m) - 1);
       uint32_t p;
       if (b >= 4) { p = (uint32_t)(phi >> (16 * (b - 4))) & 0xFFFFu; phi += 1ull << (16 * (b - 4)); }
       else { p = (uint32_t)(plo >> (16 * b)) & 0xFFFFu; plo += 1ull << (16 * b); }
-      memv[ts.brun[b] + p] = e;
+      memv[ts.brun[b] + p] = e | ((uint32_t)b << 12);  // flat index (12 bits) and block
     }
   }
   __syncthreads();
   const uint32_t nk = ts.nnz0 + ts.nnz1;  // members, block runs back to back
-  // block of member i (runs in block order)
-  auto blk_of = [&](uint32_t i) -> int {
-    int b = 0;
-    while (b + 1 < B && ts.brun[b + 1] <= i) ++b;
-    return b;
-  };
+  auto blk_of = [&](uint32_t i) -> int { return (int)(memv[i] >> 12); };
+  auto mem_e = [&](uint32_t i) -> uint32_t { return memv[i] & 0xFFFu; };
 
   prof_mark(a, ifi, 29);
   // ---- ABQ (quant.py:88-115): all blocks at once, descending level by level while some
@@ -506,7 +499,7 @@ __global__ void __launch_bounds__(KNT, 7) enc_token(EArgs a, const uint32_t* tok
       for (uint32_t i = tid; i < nk; i += KNT) {
         const int b = blk_of(i);
         if (!ts.act[b]) continue;
-        const uint32_t key = tok_raw(ts, memv[i]) & 0x7FFFFFFFu;
+        const uint32_t key = tok_raw(ts, mem_e(i)) & 0x7FFFFFFFu;
         const double vmin = ts.vmin[b];
         const uint32_t r = quant_code(key, vmin, ts.oq[b][qb], ts.iq[b][qb], lref) >> (qb - qq);
         const uint32_t cq = quant_code(key, vmin, ts.oq[b][qq], ts.iq[b][qq], lq);
@@ -616,9 +609,9 @@ __global__ void __launch_bounds__(KNT, 7) enc_token(EArgs a, const uint32_t* tok
       const int b = blk_of(i);
       const uint32_t r0 = ts.brun[b], nb = ts.bsize[b], q = ts.q[b], m = i - r0;
       const uint64_t rp = ts.meta[b] + kBlockMetaBytes;
-      const uint32_t ex = memv[i];
+      const uint32_t ex = mem_e(i);
       const uint32_t row = fk.div(ex), col = ex - row * f.K;
-      const int32_t prow = m > 0 ? (int32_t)fk.div(memv[i - 1]) : -1;
+      const int32_t prow = m > 0 ? (int32_t)fk.div(mem_e(i - 1)) : -1;
       for (int32_t r = prow + 1; r <= (int32_t)row; ++r) st_u32_le(out, rp + 4ull * (uint32_t)r, m);
       if (m + 1 == nb)  // rows after the last member hold nnz
         for (uint32_t r = row + 1; r <= f.N; ++r) st_u32_le(out, rp + 4ull * r, nb);

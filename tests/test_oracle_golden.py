@@ -86,3 +86,21 @@ def test_oracle_structural_streams():
             assert kind is None, (n, kind)
             y = O.decode_bytes(data)
             assert np.array_equal(y.reshape(-1).view(np.uint32), d[f"{n}_dec"].reshape(-1).view(np.uint32)), n
+
+
+def _wide():
+    import os
+
+    d = np.load(os.path.join(os.path.dirname(__file__), "golden", "wide.npz"))
+    return d, [str(n) for n in d["names"]]
+
+
+def test_oracle_matches_reference_many_blocks():
+    """Many-block configurations (up to 32 effective blocks, tests/golden/make_wide_golden.py)."""
+    d, names = _wide()
+    for n in names:
+        s, lam, mp, mm, qb, dl, seed = d[f"{n}_cfg"]
+        cfg = O.Cfg(s=float(s), lam=float(lam), m_plus=int(mp), m_minus=int(mm), q_bit=int(qb), delta=float(dl))
+        blob = O.encode_bytes(d[f"{n}_x"], cfg, int(seed))
+        assert blob == d[f"{n}_blob"].tobytes(), n
+        assert np.array_equal(O.decode_bytes(blob).reshape(-1).view(np.uint32), d[f"{n}_dec"].reshape(-1)), n
