@@ -352,8 +352,8 @@ def run_reference(args, conf, rank):
 # pipeline move only intermediate data and count 0.
 def _alg_bytes(name, raw, payload, dense_out):
     return {"enc_stream": raw, "enc_pack": payload, "enc_crc": payload, "sif_dcrc_kernel": payload,
-            "sif_scatter_kernel": dense_out + payload, "enc_small": raw + payload,
-            "dec_small": payload + dense_out}.get(name, 0)
+            "sif_scatter_kernel": dense_out + payload, "enc_token": raw + payload,
+            "sif_dec_small": payload + dense_out}.get(name, 0)
 
 
 def _kernel_profile(sif, step, steps):

@@ -293,6 +293,34 @@ __device__ uint32_t crc_cta_staged(const uint8_t* base, uint64_t b0, uint64_t b1
   return r;
 }
 
+// Walks the IF owning consecutive global piece numbers gp of a prefix table base[0..n]
+// (pieces of IF i are base[i] .. base[i+1]-1): one binary search for the first piece of a
+// warp's contiguous range, then forward steps (no dependent-load chain per piece).
+struct PieceWalk {
+  const uint32_t* base;
+  int n, i;
+  uint32_t b0, b1;
+  __device__ __forceinline__ void init(const uint32_t* bs, int nn) { base = bs; n = nn; i = -1; b0 = b1 = 0; }
+  __device__ __forceinline__ int at(uint64_t gp) {
+    if (i < 0) {
+      int lo = 0, hi = n - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (base[mid] <= gp) lo = mid; else hi = mid - 1;
+      }
+      i = lo;
+      b0 = base[i];
+      b1 = base[i + 1];
+    }
+    while (gp >= b1) {
+      ++i;
+      b0 = b1;
+      b1 = base[i + 1];
+    }
+    return i;
+  }
+};
+
 // Fast exact u32 division / modulo by an invariant divisor (Lemire fastmod, 64-bit M).
 struct FastDiv {
   uint64_t M;

@@ -152,16 +152,15 @@ __global__ void __launch_bounds__(DNT, 8) sif_dcrc_kernel(DecArgs a) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int k = threadIdx.x; k < 1024; k += DNT) t4[k] = (&kCrcTab4[0][0])[k];
   __syncthreads();
-  const uint64_t GW = (uint64_t)gridDim.x * (DNT / 32);
+  // each warp takes a contiguous range of the pieces (streams walked forward)
+  const uint64_t GW = (uint64_t)gridDim.x * (DNT / 32), gw = (uint64_t)blockIdx.x * (DNT / 32) + w;
   const uint64_t total = a.seg_base[a.n];
-  for (uint64_t gp = (uint64_t)blockIdx.x * (DNT / 32) + w; gp < total; gp += GW) {
-    int lo = 0, hi = a.n - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (a.seg_base[mid] <= gp) lo = mid; else hi = mid - 1;
-    }
-    const int ifi = lo;
-    const uint32_t piece = (uint32_t)(gp - a.seg_base[lo]);
+  const uint64_t p0 = total * gw / GW, p1 = total * (gw + 1) / GW;
+  PieceWalk pw;
+  pw.init(a.seg_base, a.n);
+  for (uint64_t gp = p0; gp < p1; ++gp) {
+    const int ifi = pw.at(gp);
+    const uint32_t piece = (uint32_t)(gp - pw.b0);
     const uint32_t* tab = dtab(a, ifi);
     if (tab[TROW_U32 + 0]) continue;  // length / magic failure: no CRC
     const sif_dec_desc d = a.descs[ifi];
@@ -413,10 +412,13 @@ __global__ void __launch_bounds__(DNT, 3) sif_scatter_kernel(DecArgs a) {
               wr = true;
               pos = rij * W + (col - c0);
               const uint32_t old = atomicOr(bm + (minus ? bmw : 0u) + (pos >> 5), 1u << (pos & 31));
-              if (old & (1u << (pos & 31))) ck = min(ck, corrupt_key(bj, CK_OVERLAP));  // codec.py:248-250
+              if (old & (1u << (pos & 31))) {  // codec.py:248-250 (corrupt: the first value stays)
+                ck = min(ck, corrupt_key(bj, CK_OVERLAP));
+                wr = false;
+              }
               const uint2 ov = *reinterpret_cast<const uint2*>(&pb[w][jl].z);  // o, v_min
               v = __dadd_rn(__dmul_rn((double)code, (double)__uint_as_float(ov.x)), (double)__uint_as_float(ov.y));
-              if (!minus) {
+              if (wr && !minus) {
                 const float f = __double2float_rn(v);  // f32(0 + v)
                 dst[pos] = f;
                 nf0 |= (__float_as_uint(f) & 0x7F800000u) == 0x7F800000u ? 1u : 0u;
@@ -571,7 +573,10 @@ __global__ void __launch_bounds__(DSN, 7) sif_dec_small(DecArgs a) {
         if (m > gen_u32_le(src, rpo + 4ull * r) && gen_field(src, cbit + (uint64_t)(m - 1) * cb, cb) >= col)
           ck = min(ck, corrupt_key(b, CK_COL_ORDER));  // codec.py:244-247
         const uint32_t pos = r * K + col, bit = 1u << (pos & 31u);
-        if (atomicOr(&sh.bm[minus][pos >> 5], bit) & bit) ck = min(ck, corrupt_key(b, CK_OVERLAP));  // :248-250
+        if (atomicOr(&sh.bm[minus][pos >> 5], bit) & bit) {  // codec.py:248-250 (corrupt: keep the first value)
+          ck = min(ck, corrupt_key(b, CK_OVERLAP));
+          continue;
+        }
         const uint32_t code = gen_field(src, qbit + (uint64_t)m * q, q);
         const double v = __dadd_rn(__dmul_rn((double)code, o), vmin);
         float f;

@@ -209,7 +209,7 @@ struct GatE {
 
 struct SelSh {
   uint64_t scan[40];
-  uint32_t red[40];
+  uint32_t red[72];  // >= 2 * (NT / 32) + 1 for NT <= 1024
   uint32_t fd_digit;
   uint64_t fd_above, fd_eq;
   uint32_t fd_found;
@@ -440,10 +440,10 @@ __device__ SelRes select_exact(SelSh& sh, uint32_t* scratch, const List& L, uint
   }
   gt = __reduce_add_sync(0xFFFFFFFFu, gt);
   eq = __reduce_add_sync(0xFFFFFFFFu, eq);
-  if ((tid & 31) == 0) { sh.red[tid >> 5] = gt; sh.red[16 + (tid >> 5)] = eq; }
+  if ((tid & 31) == 0) { sh.red[tid >> 5] = gt; sh.red[NW + (tid >> 5)] = eq; }
   __syncthreads();
   uint64_t tgt = 0, teq = 0;
-  for (int w = 0; w < NW; ++w) { tgt += sh.red[w]; teq += sh.red[16 + w]; }
+  for (int w = 0; w < NW; ++w) { tgt += sh.red[w]; teq += sh.red[NW + w]; }
   res.key = ks;
   res.sec = sh.sel_sec;
   res.n_gt = n_gt + tgt;
@@ -617,10 +617,10 @@ __device__ __forceinline__ uint32_t bracket_lo(const EArgs& a, const IfInfo& f, 
     // bits equal in every key (e.g. the low 16 bits of bf16 data) need no histogram level
     kor = __reduce_or_sync(0xFFFFFFFFu, kor);
     kand = __reduce_and_sync(0xFFFFFFFFu, kand);
-    if ((tid & 31) == 0) { sh.red[tid >> 5] = kor; sh.red[16 + (tid >> 5)] = kand; }
+    if ((tid & 31) == 0) { sh.red[tid >> 5] = kor; sh.red[NT / 32 + (tid >> 5)] = kand; }
     __syncthreads();
     uint32_t vary = 0, cand = 0xFFFFFFFFu;
-    for (int w = 0; w < NT / 32; ++w) { vary |= sh.red[w]; cand &= sh.red[16 + w]; }
+    for (int w = 0; w < NT / 32; ++w) { vary |= sh.red[w]; cand &= sh.red[NT / 32 + w]; }
     vary ^= cand;  // bits that differ between some keys
     uint64_t r = kk;
     uint32_t prefix = 0, mask = 0;
@@ -2248,17 +2248,16 @@ __global__ void __launch_bounds__(CNT, 6) enc_crc(EArgs a) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int k = threadIdx.x; k < 1024; k += CNT) t4[k] = (&kCrcTab4[0][0])[k];
   __syncthreads();
-  const uint64_t GW = (uint64_t)gridDim.x * (CNT / 32);
+  // each warp takes a contiguous range of the pieces (IFs walked forward, no per-piece search)
+  const uint64_t GW = (uint64_t)gridDim.x * (CNT / 32), gw = (uint64_t)blockIdx.x * (CNT / 32) + w;
   const uint64_t total = a.seg_base[a.n];
-  for (uint64_t gp = (uint64_t)blockIdx.x * (CNT / 32) + w; gp < total; gp += GW) {
-    int lo = 0, hi = a.n - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (a.seg_base[mid] <= gp) lo = mid; else hi = mid - 1;
-    }
-    const int ifi = lo;
-    const uint32_t piece = (uint32_t)(gp - a.seg_base[ifi]);
-    const uint32_t npieces = a.seg_base[ifi + 1] - a.seg_base[ifi];
+  const uint64_t p0 = total * gw / GW, p1 = total * (gw + 1) / GW;
+  PieceWalk pw;
+  pw.init(a.seg_base, a.n);
+  for (uint64_t gp = p0; gp < p1; ++gp) {
+    const int ifi = pw.at(gp);
+    const uint32_t piece = (uint32_t)(gp - pw.b0);
+    const uint32_t npieces = pw.b1 - pw.b0;
     const IfInfo& f = a.info[ifi];
     IfSt& st = a.st[ifi];
     const uint32_t err = st.err;

@@ -758,6 +758,8 @@ int sif_dec_upload(const sif_plan* p, const sif_dec_desc* d, void* ws, void* str
       check_cuda(cudaMemcpyAsync(wb + w.slist, slist.data(), 4ull * slist.size(), cudaMemcpyHostToDevice, s)))
     return SIF_ERR_CUDA;
   if (check_cuda(cudaMemsetAsync(wb + w.acc, 0, 16ull * p->n, s))) return SIF_ERR_CUDA;
+  // the table's unused words are read back by the host with each row: start them at zero
+  if (check_cuda(cudaMemsetAsync(wb + w.table, 0, 64ull * p->ws_spill_off, s))) return SIF_ERR_CUDA;
   if (check_cuda(cudaMemcpyAsync(wb + w.segbase, seg.data(), 4ull * (p->n + 1), cudaMemcpyHostToDevice, s)))
     return SIF_ERR_CUDA;
   if (check_cuda(cudaMemcpyAsync(wb + w.itembase, items.data(), 8ull * (p->n + 1), cudaMemcpyHostToDevice, s)))
