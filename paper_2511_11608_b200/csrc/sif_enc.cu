@@ -829,6 +829,7 @@ struct K3Sh {
   uint32_t cursor;
   uint32_t nA, nB;
   uint32_t keptA[2];
+  uint32_t fullb[2], lowd[2];  // lambda > 0: per sign the digit of the smallest kept key, its bin size
   uint64_t cnt_nz;
   uint32_t pend_n;
   uint32_t pend_s[MAXB], pend_d[MAXB], pend_r[MAXB], pend_ci[MAXB], pend_reg[MAXB];
@@ -990,6 +991,9 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
   int dtau = -1;  // digit of tau on the fast path (-1: every candidate bin counts fully)
   const bool use_cls = a.lam > 0.0 && kk > 0 && !only_nonzero;
   const bool fast = !zero_mode && !use_cls;
+  // lambda > 0 outside zero mode: tau, the class select and the MS cuts are all bracketed
+  // by digit histograms and resolved inside gathered bins (a few passes over the list)
+  const bool cls_fast = use_cls && !zero_mode && !FUSED && PH == 0;
   List A{reinterpret_cast<uint2*>(gbuf), me(a, f), GSM};
   uint32_t nA = 0;
   if (kk > 0 && !only_nonzero) {
@@ -998,7 +1002,7 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
       const SelRes s = select_exact<NT, LU>(sh, scratch, L, ncand, all_pred, key31, hash_of, 0, 1, kk - cnt_nz);
       h_star = s.sec;
       tie_all = s.all_ties;
-    } else if (!fast) {
+    } else if (!fast && !cls_fast) {
       const uint64_t klo = lo_neg < lo ? lo_neg : lo;
       const SelRes s = select_exact<NT, LU>(sh, scratch, L, ncand, all_pred, key31, hash_of, klo,
                                         (uint64_t)st.maxkey + 1, kk);
@@ -1008,7 +1012,7 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
       tie_all = s.all_ties;
     } else {
       prof_mark(a, ifi, 2);
-      if (!FUSED && PH == 0 && a.big_ncand && ncand > a.big_ncand) {
+      if (!FUSED && PH == 0 && fast && a.big_ncand && ncand > a.big_ncand) {
         // digit of tau over both signs; its bin is gathered by enc_gather<1> (all SMs)
         uint32_t* comb = scratch;
         for (int k = tid; k < ND; k += NT) comb[k] = hist[k] + hist[ND + k];
@@ -1066,12 +1070,84 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
   const double tau = kk > 0 ? (double)__uint_as_float(tau_key) : (double)__uint_as_float(st.maxkey);
   const double tau_p = __dmul_rn(__dadd_rn(1.0, a.lam), tau);
   const double tau_m = -__dmul_rn(__dsub_rn(1.0, a.lam), tau);
-  if (use_cls) {
-    auto ckey = [tau_p, tau_m](uint32_t b) -> uint64_t {
-      const double v = (double)__uint_as_float(b);
-      return ((v > tau_p || v < tau_m) ? (1ull << 31) : 0ull) | (uint64_t)(b & 0x7FFFFFFFu);
-    };
+  // strict classes (atkf.py:72-75) as key thresholds: x > tau_p <=> key(x) > kp for x > 0,
+  // x < tau_m <=> key(x) > km for x < 0 (kp, km = float keys of tau_p, |tau_m| rounded down)
+  const uint32_t kp = __float_as_uint(__double2float_rd(tau_p));
+  const uint32_t km = __float_as_uint(__double2float_rd(-tau_m));
+  auto ckey = [kp, km](uint32_t b) -> uint64_t {
+    const uint32_t key = b & 0x7FFFFFFFu;
+    return ((key > ((b >> 31) ? km : kp)) ? (1ull << 31) : 0ull) | (uint64_t)key;
+  };
+  if (use_cls && !cls_fast) {
     const SelRes s = select_exact<NT, LU>(sh, scratch, L, ncand, all_pred, ckey, hash_of, 0, 1ull << 32, kk);
+    ck_star = s.key;
+    h_star = s.sec;
+    tie_all = s.all_ties;
+  } else if (cls_fast) {
+    // the kk-th element of the order (strict first, |x| desc, hash asc) (atkf.py:77-84):
+    // strict count S from the per-sign histograms plus exact counts of the two boundary
+    // bins (one pass); then the class holding rank kk, the digit holding it (class-restricted
+    // histogram), that bin gathered (one pass) and the element selected inside it
+    const uint32_t dp = kp >> DSH, dm = km >> DSH;
+    if (tid < 2) k3.keptA[tid] = 0;
+    __syncthreads();
+    {
+      uint32_t c0 = 0, c1 = 0;
+      list_foreach<NT, LU>(L, ncand, [&](uint32_t b, uint32_t, bool v) {
+        const uint32_t key = b & 0x7FFFFFFFu;
+        if (!v) return;
+        if (b >> 31) c1 += ((key >> DSH) == dm && key > km) ? 1u : 0u;
+        else c0 += ((key >> DSH) == dp && key > kp) ? 1u : 0u;
+      });
+      c0 = __reduce_add_sync(0xFFFFFFFFu, c0);
+      c1 = __reduce_add_sync(0xFFFFFFFFu, c1);
+      if ((tid & 31) == 0) { atomicAdd(&k3.keptA[0], c0); atomicAdd(&k3.keptA[1], c1); }
+    }
+    __syncthreads();
+    const uint32_t bp = k3.keptA[0], bm = k3.keptA[1];  // strict members of the boundary bins
+    uint32_t* cnt = scratch;                           // class-restricted digit counts (ND)
+    uint64_t S = 0;
+    {
+      uint32_t acc = 0;
+      for (int d = tid; d < ND; d += NT)
+        acc += ((uint32_t)d > dp ? hist[d] : 0u) + ((uint32_t)d > dm ? hist[ND + d] : 0u);
+      acc = __reduce_add_sync(0xFFFFFFFFu, acc);
+      if (tid == 0) k3.s.cnt[0] = 0;
+      __syncthreads();
+      if ((tid & 31) == 0) atomicAdd(&k3.s.cnt[0], acc);
+      __syncthreads();
+      S = (uint64_t)k3.s.cnt[0] + bp + bm;
+      __syncthreads();
+    }
+    const bool strict_cls = S >= kk;
+    const uint64_t r = strict_cls ? kk : kk - S;
+    // non-strict rank kk - S lies among positives with tau <= key <= kp (every negative
+    // non-strict key is <= km < tau), so its histogram counts positives only
+    for (int d = tid; d < ND; d += NT) {
+      uint32_t c;
+      if (strict_cls)
+        c = ((uint32_t)d > dp ? hist[d] : ((uint32_t)d == dp ? bp : 0u)) +
+            ((uint32_t)d > dm ? hist[ND + d] : ((uint32_t)d == dm ? bm : 0u));
+      else
+        c = (uint32_t)d < dp ? hist[d] : ((uint32_t)d == dp ? hist[d] - bp : 0u);
+      cnt[d] = c;
+    }
+    __syncthreads();
+    find_digit<NT>(sh, cnt, ND, r);
+    const uint32_t dstar = sh.fd_digit;
+    const uint64_t rr = r - sh.fd_above;
+    __syncthreads();
+    if (tid == 0) k3.nA = 0;
+    __syncthreads();
+    list_foreach<NT, LU>(L, ncand, [&](uint32_t b, uint32_t x, bool v) {
+      if (v && ((b & 0x7FFFFFFFu) >> DSH) == dstar) A.set(atomicAdd(&k3.nA, 1u), b, x);
+    });
+    __syncthreads();
+    nA = k3.nA;
+    const uint64_t cb = strict_cls ? (1ull << 31) : 0ull;
+    const SelRes s = select_exact<NT, LU>(
+        sh, scratch, A, nA, [&](uint32_t b, uint32_t) { return (ckey(b) >> 31) == (cb >> 31); }, ckey, hash_of,
+        cb | ((uint64_t)dstar << DSH), cb | ((uint64_t)(dstar + 1) << DSH), rr);
     ck_star = s.key;
     h_star = s.sec;
     tie_all = s.all_ties;
@@ -1081,11 +1157,7 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
     const uint32_t key = b & 0x7FFFFFFFu;
     if (only_nonzero) return key != 0;
     if (!zero_mode && key == 0) return false;
-    uint64_t ck = key;
-    if (use_cls) {
-      const double v = (double)__uint_as_float(b);
-      if (v > tau_p || v < tau_m) ck |= 1ull << 31;
-    }
+    const uint64_t ck = use_cls ? ckey(b) : (uint64_t)key;
     if (ck != ck_star) return ck > ck_star;
     return tie_all || splitmix(seed, x) <= h_star;
   };
@@ -1158,18 +1230,52 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
     }
     if (keep_none) { nnz[0] = 0; nnz[1] = 0; }
   } else {
-    uint32_t c0 = 0, c1 = 0;
+    uint32_t c0 = 0, c1 = 0, m0 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu;
     list_foreach<NT, LU>(L, ncand, [&](uint32_t b, uint32_t x, bool v) {
-      if (v && (b & 0x7FFFFFFFu) != 0 && kept_of(b, x)) { if (b >> 31) ++c1; else ++c0; }
+      const uint32_t key = b & 0x7FFFFFFFu;
+      if (v && key != 0 && kept_of(b, x)) {
+        if (b >> 31) { ++c1; m1 = min(m1, key); } else { ++c0; m0 = min(m0, key); }
+      }
     });
     c0 = __reduce_add_sync(0xFFFFFFFFu, c0);
     c1 = __reduce_add_sync(0xFFFFFFFFu, c1);
-    if (tid < 2) k3.s.cnt[tid] = 0;
+    m0 = __reduce_min_sync(0xFFFFFFFFu, m0);
+    m1 = __reduce_min_sync(0xFFFFFFFFu, m1);
+    if (tid < 2) { k3.s.cnt[tid] = 0; k3.s.cnt[2 + tid] = 0xFFFFFFFFu; }
     __syncthreads();
-    if ((tid & 31) == 0) { atomicAdd(&k3.s.cnt[0], c0); atomicAdd(&k3.s.cnt[1], c1); }
+    if ((tid & 31) == 0) {
+      atomicAdd(&k3.s.cnt[0], c0); atomicAdd(&k3.s.cnt[1], c1);
+      atomicMin(&k3.s.cnt[2], m0); atomicMin(&k3.s.cnt[3], m1);
+    }
     __syncthreads();
     nnz[0] = k3.s.cnt[0];
     nnz[1] = k3.s.cnt[1];
+    if (cls_fast) {
+      // per sign the kept set is a magnitude-top set: every
+      // candidate above the digit of its smallest kept key is kept, that digit partially;
+      // the histograms become kept histograms (the partial bins' full sizes are kept for
+      // sizing the cut gathers)
+      const uint32_t dl[2] = {k3.s.cnt[2] >> DSH, k3.s.cnt[3] >> DSH};
+      __syncthreads();
+      for (int sg = 0; sg < 2; ++sg) {
+        uint32_t above = 0;
+        for (int d = tid; d < ND; d += NT) above += ((uint32_t)d > dl[sg] && nnz[sg]) ? hist[sg * ND + d] : 0u;
+        above = __reduce_add_sync(0xFFFFFFFFu, above);
+        if (tid == 0) k3.s.cnt[4 + sg] = 0;
+        __syncthreads();
+        if ((tid & 31) == 0) atomicAdd(&k3.s.cnt[4 + sg], above);
+        __syncthreads();
+        const uint32_t part = nnz[sg] ? (uint32_t)nnz[sg] - k3.s.cnt[4 + sg] : 0u;
+        if (tid == 0) k3.fullb[sg] = nnz[sg] ? hist[sg * ND + dl[sg]] : 0u;
+        __syncthreads();
+        for (int d = tid; d < ND; d += NT) {
+          if (!nnz[sg] || (uint32_t)d < dl[sg]) hist[sg * ND + d] = 0;
+          else if ((uint32_t)d == dl[sg]) hist[sg * ND + d] = part;
+        }
+        if (tid == 0) k3.lowd[sg] = nnz[sg] ? dl[sg] : 0xFFFFFFFFu;
+        __syncthreads();
+      }
+    }
     __syncthreads();
   }
   prof_mark(a, ifi, 5);
@@ -1185,7 +1291,7 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
   const int B = (int)(meff[0] + meff[1]);
   const int ncut0 = (int)meff[0] - 1;
   const int ncut = B - 2;
-  if (fast) {
+  if (fast || cls_fast) {
     // digit of every cut from the kept histograms; cuts in tau's bin resolve from A
     if (tid == 0) k3.pend_n = 0;
     __syncthreads();
@@ -1196,7 +1302,7 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
       find_digit<NT>(sh, hist + s * ND, ND, r1);
       const uint32_t dc = sh.fd_digit;
       const uint64_t rc = r1 - sh.fd_above;
-      if ((int)dc == dtau) {
+      if (fast && (int)dc == dtau) {
         const SelRes r = select_exact<NT, LU>(
             sh, scratch, A, nA, [&](uint32_t b, uint32_t x) { return (b >> 31) == s && kept_of(b, x); }, key31,
             [](uint32_t, uint32_t x) -> uint64_t { return x; }, (uint64_t)dc << DSH, (uint64_t)(dc + 1) << DSH, rc,
@@ -1248,7 +1354,9 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
             pslot[d] = (uint8_t)nreg;
             k3.reg_off[nreg] = off;
             k3.reg_cnt[nreg] = 0;
-            off += hist[d];
+            // a partial (lambda > 0) bin is gathered whole: size it by all its candidates
+            const uint32_t sg = k3.pend_s[p];
+            off += (cls_fast && k3.pend_d[p] == k3.lowd[sg]) ? k3.fullb[sg] : hist[d];
             ++nreg;
           }
           k3.pend_reg[p] = pslot[d];
@@ -1269,8 +1377,9 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
         const uint32_t g = k3.pend_reg[p];
         const List Bp{nullptr, gat + k3.reg_off[g], 0};
         const uint32_t dc = k3.pend_d[p];
+        // a bin above the kept threshold is kept whole; lambda > 0's partial bin is filtered
         const SelRes r = select_exact<NT, LU>(
-            sh, scratch, Bp, k3.reg_cnt[g], [](uint32_t, uint32_t) { return true; }, key31,
+            sh, scratch, Bp, k3.reg_cnt[g], [&](uint32_t b, uint32_t x) { return !cls_fast || kept_of(b, x); }, key31,
             [](uint32_t, uint32_t x) -> uint64_t { return x; }, (uint64_t)dc << DSH, (uint64_t)(dc + 1) << DSH,
             k3.pend_r[p], 31);
         if (tid == 0) { st.cut_key[k3.pend_ci[p]] = r.key; st.cut_idx[k3.pend_ci[p]] = (uint32_t)r.sec; }

@@ -1,5 +1,5 @@
 """Phase timestamps (globaltimer, SIF_PROF_PTR) of enc_fused (and enc_select):
-    python tools/phase_prof.py c2|c3|c4 [fused_min fused_max]"""
+    python tools/phase_prof.py c2|c3|c4 [fused_min fused_max] [lam=X]"""
 import ctypes
 import os
 import sys
@@ -11,14 +11,19 @@ import torch
 import paper_2511_11608_b200 as sif
 
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "c2"
-if len(sys.argv) > 3:
-    sif._lib.load().sif_set_fused_range(int(sys.argv[2]), int(sys.argv[3]))
+lam = 0.0
+args = [a for a in sys.argv[2:] if not a.startswith("lam=")]
+for a in sys.argv[2:]:
+    if a.startswith("lam="):
+        lam = float(a[4:])
+if len(args) >= 2:
+    sif._lib.load().sif_set_fused_range(int(args[0]), int(args[1]))
 kind, N, K, B, dt = {"c2": (0, 1024, 196, 256, torch.float32), "c3": (1, 1, 4096, 1024, torch.bfloat16),
                      "c4": (1, 2048, 4096, 32, torch.bfloat16)}[cfgname]
 xs = torch.empty((B, N, K), dtype=dt, device="cuda")
 for i in range(B):
     sif.synthetic(kind, N, K, i, out=xs[i])
-cfg = sif.CodecConfig(s=0.9, m_plus=3, m_minus=3, q_bit=8, delta=0.01)
+cfg = sif.CodecConfig(s=0.9, lam=lam, m_plus=3, m_minus=3, q_bit=8, delta=0.01)
 prof = torch.zeros(B * 32, dtype=torch.int64, device="cuda")
 os.environ["SIF_PROF_PTR"] = str(prof.data_ptr())
 enc = sif.BatchEncoder(xs, cfg, list(range(B)))
