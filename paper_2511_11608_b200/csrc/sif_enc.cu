@@ -95,6 +95,7 @@ struct IfSt {
   uint32_t nA, pend_n, nreg, sel_lo;
   uint32_t pend_s[MAXB], pend_d[MAXB], pend_r[MAXB], pend_ci[MAXB], pend_reg[MAXB];
   uint32_t reg_off[MAXB], reg_cnt[MAXB], reg_key[MAXB];
+  uint32_t nreg_pre, reg_first, pre_end;  // regions filled by enc_gather<1>, first for <2>, end offset
 };
 
 struct EArgs {
@@ -859,7 +860,7 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
   const uint64_t kk = f.kk, seed = f.seed;
   if (PH == 0 && st.sel_phase == 4) return;  // resolved by enc_select_tiny
   if (PH > 0) {
-    if (st.sel_phase != (uint32_t)PH) return;
+    if (st.sel_phase != (uint32_t)PH && !(PH == 2 && st.sel_phase == 5u)) return;
     if (PH == 2) {
       // cut bins gathered into their regions of the gather area: exact selects, one CTA
       // per pending cut (blockIdx.y); sel_phase stays 2 until the next run's enc_prep
@@ -1018,13 +1019,68 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
         for (int k = tid; k < ND; k += NT) comb[k] = hist[k] + hist[ND + k];
         __syncthreads();
         find_digit<NT>(sh, comb, ND, kk);
+        const uint32_t dt = sh.fd_digit;
+        const uint64_t rt0 = kk - sh.fd_above;
+        __syncthreads();
+        // regions of the gather area filled by enc_gather<1>: tau's bin of both signs (0, 1,
+        // contiguous), then every bin that can hold an MS cut.  A plane's kept count is
+        // n_lo .. n_hi (tau's bin kept partly), so cut j lies at plane rank
+        // j*floor(n_lo/M)+1 .. j*floor(n_hi/M)+1; the bins above tau's that this range touches
+        // are gathered now, so the cut-bin gather pass (enc_gather<2>) is usually not needed
         if (tid == 0) {
-          st.dtau = (int32_t)sh.fd_digit;
-          st.rt = kk - sh.fd_above;
+          st.reg_key[0] = dt; st.reg_off[0] = 0; st.reg_cnt[0] = 0;
+          st.reg_key[1] = ND + dt; st.reg_off[1] = hist[dt]; st.reg_cnt[1] = 0;
+          k3.pend_n = 2;
+          k3.cursor = hist[dt] + hist[ND + dt];
+        }
+        const int mcfg2[2] = {a.m_plus, a.m_minus};
+        const uint32_t cap = (uint32_t)MAXB - 2u - (uint32_t)(a.m_plus + a.m_minus);  // room left for PH1
+        for (int sg = 0; sg < 2; ++sg) {
+          uint32_t acc = 0;
+          for (int d = tid; d < ND; d += NT) acc += (uint32_t)d > dt ? hist[sg * ND + d] : 0u;
+          acc = __reduce_add_sync(0xFFFFFFFFu, acc);
+          if (tid == 0) k3.s.cnt[sg] = 0;
+          __syncthreads();
+          if ((tid & 31) == 0) atomicAdd(&k3.s.cnt[sg], acc);
+          __syncthreads();
+          const uint64_t n_lo = k3.s.cnt[sg], n_hi = n_lo + hist[sg * ND + dt];
+          const uint64_t M = (uint64_t)mcfg2[sg];
+          if (M < 2 || n_lo < M || a.m_plus + a.m_minus > MAXB - 4) continue;
+          for (uint64_t j = 1; j < M; ++j) {
+            const uint64_t ra = j * (n_lo / M) + 1, rb = min(j * (n_hi / M) + 1, n_lo);
+            if (ra > n_lo) continue;  // in tau's bin: gathered already
+            find_digit<NT>(sh, hist + sg * ND, ND, ra);
+            const uint32_t da = sh.fd_digit;
+            __syncthreads();
+            find_digit<NT>(sh, hist + sg * ND, ND, rb);
+            const uint32_t db = sh.fd_digit;
+            __syncthreads();
+            if (tid == 0)
+              for (uint32_t d = db; d <= da; ++d) {
+                if (d <= dt || hist[sg * ND + d] == 0) continue;
+                const uint32_t key = (uint32_t)sg * ND + d;
+                uint32_t g = 2;
+                while (g < k3.pend_n && st.reg_key[g] != key) ++g;
+                if (g == k3.pend_n && g < 2 + cap) {
+                  st.reg_key[g] = key; st.reg_off[g] = k3.cursor; st.reg_cnt[g] = 0;
+                  k3.cursor += hist[key];
+                  ++k3.pend_n;
+                }
+              }
+            __syncthreads();
+          }
+        }
+        if (tid == 0) {
+          st.dtau = (int32_t)dt;
+          st.rt = rt0;
           st.nA = 0;
           st.sel_lo = lo;
           st.ncand = ncand;
           st.cnt_nz = cnt_nz;
+          st.nreg = k3.pend_n;
+          st.nreg_pre = k3.pend_n;
+          st.reg_first = 0;
+          st.pre_end = k3.cursor;
           st.sel_phase = 1;
           a.big_list[atomicAdd(&a.big_list[a.n], 1u)] = (uint32_t)ifi;  // the gathers visit these IFs only
         }
@@ -1034,7 +1090,7 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
       if (PH == 1) {
         dtau = st.dtau;
         rt = st.rt;
-        nA = st.nA;
+        nA = st.reg_cnt[0] + st.reg_cnt[1];  // tau's bin of both signs (regions 0, 1; contiguous)
         // the gathered bin: first GSM entries in shared memory, the rest read from global
         const uint2* gsrc = me(a, f);
         uint2* sdst = reinterpret_cast<uint2*>(gbuf);
@@ -1319,11 +1375,14 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
     if (PH == 1 && np > 0) {
       // regions of the gather area for the pending cut bins (sizes from the histogram);
       // enc_gather<2> fills them with all SMs, enc_select<2> resolves the cuts
+      // bins predicted in PH 0 are already gathered; any other is appended as a new region
+      // (filled by enc_gather<2>, sel_phase 2; otherwise only enc_select<2> runs, sel_phase 5)
       if (tid == 0) {
-        uint32_t nreg = 0, off = 0;
+        const uint32_t npre = st.nreg_pre;
+        uint32_t nreg = npre, off = st.pre_end;
         for (uint32_t p = 0; p < np; ++p) {
           const uint32_t d = k3.pend_s[p] * ND + k3.pend_d[p];
-          uint32_t g = 0;
+          uint32_t g = 2;
           while (g < nreg && st.reg_key[g] != d) ++g;
           if (g == nreg) {
             st.reg_key[g] = d;
@@ -1336,6 +1395,7 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
           st.pend_ci[p] = k3.pend_ci[p]; st.pend_reg[p] = g;
         }
         st.nreg = nreg;
+        st.reg_first = npre;
         st.pend_n = np;
       }
     } else if (np > 0) {
@@ -1402,7 +1462,7 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
   prof_mark(a, ifi, 8);
   zero_hist(a, f);
   if (tid == 0) {
-    st.sel_phase = (PH == 1 && k3.pend_n > 0 && fast) ? 2u : 0u;
+    st.sel_phase = (PH == 1 && k3.pend_n > 0 && fast) ? (st.nreg > st.nreg_pre ? 2u : 5u) : 0u;
     uint32_t fl = 0;
     if (keep_none) fl |= F_KEEP_NONE;
     if (only_nonzero) fl |= F_ONLY_NONZERO;
@@ -1709,7 +1769,7 @@ __global__ void __launch_bounds__(CNT) enc_gather(EArgs a) {
     while (lo + 1 < hi) { const uint32_t mid = (lo + hi) >> 1; if (lpre[mid] <= v0) lo = mid; else hi = mid; }
     li = lo;
   }
-  uint32_t dtau = 0, nreg = 0, rkey = 0xFFFFFFFFu, roff = 0;
+  uint32_t nreg = 0, rkey = 0xFFFFFFFFu, roff = 0;
   for (uint32_t v = v0; v < v1 && (all || li < nbig); ++li) {
    uint32_t ifi, vb, vend, cbeg, cend;
    if (all) {
@@ -1729,10 +1789,11 @@ __global__ void __launch_bounds__(CNT) enc_gather(EArgs a) {
    IfSt& st = a.st[ifi];
    if (st.sel_phase != (uint32_t)G) continue;
    const IfInfo& f = a.info[ifi];
-   if (G == 1) dtau = (uint32_t)st.dtau;
-   else {
+   {
+     // regions to fill: <1> every region set up by enc_select<0>, <2> the ones enc_select<1> added
+     const uint32_t first = G == 1 ? 0u : st.reg_first;
      nreg = st.nreg;
-     rkey = lane < (int)nreg ? st.reg_key[lane] : 0xFFFFFFFFu;
+     rkey = (lane < (int)nreg && (G == 1 || (uint32_t)lane >= first)) ? st.reg_key[lane] : 0xFFFFFFFFu;
      roff = lane < (int)nreg ? st.reg_off[lane] : 0u;
    }
    const uint2* gl = le(a, f);
@@ -1755,23 +1816,12 @@ __global__ void __launch_bounds__(CNT) enc_gather(EArgs a) {
           const uint2 e = ev[h];
           const uint32_t dig = (e.x & 0x7FFFFFFFu) >> DSH;
           int g = -1;
-          if (G == 1) {
-            if (j < un && dig == dtau) g = 0;
-          } else {
+          {
             const uint32_t key = j < un ? ((e.x >> 31) ? (uint32_t)ND : 0u) + dig : 0xFFFFFFFEu;
             for (uint32_t k = 0; k < nreg; ++k)
               if (__shfl_sync(0xFFFFFFFFu, rkey, (int)k) == key) g = (int)k;
           }
-          if (G == 1) {
-            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, g >= 0);
-            if (bal) {
-              const uint32_t ld = (uint32_t)(__ffs(bal) - 1);
-              uint32_t base = 0;
-              if (lane == ld) base = atomicAdd(&st.nA, (uint32_t)__popc(bal));
-              base = __shfl_sync(0xFFFFFFFFu, base, (int)ld);
-              if (g >= 0) __stcg(gat + base + __popc(bal & lt), e);
-            }
-          } else {
+          {
             const uint32_t peers = __match_any_sync(0xFFFFFFFFu, g);
             const uint32_t ld = (uint32_t)(__ffs(peers) - 1);
             uint32_t base = 0;
