@@ -94,7 +94,15 @@ int resident_grid(K kfn, int threads, int smem, uint64_t work, int sms) {
   return (int)std::max<uint64_t>(1, std::min<uint64_t>(work, slots));
 }
 
-constexpr uint32_t kBigNcand = 131072;  // candidates above which an IF uses the multi-kernel select
+// Candidates above which an IF uses the multi-kernel select (all-SM gathers); env
+// SIF_BIG_NCAND overrides it (tuning experiments).
+static uint32_t big_ncand() {
+  static const uint32_t v = [] {
+    const char* e = getenv("SIF_BIG_NCAND");
+    return e && *e ? (uint32_t)strtoul(e, nullptr, 0) : 131072u;
+  }();
+  return v;
+}
 constexpr int kSmemStream = (2 * sif::CH + 2 * sif::ND) * 4;
 constexpr int kSmemSelect = (2 * sif::ND + 2 * sif::HB + sif::GCAP * 4 + 2 * sif::GSM) * 4;
 inline int smem_abq(int maxb) { return (sif::CNT / 32) * maxb * (int)(sizeof(sif::AbqPar) + 16 * 8); }
@@ -372,7 +380,7 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
   p->tiles = (int32_t)nch;
   // bit 0: ATKF-only, bit 1: multi-kernel select, bit 2: warp-per-IF select for small IFs,
   // bit 3: every IF fits one chunk (narrow enc_prep)
-  p->flags = atkf | (kmax * 2 > (uint64_t)kBigNcand ? 2 : 0) | (tiny ? 4 : 0) | (all_small ? 8 : 0);
+  p->flags = atkf | (kmax * 2 > (uint64_t)big_ncand() ? 2 : 0) | (tiny ? 4 : 0) | (all_small ? 8 : 0);
   p->ws_desc_off = w.info;
   p->ws_aux_off = w.fixedq;
   p->ws_spill_off = w.lists;
@@ -525,7 +533,7 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   a.tau3 = tau3;
   // multi-kernel select for IFs with many candidates (one CTA per IF would scan them
   // alone); enabled when the batch holds an IF whose keep count exceeds half the cut-off
-  a.big_ncand = (p->flags & 2) ? kBigNcand : 0u;
+  a.big_ncand = (p->flags & 2) ? big_ncand() : 0u;
   a.prof = reinterpret_cast<uint64_t*>(getenv("SIF_PROF_PTR") ? strtoull(getenv("SIF_PROF_PTR"), nullptr, 0) : 0ull);
   DevState* ds = dev_state();
   if (!ds) return SIF_ERR_CUDA;
