@@ -96,6 +96,7 @@ __device__ uint32_t kPieceShift[CRC_PIECES_MAX];
 // owns the 64 bytes ending 64*(31-l) bytes before e1; bytes before e0 are taken as zero
 // (leading zeros do not change a raw CRC).  stage: >= 544 words of this warp's shared
 // memory; t4: kCrcTab4 in shared memory.
+template <bool GENERIC = false>
 __device__ __forceinline__ uint32_t crc_piece_warp(const uint8_t* base, uint64_t e0, uint64_t e1, const uint32_t* t4,
                                                    uint32_t* stage) {
   const int lane = threadIdx.x & 31;
@@ -108,7 +109,7 @@ __device__ __forceinline__ uint32_t crc_piece_warp(const uint8_t* base, uint64_t
   for (int k = 0; k < 17; ++k) {
     const int j = lane + 32 * k;
     const int64_t wi = fl + j;
-    stage[j] = (wi >= w_lo && wi < w_hi) ? __ldcg(gw + wi) : 0u;
+    stage[j] = (wi >= w_lo && wi < w_hi) ? (GENERIC ? gw[wi] : __ldcg(gw + wi)) : 0u;
   }
   __syncwarp();
   uint32_t c = 0;
@@ -127,6 +128,33 @@ __device__ __forceinline__ uint32_t crc_piece_warp(const uint8_t* base, uint64_t
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c ^= __shfl_xor_sync(0xFFFFFFFFu, c, o);
   return c;
+}
+
+// Raw CRC of [b0, b1) by the warps of a CTA of NT threads: one 2 KiB piece per warp per
+// round (pieces aligned to b1, combined with kPieceShift), so a short range (a token's
+// payload) costs one warp-piece instead of NT*64 staged bytes.  Result in every thread.
+// stage: >= 544 words per warp; red: >= NT/32 words.  GENERIC: base may be shared memory.
+template <int NT, bool GENERIC = false>
+__device__ uint32_t crc_cta_pieces(const uint8_t* base, uint64_t b0, uint64_t b1, const uint32_t* t4, uint32_t* red,
+                                   uint32_t* stage) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t n = b1 > b0 ? b1 - b0 : 0;
+  const uint32_t np = (uint32_t)((n + CRC_PIECE - 1) / CRC_PIECE);
+  uint32_t acc = 0;
+  for (uint32_t piece = (uint32_t)w; piece < np; piece += NW) {
+    const uint64_t e1 = b1 - (uint64_t)piece * CRC_PIECE;
+    const uint64_t e0 = e1 - b0 > CRC_PIECE ? e1 - CRC_PIECE : b0;
+    const uint32_t raw = crc_piece_warp<GENERIC>(base, e0, e1, t4, stage + w * 544);
+    if (raw) acc ^= piece ? crc_mult(kPieceShift[piece], raw) : raw;
+  }
+  if (lane == 0) red[w] = acc;
+  __syncthreads();
+  uint32_t tot = 0;
+#pragma unroll
+  for (int k = 0; k < NW; ++k) tot ^= red[k];
+  __syncthreads();
+  return tot;
 }
 
 __device__ __forceinline__ uint32_t crc_finish(uint32_t raw_total, uint64_t len) {

@@ -530,8 +530,8 @@ __global__ void __launch_bounds__(DSN, 7) sif_dec_small(DecArgs a) {
   uint32_t crc_raw = 0;
   if (!pre) {
     uint32_t* cst = reinterpret_cast<uint32_t*>(sh.buf);
-    crc_raw = staged ? crc_cta_staged<DSN, true>(src, 4, len - 4, sh.t4, sh.red, cst)
-                     : crc_cta_staged<DSN>(d.in, 4, len - 4, sh.t4, sh.red, cst);
+    crc_raw = staged ? crc_cta_pieces<DSN, true>(src, 4, len - 4, sh.t4, sh.red, cst)
+                     : crc_cta_pieces<DSN>(d.in, 4, len - 4, sh.t4, sh.red, cst);
   }
   if (tid == 0) sh.crcok = (!pre && crc_finish(crc_raw, len - 8) == sh.tab[TROW_U32 + 1]) ? 1u : 0u;
   __syncthreads();

@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(KNT, 7) enc_token(EArgs a, const uint32_t* tok
     uint32_t* cstage = t4 + 1024;
     for (int k = tid; k < 1024; k += KNT) t4[k] = (&kCrcTab4[0][0])[k];
     __syncthreads();
-    const uint32_t raw = crc_cta_staged<KNT>(out, 4, P - 4, t4, ts.sh.red, cstage);
+    const uint32_t raw = crc_cta_pieces<KNT>(out, 4, P - 4, t4, ts.sh.red, cstage);
     if (tid == 0) {
       st_u32_le_bytes(out, P - 4, crc_finish(raw, P - 8));
       a.out_len[ifi] = P;
