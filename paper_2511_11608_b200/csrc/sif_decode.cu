@@ -495,6 +495,8 @@ struct SmallSh {
   uint32_t t4[1024];                  // CRC slice tables
   uint32_t cp[SMALL_CAP / 4 + 4];     // the stream, zero padded
   uint32_t tab[SMALL_ROWS * TROW_U32]; // the first table rows (header + blocks)
+  uint32_t pre[SMALL_ROWS];            // nnz prefix over the blocks
+  uint32_t ovl;                        // a plane overlap seen in the flattened pass
   uint32_t red[DSN / 32 + 1];
   uint32_t ck, fl, crcok;
 };
@@ -547,52 +549,99 @@ __global__ void __launch_bounds__(DSN, 7) sif_dec_small(DecArgs a) {
     for (uint32_t k = tid; k < T; k += DSN) sh.buf[k] = 0.f;
     for (uint32_t k = tid; k < 2 * SMALL_T / 32; k += DSN) (&sh.bm[0][0])[k] = 0u;
     __syncthreads();
-    for (uint32_t b = 0; b < nb; ++b) {
+    // entry m of block b: row (codec.py:238-241 ranges), col checks (codec.py:242-247),
+    // plane overlap (codec.py:248-250), float64 value (quant.py:67-73, codec.py:257-266).
+    // exact == false: an overlap only raises the plane's redo flag (the entries of a plane
+    // run in parallel, so which block saw the collision first is not the reference's order)
+    auto entry = [&](uint32_t b, uint32_t m, bool exact) {
       const uint32_t* row = tab + (2ull + b) * TROW_U32;
-      const uint32_t q = row[0], nnz = row[1];
-      const double o = (double)__uint_as_float(row[2]), vmin = (double)__uint_as_float(row[3]);
+      const uint32_t q = row[0];
       const uint64_t rpo = (uint64_t)row[4] | ((uint64_t)row[5] << 32);
       const uint64_t cbit = 8ull * ((uint64_t)row[6] | ((uint64_t)row[7] << 32));
-      const uint64_t qbit = 8ull * ((uint64_t)row[8] | ((uint64_t)row[9] << 32));
       const uint32_t minus = b >= mp ? 1u : 0u;
-      for (uint32_t r = tid; r < N; r += DSN) {  // codec.py:238-241
-        const uint32_t p0 = gen_u32_le(src, rpo + 4ull * r), p1 = gen_u32_le(src, rpo + 4ull * (r + 1));
-        if (r == 0 && p0 != 0) ck = min(ck, corrupt_key(b, CK_ROWPTR));
-        if (p1 < p0 || (r + 1 == N && p1 != nnz)) ck = min(ck, corrupt_key(b, CK_ROWPTR_NNZ));
+      // the entry's row: the last r < N with row_ptr[r] <= m
+      uint32_t lo = 0, hi = N - 1;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (gen_u32_le(src, rpo + 4ull * mid) <= m) lo = mid; else hi = mid - 1;
       }
-      for (uint32_t m = tid; m < nnz; m += DSN) {
-        // the entry's row: the last r < N with row_ptr[r] <= m
-        uint32_t lo = 0, hi = N - 1;
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi + 1) >> 1;
-          if (gen_u32_le(src, rpo + 4ull * mid) <= m) lo = mid; else hi = mid - 1;
+      const uint32_t r = lo;
+      const uint32_t col = gen_field(src, cbit + (uint64_t)m * cb, cb);
+      if (col >= K) { ck = min(ck, corrupt_key(b, CK_COL_RANGE)); return; }  // codec.py:242-243
+      if (m > gen_u32_le(src, rpo + 4ull * r) && gen_field(src, cbit + (uint64_t)(m - 1) * cb, cb) >= col)
+        ck = min(ck, corrupt_key(b, CK_COL_ORDER));  // codec.py:244-247
+      const uint32_t pos = r * K + col, bit = 1u << (pos & 31u);
+      if (atomicOr(&sh.bm[minus][pos >> 5], bit) & bit) {  // corrupt: the first value stays
+        if (exact) ck = min(ck, corrupt_key(b, CK_OVERLAP));
+        else sh.ovl = 1;
+        return;
+      }
+      const uint64_t qbit = 8ull * ((uint64_t)row[8] | ((uint64_t)row[9] << 32));
+      const double o = (double)__uint_as_float(row[2]), vmin = (double)__uint_as_float(row[3]);
+      const uint32_t code = gen_field(src, qbit + (uint64_t)m * q, q);
+      const double v = __dadd_rn(__dmul_rn((double)code, o), vmin);
+      float f;
+      if (!minus) f = __double2float_rn(v);  // f32(0 + v)
+      else if (sh.bm[0][pos >> 5] & bit)  // both planes: summed in float64 (codec.py:257-266)
+        f = __double2float_rn(__dsub_rn(plus_value(gtab, d.in, mp, r, col, cb), v));
+      else f = __double2float_rn(-v);  // f32(0 - v)
+      sh.buf[pos] = f;
+      // a minus write is final; a non-finite plus value may still be summed with a minus
+      // entry, so it only triggers the full scan below
+      if ((__float_as_uint(f) & 0x7F800000u) == 0x7F800000u) {
+        if (minus) fl = FLAG_NONFINITE;
+        else nfp = 1;
+      }
+    };
+    // row_ptr checks of every block (codec.py:238-241)
+    for (uint32_t k = tid; k < nb * N; k += DSN) {
+      const uint32_t b = k / N, r = k - b * N;
+      const uint32_t* row = tab + (2ull + b) * TROW_U32;
+      const uint64_t rpo = (uint64_t)row[4] | ((uint64_t)row[5] << 32);
+      const uint32_t p0 = gen_u32_le(src, rpo + 4ull * r), p1 = gen_u32_le(src, rpo + 4ull * (r + 1));
+      if (r == 0 && p0 != 0) ck = min(ck, corrupt_key(b, CK_ROWPTR));
+      if (p1 < p0 || (r + 1 == N && p1 != row[1])) ck = min(ck, corrupt_key(b, CK_ROWPTR_NNZ));
+    }
+    // block-ordered pass over the blocks [b0, b1): one barrier per block, overlaps charged to
+    // the later block exactly like the reference's `seen` mask
+    auto ordered = [&](uint32_t b0, uint32_t b1) {
+      for (uint32_t b = b0; b < b1; ++b) {
+        const uint32_t nnz = tab[(2ull + b) * TROW_U32 + 1];
+        for (uint32_t m = tid; m < nnz; m += DSN) entry(b, m, true);
+        __syncthreads();
+      }
+    };
+    if (nb + 2 <= SMALL_ROWS) {
+      // the table rows are in shared memory: each plane's entries in one flattened pass
+      // (entry i -> block by the nnz prefix); a plane with an overlap (corrupt) is redone
+      // in block order for the reference's error
+      if (tid == 0) {
+        uint32_t acc = 0;
+        for (uint32_t b = 0; b < nb; ++b) { sh.pre[b] = acc; acc += tab[(2ull + b) * TROW_U32 + 1]; }
+        sh.pre[nb] = acc;
+        sh.ovl = 0;
+      }
+      __syncthreads();
+      for (uint32_t pl = 0; pl < 2; ++pl) {
+        const uint32_t b0 = pl ? mp : 0u, b1 = pl ? nb : mp;
+        if (b0 >= b1) continue;
+        const uint32_t i0 = sh.pre[b0], i1 = sh.pre[b1];
+        for (uint32_t i = i0 + tid; i < i1; i += DSN) {
+          uint32_t b = b0;
+          while (b + 1 < b1 && sh.pre[b + 1] <= i) ++b;
+          entry(b, i - sh.pre[b], false);
         }
-        const uint32_t r = lo;
-        const uint32_t col = gen_field(src, cbit + (uint64_t)m * cb, cb);
-        if (col >= K) { ck = min(ck, corrupt_key(b, CK_COL_RANGE)); continue; }  // codec.py:242-243
-        if (m > gen_u32_le(src, rpo + 4ull * r) && gen_field(src, cbit + (uint64_t)(m - 1) * cb, cb) >= col)
-          ck = min(ck, corrupt_key(b, CK_COL_ORDER));  // codec.py:244-247
-        const uint32_t pos = r * K + col, bit = 1u << (pos & 31u);
-        if (atomicOr(&sh.bm[minus][pos >> 5], bit) & bit) {  // codec.py:248-250 (corrupt: keep the first value)
-          ck = min(ck, corrupt_key(b, CK_OVERLAP));
-          continue;
-        }
-        const uint32_t code = gen_field(src, qbit + (uint64_t)m * q, q);
-        const double v = __dadd_rn(__dmul_rn((double)code, o), vmin);
-        float f;
-        if (!minus) f = __double2float_rn(v);  // f32(0 + v)
-        else if (sh.bm[0][pos >> 5] & bit)  // both planes: summed in float64 (codec.py:257-266)
-          f = __double2float_rn(__dsub_rn(plus_value(gtab, d.in, mp, r, col, cb), v));
-        else f = __double2float_rn(-v);  // f32(0 - v)
-        sh.buf[pos] = f;
-        // a minus write is final; a non-finite plus value may still be summed with a minus
-        // entry, so it only triggers the full scan below
-        if ((__float_as_uint(f) & 0x7F800000u) == 0x7F800000u) {
-          if (minus) fl = FLAG_NONFINITE;
-          else nfp = 1;
+        __syncthreads();
+        if (sh.ovl) {
+          __syncthreads();
+          if (tid == 0) sh.ovl = 0;
+          for (uint32_t k = tid; k < SMALL_T / 32; k += DSN) sh.bm[pl][k] = 0u;
+          __syncthreads();
+          ordered(b0, b1);
         }
       }
-      __syncthreads();  // blocks in order: an overlap is charged to the later block
+    } else {
+      ordered(0, nb);
     }
     if (__syncthreads_or(nfp))  // non-finite outputs (tensor.py:35-36)
       for (uint32_t k = tid; k < T; k += DSN)
