@@ -150,6 +150,17 @@ int sif_dec_upload(const sif_plan* plan, const sif_dec_desc* descs, void* d_ws, 
 int sif_dec_run(const sif_plan* plan, int parse_only, void* d_ws, int32_t* d_status, void* stream);
 int sif_decode_batched(const sif_dec_desc* descs, int n, int parse_only, void* d_ws,
                        size_t ws_bytes, int32_t* d_status, void* stream);
+/* Rebind one IF / stream of an uploaded plan to new device buffers (stream-ordered, no host
+ * synchronisation): a cached plan then serves a new call with the same shapes and config.
+ * Encode: x and out as in sif_enc_desc (16-byte aligned; out of the plan's capacity), seed.
+ * Decode (the plan must have been made with the stream's CAPACITY as in_len): in (4-byte
+ * aligned), its length len (<= that capacity; written to the device slot d_len_slot, which
+ * becomes the descriptor's in_len_dev), out (rows x cols fp32). */
+int sif_enc_set_input(const sif_plan* plan, void* d_ws, int i, const void* d_x, uint8_t* d_out,
+                      uint64_t seed, void* stream);
+int sif_dec_set_input(const sif_plan* plan, void* d_ws, int i, const uint8_t* d_in, uint64_t len,
+                      uint64_t* d_len_slot, float* d_out, void* stream);
+
 /* Size class: streams of at most max_elems dense elements (default and maximum 4096; 0 =
  * none) are decoded by one CTA each in a single launch (the stream staged in shared
  * memory), the others by the four-kernel path; both give the same output, status and

@@ -18,6 +18,7 @@ CPU fallback: every call goes through libsif.so on a CUDA device.
 from __future__ import annotations
 
 import ctypes
+import os
 import struct
 import zlib
 from dataclasses import dataclass, field
@@ -574,6 +575,33 @@ def encode_list(xs: list, cfg: CodecConfig, seeds) -> list:
     return enc.payloads()
 
 
+# Single-IF calls (the reference-shaped encode() / decode()) reuse a plan per (device,
+# stream, shape, dtype, config): only the buffers are rebound on the device
+# (sif_enc_set_input / sif_dec_set_input), so a call is a few launches and one status read.
+_PLAN_CACHE: dict = {}
+_PLAN_CACHE_MAX = 32
+
+
+_PLAN_CACHE_ON = os.environ.get("SIF_PLAN_CACHE", "1") != "0"
+
+
+def _cache_get(key, make):
+    if not _PLAN_CACHE_ON:
+        return make()
+    obj = _PLAN_CACHE.get(key)
+    if obj is None:
+        if len(_PLAN_CACHE) >= _PLAN_CACHE_MAX:
+            _PLAN_CACHE.pop(next(iter(_PLAN_CACHE)))
+        obj = make()
+        _PLAN_CACHE[key] = obj
+    return obj
+
+
+def _cfg_key(cfg: CodecConfig) -> tuple:
+    return (float(cfg.s), float(cfg.lam), int(cfg.m_plus), int(cfg.m_minus), int(cfg.q_bit), float(cfg.delta),
+            cfg.mode, tuple(int(q) for q in cfg.fixed_q))
+
+
 def encode(x, cfg: CodecConfig, seed: int = 0) -> CompressedIF:
     """encode(x, cfg, seed) of the reference (codec.py:186-232), computed on the GPU: the
     result's `.sif` stream (== serialize(encode(...)) of the reference) stays in device
@@ -582,9 +610,15 @@ def encode(x, cfg: CodecConfig, seed: int = 0) -> CompressedIF:
         raise ConfigError("cfg must be a CodecConfig")
     seed = _check_seed(seed)
     xt, dt = _as_if(x)
-    enc = BatchEncoder(xt.unsqueeze(0), cfg, [seed])
+    rows, cols = xt.shape
+    key = ("enc", xt.device.index, torch.cuda.current_stream().cuda_stream, rows, cols, dt, _cfg_key(cfg))
+    enc = _cache_get(key, lambda: BatchEncoder(xt.unsqueeze(0), cfg, [seed]))
+    out = torch.empty(enc.cap, dtype=torch.uint8, device=xt.device)  # the result keeps its own buffer
+    raise_for(_L().sif_enc_set_input(ctypes.byref(enc.plan), ctypes.c_void_p(enc.ws.data_ptr()), 0,
+                                     ctypes.c_void_p(xt.data_ptr()), ctypes.c_void_p(out.data_ptr()), seed,
+                                     _stream()), "sif_enc_set_input")
     enc.run().check()
-    return CompressedIF._from_stream(enc.payloads()[0])
+    return CompressedIF._from_stream(Payload(out, int(enc.out_len[0].item()), rows, cols))
 
 
 def encode_batch(xs: torch.Tensor, cfg: CodecConfig, seeds) -> list:
@@ -751,9 +785,26 @@ def decode(p) -> torch.Tensor:
         # the framing and CRC checks run first (codec.py:320-385): a damaged shape field
         # raises StreamFormatError instead of sizing the output from it
         p = _check_stream(p)
-    dec = BatchDecoder([p.buf.data_ptr()], [p.nbytes], p.rows, p.cols)
+    cap = int(p.buf.numel())
+    if p.buf.data_ptr() % 4 or cap < p.nbytes:
+        dec = BatchDecoder([p.buf.data_ptr()], [p.nbytes], p.rows, p.cols)
+        dec.run().check()
+        return dec.out[0]
+    key = ("dec", p.buf.device.index, torch.cuda.current_stream().cuda_stream, p.rows, p.cols, cap)
+
+    def make():
+        slot = torch.zeros(1, dtype=torch.int64, device=p.buf.device)
+        d = BatchDecoder([p.buf.data_ptr()], [cap], p.rows, p.cols, len_ptrs=[slot.data_ptr()])
+        d.slot = slot
+        return d
+
+    dec = _cache_get(key, make)
+    out = torch.empty((p.rows, p.cols), dtype=torch.float32, device=p.buf.device)
+    raise_for(_L().sif_dec_set_input(ctypes.byref(dec.plan), ctypes.c_void_p(dec.ws.data_ptr()), 0,
+                                     ctypes.c_void_p(p.buf.data_ptr()), p.nbytes, ctypes.c_void_p(dec.slot.data_ptr()),
+                                     ctypes.c_void_p(out.data_ptr()), _stream()), "sif_dec_set_input")
     dec.run().check()
-    return dec.out[0]
+    return out
 
 
 def decode_batch(payloads: list, out: torch.Tensor | None = None) -> torch.Tensor:

@@ -679,6 +679,14 @@ __global__ void __launch_bounds__(DSN, 7) sif_dec_small(DecArgs a) {
   }
 }
 
+// Rebind stream i of an uploaded plan (sif_dec_set_input): buffers and device length.
+__global__ void set_dec_input_kernel(sif_dec_desc* d, const uint8_t* in, uint64_t* len_slot, uint64_t len, float* out) {
+  d->in = in;
+  d->out = out;
+  *len_slot = len;
+  d->in_len_dev = len_slot;
+}
+
 // ------------------------------------------------------------------------------- finalize
 // One thread per stream: the reference's error precedence (codec.py:320-385, :235-252,
 // tensor.py:27-36) from framing, CRC and validation flags; resets the accumulators.

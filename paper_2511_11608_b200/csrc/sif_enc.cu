@@ -128,6 +128,13 @@ struct EArgs {
   uint32_t inject;           // test-only fault injection (SIF_TEST_INJECT): bit 0 = sampled bracket misses
 };
 
+// Rebind IF i of an uploaded plan (sif_enc_set_input): input, payload buffer, seed.
+__global__ void set_enc_input_kernel(IfInfo* info, const void* x, uint8_t* out, uint64_t seed) {
+  info->x = x;
+  info->out = out;
+  info->seed = seed;
+}
+
 __device__ __forceinline__ void prof_mark(const EArgs& a, int ifi, int k) {
   if (a.prof && threadIdx.x == 0) {
     uint64_t t;

@@ -834,6 +834,29 @@ int sif_decode_batched(const sif_dec_desc* d, int n, int parse_only, void* ws, s
   return sif_dec_run(&p, parse_only, ws, status, stream);
 }
 
+// ------------------------------------------------------------------ input rebinding
+// A plan's descriptors live in its workspace; these rebind one IF's / stream's buffers on
+// the device (a one-thread kernel: stream-ordered, no host synchronisation), so a cached
+// plan serves a new call with the same shapes (the single-IF encode() / decode() API).
+int sif_enc_set_input(const sif_plan* p, void* ws, int i, const void* x, uint8_t* out, uint64_t seed, void* stream) {
+  if (!p || !ws || i < 0 || i >= p->n || !x || (reinterpret_cast<uintptr_t>(x) & 15) || !out ||
+      (reinterpret_cast<uintptr_t>(out) & 15))
+    return SIF_ERR_INVALID_ARG;
+  sif::IfInfo* info = reinterpret_cast<sif::IfInfo*>((uint8_t*)ws + p->ws_desc_off) + i;
+  sif::set_enc_input_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(info, x, out, seed);
+  return check_cuda(cudaGetLastError());
+}
+
+int sif_dec_set_input(const sif_plan* p, void* ws, int i, const uint8_t* in, uint64_t len, uint64_t* d_len_slot,
+                      float* out, void* stream) {
+  if (!p || !ws || i < 0 || i >= p->n || !in || (reinterpret_cast<uintptr_t>(in) & 3) || !d_len_slot ||
+      (reinterpret_cast<uintptr_t>(d_len_slot) & 7) || !out)
+    return SIF_ERR_INVALID_ARG;
+  sif_dec_desc* d = reinterpret_cast<sif_dec_desc*>((uint8_t*)ws + p->ws_desc_off) + i;
+  sif::set_dec_input_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(d, in, d_len_slot, len, out);
+  return check_cuda(cudaGetLastError());
+}
+
 // ------------------------------------------------------------------ synthetic inputs
 int sif_gen_synthetic(void* x, uint32_t rows, uint32_t cols, uint32_t dtype, uint32_t kind, uint64_t sid, void* stream) {
   if (!x || rows == 0 || cols == 0) return SIF_ERR_INVALID_ARG;
