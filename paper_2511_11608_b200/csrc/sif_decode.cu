@@ -632,8 +632,9 @@ __global__ void __launch_bounds__(DSN, 7) sif_dec_small(DecArgs a) {
           entry(b, i - sh.pre[b], false);
         }
         __syncthreads();
-        if (sh.ovl) {
-          __syncthreads();
+        const bool redo = sh.ovl != 0;
+        __syncthreads();  // every thread has read the flag before the next plane may set it
+        if (redo) {
           if (tid == 0) sh.ovl = 0;
           for (uint32_t k = tid; k < SMALL_T / 32; k += DSN) sh.bm[pl][k] = 0u;
           __syncthreads();
