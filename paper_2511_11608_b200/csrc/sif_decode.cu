@@ -499,6 +499,7 @@ struct SmallSh {
   uint32_t ovl;                        // a plane overlap seen in the flattened pass
   uint32_t red[DSN / 32 + 1];
   uint32_t ck, fl, crcok;
+  uint64_t bar;                        // mbarrier of the bulk stream copy
 };
 
 __global__ void __launch_bounds__(DSN, 7) sif_dec_small(DecArgs a) {
@@ -510,10 +511,18 @@ __global__ void __launch_bounds__(DSN, 7) sif_dec_small(DecArgs a) {
   bool over;
   const uint64_t len = stream_len(d, over);
   const bool staged = len <= SMALL_CAP;
+  // stage the stream: a 16-byte aligned stream's whole 16-byte part by one bulk-async copy
+  // (cp.async.bulk, completing on an mbarrier), the rest (tail, zero padding) by plain loads
+  const bool bulk = staged && (reinterpret_cast<uintptr_t>(d.in) & 15u) == 0 && len >= 16;
+  const uint32_t nb16 = bulk ? (uint32_t)(len & ~15ull) : 0u;
+  if (bulk && tid == 0) {
+    mbar_init(&sh.bar, 1);
+    bulk_copy_g2s(sh.cp, d.in, nb16, &sh.bar);
+  }
   if (staged) {
     const uint32_t* gw = reinterpret_cast<const uint32_t*>(d.in);
     const uint32_t nfull = (uint32_t)(len / 4), nw = (uint32_t)((len + 3) / 4);
-    for (uint32_t k = tid; k < nw + 4; k += DSN) {
+    for (uint32_t k = nb16 / 4 + tid; k < nw + 4; k += DSN) {
       uint32_t v = 0;
       if (k < nfull) v = __ldg(gw + k);
       else if (k < nw)  // the partial last word: byte loads (nothing past the stream is read)
@@ -523,7 +532,8 @@ __global__ void __launch_bounds__(DSN, 7) sif_dec_small(DecArgs a) {
   }
   for (int k = tid; k < 1024; k += DSN) sh.t4[k] = (&kCrcTab4[0][0])[k];
   if (tid == 0) { sh.ck = 0xFFFFFFFFu; sh.fl = 0; }
-  __syncthreads();
+  __syncthreads();  // (orders the barrier's init before the other threads wait on it)
+  if (bulk) mbar_wait_parity(&sh.bar, 0);
   const uint8_t* src = staged ? reinterpret_cast<const uint8_t*>(sh.cp) : d.in;
   if (tid == 0) parse_stream(a, i, src, len, over, sh.tab, SMALL_ROWS);
   __syncthreads();  // the table rows written by thread 0 are visible to the CTA
