@@ -46,7 +46,7 @@ enum { SIF_MODE_ABQ = 0, SIF_MODE_FIXED = 1 };
 
 /* Effective blocks (min(M+, k) + min(M-, k), msplit.py:34-38) per IF the encoder supports;
  * sif_enc_plan returns SIF_ERR_CONFIG above it (the reference has no limit). */
-#define SIF_MAX_BLOCKS 32
+#define SIF_MAX_BLOCKS 64
 
 /* CodecConfig (codec.py:61-92).  fixed_q is a HOST pointer with m_plus+m_minus entries
  * (plus-plane entries first), read only during sif_enc_upload / sif_encode_batched. */

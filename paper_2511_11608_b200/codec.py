@@ -451,7 +451,7 @@ def _enc_descs(xs, outs, caps, seeds, dtypes):
     return arr
 
 
-MAX_BLOCKS = 32  # effective blocks (M+ + M-) per IF the device encoder supports (SIF_MAX_BLOCKS)
+MAX_BLOCKS = 64  # effective blocks (M+ + M-) per IF the device encoder supports (SIF_MAX_BLOCKS)
 
 
 def _check_block_count(cfg, sizes) -> None:

@@ -39,7 +39,8 @@ constexpr int UE = CH / UNITS;     // elements per unit
 constexpr int CNT = 256;           // threads of chunk kernels
 constexpr int DSH = 19;            // digit = |x| key >> 19 (12 bits)
 constexpr int ND = 4096;           // digits per sign
-constexpr int MAXB = 32;           // max effective blocks (M+ + M-) per IF (lane-per-block code)
+constexpr int MAXB = 64;           // max effective blocks (M+ + M-) per IF (two per lane in the chunk kernels)
+constexpr int MAXREG = 32;         // gather regions per IF (one per lane in enc_gather)
 constexpr int SNT = 512;           // threads of the per-IF select kernel
 constexpr int HB = 2048;           // radix histogram bins inside select_exact
 constexpr int GCAP = 1024;         // in-SMEM exact ranking capacity
@@ -1041,7 +1042,7 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
           k3.cursor = hist[dt] + hist[ND + dt];
         }
         const int mcfg2[2] = {a.m_plus, a.m_minus};
-        const uint32_t cap = (uint32_t)MAXB - 2u - (uint32_t)(a.m_plus + a.m_minus);  // room left for PH1
+        const int cap = MAXREG - 2 - (a.m_plus + a.m_minus);  // room left for PH1 (checked below)
         for (int sg = 0; sg < 2; ++sg) {
           uint32_t acc = 0;
           for (int d = tid; d < ND; d += NT) acc += (uint32_t)d > dt ? hist[sg * ND + d] : 0u;
@@ -1052,7 +1053,7 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
           __syncthreads();
           const uint64_t n_lo = k3.s.cnt[sg], n_hi = n_lo + hist[sg * ND + dt];
           const uint64_t M = (uint64_t)mcfg2[sg];
-          if (M < 2 || n_lo < M || a.m_plus + a.m_minus > MAXB - 4) continue;
+          if (M < 2 || n_lo < M || cap < 2) continue;
           for (uint64_t j = 1; j < M; ++j) {
             const uint64_t ra = j * (n_lo / M) + 1, rb = min(j * (n_hi / M) + 1, n_lo);
             if (ra > n_lo) continue;  // in tau's bin: gathered already
@@ -1068,7 +1069,7 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
                 const uint32_t key = (uint32_t)sg * ND + d;
                 uint32_t g = 2;
                 while (g < k3.pend_n && st.reg_key[g] != key) ++g;
-                if (g == k3.pend_n && g < 2 + cap) {
+                if (g == k3.pend_n && g < 2u + (uint32_t)cap) {
                   st.reg_key[g] = key; st.reg_off[g] = k3.cursor; st.reg_cnt[g] = 0;
                   k3.cursor += hist[key];
                   ++k3.pend_n;
@@ -1354,6 +1355,7 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
   const int B = (int)(meff[0] + meff[1]);
   const int ncut0 = (int)meff[0] - 1;
   const int ncut = B - 2;
+  bool use_reg = false;  // PH 1: pending cut bins go to the all-SM gathers (enc_gather<2>)
   if (fast || cls_fast) {
     // digit of every cut from the kept histograms; cuts in tau's bin resolve from A
     if (tid == 0) k3.pend_n = 0;
@@ -1379,7 +1381,25 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
     }
     prof_mark(a, ifi, 6);
     const uint32_t np = k3.pend_n;
+    // the all-SM gathers hold one region per lane: more distinct cut bins than MAXREG
+    // (many blocks) are gathered in this CTA instead
     if (PH == 1 && np > 0) {
+      if (tid == 0) {
+        uint32_t nreg = st.nreg_pre;
+        for (uint32_t p = 0; p < np; ++p) {
+          const uint32_t d = k3.pend_s[p] * ND + k3.pend_d[p];
+          bool seen = false;
+          for (uint32_t g = 2; g < st.nreg_pre; ++g) seen |= st.reg_key[g] == d;
+          for (uint32_t q = 0; q < p; ++q) seen |= k3.pend_s[q] * ND + k3.pend_d[q] == d;
+          nreg += seen ? 0u : 1u;
+        }
+        k3.s.cnt[0] = nreg;
+      }
+      __syncthreads();
+      use_reg = k3.s.cnt[0] <= (uint32_t)MAXREG;
+      __syncthreads();
+    }
+    if (use_reg) {
       // regions of the gather area for the pending cut bins (sizes from the histogram);
       // enc_gather<2> fills them with all SMs, enc_select<2> resolves the cuts
       // bins predicted in PH 0 are already gathered; any other is appended as a new region
@@ -1469,7 +1489,7 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
   prof_mark(a, ifi, 8);
   zero_hist(a, f);
   if (tid == 0) {
-    st.sel_phase = (PH == 1 && k3.pend_n > 0 && fast) ? (st.nreg > st.nreg_pre ? 2u : 5u) : 0u;
+    st.sel_phase = (use_reg && fast) ? (st.nreg > st.nreg_pre ? 2u : 5u) : 0u;
     uint32_t fl = 0;
     if (keep_none) fl |= F_KEEP_NONE;
     if (only_nonzero) fl |= F_ONLY_NONZERO;
@@ -1879,7 +1899,7 @@ __global__ void __launch_bounds__(CNT, 6) enc_members(EArgs a) {
         kc.ncut0 = (int)st.ncut0; kc.ncut = (int)st.ncut; kc.meff0 = (int)st.meff0;
       }
       const int nc = (int)st.ncut;
-      if (lane < nc) { kc.ck[lane] = st.cut_key[lane]; kc.cx[lane] = st.cut_idx[lane]; }
+      for (int k = lane; k < nc; k += 32) { kc.ck[k] = st.cut_key[k]; kc.cx[k] = st.cut_idx[k]; }
       __syncwarp();
       cur = ifi;
       B = (int)st.B;
@@ -1895,7 +1915,7 @@ __global__ void __launch_bounds__(CNT, 6) enc_members(EArgs a) {
       if (k + 1 == f.nch)
         for (uint64_t z = (uint64_t)n16 * 16 + lane; z < f.cap; z += 32) f.out[z] = 0;
     }
-    if (lane < B) { ws.cnt[lane] = 0; ws.mn[lane] = 0x7FFFFFFFu; ws.mx[lane] = 0; ws.xl[lane] = 0; }
+    for (int b = lane; b < B; b += 32) { ws.cnt[b] = 0; ws.mn[b] = 0x7FFFFFFFu; ws.mx[b] = 0; ws.xl[b] = 0; }
     __syncwarp();
     const uint2* gl = le(a, f);
     uint2* om = me(a, f) + (uint64_t)(c - f.ch0) * CH;
@@ -1953,19 +1973,24 @@ __global__ void __launch_bounds__(CNT, 6) enc_members(EArgs a) {
       }
       i += un;
     }
-    const uint32_t cnt = lane < B ? ws.cnt[lane] : 0u;
-    const uint32_t sinc = warp_incl_scan_u32(cnt);
-    if (lane < B) {
-      const uint32_t rs = one ? (uint32_t)lane * n : sinc - cnt;
-      ws.pos[lane] = rs;
-      const uint64_t ci = (uint64_t)c * a.maxb + lane;
-      a.ch_bcnt[ci] = cnt;
-      a.ch_brs[ci] = rs;
-      a.ch_blast[ci] = ws.xl[lane] ? (int32_t)fk.div(ws.xl[lane] - 1u) : -1;
-      if (cnt) {
-        atomicMin(&st.bmin[lane], ws.mn[lane]);
-        atomicMax(&st.bmax[lane], ws.mx[lane]);
-        atomicAdd(&st.bcount[lane], cnt);
+    uint32_t carry = 0;
+    for (int b0 = 0; b0 < B; b0 += 32) {  // blocks b0 + lane (two rounds above 32 blocks)
+      const int b = b0 + lane;
+      const uint32_t cnt = b < B ? ws.cnt[b] : 0u;
+      const uint32_t sinc = warp_incl_scan_u32(cnt) + carry;
+      carry = __shfl_sync(0xFFFFFFFFu, sinc, 31);
+      if (b < B) {
+        const uint32_t rs = one ? (uint32_t)b * n : sinc - cnt;
+        ws.pos[b] = rs;
+        const uint64_t ci = (uint64_t)c * a.maxb + b;
+        a.ch_bcnt[ci] = cnt;
+        a.ch_brs[ci] = rs;
+        a.ch_blast[ci] = ws.xl[b] ? (int32_t)fk.div(ws.xl[b] - 1u) : -1;
+        if (cnt) {
+          atomicMin(&st.bmin[b], ws.mn[b]);
+          atomicMax(&st.bmax[b], ws.mx[b]);
+          atomicAdd(&st.bcount[b], cnt);
+        }
       }
     }
     __syncwarp();
@@ -2014,7 +2039,7 @@ struct AbqPar {
   uint32_t act;
 };
 
-template <int FIRST>
+template <int FIRST, bool WIDE>  // WIDE: more than 32 blocks per IF in the batch
 __global__ void __launch_bounds__(CNT, 4) enc_abq(EArgs a) {
   extern __shared__ __align__(16) uint8_t dsm_raw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -2049,8 +2074,9 @@ __global__ void __launch_bounds__(CNT, 4) enc_abq(EArgs a) {
       skipif = false;
       if (!FIRST) {  // pass B: nothing to do unless some block stays within delta at q_bit-1
         bool act = false;
-        if (lane < B && st.bmin[lane] < st.bmax[lane])
-          act = !(__ddiv_rn((double)st.S[lane * 16 + qb - 1], (double)st.bcount[lane]) > a.delta);
+        for (int b = lane; b < B; b += 32)
+          if (st.bmin[b] < st.bmax[b])
+            act |= !(__ddiv_rn((double)st.S[b * 16 + qb - 1], (double)st.bcount[b]) > a.delta);
         skipif = !__any_sync(0xFFFFFFFFu, act);
         if (skipif) continue;
       }
@@ -2078,14 +2104,17 @@ __global__ void __launch_bounds__(CNT, 4) enc_abq(EArgs a) {
       __syncwarp();
     }
     if (skipif) continue;
-    const uint32_t bcnt = lane < B ? a.ch_bcnt[(uint64_t)c * maxb + lane] : 0u;
-    const uint32_t brs = lane < B ? a.ch_brs[(uint64_t)c * maxb + lane] : 0u;
+    // blocks in groups of 32: counts and run starts of group b0 in lane registers
+    const uint64_t cb0 = (uint64_t)c * maxb;
     const uint2* gm = me(a, f) + (uint64_t)(c - f.ch0) * CH;
     const uint32_t lref = (1u << qb) - 1u;
-    for (int b = 0; b < B; ++b) {
-      const uint32_t nb = __shfl_sync(0xFFFFFFFFu, bcnt, b);
+    for (int b0 = 0; b0 < (WIDE ? B : 1); b0 += 32) {
+    const uint32_t bcnt = b0 + lane < B ? a.ch_bcnt[cb0 + b0 + lane] : 0u;
+    const uint32_t brs = b0 + lane < B ? a.ch_brs[cb0 + b0 + lane] : 0u;
+    for (int b = b0; b < (WIDE ? min(B, b0 + 32) : B); ++b) {
+      const uint32_t nb = __shfl_sync(0xFFFFFFFFu, bcnt, b - b0);
       if (nb == 0 || !par[b].act) continue;
-      const uint32_t rs = __shfl_sync(0xFFFFFFFFu, brs, b);
+      const uint32_t rs = __shfl_sync(0xFFFFFFFFu, brs, b - b0);
       const double vmin = par[b].vmin;
       const double oref = par[b].o[qb], iref = par[b].inv[qb];
       if (FIRST) {
@@ -2134,6 +2163,7 @@ __global__ void __launch_bounds__(CNT, 4) enc_abq(EArgs a) {
           }
         }
       }
+    }
     }
   }
   flush();
@@ -2319,6 +2349,7 @@ __device__ __forceinline__ void pack_window(uint32_t* out32, uint32_t* buf, uint
   __syncwarp();
 }
 
+template <bool WIDE>  // WIDE: more than 32 blocks per IF in the batch
 __global__ void __launch_bounds__(CNT, 4) enc_pack(EArgs a) {
   extern __shared__ __align__(16) uint8_t dsm_raw[];
   __shared__ uint32_t pbuf[CNT / 32][2][40];
@@ -2339,36 +2370,39 @@ __global__ void __launch_bounds__(CNT, 4) enc_pack(EArgs a) {
     if (ifi != cur) {
       __syncwarp();
       B = (int)st.B;
-      if (lane < B) {
-        PackPar& p = par[lane];
-        p.vmin = (double)__uint_as_float(st.bmin[lane]);
-        p.o64 = st.o64[lane];
-        p.inv = st.inv64[lane];
-        p.rp = st.off_meta[lane] + kBlockMetaBytes;
-        p.bc = st.bit_cols[lane];
-        p.bq = st.bit_codes[lane];
-        p.q = st.q[lane];
-        p.degen = st.bmin[lane] == st.bmax[lane] ? 1u : 0u;
+      for (int b = lane; b < B; b += 32) {
+        PackPar& p = par[b];
+        p.vmin = (double)__uint_as_float(st.bmin[b]);
+        p.o64 = st.o64[b];
+        p.inv = st.inv64[b];
+        p.rp = st.off_meta[b] + kBlockMetaBytes;
+        p.bc = st.bit_cols[b];
+        p.bq = st.bit_codes[b];
+        p.q = st.q[b];
+        p.degen = st.bmin[b] == st.bmax[b] ? 1u : 0u;
       }
       __syncwarp();
       cur = ifi;
       fk.init(f.K);
     }
-    const uint64_t ci = (uint64_t)c * maxb + lane;
-    const uint32_t bcnt = lane < B ? a.ch_bcnt[ci] : 0u;
-    const uint32_t bpre = lane < B ? a.ch_bpre[ci] : 0u;
-    const int32_t bprev = lane < B ? a.ch_bprev[ci] : -1;
-    const uint32_t brs = lane < B ? a.ch_brs[ci] : 0u;
+    // blocks in groups of 32: the chunk fields of group b0 in lane registers
+    for (int b0 = 0; b0 < (WIDE ? B : 1); b0 += 32) {
+    const uint64_t ci = (uint64_t)c * maxb + b0 + lane;
+    const bool inb = b0 + lane < B;
+    const uint32_t bcnt = inb ? a.ch_bcnt[ci] : 0u;
+    const uint32_t bpre = inb ? a.ch_bpre[ci] : 0u;
+    const int32_t bprev = inb ? a.ch_bprev[ci] : -1;
+    const uint32_t brs = inb ? a.ch_brs[ci] : 0u;
     const uint2* gm = me(a, f) + (uint64_t)(c - f.ch0) * CH;
     uint8_t* out = f.out;
     uint32_t* out32 = reinterpret_cast<uint32_t*>(out);
     const uint32_t cb = f.cb;
-    for (int b = 0; b < B; ++b) {
-      const uint32_t n = __shfl_sync(0xFFFFFFFFu, bcnt, b);
+    for (int b = b0; b < (WIDE ? min(B, b0 + 32) : B); ++b) {
+      const uint32_t n = __shfl_sync(0xFFFFFFFFu, bcnt, b - b0);
       if (n == 0) continue;
-      const uint32_t rs = __shfl_sync(0xFFFFFFFFu, brs, b);
-      const uint32_t p0 = __shfl_sync(0xFFFFFFFFu, bpre, b);
-      int32_t rprev = __shfl_sync(0xFFFFFFFFu, bprev, b);
+      const uint32_t rs = __shfl_sync(0xFFFFFFFFu, brs, b - b0);
+      const uint32_t p0 = __shfl_sync(0xFFFFFFFFu, bpre, b - b0);
+      int32_t rprev = __shfl_sync(0xFFFFFFFFu, bprev, b - b0);
       const PackPar p = par[b];
       const uint32_t lv_ = (1u << p.q) - 1u;
       const uint32_t Rc = (uint32_t)p.bc + p0 * cb, Rq = (uint32_t)p.bq + p0 * p.q;
@@ -2398,6 +2432,7 @@ __global__ void __launch_bounds__(CNT, 4) enc_pack(EArgs a) {
         if (p.q == 8) { if (valid) out[(Rq >> 3) + j] = (uint8_t)code; }
         else pack_window(out32, pbuf[w][1], code, valid, p.q, Rq, Eq, j0, nv, cyq);
       }
+    }
     }
   }
 }

@@ -140,9 +140,12 @@ int dev_init(DevState& ds, int dev) {
       check_cuda(cudaFuncSetAttribute(sif::enc_select<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
       check_cuda(cudaFuncSetAttribute(sif::enc_select<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
 
-      check_cuda(cudaFuncSetAttribute(sif::enc_abq<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_abq(sif::MAXB))) ||
-      check_cuda(cudaFuncSetAttribute(sif::enc_abq<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_abq(sif::MAXB))) ||
-      check_cuda(cudaFuncSetAttribute(sif::enc_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pack(sif::MAXB))) ||
+      check_cuda(cudaFuncSetAttribute(sif::enc_abq<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_abq(32))) ||
+      check_cuda(cudaFuncSetAttribute(sif::enc_abq<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_abq(32))) ||
+      check_cuda(cudaFuncSetAttribute(sif::enc_pack<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pack(32))) ||
+      check_cuda(cudaFuncSetAttribute(sif::enc_abq<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_abq(sif::MAXB))) ||
+      check_cuda(cudaFuncSetAttribute(sif::enc_abq<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_abq(sif::MAXB))) ||
+      check_cuda(cudaFuncSetAttribute(sif::enc_pack<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pack(sif::MAXB))) ||
       check_cuda(cudaFuncSetAttribute(sif::sif_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kSmemScatterMax)))
     return SIF_ERR_CUDA;
@@ -542,8 +545,10 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   {
     std::lock_guard<std::mutex> lk(ds->mu);
     if (!ds->g_abq[maxb]) {
-      ds->g_abq[maxb] = resident_grid(sif::enc_abq<1>, sif::CNT, smem_abq(maxb), 1ull << 30, ds->sms);
-      ds->g_pack[maxb] = resident_grid(sif::enc_pack, sif::CNT, smem_pack(maxb), 1ull << 30, ds->sms);
+      ds->g_abq[maxb] = maxb > 32 ? resident_grid(sif::enc_abq<1, true>, sif::CNT, smem_abq(maxb), 1ull << 30, ds->sms)
+                                  : resident_grid(sif::enc_abq<1, false>, sif::CNT, smem_abq(maxb), 1ull << 30, ds->sms);
+      ds->g_pack[maxb] = maxb > 32 ? resident_grid(sif::enc_pack<true>, sif::CNT, smem_pack(maxb), 1ull << 30, ds->sms)
+                                   : resident_grid(sif::enc_pack<false>, sif::CNT, smem_pack(maxb), 1ull << 30, ds->sms);
     }
     g_abq = ds->g_abq[maxb];
     g_pack = ds->g_pack[maxb];
@@ -589,11 +594,21 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   if (!atkf) {
     { ProfScope ps(KP_MEMBERS, s); sif::enc_members<<<std::min<unsigned>(wgrid, g_members), sif::CNT, 0, s>>>(a); }
     if (c->mode != SIF_MODE_FIXED) {
-      { ProfScope ps(KP_ABQ1, s); sif::enc_abq<1><<<std::min<unsigned>(wgrid, g_abq), sif::CNT, smem_abq(maxb), s>>>(a); }
-      { ProfScope ps(KP_ABQ2, s); sif::enc_abq<0><<<std::min<unsigned>(wgrid, g_abq), sif::CNT, smem_abq(maxb), s>>>(a); }
+      const unsigned ga = std::min<unsigned>(wgrid, g_abq);
+      if (maxb > 32) {
+        { ProfScope ps(KP_ABQ1, s); sif::enc_abq<1, true><<<ga, sif::CNT, smem_abq(maxb), s>>>(a); }
+        { ProfScope ps(KP_ABQ2, s); sif::enc_abq<0, true><<<ga, sif::CNT, smem_abq(maxb), s>>>(a); }
+      } else {
+        { ProfScope ps(KP_ABQ1, s); sif::enc_abq<1, false><<<ga, sif::CNT, smem_abq(maxb), s>>>(a); }
+        { ProfScope ps(KP_ABQ2, s); sif::enc_abq<0, false><<<ga, sif::CNT, smem_abq(maxb), s>>>(a); }
+      }
     }
     { ProfScope ps(KP_LAYOUT, s); sif::enc_layout<<<n, 256, 0, s>>>(a); }
-    { ProfScope ps(KP_PACK, s); sif::enc_pack<<<std::min<unsigned>(wgrid, g_pack), sif::CNT, smem_pack(maxb), s>>>(a); }
+    {
+      ProfScope ps(KP_PACK, s);
+      if (maxb > 32) sif::enc_pack<true><<<std::min<unsigned>(wgrid, g_pack), sif::CNT, smem_pack(maxb), s>>>(a);
+      else sif::enc_pack<false><<<std::min<unsigned>(wgrid, g_pack), sif::CNT, smem_pack(maxb), s>>>(a);
+    }
     { ProfScope ps(KP_CRC, s); sif::enc_crc<<<std::min<unsigned>((unsigned)p->cluster, g_crc), sif::CNT, 0, s>>>(a); }
   }
   return check_cuda(cudaGetLastError());

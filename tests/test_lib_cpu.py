@@ -106,8 +106,10 @@ def test_encode_plan_routing_host_only(lib):
     assert st == 0 and p.reserved == 0  # lambda > 0: pipeline
     st, p = _enc_plan(lib, [(1, 4096)] * 3, sif.CodecConfig(**{**base, "m_plus": 5, "m_minus": 5}))
     assert st == 0 and p.reserved == 0  # 10 blocks: pipeline
-    st, _ = _enc_plan(lib, [(64, 512)], sif.CodecConfig(**{**base, "m_plus": 20, "m_minus": 20}))
-    assert st == 1  # 40 planned blocks > SIF_MAX_BLOCKS
+    st, _ = _enc_plan(lib, [(64, 512)], sif.CodecConfig(**{**base, "m_plus": 32, "m_minus": 32}))
+    assert st == 0  # 64 planned blocks: at the limit
+    st, _ = _enc_plan(lib, [(64, 512)], sif.CodecConfig(**{**base, "m_plus": 40, "m_minus": 40}))
+    assert st == 1  # 80 planned blocks > SIF_MAX_BLOCKS
     st, _ = _enc_plan(lib, [(1 << 16, 1 << 15)], sif.CodecConfig(**base))
     assert st == 8  # SIF_ERR_INVALID_ARG: 2^31 elements
 

@@ -96,7 +96,10 @@ def _wide():
 
 
 def test_oracle_matches_reference_many_blocks():
-    """Many-block configurations (up to 32 effective blocks, tests/golden/make_wide_golden.py)."""
+    """Many-block configurations (up to 64 effective blocks, tests/golden/make_wide_golden.py),
+    including the two 1M-element cases pinned by SHA-256 of the reference's payload and decode."""
+    from oracle.synth import synth
+
     d, names = _wide()
     for n in names:
         s, lam, mp, mm, qb, dl, seed = d[f"{n}_cfg"]
@@ -104,3 +107,11 @@ def test_oracle_matches_reference_many_blocks():
         blob = O.encode_bytes(d[f"{n}_x"], cfg, int(seed))
         assert blob == d[f"{n}_blob"].tobytes(), n
         assert np.array_equal(O.decode_bytes(blob).reshape(-1).view(np.uint32), d[f"{n}_dec"].reshape(-1)), n
+    for n in [str(x) for x in d["big_names"]]:
+        kind, r, c = (int(v) for v in d[f"{n}_shape"])
+        s, lam, mp, mm, qb, dl, seed = d[f"{n}_cfg"]
+        cfg = O.Cfg(s=float(s), lam=float(lam), m_plus=int(mp), m_minus=int(mm), q_bit=int(qb), delta=float(dl))
+        blob = O.encode_bytes(synth(kind, r, c, int(seed)).astype(np.float32), cfg, int(seed))
+        assert hashlib.sha256(blob).hexdigest() == str(d[f"{n}_blob_sha"]), n
+        y = np.ascontiguousarray(O.decode_bytes(blob), np.float32)
+        assert hashlib.sha256(y.view(np.uint32).tobytes()).hexdigest() == str(d[f"{n}_dec_sha"]), n
