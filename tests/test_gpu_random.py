@@ -36,6 +36,8 @@ def _case(rng):
     s = float(rng.choice([0.0, 1.0, rng.random(), rng.random(), rng.uniform(0.8, 0.99)]))
     lam = 0.0 if rng.random() < 0.7 else float(rng.uniform(0, 0.9))
     mp, mm = int(rng.integers(1, 5)), int(rng.integers(1, 5))
+    if rng.random() < 0.1:  # many blocks (up to SIF_MAX_BLOCKS = 64 effective)
+        mp, mm = int(rng.integers(5, 33)), int(rng.integers(5, 33))
     qb = int(rng.choice([1, 2, 4, 8, 8, 8, 12, 16]))
     delta = float(rng.choice([0.0, 0.01, 0.01, 0.1, 1.0]))
     fixed = ()
@@ -109,7 +111,9 @@ def test_multi_kernel_select_path_matches_oracle(sif):
     cfgs = [dict(s=0.9, m_plus=3, m_minus=3, q_bit=8, delta=0.01),
             dict(s=0.8, lam=0.0, m_plus=4, m_minus=2, q_bit=6, delta=0.2),
             dict(s=0.9, lam=0.3, m_plus=2, m_minus=3, q_bit=8, delta=0.05),  # lambda > 0: generic select
-            dict(s=0.85, m_plus=3, m_minus=3, q_bit=8, mode="fixed_q", fixed_q=(9, 6, 4, 8, 5, 3))]
+            dict(s=0.85, m_plus=3, m_minus=3, q_bit=8, mode="fixed_q", fixed_q=(9, 6, 4, 8, 5, 3)),
+            dict(s=0.9, m_plus=32, m_minus=31, q_bit=8, delta=0.01),  # 63 blocks: in-CTA cut-bin gather
+            dict(s=0.8, lam=0.1, m_plus=20, m_minus=24, q_bit=6, delta=0.1)]
     for kw in cfgs:
         refs = [O.encode_bytes(x, O.Cfg(**kw), sd) for x, sd in ((x1, 5), (x2, 6))]
         xs = [torch.from_numpy(x1).cuda().to(torch.bfloat16), torch.from_numpy(x2).cuda()]
@@ -193,7 +197,7 @@ def test_ms_cut_at_last_element_of_large_tie_group(sif):
 def test_per_if_back_end_matches_oracle(sif):
     """The opt-in per-IF encoder back end (sif_set_fused_range; enc_post) on C2-shaped IFs,
     a bracket-miss IF (fault injection off: heavy ties force many candidates), lambda > 0,
-    fixed-Q and delta large enough to descend: byte-identical to the oracle."""
+    fixed-Q, delta large enough to descend and 30 + 30 blocks: byte-identical to the oracle."""
     import ctypes
 
     from oracle import sif_oracle as O
@@ -211,7 +215,8 @@ def test_per_if_back_end_matches_oracle(sif):
         cfgs = [dict(s=0.9, m_plus=3, m_minus=3, q_bit=8, delta=0.01),
                 dict(s=0.8, lam=0.2, m_plus=2, m_minus=3, q_bit=8, delta=0.05),
                 dict(s=0.7, m_plus=4, m_minus=4, q_bit=6, delta=0.5),
-                dict(s=0.85, m_plus=3, m_minus=3, q_bit=8, mode="fixed_q", fixed_q=(9, 6, 4, 8, 5, 3))]
+                dict(s=0.85, m_plus=3, m_minus=3, q_bit=8, mode="fixed_q", fixed_q=(9, 6, 4, 8, 5, 3)),
+                dict(s=0.8, m_plus=30, m_minus=30, q_bit=7, delta=0.3)]
         for kw in cfgs:
             ps = sif.encode_list([torch.from_numpy(x).cuda() for x in xs], sif.CodecConfig(**kw), [5, 6, 7, 8])
             for p, x, sd in zip(ps, xs, (5, 6, 7, 8)):
