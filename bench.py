@@ -693,6 +693,9 @@ def run_latency(args, conf, d, local_rank):
     kprof = _kernel_profile(sif, pipe.slots[0]["fn"], args.steps)
     # host in / host out through the drop-in API
     xh = x.cpu()
+    for _ in range(args.warmup):
+        sif.decode(sif.encode(xh, cfg, seed=d.rank)).cpu()
+    torch.cuda.synchronize()
     h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     h0.record(stream)
     for _ in range(args.steps):

@@ -181,6 +181,7 @@ uint64_t sif_dec_table_offset(const sif_plan* plan, const sif_dec_desc* descs, i
  * returns the number of kernel kinds (or -status on failure); sif_profile_kernel_name(k)
  * names kind k. */
 int sif_profile_enable(int on);
+int sif_profile_enabled(void); /* 1 while enabled (graph-replayed calls bypass the brackets) */
 int sif_profile_read(double* ms, int32_t* count, int maxk);
 const char* sif_profile_kernel_name(int k);
 

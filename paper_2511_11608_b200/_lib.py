@@ -63,6 +63,7 @@ EXPORTS = {
     "sif_dec_set_input": (c_int, [POINTER(Plan), c_void_p, c_int, c_void_p, c_uint64, c_void_p, c_void_p, c_void_p]),
     "sif_gen_synthetic": (c_int, [c_void_p, c_uint32, c_uint32, c_uint32, c_uint32, c_uint64, c_void_p]),
     "sif_profile_enable": (c_int, [c_int]),
+    "sif_profile_enabled": (c_int, []),
     "sif_profile_read": (c_int, [POINTER(c_double), POINTER(c_int32), c_int]),
     "sif_profile_kernel_name": (ctypes.c_char_p, [c_int]),
     "sif_fixture_tensor": (c_int, [c_void_p, c_uint64, c_uint64, c_int, c_void_p]),

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import math
 import struct
 import zlib
 from dataclasses import dataclass, field
@@ -197,8 +198,22 @@ def _canonical_vmax(q: int, o: float, v_min: float, degenerate: bool) -> float:
     """canonicalize_spec (quant.py:76-85): v_max recoverable from the wire fields."""
     if degenerate:
         return float(v_min)
-    with np.errstate(over="ignore"):  # a corrupt-but-framed stream may overflow to inf, as in the reference
-        return float(np.float32(np.float64(np.float32(v_min)) + np.float64(np.float32(o)) * ((1 << q) - 1)))
+    # float32(float64(f32 v_min) + float64(f32 o) * (2^q - 1)) with Python floats (IEEE
+    # binary64) and a round-to-nearest float32 pack; a corrupt-but-framed stream may
+    # overflow to inf, as in the reference
+    d = _f32(v_min) + _f32(o) * ((1 << q) - 1)
+    return _f32(d)
+
+
+_F32 = struct.Struct("<f")
+
+
+def _f32(v: float) -> float:
+    """float(np.float32(v)) without numpy: round to nearest float32, overflow to +-inf."""
+    try:
+        return _F32.unpack(_F32.pack(v))[0]
+    except OverflowError:
+        return math.copysign(math.inf, v)
 
 
 def _unpack_fields(buf: np.ndarray, byte_off: int, n: int, w: int) -> np.ndarray:
@@ -381,11 +396,12 @@ class CompressedIF:
     def _from_stream(cls, p: "Payload", host: np.ndarray | None = None) -> "CompressedIF":
         """View of a well-formed `.sif` stream (already checked on the device): header and
         block fields parsed like codec.py:328-399, arrays unpacked lazily."""
-        if host is None:
-            host = p.buf[: p.nbytes].cpu().numpy()
-        hb = host.tobytes() if host.size < 4096 else None
-        ver, rows, cols, s, lam, qb, dl, mode_code, mp, mm = struct.unpack_from("<HIIffBfBHH", hb or host[:32].tobytes(),
-                                                                               4)
+        if host is None:  # one copy into (cached) pinned host memory, kept alive by the view
+            ht = torch.empty(p.nbytes, dtype=torch.uint8, pin_memory=True)
+            ht.copy_(p.buf[: p.nbytes], non_blocking=True)
+            torch.cuda.current_stream(p.buf.device).synchronize()
+            host = ht.numpy()
+        ver, rows, cols, s, lam, qb, dl, mode_code, mp, mm = struct.unpack_from("<HIIffBfBHH", host, 4)
         mode = MODE_FIXED if mode_code == 1 else MODE_ABQ
         pos = HEADER_BYTES
         qv = ()
@@ -395,7 +411,7 @@ class CompressedIF:
         cb = col_bits(cols)
         blocks = []
         for _ in range(mp + mm):
-            q, o, v_min, nnz = struct.unpack_from("<BffI", host[pos: pos + 13].tobytes(), 0)
+            q, o, v_min, nnz = struct.unpack_from("<BffI", host, pos)
             rp = pos + BLOCK_FIXED_BYTES
             co = rp + 4 * (rows + 1)
             cbytes = (nnz * cb + 7) // 8
@@ -583,6 +599,50 @@ _PLAN_CACHE_MAX = 32
 
 
 _PLAN_CACHE_ON = os.environ.get("SIF_PLAN_CACHE", "1") != "0"
+# a cached plan's launch sequence is captured as one CUDA graph on its second call and
+# replayed after the device-side rebind (SIF_CALL_GRAPHS=0: plain launches every call)
+_CALL_GRAPHS_ON = os.environ.get("SIF_CALL_GRAPHS", "1") != "0"
+
+
+def _run_cached(obj) -> None:
+    """Launch a cached encoder/decoder's kernels on the current stream: eagerly on its first
+    call, as a captured CUDA graph afterwards (one launch instead of one per kernel).  The
+    inputs are rebound on the device before (sif_enc_set_input / sif_dec_set_input), so the
+    graph's kernel arguments never change.  Per-kernel profiling brackets launches on the
+    host, so a profiled call runs eagerly."""
+    if not (_CALL_GRAPHS_ON and _PLAN_CACHE_ON) or _L().sif_profile_enabled():
+        obj.run()
+        return
+    g = obj.__dict__.get("_graph")
+    if g is None:
+        if not obj.__dict__.get("_ran"):
+            obj._ran = True
+            obj.run()
+            return
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            obj.run()
+        obj._graph = g
+    g.replay()
+
+
+def _single_io(obj) -> None:
+    """Point a cached single-IF encoder's payload length and status at one 16-byte device
+    word pair, so a call reads both with one copy (`_read_io`)."""
+    io = torch.zeros(2, dtype=torch.int64, device=obj.status.device)
+    io[1] = -1
+    obj.out_len = io[0:1]
+    obj.status = io.view(torch.int32)[2:3]
+    obj._io = io
+    obj._io_host = torch.empty(2, dtype=torch.int64, pin_memory=True)
+
+
+def _read_io(obj) -> tuple:
+    """(payload length, status) of the call just launched: one D2H copy and one sync."""
+    h = obj._io_host
+    h.copy_(obj._io, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return int(h[0]), int(h.view(torch.int32)[2])
 
 
 def _cache_get(key, make):
@@ -612,13 +672,22 @@ def encode(x, cfg: CodecConfig, seed: int = 0) -> CompressedIF:
     xt, dt = _as_if(x)
     rows, cols = xt.shape
     key = ("enc", xt.device.index, torch.cuda.current_stream().cuda_stream, rows, cols, dt, _cfg_key(cfg))
-    enc = _cache_get(key, lambda: BatchEncoder(xt.unsqueeze(0), cfg, [seed]))
+
+    def make():
+        e = BatchEncoder(xt.unsqueeze(0), cfg, [seed])
+        _single_io(e)
+        return e
+
+    enc = _cache_get(key, make)
     out = torch.empty(enc.cap, dtype=torch.uint8, device=xt.device)  # the result keeps its own buffer
     raise_for(_L().sif_enc_set_input(ctypes.byref(enc.plan), ctypes.c_void_p(enc.ws.data_ptr()), 0,
                                      ctypes.c_void_p(xt.data_ptr()), ctypes.c_void_p(out.data_ptr()), seed,
                                      _stream()), "sif_enc_set_input")
-    enc.run().check()
-    return CompressedIF._from_stream(Payload(out, int(enc.out_len[0].item()), rows, cols))
+    _run_cached(enc)
+    n, st = _read_io(enc)
+    if st != 0:
+        _raise_enc(st, 0, 1)
+    return CompressedIF._from_stream(Payload(out, n, rows, cols))
 
 
 def encode_batch(xs: torch.Tensor, cfg: CodecConfig, seeds) -> list:
@@ -803,7 +872,8 @@ def decode(p) -> torch.Tensor:
     raise_for(_L().sif_dec_set_input(ctypes.byref(dec.plan), ctypes.c_void_p(dec.ws.data_ptr()), 0,
                                      ctypes.c_void_p(p.buf.data_ptr()), p.nbytes, ctypes.c_void_p(dec.slot.data_ptr()),
                                      ctypes.c_void_p(out.data_ptr()), _stream()), "sif_dec_set_input")
-    dec.run().check()
+    _run_cached(dec)
+    dec.check()
     return out
 
 

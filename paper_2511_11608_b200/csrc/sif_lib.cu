@@ -221,6 +221,8 @@ int sif_profile_enable(int on) {
   return SIF_OK;
 }
 
+int sif_profile_enabled(void) { return g_prof.load() ? 1 : 0; }
+
 int sif_profile_read(double* ms, int32_t* count, int maxk) {
   if (!ms || !count || maxk < 0) return SIF_ERR_INVALID_ARG;
   for (int k = 0; k < maxk; ++k) { ms[k] = 0.0; count[k] = 0; }
