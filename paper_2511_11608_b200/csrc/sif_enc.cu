@@ -875,12 +875,25 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
       auto key31 = [](uint32_t b) -> uint64_t { return b & 0x7FFFFFFFu; };
       const uint32_t np = st.pend_n;
       uint2* gat = me(a, f);
+      // lambda > 0: the partial bin at the kept threshold was gathered whole; members are the
+      // kept candidates (KeptCtx::kept over the IfSt written by enc_select<0>)
+      const uint32_t flg = st.flags;
+      const uint64_t cks = st.ck_star, hst = st.h_star;
+      const double tp = st.tau_p, tm = st.tau_m;
+      auto kept = [=](uint32_t b, uint32_t x) -> bool {
+        if (!(flg & F_USE_CLS)) return true;
+        uint64_t c = b & 0x7FFFFFFFu;
+        const double v = (double)__uint_as_float(b);
+        if (v > tp || v < tm) c |= 1ull << 31;
+        if (c != cks) return c > cks;
+        return (flg & F_TIE_ALL) || splitmix(seed, x) <= hst;
+      };
       for (uint32_t p = blockIdx.y; p < np; p += gridDim.y) {
         const uint32_t g = st.pend_reg[p];
         const List Bp{nullptr, gat + st.reg_off[g], 0};
         const uint32_t dc = st.pend_d[p];
         const SelRes r = select_exact<NT, LU>(
-            sh, scratch, Bp, st.reg_cnt[g], [](uint32_t, uint32_t) { return true; }, key31,
+            sh, scratch, Bp, st.reg_cnt[g], kept, key31,
             [](uint32_t, uint32_t x) -> uint64_t { return x; }, (uint64_t)dc << DSH, (uint64_t)(dc + 1) << DSH,
             st.pend_r[p], 31);
         if (tid == 0) { st.cut_key[st.pend_ci[p]] = r.key; st.cut_idx[st.pend_ci[p]] = (uint32_t)r.sec; }
@@ -1355,7 +1368,8 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
   const int B = (int)(meff[0] + meff[1]);
   const int ncut0 = (int)meff[0] - 1;
   const int ncut = B - 2;
-  bool use_reg = false;  // PH 1: pending cut bins go to the all-SM gathers (enc_gather<2>)
+  bool use_reg = false;   // PH 1: pending cut bins go to the all-SM gathers (enc_gather<2>)
+  bool cls_hand = false;  // PH 0, lambda > 0: the same, set up here
   if (fast || cls_fast) {
     // digit of every cut from the kept histograms; cuts in tau's bin resolve from A
     if (tid == 0) k3.pend_n = 0;
@@ -1399,7 +1413,44 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
       use_reg = k3.s.cnt[0] <= (uint32_t)MAXREG;
       __syncthreads();
     }
-    if (use_reg) {
+    // lambda > 0 on a large IF: the cut bins (the partial bin at the kept threshold whole)
+    // go to the all-SM gather (enc_gather<2>) and one CTA per pending cut (enc_select<2>,
+    // kept test from IfSt) instead of a gather pass and sequential selects in this CTA
+    if (PH == 0 && cls_fast && np > 0 && a.big_ncand && ncand > a.big_ncand) {
+      if (tid == 0) {
+        uint32_t nreg = 0, off = 0;
+        bool fits = true;
+        for (uint32_t p = 0; p < np && fits; ++p) {
+          const uint32_t sg = k3.pend_s[p];
+          const uint32_t d = sg * ND + k3.pend_d[p];
+          uint32_t g = 0;
+          while (g < nreg && st.reg_key[g] != d) ++g;
+          if (g == nreg) {
+            if (nreg == (uint32_t)MAXREG) { fits = false; break; }
+            st.reg_key[g] = d;
+            st.reg_off[g] = off;
+            st.reg_cnt[g] = 0;
+            off += k3.pend_d[p] == k3.lowd[sg] ? k3.fullb[sg] : hist[d];
+            ++nreg;
+          }
+          st.pend_s[p] = sg; st.pend_d[p] = k3.pend_d[p]; st.pend_r[p] = k3.pend_r[p];
+          st.pend_ci[p] = k3.pend_ci[p]; st.pend_reg[p] = g;
+        }
+        if (fits) {
+          st.nreg = nreg;
+          st.reg_first = 0;
+          st.pend_n = np;
+          a.big_list[atomicAdd(&a.big_list[a.n], 1u)] = (uint32_t)ifi;  // the gathers visit listed IFs only
+        }
+        k3.s.cnt[0] = fits ? 1u : 0u;
+      }
+      __syncthreads();
+      cls_hand = k3.s.cnt[0] != 0;
+      __syncthreads();
+    }
+    if (cls_hand) {
+      // resolved by enc_gather<2> + enc_select<2> (sel_phase 2)
+    } else if (use_reg) {
       // regions of the gather area for the pending cut bins (sizes from the histogram);
       // enc_gather<2> fills them with all SMs, enc_select<2> resolves the cuts
       // bins predicted in PH 0 are already gathered; any other is appended as a new region
@@ -1489,7 +1540,7 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
   prof_mark(a, ifi, 8);
   zero_hist(a, f);
   if (tid == 0) {
-    st.sel_phase = (use_reg && fast) ? (st.nreg > st.nreg_pre ? 2u : 5u) : 0u;
+    st.sel_phase = cls_hand ? 2u : (use_reg && fast) ? (st.nreg > st.nreg_pre ? 2u : 5u) : 0u;
     uint32_t fl = 0;
     if (keep_none) fl |= F_KEEP_NONE;
     if (only_nonzero) fl |= F_ONLY_NONZERO;

@@ -1,0 +1,7 @@
+# usage: bash tools/gpurun_lam2.sh TAG -- GPU tests, lambda = 0.1 per-kernel times and phases of C4, the C4 sweep
+O=gpurun_out; TAG=${1:-lam2}
+timeout 900 python -m pytest tests -x -q -m gpu > $O/${TAG}_pytest.log 2>&1; echo "pytest rc=$?" >> $O/${TAG}_pytest.log
+timeout 300 python tools/kprof.py 1 2048 4096 32 bf16 lam=0.1 > $O/${TAG}_kp_c4_lam0.1.txt 2>&1
+timeout 300 python tools/phase_prof.py c4 lam=0.1 > $O/${TAG}_ph_c4_lam0.1.txt 2>&1
+timeout 900 python bench.py --config c4sweep --steps 3 --warmup 3 --no-cpu-baseline > $O/${TAG}_bench_c4sweep.json 2> $O/${TAG}_bench_c4sweep.err
+timeout 400 python bench.py --config c4 --steps 20 --warmup 5 --no-cpu-baseline > $O/${TAG}_bench_c4.json 2> $O/${TAG}_bench_c4.err
