@@ -854,10 +854,12 @@ struct K3Sh {
 // shared memory of kSmemSelect bytes (hist | scratch | gbuf).  FUSED: called by the fused
 // per-IF encoder (enc_fused), whose stream phase already left the IF's digit histogram in
 // `hist` and resolved any bracket miss; no multi-kernel split.
-template <int PH, int NT, bool FUSED>
+template <int PH, int NT, bool FUSED, bool DEEP = false>
 __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_t* dsm, K3Sh& k3,
                                           const List* Lin = nullptr) {
-  constexpr int LU = PH > 0 ? 16 : 8;  // loads in flight per thread in list passes (big IFs: deep)
+  // loads in flight per thread in list passes: deep for the big-IF phases and for a batch
+  // with lambda > 0 IFs large enough that their whole select runs here (DEEP)
+  constexpr int LU = (PH > 0 || DEEP) ? 16 : 8;
   SelSh& sh = k3.s;
   uint32_t* hist = dsm;                         // 2*ND
   uint32_t* scratch = dsm + 2 * ND;             // 2*HB + GCAP*4
@@ -1560,12 +1562,12 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
   }
 }
 
-template <int PH>
+template <int PH, bool DEEP = false>
 __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   extern __shared__ __align__(16) uint8_t dsm_raw[];
   __shared__ K3Sh k3;
   if (a.info[blockIdx.x].path != PATH_PIPE) return;  // selected by enc_post
-  select_if<PH, SNT, false>(a, (int)blockIdx.x, reinterpret_cast<uint32_t*>(dsm_raw), k3);
+  select_if<PH, SNT, false, DEEP>(a, (int)blockIdx.x, reinterpret_cast<uint32_t*>(dsm_raw), k3);
 }
 
 

@@ -137,6 +137,7 @@ int dev_init(DevState& ds, int dev) {
   if (cudaMemcpyToSymbol(sif::kPieceShift, t.data(), 4ull * sif::CRC_PIECES_MAX) != cudaSuccess) return SIF_ERR_CUDA;
   if (check_cuda(cudaFuncSetAttribute(sif::enc_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemStream)) ||
       check_cuda(cudaFuncSetAttribute(sif::enc_select<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
+      check_cuda(cudaFuncSetAttribute(sif::enc_select<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
       check_cuda(cudaFuncSetAttribute(sif::enc_select<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
       check_cuda(cudaFuncSetAttribute(sif::enc_select<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
 
@@ -580,7 +581,14 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
     ProfScope ps(KP_SELECT_TINY, s);
     sif::enc_select_tiny<<<(n + sif::TNT / 32 - 1) / (sif::TNT / 32), sif::TNT, 0, s>>>(a);
   }
-  { ProfScope ps(KP_SELECT, s); sif::enc_select<0><<<n, sif::SNT, kSmemSelect, s>>>(a); }
+  {
+    // lambda > 0 with IFs on the multi-kernel path: their tau / class / kept-count passes run
+    // in enc_select<0>, deeper load pipelining measured faster there (C4 lambda = 0.1:
+    // 1967 -> 1710 us) and slower for small IFs (C2: 64 -> 110 us)
+    ProfScope ps(KP_SELECT, s);
+    if (a.big_ncand && c->lam > 0.0) sif::enc_select<0, true><<<n, sif::SNT, kSmemSelect, s>>>(a);
+    else sif::enc_select<0><<<n, sif::SNT, kSmemSelect, s>>>(a);
+  }
   if (a.big_ncand) {  // some IF is large enough for the multi-kernel select
     { ProfScope ps(KP_GATHER1, s); sif::enc_gather<1><<<std::min<unsigned>(wgrid, g_gather), sif::CNT, 0, s>>>(a); }
     { ProfScope ps(KP_SELECT1, s); sif::enc_select<1><<<n, sif::SNT, kSmemSelect, s>>>(a); }
