@@ -328,13 +328,13 @@ def run_reference(args, conf, rank):
     gold = _golden()
     par = Parity(gold, {"c4sweep": "c4", "c1": "c2"}.get(name, name))
     steps = args.steps if name not in ("c4", "c4sweep") else max(1, min(args.steps, 3))
-    r = cpu_measure(conf, name, impl, steps, min(args.warmup, 1), cores, par=par)
+    r = cpu_measure(conf, name, impl, steps, args.warmup, cores, par=par)  # W warm-up steps (each a bounded sample)
     port = None
     if impl == "reference":  # the NumPy port beside it, same sample rule
         p2 = cpu_measure(conf, name, "port", max(1, min(steps, 3)), 1, cores)
         port = dict(value=round(p2["value"], 6), unit="GB/s", cores=cores, kind="port", sample=p2["sample"])
     line = dict(metric=METRIC, value=round(r["value"], 6), unit="GB/s", n_gpus=args.gpus, steps=steps,
-                warmup=min(args.warmup, 1), ms_per_step=r["seconds"] * 1e3 / max(1, steps), higher_is_better=True,
+                warmup=args.warmup, ms_per_step=r["seconds"] * 1e3 / max(1, steps), higher_is_better=True,
                 scaling="strong" if conf.get("mixed") else "weak", vs_baseline=None, dtype=conf["dtype"],
                 data="synthetic", config=dict(workload=conf["workload"], codec=CODEC, sample=r["sample"]),
                 impl="reference",
