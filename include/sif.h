@@ -166,6 +166,9 @@ int sif_dec_set_input(const sif_plan* plan, void* d_ws, int i, const uint8_t* d_
  * memory), the others by the four-kernel path; both give the same output, status and
  * block table.  Process-wide, read by sif_dec_plan (a plan keeps its routing). */
 int sif_set_small_decode(uint64_t max_elems);
+/* Incremented by sif_set_fused_range / sif_set_small_decode: callers that cache plans key
+ * them on it so a routing change takes effect on the next call. */
+uint64_t sif_routing_epoch(void);
 
 /* Block table written by decode/parse: 64-byte rows of uint32.  Row 0 holds {status,
  * rows, cols, m_plus, m_minus, mode, q_bit, nblocks}; row 1 {framing status, crc, len lo,

@@ -59,6 +59,7 @@ EXPORTS = {
     "sif_decode_batched": (c_int, [POINTER(DecDesc), c_int, c_int, c_void_p, c_size_t, c_void_p, c_void_p]),
     "sif_dec_table_offset": (c_uint64, [POINTER(Plan), POINTER(DecDesc), c_int]),
     "sif_set_small_decode": (c_int, [c_uint64]),
+    "sif_routing_epoch": (c_uint64, []),
     "sif_enc_set_input": (c_int, [POINTER(Plan), c_void_p, c_int, c_void_p, c_void_p, c_uint64, c_void_p]),
     "sif_dec_set_input": (c_int, [POINTER(Plan), c_void_p, c_int, c_void_p, c_uint64, c_void_p, c_void_p, c_void_p]),
     "sif_gen_synthetic": (c_int, [c_void_p, c_uint32, c_uint32, c_uint32, c_uint32, c_uint64, c_void_p]),

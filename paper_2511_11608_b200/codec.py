@@ -671,7 +671,8 @@ def encode(x, cfg: CodecConfig, seed: int = 0) -> CompressedIF:
     seed = _check_seed(seed)
     xt, dt = _as_if(x)
     rows, cols = xt.shape
-    key = ("enc", xt.device.index, torch.cuda.current_stream().cuda_stream, rows, cols, dt, _cfg_key(cfg))
+    key = ("enc", xt.device.index, torch.cuda.current_stream().cuda_stream, rows, cols, dt, _cfg_key(cfg),
+           _L().sif_routing_epoch())
 
     def make():
         e = BatchEncoder(xt.unsqueeze(0), cfg, [seed])
@@ -859,7 +860,8 @@ def decode(p) -> torch.Tensor:
         dec = BatchDecoder([p.buf.data_ptr()], [p.nbytes], p.rows, p.cols)
         dec.run().check()
         return dec.out[0]
-    key = ("dec", p.buf.device.index, torch.cuda.current_stream().cuda_stream, p.rows, p.cols, cap)
+    key = ("dec", p.buf.device.index, torch.cuda.current_stream().cuda_stream, p.rows, p.cols, cap,
+           _L().sif_routing_epoch())
 
     def make():
         slot = torch.zeros(1, dtype=torch.int64, device=p.buf.device)

@@ -397,13 +397,18 @@ static int enc_plan_impl(const sif_enc_desc* d, int n, const sif_codec_cfg* c, i
   return SIF_OK;
 }
 
+static std::atomic<uint64_t> g_routing_epoch{0};  // bumped by every routing setter
+
 int sif_set_fused_range(uint64_t tmin, uint64_t tmax) {
   uint64_t a, b;
   fused_range(a, b);  // env defaults first, then the override
   g_fmin = tmin;
   g_fmax = tmax;
+  g_routing_epoch.fetch_add(1);
   return SIF_OK;
 }
+
+uint64_t sif_routing_epoch(void) { return g_routing_epoch.load(); }
 
 int sif_get_fused_range(uint64_t* tmin, uint64_t* tmax) {
   if (!tmin || !tmax) return SIF_ERR_INVALID_ARG;
@@ -692,6 +697,7 @@ static bool dec_is_small(const sif_dec_desc& d) {
 int sif_set_small_decode(uint64_t max_elems) {
   if (max_elems > sif::SMALL_T) return SIF_ERR_INVALID_ARG;
   g_small_max.store(max_elems);
+  g_routing_epoch.fetch_add(1);
   return SIF_OK;
 }
 
