@@ -854,7 +854,7 @@ struct K3Sh {
 // shared memory of kSmemSelect bytes (hist | scratch | gbuf).  FUSED: called by the fused
 // per-IF encoder (enc_fused), whose stream phase already left the IF's digit histogram in
 // `hist` and resolved any bracket miss; no multi-kernel split.
-template <int PH, int NT, bool FUSED, bool DEEP = false>
+template <int PH, int NT, bool FUSED, bool DEEP = false, bool NOCLS = false>
 __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_t* dsm, K3Sh& k3,
                                           const List* Lin = nullptr) {
   // loads in flight per thread in list passes: deep for the big-IF phases and for a batch
@@ -1013,7 +1013,8 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
   uint64_t ck_star = 0, h_star = 0;
   bool tie_all = true;
   int dtau = -1;  // digit of tau on the fast path (-1: every candidate bin counts fully)
-  const bool use_cls = a.lam > 0.0 && kk > 0 && !only_nonzero;
+  // NOCLS: a lambda = 0 batch; the class-select code is compiled out of this instantiation
+  const bool use_cls = !NOCLS && a.lam > 0.0 && kk > 0 && !only_nonzero;
   const bool fast = !zero_mode && !use_cls;
   // lambda > 0 outside zero mode: tau, the class select and the MS cuts are all bracketed
   // by digit histograms and resolved inside gathered bins (a few passes over the list)
@@ -1562,12 +1563,12 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
   }
 }
 
-template <int PH, bool DEEP = false>
+template <int PH, bool DEEP = false, bool NOCLS = false>
 __global__ void __launch_bounds__(SNT) enc_select(EArgs a) {
   extern __shared__ __align__(16) uint8_t dsm_raw[];
   __shared__ K3Sh k3;
   if (a.info[blockIdx.x].path != PATH_PIPE) return;  // selected by enc_post
-  select_if<PH, SNT, false, DEEP>(a, (int)blockIdx.x, reinterpret_cast<uint32_t*>(dsm_raw), k3);
+  select_if<PH, SNT, false, DEEP, NOCLS>(a, (int)blockIdx.x, reinterpret_cast<uint32_t*>(dsm_raw), k3);
 }
 
 
