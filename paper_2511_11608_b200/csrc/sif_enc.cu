@@ -1003,7 +1003,8 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
     cnt_nz += k3.cnt_nz;
     __syncthreads();
   }
-  const bool zero_mode = kk > 0 && lo == 0;
+  // (NOCLS instantiations serve encode batches only: lo >= 1 there, so no zero mode)
+  const bool zero_mode = !NOCLS && kk > 0 && lo == 0;
   const bool keep_none = kk == 0;
   const bool only_nonzero = kk > 0 && cnt_nz < kk && !zero_mode;
   auto hash_of = [seed](uint32_t, uint32_t x) -> uint64_t { return splitmix(seed, x); };
@@ -1013,7 +1014,8 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
   uint64_t ck_star = 0, h_star = 0;
   bool tie_all = true;
   int dtau = -1;  // digit of tau on the fast path (-1: every candidate bin counts fully)
-  // NOCLS: a lambda = 0 batch; the class-select code is compiled out of this instantiation
+  // NOCLS: a lambda = 0 encode batch; the class-select, zero-mode and ATKF-only output code
+  // is compiled out of this instantiation
   const bool use_cls = !NOCLS && a.lam > 0.0 && kk > 0 && !only_nonzero;
   const bool fast = !zero_mode && !use_cls;
   // lambda > 0 outside zero mode: tau, the class select and the MS cuts are all bracketed
@@ -1242,7 +1244,7 @@ __device__ __forceinline__ void select_if(const EArgs& a, const int ifi, uint32_
     return tie_all || splitmix(seed, x) <= h_star;
   };
   // ---- ATKF-only: kept flat indices in ascending order, tau
-  if (a.atkf_only) {
+  if (!NOCLS && a.atkf_only) {
     int64_t* out = a.kept_out + a.kept_off[ifi];
     uint64_t run = 0;
     for (uint64_t u = (uint64_t)f.ch0 * UNITS; u < (uint64_t)(f.ch0 + f.nch) * UNITS; ++u) {

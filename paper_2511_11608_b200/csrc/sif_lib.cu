@@ -593,8 +593,8 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
     // 1967 -> 1710 us) and slower for small IFs (C2: 64 -> 110 us)
     ProfScope ps(KP_SELECT, s);
     if (a.big_ncand && c->lam > 0.0) sif::enc_select<0, true><<<n, sif::SNT, kSmemSelect, s>>>(a);
-    else if (c->lam > 0.0) sif::enc_select<0><<<n, sif::SNT, kSmemSelect, s>>>(a);
-    else sif::enc_select<0, false, true><<<n, sif::SNT, kSmemSelect, s>>>(a);  // lambda = 0: no class code
+    else if (c->lam > 0.0 || atkf) sif::enc_select<0><<<n, sif::SNT, kSmemSelect, s>>>(a);
+    else sif::enc_select<0, false, true><<<n, sif::SNT, kSmemSelect, s>>>(a);  // lambda = 0 encode
   }
   if (a.big_ncand) {  // some IF is large enough for the multi-kernel select
     { ProfScope ps(KP_GATHER1, s); sif::enc_gather<1><<<std::min<unsigned>(wgrid, g_gather), sif::CNT, 0, s>>>(a); }
