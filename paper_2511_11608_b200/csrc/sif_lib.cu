@@ -140,6 +140,7 @@ int dev_init(DevState& ds, int dev) {
       check_cuda(cudaFuncSetAttribute(sif::enc_select<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
       check_cuda(cudaFuncSetAttribute(sif::enc_select<0, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
       check_cuda(cudaFuncSetAttribute(sif::enc_select<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
+      check_cuda(cudaFuncSetAttribute(sif::enc_select<1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
       check_cuda(cudaFuncSetAttribute(sif::enc_select<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSelect)) ||
 
       check_cuda(cudaFuncSetAttribute(sif::enc_abq<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_abq(32))) ||
@@ -598,7 +599,11 @@ static int enc_launch(const sif_plan* p, const sif_codec_cfg* c, void* ws, uint6
   }
   if (a.big_ncand) {  // some IF is large enough for the multi-kernel select
     { ProfScope ps(KP_GATHER1, s); sif::enc_gather<1><<<std::min<unsigned>(wgrid, g_gather), sif::CNT, 0, s>>>(a); }
-    { ProfScope ps(KP_SELECT1, s); sif::enc_select<1><<<n, sif::SNT, kSmemSelect, s>>>(a); }
+    {
+      ProfScope ps(KP_SELECT1, s);
+      if (c->lam > 0.0 || atkf) sif::enc_select<1><<<n, sif::SNT, kSmemSelect, s>>>(a);
+      else sif::enc_select<1, false, true><<<n, sif::SNT, kSmemSelect, s>>>(a);  // lambda = 0 encode
+    }
     if (!atkf) {
       { ProfScope ps(KP_GATHER2, s); sif::enc_gather<2><<<std::min<unsigned>(wgrid, g_gather), sif::CNT, 0, s>>>(a); }
       {
